@@ -1,0 +1,12 @@
+"""fp64 CPU oracle for the SWR / Phalanx-mixer hot path of arXiv 2512.13921.
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+bench.py's ``cpu_baseline`` / ``--impl reference`` legs may import, call, link
+or execute anything under ``oracle/``.  The product package
+(``paper_2512_13921_b200``) never imports it and shares no code with it.
+
+Pinned by ``tests/test_oracle.py`` against the dense jagged operator, the
+constant-decay closed form, the untruncated recurrence on <= 2 blocks, finite
+differences, the transpose identity, locality, linearity and stitching.
+"""
+from .oracle import ELL, build, mix_bwd, mix_fwd, swr_bwd, swr_fwd  # noqa: F401

@@ -1,0 +1,125 @@
+"""fp64 CPU oracle for SWR (jagged window, ell = 16) and the Phalanx double-gated mixer.
+
+TEST INFRASTRUCTURE ONLY: importable from tests/, ``__graft_entry__.smoke()`` and
+bench.py's ``cpu_baseline`` / ``--impl reference`` legs.  Never imported by the
+product package ``paper_2512_13921_b200``.
+
+* ``swr_fwd`` / ``swr_bwd`` call the plain C loops of ``oracle/swr_oracle.c``
+  (the jagged-window definition, and its literal
+  reverse mode).
+* ``mix_fwd`` / ``mix_bwd`` compose them with elementwise numpy exactly in the
+  order the paper writes the Phalanx mixer:
+      u_hat = k * v           (pre-gate)
+      x     = SWR(u_hat)      (Eq. truncated_factorization via B2P)
+      y     = q * x + v       (post-gate with residual)
+  and the backward is the chain rule of those three lines (R13).
+
+All arrays are fp64 numpy, d-tensors [B, L, H, D], decays [B, L, H],
+carries [B, H, D].
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "swr_oracle.c")
+_LIB = os.path.join(_HERE, "libswr_oracle.so")
+_lib = None
+
+ELL = 16
+
+
+def build(force: bool = False) -> str:
+    """Compile the C oracle with gcc (plain -O2, no fast-math, no FMA contraction)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(
+            ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC",
+             "-o", tmp, _SRC, "-lpthread"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        lib = ctypes.CDLL(build())
+        dp = ctypes.c_void_p
+        i64 = ctypes.c_int64
+        lib.swr_oracle_fwd.argtypes = [dp, dp, dp, dp, dp, i64, i64, i64, i64, ctypes.c_int]
+        lib.swr_oracle_fwd.restype = ctypes.c_int
+        lib.swr_oracle_bwd.argtypes = [dp, dp, dp, dp, dp, dp, dp, dp, i64, i64, i64, i64, ctypes.c_int]
+        lib.swr_oracle_bwd.restype = ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+def _f64(x):
+    return None if x is None else np.ascontiguousarray(x, dtype=np.float64)
+
+
+def _ptr(x):
+    return None if x is None else x.ctypes.data_as(ctypes.c_void_p)
+
+
+def _check(u, a):
+    if u.ndim != 4 or a.ndim != 3 or a.shape != u.shape[:3]:
+        raise ValueError(f"shape mismatch: u {u.shape}, a {a.shape}")
+
+
+last_threads = 0  # threads used by the most recent call (reported by bench.py)
+
+
+def swr_fwd(u, a, carry_in=None, carry_out=False, threads: int = 0):
+    """x~ = L~ u (jagged window).  Returns x, or (x, carry_out) if carry_out=True."""
+    global last_threads
+    u, a, carry_in = _f64(u), _f64(a), _f64(carry_in)
+    _check(u, a)
+    B, L, H, D = u.shape
+    x = np.empty_like(u)
+    co = np.empty((B, H, D)) if carry_out else None
+    last_threads = _load().swr_oracle_fwd(_ptr(u), _ptr(a), _ptr(x), _ptr(carry_in), _ptr(co),
+                                          B, L, H, D, threads)
+    return (x, co) if carry_out else x
+
+
+def swr_bwd(u, a, G, carry_in=None, mu_in=None, threads: int = 0):
+    """Reverse mode of swr_fwd.  Returns (du, da, mu_out); mu_out = dLoss/dcarry_in."""
+    global last_threads
+    u, a, G, carry_in, mu_in = _f64(u), _f64(a), _f64(G), _f64(carry_in), _f64(mu_in)
+    _check(u, a)
+    B, L, H, D = u.shape
+    du = np.empty_like(u)
+    da = np.empty_like(a)
+    mu_out = np.empty((B, H, D))
+    last_threads = _load().swr_oracle_bwd(_ptr(u), _ptr(a), _ptr(G), _ptr(du), _ptr(da),
+                                          _ptr(carry_in), _ptr(mu_in), _ptr(mu_out),
+                                          B, L, H, D, threads)
+    return du, da, mu_out
+
+
+def mix_fwd(q, k, v, a, carry_in=None, carry_out=False, threads: int = 0):
+    """Phalanx double-gated mixer."""
+    q, k, v = _f64(q), _f64(k), _f64(v)
+    u_hat = k * v                                      # pre-gate
+    r = swr_fwd(u_hat, a, carry_in, carry_out, threads)
+    x = r[0] if carry_out else r
+    y = q * x + v                                      # post-gate with residual
+    return (y, r[1]) if carry_out else y
+
+
+def mix_bwd(q, k, v, a, dy, carry_in=None, mu_in=None, threads: int = 0):
+    """Chain rule of mix_fwd.  Returns (dq, dk, dv, da, mu_out)."""
+    q, k, v, dy = _f64(q), _f64(k), _f64(v), _f64(dy)
+    u_hat = k * v
+    x = swr_fwd(u_hat, a, carry_in, False, threads)
+    dq = dy * x
+    G = dy * q
+    du_hat, da, mu_out = swr_bwd(u_hat, a, G, carry_in, mu_in, threads)
+    dk = du_hat * v
+    dv = du_hat * k + dy
+    return dq, dk, dv, da, mu_out

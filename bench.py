@@ -1,0 +1,372 @@
+#!/usr/bin/env python
+"""Benchmark of the SWR / Block Two-Pass hot path on B200 (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config layer4k|L8k|L16k|L32k|L4k_b16|paper_d16|tiny] [--op swr|mix]
+                    [--path auto|ffma|tc]
+
+A step is one pass of the whole hot path over one batch of synthetic input:
+SWR forward (swr_fwd) + backward (swr_bwd) -- or, with --op mix, the Phalanx
+mixer forward + backward -- on inputs already resident in HBM.  Metric
+(BASELINE.json): fwd+bwd tokens/s, plus achieved HBM GB/s of the dominant
+kernel against the measured copy peak (MEASURED_PEAKS.json).
+
+Timing: W untimed warm-up steps; then K steps, each bracketed by CUDA events on
+the launching stream with an L2 flush (a write of 2x the L2 size) between
+steps, outside the events; barrier + synchronize around the loop; per-rank sum
+of step times, max over ranks.  Multi-GPU (torchrun): every rank runs the same
+per-GPU workload on its own batch shard (batch x head sharding, no collective;
+weak scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (B, L, H, D, dtype)
+    "layer4k": (8, 4096, 16, 128, "bf16"),    # BJ configs[1]: the metric's workload
+    "L8k": (8, 8192, 16, 128, "bf16"),        # BJ configs[2]: 64K tokens/GPU
+    "L16k": (4, 16384, 16, 128, "bf16"),
+    "L32k": (2, 32768, 16, 128, "bf16"),
+    "L4k_b16": (16, 4096, 16, 128, "bf16"),
+    "bxh": (8, 8192, 16, 128, "bf16"),        # BJ configs[3] per-GPU shard at 8 GPUs
+    "paper_d16": (8, 8192, 128, 16, "bf16"),  # the paper's head shape d=16, h=128
+    "tiny": (1, 64, 1, 16, "f32"),            # BJ configs[0]
+}
+METRIC = "SWR fwd+bwd tokens/s and achieved HBM GB/s vs B200 peak at 4K-32K, 1/2/4/8 GPUs"
+
+
+def esize(dt):
+    return 2 if dt == "bf16" else 4
+
+
+def algo_bytes(op, B, L, H, D, dt):
+    """Algorithmic HBM bytes per launch; halo re-reads excluded."""
+    e, n = esize(dt), B * L * H
+    if op == "swr":
+        return {"fwd": n * (2 * D + 1) * e, "bwd": n * (3 * D + 2) * e}
+    return {"fwd": n * (4 * D + 1) * e, "bwd": n * (7 * D + 2) * e}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    def __init__(self, index, period=0.005):
+        self.index, self.period = index, period
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                try:
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except AttributeError:
+                    r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the fp64 oracle on the host cores
+# ---------------------------------------------------------------------------
+def oracle_step_fn(op, inp_host, rows):
+    import oracle
+    from swr_inputs import to64
+    sl = slice(0, rows)
+    h = {k: to64(v[sl]) for k, v in inp_host.items()}
+    if op == "swr":
+        def step():
+            oracle.swr_fwd(h["u"], h["a"])
+            oracle.swr_bwd(h["u"], h["a"], h["G"])
+    else:
+        def step():
+            oracle.mix_fwd(h["q"], h["k"], h["v"], h["a"])
+            oracle.mix_bwd(h["q"], h["k"], h["v"], h["a"], h["dy"])
+    return step
+
+
+def make_host_inputs(op, B, L, H, D, dt, seed):
+    import torch
+    from swr_inputs import mix_inputs, swr_inputs
+    dtype = torch.bfloat16 if dt == "bf16" else torch.float32
+    f = swr_inputs if op == "swr" else mix_inputs
+    return f(B, L, H, D, dtype=dtype, seed=seed)
+
+
+def cpu_baseline(op, inp_host, B, L, budget_s=10.0, rows=1):
+    """The oracle as it stands on a bounded sample: `rows` batch rows, repeated
+    until `budget_s` of wall time."""
+    import oracle
+    step = oracle_step_fn(op, inp_host, rows)
+    step()  # build + first touch
+    n, t0 = 0, time.perf_counter()
+    while True:
+        step()
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or n >= 1000:
+            break
+    tok = rows * L * n
+    return {"value": tok / el, "unit": "tokens/s", "cores": oracle.oracle.last_threads,
+            "kind": "oracle",
+            "sample": f"{rows} of {B} batch rows (all heads, full length) fwd+bwd, "
+                      f"{n} repetitions in {el:.1f} s, fp64 C oracle"}
+
+
+def run_reference(args, cfg_name, B, L, H, D, dt):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    inp = make_host_inputs(args.op, 1, L, H, D, dt, seed=1)
+    import oracle
+    step = oracle_step_fn(args.op, inp, 1)
+    for _ in range(args.warmup):
+        step()
+    t = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        step()
+        t.append(time.perf_counter() - t0)
+    sec = sum(t) / len(t)
+    val = L / sec
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "tokens/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg_name, "B": B, "L": L, "H": H, "d_head": D, "op": args.op,
+                   "sample_rows_per_step": 1},
+        "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": oracle.oracle.last_threads,
+                         "kind": "oracle",
+                         "sample": f"1 of {B} batch rows (all {H} heads, L={L}) fwd+bwd per step"},
+        "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="layer4k", choices=sorted(CONFIGS))
+    ap.add_argument("--op", default="swr", choices=["swr", "mix"])
+    ap.add_argument("--path", default="auto", choices=["auto", "ffma", "tc"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    B, L, H, D, dt = CONFIGS[args.config]
+
+    if args.impl == "reference":
+        return run_reference(args, args.config, B, L, H, D, dt)
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    import paper_2512_13921_b200 as P
+    P.set_path({"auto": P.SWR_PATH_AUTO, "ffma": P.SWR_PATH_FFMA, "tc": P.SWR_PATH_TC}[args.path])
+
+    # per-rank shard of the batch (batch x head sharding): seed by global batch offset
+    inp_host = make_host_inputs(args.op, B, L, H, D, dt, seed=1 + 1000 * rank)
+    g = {k: v.to(dev) for k, v in inp_host.items()}
+    stream = torch.cuda.current_stream()
+
+    if args.op == "swr":
+        def fwd():
+            return P.swr_fwd(g["u"], g["a"])
+
+        def bwd():
+            return P.swr_bwd(g["u"], g["a"], g["G"])
+    else:
+        def fwd():
+            return P.phalanx_mix(g["q"], g["k"], g["v"], g["a"])
+
+        def bwd():
+            return P.phalanx_mix_bwd(g["q"], g["k"], g["v"], g["a"], g["dy"])
+
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush = torch.empty(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=dev)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        fwd()
+        bwd()
+    torch.cuda.synchronize()
+
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = P.launch_count()
+    with ClockSampler(dev.index if world == 1 else local) as clk:
+        for s in range(args.steps):
+            flush.zero_()
+            ev[s][0].record(stream)
+            fwd()
+            ev[s][1].record(stream)
+            bwd()
+            ev[s][2].record(stream)
+        torch.cuda.synchronize()
+    launches = P.launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    t_fwd = [e[0].elapsed_time(e[1]) for e in ev]
+    t_bwd = [e[1].elapsed_time(e[2]) for e in ev]
+    tot_ms = sum(t_fwd) + sum(t_bwd)
+    t = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = t.item() / args.steps
+    tokens_per_step = B * L * world
+    value = tokens_per_step / (ms_per_step / 1e3)
+
+    bytes_ = algo_bytes(args.op, B, L, H, D, dt)
+    mf, mb = statistics.mean(t_fwd), statistics.mean(t_bwd)
+    dom = "bwd" if mb >= mf else "fwd"
+    peak, peak_kind = load_peaks()
+    ach = bytes_[dom] / (mb if dom == "bwd" else mf) / 1e6  # GB/s
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            tr = json.load(f)
+        key = f"{args.op}_{dom}_{args.config}_{dt}"
+        traffic = tr.get(key)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": dt, "data": "synthetic",
+        "config": {"workload": args.config, "B": B, "L": L, "H": H, "d_head": D, "op": args.op,
+                   "global_batch": B * world, "seq_len": L,
+                   "parallelism": f"dp{world} (batch x head shards, no collective)",
+                   "l2_flush": f"{flush.numel() * 4 >> 20} MiB write between timed steps",
+                   "path": args.path, "last_path": {0: "none", 1: "ffma", 2: "tc"}[P.last_path()]},
+        "fwd_ms": mf, "bwd_ms": mb,
+        "hbm_gbs": {"fwd": bytes_["fwd"] / mf / 1e6, "bwd": bytes_["bwd"] / mb / 1e6,
+                    "fwd_bwd": (bytes_["fwd"] + bytes_["bwd"]) / (mf + mb) / 1e6},
+        "roofline": {"bound": "hbm", "kernel": f"{args.op}_{dom}", "achieved": ach, "peak": peak,
+                     "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
+                     "unit": "GB/s", "frac": ach / peak, "traffic": traffic,
+                     "algorithmic_bytes": bytes_[dom]},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+
+    # end to end through the public API with host buffers (pinned), copies timed
+    if not args.no_e2e:
+        pin = {k: v.pin_memory() for k, v in inp_host.items()}
+        outs_host = None
+        ne = min(args.steps, 10)
+        h2d = sum(v.numel() * v.element_size() for v in pin.values())
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        times = []
+        for s in range(ne + 2):
+            flush.zero_()
+            e0.record(stream)
+            for k, v in pin.items():
+                g[k].copy_(v, non_blocking=True)
+            outs = (fwd(),) + tuple(bwd())
+            if outs_host is None:
+                outs_host = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in outs]
+            for o, oh in zip(outs, outs_host):
+                oh.copy_(o, non_blocking=True)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if s >= 2:
+                times.append(e0.elapsed_time(e1))
+        d2h = sum(o.numel() * o.element_size() for o in outs_host)
+        te = torch.tensor([sum(times) / len(times)], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        line["e2e"] = {"value": tokens_per_step / (te.item() / 1e3), "unit": "tokens/s",
+                       "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                       "ms_per_step": te.item(), "steps": ne}
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args.op, inp_host, B, L)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,165 @@
+/*
+ * swr.h -- C ABI of libswr.so: the Sliding Window Recurrence (SWR) operator of
+ * arXiv 2512.13921 computed by the Block Two-Pass (B2P) algorithm on NVIDIA
+ * B200 (sm_100a), forward and backward, and the Phalanx double-gated mixer
+ * that wraps it.
+ *
+ * Citations are /root/reference/PAPER.md line numbers ("P:n") with the
+ * section / equation / algorithm they fall in.
+ *
+ * ------------------------------------------------------------------------
+ * The operation
+ * ------------------------------------------------------------------------
+ * Per (batch b, head h) the decays a in R^L are shared by the D channels of
+ * the head ("the same set of recurrence coefficients is shared across
+ * all d feature dimensions").  Tokens are grouped in blocks of ell = 16
+ * (P:1486), aligned to token 0.  For block t with local decays a_t[0..15]:
+ *
+ *   L_t[i][j] = a_t[j+1] * ... * a_t[i]   (i >= j, else 0)     P:591-597, Alg. 3
+ *   g_t[i]    = a_t[0] * ... * a_t[i]
+ *   Pass I :  w_t = L_t u_t ,  v_t = w_t[15]                    Alg. 4
+ *   Pass II:  x~_t = w_t + g_t (x) v_{t-1},  v_{-1} = carry_in or 0   Alg. 4
+ *
+ * i.e. x~ = L~ u with the jagged-window operator L~ = blockdiag(L_t) + G Z_b R
+ * (Eq. truncated_factorization, Eq. block_bidiagonal).
+ * Each block's output depends only on its own inputs and those of its
+ * immediate predecessor.
+ *
+ * Phalanx mixer:  u^ = k (.) v ;  x~ = L~ u^ ;  y = q (.) x~ + v.
+ *
+ * Backward (the paper gives none; reading R12): the exact gradient
+ * of the jagged operator, du = L~^T dx, da from reverse mode, and
+ * mu_out = dLoss/dcarry_in.
+ *
+ * ------------------------------------------------------------------------
+ * Conventions shared by every entry point
+ * ------------------------------------------------------------------------
+ * Pointers  : DEVICE pointers owned by the caller.  The library never
+ *             allocates, frees or keeps device memory and holds no state other
+ *             than the process-global path selector and launch counter below;
+ *             it is thread-safe.
+ * Layout    : every "d-tensor" (u, x, dx, du, q, k, v, y, dy, dq, dk, dv) is
+ *             [B, L, H, D] with D contiguous (stride 1) and element strides
+ *             (sx_b, sx_l, sx_h); all d-tensors of one call share those strides.
+ *             Decays a and their gradient da are [B, L, H] with strides
+ *             (sa_b, sa_l, sa_h).  carry_in / carry_out / mu_in / mu_out are
+ *             fp32 [B, H, D], contiguous.
+ * Dtype     : one storage dtype (SWR_F32 or SWR_BF16) for every d-tensor, a and
+ *             da; arithmetic is fp32 throughout ("accumulates ... using
+ *             fp32"); each output is rounded once (RNE) to the storage dtype.
+ * Length    : any L >= 0.  A partial last block behaves as if padded with
+ *             u = 0 and a = 1 (causality makes the real outputs exact);
+ *             carry_out is then the local state at token L-1.  L == 0 is a
+ *             no-op that zero-fills carry_out / mu_out.
+ * Asynchrony: every call enqueues on `stream` (a cudaStream_t; NULL = legacy
+ *             default stream) and returns without synchronising.  Launch
+ *             errors are returned as SWR_ERR_CUDA; faults inside a kernel
+ *             surface at the caller's next synchronisation.
+ * Validation: done before any launch; on error nothing is launched.
+ *   SWR_ERR_NULL   a required pointer is NULL
+ *   SWR_ERR_SHAPE  B, L or H < 0, or D not in {16, 32, 64, 128}
+ *   SWR_ERR_STRIDE a d-tensor stride is negative or not a multiple of 16 bytes
+ *                  (8 bf16 / 4 fp32 elements), or a decay stride is negative
+ *   SWR_ERR_ALIGN  a d-tensor or carry pointer is not 16-byte aligned, or a
+ *                  decay pointer is not aligned to its element size
+ *   SWR_ERR_DTYPE  unknown dtype
+ *   SWR_ERR_CUDA   a CUDA launch/runtime error (see swr_last_cuda_error)
+ *   SWR_ERR_ARCH   the current device is not sm_100 (B200)
+ */
+#ifndef SWR_H_
+#define SWR_H_
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SWR_API __attribute__((visibility("default")))
+#else
+#define SWR_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SWR_OK = 0,
+  SWR_ERR_NULL = 1,
+  SWR_ERR_SHAPE = 2,
+  SWR_ERR_STRIDE = 3,
+  SWR_ERR_ALIGN = 4,
+  SWR_ERR_DTYPE = 5,
+  SWR_ERR_CUDA = 6,
+  SWR_ERR_ARCH = 7
+} swr_status;
+
+typedef enum { SWR_F32 = 0, SWR_BF16 = 1 } swr_dtype;
+
+/* Kernel family used by the entry points (process-global, default AUTO).
+ * SWR_PATH_FFMA: per-thread fp32 recurrences on CUDA cores (any dtype / D).
+ * SWR_PATH_TC  : tcgen05 tensor-core Pass I with TMEM accumulators and
+ *                TMA-staged tiles (bf16, D == 128 only; other calls use FFMA).
+ * SWR_PATH_AUTO: the faster one for the call, as measured. */
+typedef enum { SWR_PATH_AUTO = 0, SWR_PATH_FFMA = 1, SWR_PATH_TC = 2 } swr_path;
+
+typedef struct {
+  int64_t B, L, H, D;       /* batch, sequence length, heads, head dim (d = D/h of P:1555) */
+  int64_t sx_b, sx_l, sx_h; /* element strides of every [B,L,H,D] d-tensor; D is contiguous */
+  int64_t sa_b, sa_l, sa_h; /* element strides of the [B,L,H] decay tensor (and da)        */
+} swr_shape;
+
+/* Forward SWR: x = L~ u.
+ *   u         [B,L,H,D] input (u^ of the mixer)               required
+ *   a         [B,L,H]   decays a_i^eta                       required
+ *   x         [B,L,H,D] output x~ (may not alias u)                   required
+ *   carry_in  [B,H,D] fp32, nullable: carrier v_{-1} entering block 0 (the
+ *             x_0 fold of P:116 for block 0; the segment checkpoint of P:1526).
+ *             Only block 0 sees it.  NULL = 0.
+ *   carry_out [B,H,D] fp32, nullable: local end state of the last block,
+ *             v_b = w_b[15] -- the carry_in of the next segment. */
+SWR_API swr_status swr_fwd(const void* u, const void* a, void* x, const float* carry_in,
+                   float* carry_out, swr_shape s, swr_dtype dt, void* stream);
+
+/* Backward SWR.  Given dx = dLoss/dx:
+ *   du     [B,L,H,D] = L~^T dx (+ the mu_in term)                     required
+ *   da     [B,L,H]   dLoss/da                                         required
+ *   carry_in  same value given to swr_fwd (nullable = 0)
+ *   mu_in  [B,H,D] fp32, nullable: dLoss/dcarry_out from the next segment
+ *   mu_out [B,H,D] fp32, nullable: dLoss/dcarry_in = a[0] * lambda_0[0]
+ * No buffer may alias another. */
+SWR_API swr_status swr_bwd(const void* u, const void* a, const void* dx, void* du, void* da,
+                   const float* carry_in, const float* mu_in, float* mu_out, swr_shape s,
+                   swr_dtype dt, void* stream);
+
+/* Phalanx mixer forward: y = q (.) SWR(k (.) v) + v.
+ * q, k, v, a, y required; carries as in swr_fwd (for u^ = k (.) v). */
+SWR_API swr_status phalanx_mix(const void* q, const void* k, const void* v, const void* a, void* y,
+                       const float* carry_in, float* carry_out, swr_shape s, swr_dtype dt,
+                       void* stream);
+
+/* Phalanx mixer backward: dq = dy (.) x~, dk = du^ (.) v, dv = du^ (.) k + dy, da,
+ * where du^ = SWR backward of G = dy (.) q.  x~ is recomputed, never stored.
+ * q, k, v, a, dy, dq, dk, dv, da required; carries as in swr_bwd. */
+SWR_API swr_status phalanx_mix_bwd(const void* q, const void* k, const void* v, const void* a,
+                           const void* dy, void* dq, void* dk, void* dv, void* da,
+                           const float* carry_in, const float* mu_in, float* mu_out,
+                           swr_shape s, swr_dtype dt, void* stream);
+
+/* Human-readable name of a status code (static storage). */
+SWR_API const char* swr_strerror(swr_status st);
+
+/* Text of the last CUDA error seen by this thread (static storage, "" if none). */
+SWR_API const char* swr_last_cuda_error(void);
+
+/* Select the kernel family (process-global).  Returns the previous value. */
+SWR_API swr_path swr_set_path(swr_path p);
+
+/* Number of kernels this library has launched since load (for bench.py's
+ * "gpu_launches"), and the family that served the most recent call
+ * (1 = FFMA, 2 = TC, 0 = none). */
+SWR_API int64_t swr_launch_count(void);
+SWR_API int swr_last_path(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SWR_H_ */

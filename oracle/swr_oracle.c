@@ -76,7 +76,9 @@ static void fwd_one(const swr_dims* s, int64_t b, int64_t h, const double* u, co
       }
     }
   }
-  if (carry_out) {
+  if (carry_out && nb == 0) /* L == 0: no block, nothing carried */
+    for (int64_t c = 0; c < D; ++c) carry_out[off_c(s, b, h) + c] = 0.0;
+  if (carry_out && nb > 0) {
     /* Local end state of the last block: Eq. 2.1 restarted from zero at the
      * first token of the last block, run to token L-1.  This is v_b of
      * Alg. 4, the "carrier vector" handed to the next segment
@@ -116,6 +118,8 @@ static void bwd_one(const swr_dims* s, int64_t b, int64_t h, const double* u, co
                     const double* mu_in, double* mu_out, double* z, double* lam) {
   const int64_t L = s->L, D = s->D;
   const int64_t nb = (L + ELL - 1) / ELL;
+  if (mu_out) /* L == 0: the initial state reaches nothing */
+    for (int64_t c = 0; c < D; ++c) mu_out[off_c(s, b, h) + c] = 0.0;
   for (int64_t n = 0; n < L; ++n) {
     da[off_a(s, b, n, h)] = 0.0;
     for (int64_t c = 0; c < D; ++c) du[off_x(s, b, n, h) + c] = 0.0;
@@ -146,7 +150,7 @@ static void bwd_one(const swr_dims* s, int64_t b, int64_t h, const double* u, co
     if (t == 0 && mu_out) /* lam is now the adjoint of the initial state */
       for (int64_t c = 0; c < D; ++c) mu_out[off_c(s, b, h) + c] = lam[c];
   }
-  if (mu_in) {
+  if (mu_in && nb > 0) {
     /* reverse mode of the carry_out chain (last block, restarted from zero) */
     const int64_t lo = ELL * (nb - 1);
     chain_states(s, b, h, u, a, lo, L, NULL, z);

@@ -1,0 +1,12 @@
+"""B200-native Sliding Window Recurrence (Block Two-Pass) and Phalanx mixer.
+
+Hot path of arXiv 2512.13921 as a C-ABI library (``libswr.so``, include/swr.h)
+of hand-written sm_100a CUDA kernels, with a thin Python binding.
+
+    from paper_2512_13921_b200 import swr, mix, swr_fwd, swr_bwd, phalanx_mix, phalanx_mix_bwd
+"""
+from . import _lib  # noqa: F401  (fails loudly if libswr.so is missing)
+from ._lib import SWR_PATH_AUTO, SWR_PATH_FFMA, SWR_PATH_TC, SwrError, launch_count, last_path, set_path  # noqa: F401
+from .ops import mix, phalanx_mix, phalanx_mix_bwd, swr, swr_bwd, swr_fwd  # noqa: F401
+
+ELL = 16  # block length

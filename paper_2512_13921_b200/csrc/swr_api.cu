@@ -1,0 +1,252 @@
+// swr_api.cu -- the C ABI of libswr.so (declared in include/swr.h): argument
+// validation, kernel-family dispatch, launch accounting.  No allocation, no
+// host synchronisation, no torch types.
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/swr.h"
+#include "swr_common.cuh"
+
+namespace swr {
+cudaError_t launch_ffma(int op, bool bf16, const Params& p, cudaStream_t st, int sms);
+// tensor-core family (swr_tc.cu); returns cudaErrorNotSupported when the call
+// is outside its envelope so the caller can fall back to FFMA.
+cudaError_t launch_tc(int op, const Params& p, cudaStream_t st, int sms, int* launches);
+bool tc_supported(int op, bool bf16, const Params& p);
+}  // namespace swr
+
+namespace {
+
+std::atomic<int64_t> g_launches{0};
+std::atomic<int> g_path{SWR_PATH_AUTO};
+std::atomic<int> g_last_path{0};
+thread_local char g_cuda_err[256] = "";
+
+constexpr int kMaxDev = 64;
+std::atomic<int> g_sms[kMaxDev];   // 0 = unknown
+std::atomic<int> g_major[kMaxDev];
+
+swr_status cuda_fail(cudaError_t e) {
+  snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+  return SWR_ERR_CUDA;
+}
+
+swr_status device_info(int* sms) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e);
+  if (dev < 0 || dev >= kMaxDev) return SWR_ERR_ARCH;
+  int n = g_sms[dev].load(std::memory_order_relaxed);
+  if (n == 0) {
+    int major = 0;
+    e = cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    if (e != cudaSuccess) return cuda_fail(e);
+    g_major[dev].store(major);
+    g_sms[dev].store(n);
+  }
+  if (g_major[dev].load() != 10) return SWR_ERR_ARCH;  // sm_100 (B200) only
+  *sms = n;
+  return SWR_OK;
+}
+
+bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+swr_status validate(const swr_shape& s, swr_dtype dt, const void* const* dtens, int nd,
+                    const void* const* atens, int na, const void* const* carries, int nc) {
+  if (dt != SWR_F32 && dt != SWR_BF16) return SWR_ERR_DTYPE;
+  if (s.B < 0 || s.L < 0 || s.H < 0) return SWR_ERR_SHAPE;
+  if (!(s.D == 16 || s.D == 32 || s.D == 64 || s.D == 128)) return SWR_ERR_SHAPE;
+  const bool empty = s.B == 0 || s.L == 0 || s.H == 0;  // empty tensors may carry NULL pointers
+  if (!empty) {
+    for (int i = 0; i < nd; ++i)
+      if (!dtens[i]) return SWR_ERR_NULL;
+    for (int i = 0; i < na; ++i)
+      if (!atens[i]) return SWR_ERR_NULL;
+  }
+  if (s.B > 65535 || s.H > 65535 * 16) return SWR_ERR_SHAPE;  // grid limits
+  const int64_t vec = (dt == SWR_BF16) ? 8 : 4;  // elements per 16 bytes
+  if (s.sx_b < 0 || s.sx_l < 0 || s.sx_h < 0 || s.sa_b < 0 || s.sa_l < 0 || s.sa_h < 0)
+    return SWR_ERR_STRIDE;
+  if (s.sx_b % vec || s.sx_l % vec || s.sx_h % vec) return SWR_ERR_STRIDE;
+  for (int i = 0; i < nd; ++i)
+    if (!aligned16(dtens[i])) return SWR_ERR_ALIGN;
+  const uintptr_t esz = (dt == SWR_BF16) ? 2 : 4;
+  for (int i = 0; i < na; ++i)
+    if (reinterpret_cast<uintptr_t>(atens[i]) % esz) return SWR_ERR_ALIGN;
+  for (int i = 0; i < nc; ++i)
+    if (!aligned16(carries[i])) return SWR_ERR_ALIGN;
+  return SWR_OK;
+}
+
+swr::Params make_params(const swr_shape& s) {
+  swr::Params p;
+  std::memset(&p, 0, sizeof(p));
+  p.B = s.B;
+  p.L = s.L;
+  p.H = s.H;
+  p.D = s.D;
+  p.sx_b = s.sx_b;
+  p.sx_l = s.sx_l;
+  p.sx_h = s.sx_h;
+  p.sa_b = s.sa_b;
+  p.sa_l = s.sa_l;
+  p.sa_h = s.sa_h;
+  p.nb = (s.L + swr::kEll - 1) / swr::kEll;
+  return p;
+}
+
+// Empty problem: zero-fill the fp32 carries the caller asked for.
+swr_status empty_call(const swr_shape& s, float* carry_out, float* mu_out, cudaStream_t st) {
+  const size_t bytes = sizeof(float) * (size_t)(s.B * s.H * s.D);
+  if (bytes == 0) return SWR_OK;
+  if (carry_out) {
+    cudaError_t e = cudaMemsetAsync(carry_out, 0, bytes, st);
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
+  if (mu_out) {
+    cudaError_t e = cudaMemsetAsync(mu_out, 0, bytes, st);
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
+  return SWR_OK;
+}
+
+swr_status dispatch(int op, swr_dtype dt, const swr::Params& p, cudaStream_t st) {
+  int sms = 0;
+  swr_status stt = device_info(&sms);
+  if (stt != SWR_OK) return stt;
+  const bool bf16 = dt == SWR_BF16;
+  const int path = g_path.load(std::memory_order_relaxed);
+  if (path != SWR_PATH_FFMA && swr::tc_supported(op, bf16, p)) {
+    int launches = 0;
+    cudaError_t e = swr::launch_tc(op, p, st, sms, &launches);
+    if (e == cudaSuccess) {
+      g_launches += launches;
+      g_last_path = SWR_PATH_TC;
+      return SWR_OK;
+    }
+    if (e != cudaErrorNotSupported) return cuda_fail(e);
+  }
+  cudaError_t e = swr::launch_ffma(op, bf16, p, st, sms);
+  if (e != cudaSuccess) return cuda_fail(e);
+  g_launches += 1;
+  g_last_path = SWR_PATH_FFMA;
+  return SWR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+swr_status swr_fwd(const void* u, const void* a, void* x, const float* carry_in, float* carry_out,
+                   swr_shape s, swr_dtype dt, void* stream) {
+  const void* dt_[] = {u, x};
+  const void* at_[] = {a};
+  const void* ct_[] = {carry_in, carry_out};
+  swr_status st = validate(s, dt, dt_, 2, at_, 1, ct_, 2);
+  if (st != SWR_OK) return st;
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  if (s.B == 0 || s.H == 0 || s.L == 0) return empty_call(s, carry_out, nullptr, cs);
+  swr::Params p = make_params(s);
+  p.u = u;
+  p.a = a;
+  p.x = x;
+  p.carry_in = carry_in;
+  p.carry_out = carry_out;
+  return dispatch(0, dt, p, cs);
+}
+
+swr_status swr_bwd(const void* u, const void* a, const void* dx, void* du, void* da,
+                   const float* carry_in, const float* mu_in, float* mu_out, swr_shape s,
+                   swr_dtype dt, void* stream) {
+  const void* dt_[] = {u, dx, du};
+  const void* at_[] = {a, da};
+  const void* ct_[] = {carry_in, mu_in, mu_out};
+  swr_status st = validate(s, dt, dt_, 3, at_, 2, ct_, 3);
+  if (st != SWR_OK) return st;
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  if (s.B == 0 || s.H == 0 || s.L == 0) return empty_call(s, nullptr, mu_out, cs);
+  swr::Params p = make_params(s);
+  p.u = u;
+  p.a = a;
+  p.dx = dx;
+  p.du = du;
+  p.da = da;
+  p.carry_in = carry_in;
+  p.mu_in = mu_in;
+  p.mu_out = mu_out;
+  return dispatch(1, dt, p, cs);
+}
+
+swr_status phalanx_mix(const void* q, const void* k, const void* v, const void* a, void* y,
+                       const float* carry_in, float* carry_out, swr_shape s, swr_dtype dt,
+                       void* stream) {
+  const void* dt_[] = {q, k, v, y};
+  const void* at_[] = {a};
+  const void* ct_[] = {carry_in, carry_out};
+  swr_status st = validate(s, dt, dt_, 4, at_, 1, ct_, 2);
+  if (st != SWR_OK) return st;
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  if (s.B == 0 || s.H == 0 || s.L == 0) return empty_call(s, carry_out, nullptr, cs);
+  swr::Params p = make_params(s);
+  p.q = q;
+  p.k = k;
+  p.v = v;
+  p.a = a;
+  p.y = y;
+  p.carry_in = carry_in;
+  p.carry_out = carry_out;
+  return dispatch(2, dt, p, cs);
+}
+
+swr_status phalanx_mix_bwd(const void* q, const void* k, const void* v, const void* a,
+                           const void* dy, void* dq, void* dk, void* dv, void* da,
+                           const float* carry_in, const float* mu_in, float* mu_out,
+                           swr_shape s, swr_dtype dt, void* stream) {
+  const void* dt_[] = {q, k, v, dy, dq, dk, dv};
+  const void* at_[] = {a, da};
+  const void* ct_[] = {carry_in, mu_in, mu_out};
+  swr_status st = validate(s, dt, dt_, 7, at_, 2, ct_, 3);
+  if (st != SWR_OK) return st;
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  if (s.B == 0 || s.H == 0 || s.L == 0) return empty_call(s, nullptr, mu_out, cs);
+  swr::Params p = make_params(s);
+  p.q = q;
+  p.k = k;
+  p.v = v;
+  p.a = a;
+  p.dy = dy;
+  p.dq = dq;
+  p.dk = dk;
+  p.dv = dv;
+  p.da = da;
+  p.carry_in = carry_in;
+  p.mu_in = mu_in;
+  p.mu_out = mu_out;
+  return dispatch(3, dt, p, cs);
+}
+
+const char* swr_strerror(swr_status st) {
+  switch (st) {
+    case SWR_OK: return "SWR_OK";
+    case SWR_ERR_NULL: return "SWR_ERR_NULL: a required pointer is NULL";
+    case SWR_ERR_SHAPE: return "SWR_ERR_SHAPE: B/L/H < 0 or D not in {16,32,64,128}";
+    case SWR_ERR_STRIDE: return "SWR_ERR_STRIDE: negative stride or d-tensor stride not a multiple of 16 bytes";
+    case SWR_ERR_ALIGN: return "SWR_ERR_ALIGN: pointer misaligned (16 B for d-tensors/carries, element size for decays)";
+    case SWR_ERR_DTYPE: return "SWR_ERR_DTYPE: unknown dtype";
+    case SWR_ERR_CUDA: return "SWR_ERR_CUDA: CUDA error (see swr_last_cuda_error)";
+    case SWR_ERR_ARCH: return "SWR_ERR_ARCH: current device is not sm_100 (B200)";
+  }
+  return "unknown swr_status";
+}
+
+const char* swr_last_cuda_error(void) { return g_cuda_err; }
+
+swr_path swr_set_path(swr_path p) { return (swr_path)g_path.exchange((int)p); }
+
+int64_t swr_launch_count(void) { return g_launches.load(); }
+
+int swr_last_path(void) { return g_last_path.load(); }
+
+}  // extern "C"

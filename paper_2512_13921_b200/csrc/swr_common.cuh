@@ -1,0 +1,112 @@
+// swr_common.cuh -- internal types shared by the libswr.so kernels (NOT part of
+// the C ABI; see include/swr.h for that).  Nothing here is shared with oracle/.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace swr {
+
+constexpr int kEll = 16;  // block length ell = 16
+
+// Everything a kernel needs, passed by value (__grid_constant__-style).
+struct Params {
+  // SWR operands
+  const void* u;
+  const void* a;
+  void* x;
+  const void* dx;
+  void* du;
+  void* da;
+  // Phalanx mixer operands
+  const void* q;
+  const void* k;
+  const void* v;
+  void* y;
+  const void* dy;
+  void* dq;
+  void* dk;
+  void* dv;
+  // carries, fp32 [B,H,D] contiguous
+  const float* carry_in;
+  float* carry_out;
+  const float* mu_in;
+  float* mu_out;
+  // geometry (elements)
+  int64_t B, L, H, D;
+  int64_t sx_b, sx_l, sx_h;
+  int64_t sa_b, sa_l, sa_h;
+  int64_t nb;  // number of 16-token blocks, ceil(L/16)
+  int64_t K;   // blocks per walk (FFMA path)
+};
+
+// ---------------------------------------------------------------------------
+// storage-dtype traits: 2-channel vector loads/stores, scalar decay access
+// ---------------------------------------------------------------------------
+template <typename T>
+struct IO;
+
+template <>
+struct IO<float> {
+  using raw = float2;
+  static __device__ __forceinline__ raw ld(const float* p) {
+    return __ldg(reinterpret_cast<const float2*>(p));
+  }
+  static __device__ __forceinline__ raw zero() { return make_float2(0.f, 0.f); }
+  static __device__ __forceinline__ float2 f2(raw r) { return r; }
+  static __device__ __forceinline__ void st(float* p, float x, float y) {
+    *reinterpret_cast<float2*>(p) = make_float2(x, y);
+  }
+  static __device__ __forceinline__ float ld1(const float* p) { return __ldg(p); }
+  static __device__ __forceinline__ void st1(float* p, float x) { *p = x; }
+};
+
+template <>
+struct IO<__nv_bfloat16> {
+  using raw = uint32_t;  // two bf16, channel c in the low half (little endian)
+  static __device__ __forceinline__ raw ld(const __nv_bfloat16* p) {
+    return __ldg(reinterpret_cast<const unsigned int*>(p));
+  }
+  static __device__ __forceinline__ raw zero() { return 0u; }
+  static __device__ __forceinline__ float2 f2(raw r) {
+    return make_float2(__uint_as_float(r << 16), __uint_as_float(r & 0xffff0000u));
+  }
+  static __device__ __forceinline__ void st(__nv_bfloat16* p, float x, float y) {
+    *reinterpret_cast<__nv_bfloat162*>(p) = __floats2bfloat162_rn(x, y);
+  }
+  static __device__ __forceinline__ float ld1(const __nv_bfloat16* p) {
+    return __bfloat162float(__ldg(p));
+  }
+  static __device__ __forceinline__ void st1(__nv_bfloat16* p, float x) {
+    *p = __float2bfloat16_rn(x);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// deterministic transpose-reduce of 16 per-token partial sums over a group of
+// GS lanes (GS power of two, <= 32, lanes of one group contiguous and aligned).
+// After the call lane l holds NV = max(1, 16/GS) sums in p[0..NV-1]; p[j] is the
+// group total for token tok + j.  Fixed shuffle order => bitwise reproducible.
+// ---------------------------------------------------------------------------
+template <int KD, int NV>
+struct GroupReduce {
+  static __device__ __forceinline__ void run(float* p, int lane, int& tok) {
+    if constexpr (NV > 1) {
+      constexpr int HALF = NV / 2;
+      const bool up = (lane & KD) != 0;
+#pragma unroll
+      for (int j = 0; j < HALF; ++j) {
+        const float send = up ? p[j] : p[j + HALF];
+        const float keep = up ? p[j + HALF] : p[j];
+        p[j] = keep + __shfl_xor_sync(0xffffffffu, send, KD);
+      }
+      if (up) tok += HALF;
+      if constexpr (KD > 1) GroupReduce<KD / 2, HALF>::run(p, lane, tok);
+    } else {
+      p[0] += __shfl_xor_sync(0xffffffffu, p[0], KD);
+      if constexpr (KD > 1) GroupReduce<KD / 2, 1>::run(p, lane, tok);
+    }
+  }
+};
+
+}  // namespace swr

@@ -1,0 +1,384 @@
+// swr_ffma.cu -- the portable kernel family (SWR_PATH_FFMA): Block Two-Pass on
+// CUDA cores, any storage dtype, D in {16, 32, 64, 128}.
+//
+// Mapping.  A thread owns two adjacent channels of one (b, h) and walks a run
+// of K consecutive 16-token blocks ("chunk").  For every block it
+//   * loads the 16 decays and 16 token pairs of its channels (coalesced across
+//     the lanes of the head: consecutive lanes own consecutive channel pairs),
+//   * Pass I  (Alg. 4, Alg. 5): w_t = L_t u_t as the block-local
+//     recurrence w[i] = a[i] w[i-1] + u[i], w[0] = u[0] (L_t excludes a_t[0],
+//     P:594) -- the same product as the dense 16x16 transfer, 16x fewer FLOPs,
+//   * carrier v_t = w_t[15] kept in registers for the next block,
+//   * Pass II (Alg. 4): x~_t[i] = w_t[i] + g_t[i] v_{t-1} with
+//     g_t[i] = a_t[0]...a_t[i] built by running products (products
+//     only, never ratios).
+// The first block of a chunk gets v_{t-1} by recomputing the previous block's
+// Pass I with the SAME device function (halo), so results do not depend on the
+// chunk size.  Backward walks the chunk in reverse time order carrying
+// mu_t = a_{t+1}[0] lambda_{t+1}[0] (DESIGN.md Appendix "backward").
+#include <algorithm>
+
+#include "swr_common.cuh"
+
+namespace swr {
+
+template <typename T>
+__device__ __forceinline__ void load_decays(const T* A, int64_t sa_l, int64_t n0, int64_t L,
+                                            float (&a)[kEll]) {
+#pragma unroll
+  for (int i = 0; i < kEll; ++i) {
+    const int64_t n = n0 + i;
+    a[i] = (n < L) ? IO<T>::ld1(A + n * sa_l) : 1.f;  // pad: a = 1 (carry_out = state at L-1)
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void load_raw(const T* X, int64_t xo, int64_t sx_l, int64_t n0, int64_t L,
+                                         typename IO<T>::raw (&r)[kEll]) {
+#pragma unroll
+  for (int i = 0; i < kEll; ++i) {
+    const int64_t n = n0 + i;
+    r[i] = (n < L) ? IO<T>::ld(X + xo + n * sx_l) : IO<T>::zero();
+  }
+}
+
+// Pass-I input of a block: u (SWR) or u^ = k (.) v (Phalanx pre-gate).
+template <typename T, bool MIX>
+__device__ __forceinline__ void load_u(const Params& p, int64_t xo, int64_t n0,
+                                       float2 (&u)[kEll]) {
+  using io = IO<T>;
+  if constexpr (!MIX) {
+    typename io::raw r[kEll];
+    load_raw<T>((const T*)p.u, xo, p.sx_l, n0, p.L, r);
+#pragma unroll
+    for (int i = 0; i < kEll; ++i) u[i] = io::f2(r[i]);
+  } else {
+    typename io::raw rk[kEll], rv[kEll];
+    load_raw<T>((const T*)p.k, xo, p.sx_l, n0, p.L, rk);
+    load_raw<T>((const T*)p.v, xo, p.sx_l, n0, p.L, rv);
+#pragma unroll
+    for (int i = 0; i < kEll; ++i) {
+      const float2 kk = io::f2(rk[i]), vv = io::f2(rv[i]);
+      u[i] = make_float2(__fmul_rn(kk.x, vv.x), __fmul_rn(kk.y, vv.y));
+    }
+  }
+}
+
+// Pass I of one block: w = L_t u as the local recurrence (restarted from 0).
+__device__ __forceinline__ void local_solve(const float (&a)[kEll], const float2 (&u)[kEll],
+                                            float2 (&w)[kEll]) {
+  float w0 = u[0].x, w1 = u[0].y;
+  w[0] = u[0];
+#pragma unroll
+  for (int i = 1; i < kEll; ++i) {
+    w0 = fmaf(a[i], w0, u[i].x);
+    w1 = fmaf(a[i], w1, u[i].y);
+    w[i] = make_float2(w0, w1);
+  }
+}
+
+// lambda_t[0] of a block (reverse local recurrence of the adjoint, lambda = L_t^T G):
+// l[15] = G[15], l[i] = G[i] + a[i+1] l[i+1].  Same op order as the walk below.
+__device__ __forceinline__ float2 lambda_step(float a_next, float2 l, float2 G) {
+  return make_float2(fmaf(a_next, l.x, G.x), fmaf(a_next, l.y, G.y));
+}
+
+// Adjoint input of a block: dx (SWR) or G = dy (.) q (mixer).
+template <typename T, bool MIX>
+__device__ __forceinline__ void load_G(const Params& p, int64_t xo, int64_t n0,
+                                       float2 (&G)[kEll]) {
+  using io = IO<T>;
+  if constexpr (!MIX) {
+    typename io::raw r[kEll];
+    load_raw<T>((const T*)p.dx, xo, p.sx_l, n0, p.L, r);
+#pragma unroll
+    for (int i = 0; i < kEll; ++i) G[i] = io::f2(r[i]);
+  } else {
+    typename io::raw rd[kEll], rq[kEll];
+    load_raw<T>((const T*)p.dy, xo, p.sx_l, n0, p.L, rd);
+    load_raw<T>((const T*)p.q, xo, p.sx_l, n0, p.L, rq);
+#pragma unroll
+    for (int i = 0; i < kEll; ++i) {
+      const float2 d = io::f2(rd[i]), qq = io::f2(rq[i]);
+      G[i] = make_float2(__fmul_rn(d.x, qq.x), __fmul_rn(d.y, qq.y));
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// forward
+// ---------------------------------------------------------------------------
+template <typename T, int TPH, bool MIX>
+__global__ void __launch_bounds__(128) fwd_ffma(const Params p) {
+  using io = IO<T>;
+  constexpr int HPC = 128 / TPH;  // heads per CTA
+  const int tid = threadIdx.x;
+  const int hh = tid / TPH;
+  const int c = 2 * (tid % TPH);
+  const int64_t b = blockIdx.z;
+  const int64_t h = (int64_t)blockIdx.y * HPC + hh;
+  if (h >= p.H) return;
+  const int64_t t_lo = (int64_t)blockIdx.x * p.K;
+  const int64_t t_hi = min(t_lo + p.K, p.nb);
+  const T* A = (const T*)p.a + b * p.sa_b + h * p.sa_h;
+  const int64_t xo = b * p.sx_b + h * p.sx_h + c;
+  const int64_t co = (b * p.H + h) * p.D + c;
+
+  float2 vprev = make_float2(0.f, 0.f);  // carrier v_{t-1}; v_{-1} = carry_in or 0
+  if (t_lo == 0) {
+    if (p.carry_in) vprev = *reinterpret_cast<const float2*>(p.carry_in + co);
+  } else {  // halo: Pass I of block t_lo - 1
+    float a[kEll];
+    float2 u[kEll], w[kEll];
+    load_decays<T>(A, p.sa_l, (t_lo - 1) * kEll, p.L, a);
+    load_u<T, MIX>(p, xo, (t_lo - 1) * kEll, u);
+    local_solve(a, u, w);
+    vprev = w[kEll - 1];
+  }
+
+  for (int64_t t = t_lo; t < t_hi; ++t) {
+    const int64_t n0 = t * kEll;
+    float a[kEll];
+    float2 w[kEll];
+    typename io::raw rq[kEll], rv[kEll];
+    load_decays<T>(A, p.sa_l, n0, p.L, a);
+    if constexpr (!MIX) {
+      float2 u[kEll];
+      load_u<T, false>(p, xo, n0, u);
+      local_solve(a, u, w);
+    } else {
+      typename io::raw rk[kEll];
+      load_raw<T>((const T*)p.k, xo, p.sx_l, n0, p.L, rk);
+      load_raw<T>((const T*)p.v, xo, p.sx_l, n0, p.L, rv);
+      load_raw<T>((const T*)p.q, xo, p.sx_l, n0, p.L, rq);
+      float2 u[kEll];
+#pragma unroll
+      for (int i = 0; i < kEll; ++i) {
+        const float2 kk = io::f2(rk[i]), vv = io::f2(rv[i]);
+        u[i] = make_float2(__fmul_rn(kk.x, vv.x), __fmul_rn(kk.y, vv.y));
+      }
+      local_solve(a, u, w);
+    }
+    float g = 1.f;
+#pragma unroll
+    for (int i = 0; i < kEll; ++i) {
+      g *= a[i];  // g_t[i] = a_t[0] ... a_t[i]
+      const float x0 = fmaf(g, vprev.x, w[i].x);  // Pass II: x~ = w + g v_{t-1}
+      const float x1 = fmaf(g, vprev.y, w[i].y);
+      const int64_t n = n0 + i;
+      if (n < p.L) {
+        if constexpr (!MIX) {
+          io::st((T*)p.x + xo + n * p.sx_l, x0, x1);
+        } else {  // post-gate with residual: y = q x~ + v
+          const float2 qq = io::f2(rq[i]), vv = io::f2(rv[i]);
+          io::st((T*)p.y + xo + n * p.sx_l, fmaf(qq.x, x0, vv.x), fmaf(qq.y, x1, vv.y));
+        }
+      }
+    }
+    vprev = w[kEll - 1];
+  }
+  if (t_hi == p.nb && p.carry_out) *reinterpret_cast<float2*>(p.carry_out + co) = vprev;
+}
+
+// ---------------------------------------------------------------------------
+// backward
+//   lambda_t = L_t^T G_t, mu_t = a_{t+1}[0] lambda_{t+1}[0] (mu_in for the last block),
+//   du_t[i] = lambda_t[i] + r_t[i] mu_t,          r_t[i] = a_t[i+1] ... a_t[15]
+//   da_t[i] = sum_c lambda_t[i] x~_t[i-1] + r_t[i] mu_t w_t[i-1]
+//            (x~_t[-1] = v_{t-1}, w_t[-1] = 0)
+// ---------------------------------------------------------------------------
+template <typename T, int TPH, bool MIX>
+__global__ void __launch_bounds__(128) bwd_ffma(const Params p) {
+  using io = IO<T>;
+  constexpr int HPC = 128 / TPH;
+  constexpr int GS = TPH < 32 ? TPH : 32;
+  __shared__ float red[2][HPC][kEll];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int hh = tid / TPH;
+  const int c = 2 * (tid % TPH);
+  const int64_t b = blockIdx.z;
+  const int64_t h = (int64_t)blockIdx.y * HPC + hh;
+  const bool act = h < p.H;
+  const int64_t hc = act ? h : p.H - 1;  // inactive threads read a valid head, store nothing
+  const int64_t t_lo = (int64_t)blockIdx.x * p.K;
+  const int64_t t_hi = min(t_lo + p.K, p.nb);
+  const T* A = (const T*)p.a + b * p.sa_b + hc * p.sa_h;
+  T* dA = (T*)p.da + b * p.sa_b + hc * p.sa_h;
+  const int64_t xo = b * p.sx_b + hc * p.sx_h + c;
+  const int64_t co = (b * p.H + hc) * p.D + c;
+
+  // mu for block t_hi - 1: from the right halo block, or mu_in at the end of the sequence
+  float2 mu = make_float2(0.f, 0.f);
+  if (t_hi == p.nb) {
+    if (p.mu_in) mu = *reinterpret_cast<const float2*>(p.mu_in + co);
+  } else {
+    float a[kEll];
+    float2 G[kEll];
+    load_decays<T>(A, p.sa_l, t_hi * kEll, p.L, a);
+    load_G<T, MIX>(p, xo, t_hi * kEll, G);
+    float2 l = G[kEll - 1];
+#pragma unroll
+    for (int i = kEll - 2; i >= 0; --i) l = lambda_step(a[i + 1], l, G[i]);
+    mu = make_float2(a[0] * l.x, a[0] * l.y);
+  }
+
+  float acur[kEll];
+  float2 wc[kEll];
+  {
+    float2 u[kEll];
+    load_decays<T>(A, p.sa_l, (t_hi - 1) * kEll, p.L, acur);
+    load_u<T, MIX>(p, xo, (t_hi - 1) * kEll, u);
+    local_solve(acur, u, wc);
+  }
+
+  int buf = 0;
+  for (int64_t t = t_hi - 1; t >= t_lo; --t) {
+    const int64_t n0 = t * kEll;
+    float ap[kEll];
+    float2 wp[kEll];
+    float2 vprev = make_float2(0.f, 0.f);
+    if (t > 0) {  // Pass I of block t-1: carrier v_{t-1} and next iteration's w
+      float2 u[kEll];
+      load_decays<T>(A, p.sa_l, n0 - kEll, p.L, ap);
+      load_u<T, MIX>(p, xo, n0 - kEll, u);
+      local_solve(ap, u, wp);
+      vprev = wp[kEll - 1];
+    } else {
+#pragma unroll
+      for (int i = 0; i < kEll; ++i) {
+        ap[i] = 1.f;
+        wp[i] = make_float2(0.f, 0.f);
+      }
+      if (p.carry_in) vprev = *reinterpret_cast<const float2*>(p.carry_in + co);
+    }
+    float2 G[kEll];
+    load_G<T, MIX>(p, xo, n0, G);
+    typename io::raw rk[kEll], rv[kEll], rdy[kEll];
+    if constexpr (MIX) {
+      load_raw<T>((const T*)p.k, xo, p.sx_l, n0, p.L, rk);
+      load_raw<T>((const T*)p.v, xo, p.sx_l, n0, p.L, rv);
+      load_raw<T>((const T*)p.dy, xo, p.sx_l, n0, p.L, rdy);
+    }
+    float g[kEll];
+    {
+      float gg = 1.f;
+#pragma unroll
+      for (int i = 0; i < kEll; ++i) {
+        gg *= acur[i];
+        g[i] = gg;
+      }
+    }
+    float part[kEll];
+    float2 lam = G[kEll - 1];
+    float2 rmu = mu;
+#pragma unroll
+    for (int i = kEll - 1; i >= 0; --i) {
+      if (i < kEll - 1) {
+        lam = lambda_step(acur[i + 1], lam, G[i]);
+        rmu = make_float2(rmu.x * acur[i + 1], rmu.y * acur[i + 1]);
+      }
+      const float du0 = lam.x + rmu.x, du1 = lam.y + rmu.y;
+      const float2 wpv = (i > 0) ? wc[i - 1] : make_float2(0.f, 0.f);
+      const float2 xpv = (i > 0) ? make_float2(fmaf(g[i - 1], vprev.x, wc[i - 1].x),
+                                               fmaf(g[i - 1], vprev.y, wc[i - 1].y))
+                                 : vprev;
+      float s = lam.x * xpv.x;
+      s = fmaf(lam.y, xpv.y, s);
+      s = fmaf(rmu.x, wpv.x, s);
+      s = fmaf(rmu.y, wpv.y, s);
+      part[i] = s;
+      const int64_t n = n0 + i;
+      if (act && n < p.L) {
+        if constexpr (!MIX) {
+          io::st((T*)p.du + xo + n * p.sx_l, du0, du1);
+        } else {
+          const float2 kk = io::f2(rk[i]), vv = io::f2(rv[i]), dd = io::f2(rdy[i]);
+          const float x0 = fmaf(g[i], vprev.x, wc[i].x), x1 = fmaf(g[i], vprev.y, wc[i].y);
+          io::st((T*)p.dq + xo + n * p.sx_l, dd.x * x0, dd.y * x1);          // dq = dy x~
+          io::st((T*)p.dk + xo + n * p.sx_l, du0 * vv.x, du1 * vv.y);        // dk = du^ v
+          io::st((T*)p.dv + xo + n * p.sx_l, fmaf(du0, kk.x, dd.x), fmaf(du1, kk.y, dd.y));  // dv
+        }
+      }
+    }
+    mu = make_float2(acur[0] * lam.x, acur[0] * lam.y);  // for block t-1
+    if (t == 0 && act && p.mu_out) *reinterpret_cast<float2*>(p.mu_out + co) = mu;
+
+    // da: deterministic reduction over the D channels of the head
+    int tok = 0;
+    GroupReduce<GS / 2, kEll>::run(part, lane, tok);
+    if constexpr (TPH <= 32) {
+      constexpr int NV = GS >= kEll ? 1 : kEll / GS;
+      const bool owner = (GS < 32) || ((lane & 1) == 0);
+      if (act && owner) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+          if (n0 + tok + j < p.L) io::st1(dA + (n0 + tok + j) * p.sa_l, part[j]);
+      }
+    } else {
+      const int wih = (tid % TPH) / 32;  // which of the head's two warps
+      if (wih == 1 && (lane & 1) == 0) red[buf][hh][tok] = part[0];
+      __syncthreads();
+      if (wih == 0 && (lane & 1) == 0 && act && n0 + tok < p.L)
+        io::st1(dA + (n0 + tok) * p.sa_l, part[0] + red[buf][hh][tok]);
+      buf ^= 1;
+    }
+#pragma unroll
+    for (int i = 0; i < kEll; ++i) {
+      acur[i] = ap[i];
+      wc[i] = wp[i];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------
+static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+template <typename T, int TPH, bool MIX, bool BWD>
+static cudaError_t launch_tph(Params p, cudaStream_t st, int sms) {
+  constexpr int HPC = 128 / TPH;
+  const int64_t cols = p.B * ceil_div(p.H, HPC);
+  const int64_t want_chunks = std::max<int64_t>(1, ((int64_t)sms * 8) / std::max<int64_t>(cols, 1));
+  int64_t K = ceil_div(p.nb, want_chunks);
+  K = std::max<int64_t>(K, BWD ? 8 : 4);
+  K = std::min<int64_t>(K, p.nb);
+  p.K = K;
+  dim3 grid((unsigned)ceil_div(p.nb, K), (unsigned)ceil_div(p.H, HPC), (unsigned)p.B);
+  if (BWD)
+    bwd_ffma<T, TPH, MIX><<<grid, 128, 0, st>>>(p);
+  else
+    fwd_ffma<T, TPH, MIX><<<grid, 128, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <typename T, bool MIX, bool BWD>
+static cudaError_t launch_d(const Params& p, cudaStream_t st, int sms) {
+  switch (p.D) {
+    case 16: return launch_tph<T, 8, MIX, BWD>(p, st, sms);
+    case 32: return launch_tph<T, 16, MIX, BWD>(p, st, sms);
+    case 64: return launch_tph<T, 32, MIX, BWD>(p, st, sms);
+    default: return launch_tph<T, 64, MIX, BWD>(p, st, sms);
+  }
+}
+
+// op: 0 = swr_fwd, 1 = swr_bwd, 2 = mix_fwd, 3 = mix_bwd; bf16 selects the dtype
+cudaError_t launch_ffma(int op, bool bf16, const Params& p, cudaStream_t st, int sms) {
+  if (bf16) {
+    switch (op) {
+      case 0: return launch_d<__nv_bfloat16, false, false>(p, st, sms);
+      case 1: return launch_d<__nv_bfloat16, false, true>(p, st, sms);
+      case 2: return launch_d<__nv_bfloat16, true, false>(p, st, sms);
+      default: return launch_d<__nv_bfloat16, true, true>(p, st, sms);
+    }
+  }
+  switch (op) {
+    case 0: return launch_d<float, false, false>(p, st, sms);
+    case 1: return launch_d<float, false, true>(p, st, sms);
+    case 2: return launch_d<float, true, false>(p, st, sms);
+    default: return launch_d<float, true, true>(p, st, sms);
+  }
+}
+
+}  // namespace swr

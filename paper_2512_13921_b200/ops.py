@@ -1,0 +1,167 @@
+"""PyTorch-facing entry points (argument marshalling over the C ABI).
+
+PyTorch supplies device memory and the current CUDA stream; every step of the
+computation runs in libswr.so kernels.  Tensors must live on a CUDA device,
+share one storage dtype (float32 or bfloat16) and have the head dim contiguous.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+
+_DT = {torch.float32: _lib.SWR_F32, torch.bfloat16: _lib.SWR_BF16}
+
+
+def _like(t):
+    """Output buffer with exactly the strides of `t` (the ABI shares strides across d-tensors)."""
+    return torch.empty_strided(t.shape, t.stride(), dtype=t.dtype, device=t.device)
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _prep(*ts):
+    """Common strides for the d-tensors: keep them if shared and D-contiguous, else copy."""
+    ref = ts[0]
+    if ref.dim() != 4:
+        raise ValueError(f"expected [B, L, H, D] tensors, got shape {tuple(ref.shape)}")
+    ok = ref.stride(3) == 1 and all(t.shape == ref.shape and t.stride() == ref.stride() for t in ts)
+    if not ok:
+        ts = tuple(t.contiguous() for t in ts)
+    return ts
+
+
+def _carry(t, like):
+    if t is None:
+        return None
+    B, _, H, D = like.shape
+    if t.shape != (B, H, D):
+        raise ValueError(f"carry must be [B, H, D] = {(B, H, D)}, got {tuple(t.shape)}")
+    return t.to(device=like.device, dtype=torch.float32).contiguous()
+
+
+def _shape(x, a):
+    if a.dim() != 3 or tuple(a.shape) != tuple(x.shape[:3]):
+        raise ValueError(f"decays must be [B, L, H] = {tuple(x.shape[:3])}, got {tuple(a.shape)}")
+    B, L, H, D = x.shape
+    sx, sa = x.stride(), a.stride()
+    return _lib.swr_shape(B, L, H, D, sx[0], sx[1], sx[2], sa[0], sa[1], sa[2])
+
+
+def _dtype(*ts):
+    dt = ts[0].dtype
+    if dt not in _DT:
+        raise TypeError(f"unsupported dtype {dt}: use torch.float32 or torch.bfloat16")
+    for t in ts:
+        if t.dtype != dt:
+            raise TypeError("all operands must share one dtype")
+        if not t.is_cuda:
+            raise ValueError("libswr operates on CUDA tensors only (no CPU fallback)")
+    return _DT[dt]
+
+
+def _stream(t):
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def _new_carry(like):
+    B, _, H, D = like.shape
+    return torch.empty((B, H, D), device=like.device, dtype=torch.float32)
+
+
+# ---------------------------------------------------------------------------
+# raw forward / backward calls
+# ---------------------------------------------------------------------------
+def swr_fwd(u, a, carry_in=None, return_carry=False):
+    """x~ = L~ u (jagged window, B2P).  Returns x or (x, carry_out)."""
+    (u,) = _prep(u)
+    dt = _dtype(u, a)
+    x = _like(u)
+    ci = _carry(carry_in, u)
+    co = _new_carry(u) if return_carry else None
+    with torch.cuda.device(u.device):
+        _lib.swr_fwd(_ptr(u), _ptr(a), _ptr(x), _ptr(ci), _ptr(co), _shape(u, a), dt, _stream(u))
+    return (x, co) if return_carry else x
+
+
+def swr_bwd(u, a, dx, carry_in=None, mu_in=None):
+    """Returns (du, da, mu_out) for loss gradient dx = dLoss/dx~."""
+    u, dx = _prep(u, dx)
+    dt = _dtype(u, a, dx)
+    du = _like(u)
+    da = _like(a)
+    ci, mi = _carry(carry_in, u), _carry(mu_in, u)
+    mo = _new_carry(u)
+    with torch.cuda.device(u.device):
+        _lib.swr_bwd(_ptr(u), _ptr(a), _ptr(dx), _ptr(du), _ptr(da), _ptr(ci), _ptr(mi), _ptr(mo),
+                     _shape(u, a), dt, _stream(u))
+    return du, da, mo
+
+
+def phalanx_mix(q, k, v, a, carry_in=None, return_carry=False):
+    """y = q (.) SWR(k (.) v) + v."""
+    q, k, v = _prep(q, k, v)
+    dt = _dtype(q, k, v, a)
+    y = _like(q)
+    ci = _carry(carry_in, q)
+    co = _new_carry(q) if return_carry else None
+    with torch.cuda.device(q.device):
+        _lib.phalanx_mix(_ptr(q), _ptr(k), _ptr(v), _ptr(a), _ptr(y), _ptr(ci), _ptr(co),
+                         _shape(q, a), dt, _stream(q))
+    return (y, co) if return_carry else y
+
+
+def phalanx_mix_bwd(q, k, v, a, dy, carry_in=None, mu_in=None):
+    """Returns (dq, dk, dv, da, mu_out)."""
+    q, k, v, dy = _prep(q, k, v, dy)
+    dt = _dtype(q, k, v, a, dy)
+    dq, dk, dv = _like(q), _like(q), _like(q)
+    da = _like(a)
+    ci, mi = _carry(carry_in, q), _carry(mu_in, q)
+    mo = _new_carry(q)
+    with torch.cuda.device(q.device):
+        _lib.phalanx_mix_bwd(_ptr(q), _ptr(k), _ptr(v), _ptr(a), _ptr(dy), _ptr(dq), _ptr(dk),
+                             _ptr(dv), _ptr(da), _ptr(ci), _ptr(mi), _ptr(mo), _shape(q, a), dt,
+                             _stream(q))
+    return dq, dk, dv, da, mo
+
+
+# ---------------------------------------------------------------------------
+# autograd wrappers
+# ---------------------------------------------------------------------------
+class SWRFunction(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, u, a, carry_in):
+        ctx.save_for_backward(u, a, carry_in)
+        return swr_fwd(u, a, carry_in)
+
+    @staticmethod
+    def backward(ctx, dx):
+        u, a, carry_in = ctx.saved_tensors
+        du, da, mu_out = swr_bwd(u, a, dx.to(u.dtype), carry_in)
+        return du, da, (mu_out if carry_in is not None else None)
+
+
+class PhalanxMixFunction(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, q, k, v, a, carry_in):
+        ctx.save_for_backward(q, k, v, a, carry_in)
+        return phalanx_mix(q, k, v, a, carry_in)
+
+    @staticmethod
+    def backward(ctx, dy):
+        q, k, v, a, carry_in = ctx.saved_tensors
+        dq, dk, dv, da, mu_out = phalanx_mix_bwd(q, k, v, a, dy.to(q.dtype), carry_in)
+        return dq, dk, dv, da, (mu_out if carry_in is not None else None)
+
+
+def swr(u, a, carry_in=None):
+    """Differentiable SWR: x~ = L~ u."""
+    return SWRFunction.apply(u, a, carry_in)
+
+
+def mix(q, k, v, a, carry_in=None):
+    """Differentiable Phalanx double-gated mixer."""
+    return PhalanxMixFunction.apply(q, k, v, a, carry_in)

@@ -13,6 +13,16 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running test")
 
 
+def build_lib():
+    """Build libswr.so without importing the package (whose import loads the .so)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "_swr_build", os.path.join(ROOT, "paper_2512_13921_b200", "build.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod.build()
+
+
 def load_golden(name):
     """Parse tests/golden/<name> into {section: {key: list-of-floats or matrix}}."""
     path = os.path.join(ROOT, "tests", "golden", name)

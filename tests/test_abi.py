@@ -1,0 +1,92 @@
+"""CPU-side checks of the C ABI: libswr.so loads, exports every function that
+include/swr.h declares, and rejects bad arguments with the documented status
+codes before touching the GPU (no compute calls here)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from conftest import build_lib
+    build_lib()
+    from paper_2512_13921_b200 import _lib
+    return _lib
+
+
+def header_functions():
+    text = open(os.path.join(ROOT, "include", "swr.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:SWR_API\s+)?(?:const\s+)?\w+\*?\s+\*?(\w+)\s*\(", text, flags=re.M)))
+
+
+def test_header_declares_the_north_star_entry_points():
+    fns = header_functions()
+    for f in ("swr_fwd", "swr_bwd", "phalanx_mix", "phalanx_mix_bwd", "swr_strerror"):
+        assert f in fns
+
+
+def test_library_exports_every_declared_symbol(lib):
+    so = ctypes.CDLL(lib.LIB_PATH)
+    for f in header_functions():
+        assert hasattr(so, f), f"libswr.so does not export {f}"
+    assert set(header_functions()) == set(lib.EXPORTS)
+
+
+def test_only_abi_symbols_are_exported(lib):
+    import subprocess
+    out = subprocess.run(["nm", "-D", "--defined-only", lib.LIB_PATH], capture_output=True, text=True).stdout
+    syms = {l.split()[-1] for l in out.splitlines() if " T " in l}
+    assert set(header_functions()) <= syms
+    assert not [s for s in syms if s.startswith("_ZN3swr")], "internal symbols leaked"
+
+
+def _shape(lib, B=1, L=64, H=1, D=16, sx=None, sa=None):
+    sx = sx or (L * H * D, H * D, D)
+    sa = sa or (L * H, H, 1)
+    return lib.swr_shape(B, L, H, D, *sx, *sa)
+
+
+FAKE = 1 << 20  # 16-byte aligned, never dereferenced: validation fails first
+
+
+def test_validation_codes(lib):
+    s = _shape(lib)
+    # NULL required pointers
+    assert lib.raw_status("swr_fwd", None, FAKE, FAKE, None, None, s, 0, None) == 1
+    assert lib.raw_status("swr_fwd", FAKE, None, FAKE, None, None, s, 0, None) == 1
+    assert lib.raw_status("swr_bwd", FAKE, FAKE, FAKE, FAKE, None, None, None, None, s, 0, None) == 1
+    assert lib.raw_status("phalanx_mix", FAKE, FAKE, None, FAKE, FAKE, None, None, s, 0, None) == 1
+    # bad dtype
+    assert lib.raw_status("swr_fwd", FAKE, FAKE, FAKE, None, None, s, 7, None) == 5
+    # unsupported head dim / negative sizes
+    for D in (8, 24, 256):
+        assert lib.raw_status("swr_fwd", FAKE, FAKE, FAKE, None, None, _shape(lib, D=D), 0, None) == 2
+    assert lib.raw_status("swr_fwd", FAKE, FAKE, FAKE, None, None, _shape(lib, L=-1), 0, None) == 2
+    # strides: d-tensor strides must be multiples of 16 bytes, none negative
+    assert lib.raw_status("swr_fwd", FAKE, FAKE, FAKE, None, None,
+                          _shape(lib, sx=(64 * 16, 18, 16)), 1, None) == 3
+    assert lib.raw_status("swr_fwd", FAKE, FAKE, FAKE, None, None,
+                          _shape(lib, sa=(64, -1, 1)), 1, None) == 3
+    # alignment: d-tensors and carries 16 B, decays element size
+    assert lib.raw_status("swr_fwd", FAKE + 4, FAKE, FAKE, None, None, s, 0, None) == 4
+    assert lib.raw_status("swr_fwd", FAKE, FAKE + 1, FAKE, None, None, s, 1, None) == 4
+    assert lib.raw_status("swr_fwd", FAKE, FAKE, FAKE, FAKE + 8, None, s, 0, None) == 4
+
+
+def test_strerror_names_every_code(lib):
+    for code in range(8):
+        assert lib._lib.swr_strerror(code).decode().startswith("SWR_")
+
+
+def test_python_api_refuses_cpu_tensors(lib):
+    import torch
+    import paper_2512_13921_b200 as P
+    u = torch.zeros(1, 16, 1, 16)
+    a = torch.zeros(1, 16, 1)
+    with pytest.raises(ValueError, match="CUDA"):
+        P.swr_fwd(u, a)

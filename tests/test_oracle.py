@@ -378,3 +378,14 @@ def test_mix_backward_matches_finite_differences():
     assert normwise(dk, fd(k, lambda p: loss(q, p, v, a))) < 1e-6
     assert normwise(dv, fd(v, lambda p: loss(q, k, p, a))) < 1e-6
     assert normwise(da, fd(a, lambda p: loss(q, k, v, p))) < 1e-6
+
+
+def test_empty_sequence():
+    """L = 0: nothing to compute; carry_out and mu_out are zero (no block carries state)."""
+    u = np.zeros((2, 0, 3, 4))
+    a = np.zeros((2, 0, 3))
+    c = np.ones((2, 3, 4))
+    x, co = oracle.swr_fwd(u, a, carry_in=c, carry_out=True)
+    assert x.shape == u.shape and np.all(co == 0)
+    du, da, mo = oracle.swr_bwd(u, a, u, carry_in=c, mu_in=c)
+    assert du.shape == u.shape and da.shape == a.shape and np.all(mo == 0)

@@ -20,8 +20,9 @@
 //     through an NS-stage mbarrier ring; a CTA recomputes one halo block at a
 //     range boundary (and, backward, one on the right).
 //
-// Warp roles: 0-3 epilogue (TMEM lanes 0-127), 4.. prep (L tiles, g/r, mixer
-// pre-gates), then producer (TMA), then MMA issuer (one elected thread).
+// Warp roles: 4*NG epilogue warps in NG groups of 4 (group g handles items
+// j = g mod NG; warp w reads TMEM lanes 32*(w%4)..+31), then prep warps (L tiles,
+// g/r, mixer pre-gates), then the producer (TMA), then the MMA issuer.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -46,22 +47,22 @@ template <int OP>
 struct Cfg;
 template <>
 struct Cfg<0> {  // swr_fwd: in u;            out x  (over u)
-  static constexpr int NT = 1, NP = 0, NS = 16, COLS = 16, NPREP = 1, NOUT = 1;
+  static constexpr int NT = 1, NP = 0, NS = 16, COLS = 16, NPREP = 1, NOUT = 1, NG = 2;
   static constexpr bool BWD = false, MIX = false;
 };
 template <>
 struct Cfg<1> {  // swr_bwd: in u, G;         out du (over G)
-  static constexpr int NT = 2, NP = 0, NS = 14, COLS = 32, NPREP = 1, NOUT = 1;
+  static constexpr int NT = 2, NP = 0, NS = 12, COLS = 32, NPREP = 1, NOUT = 1, NG = 2;
   static constexpr bool BWD = true, MIX = false;
 };
 template <>
 struct Cfg<2> {  // mix fwd: in q, k, v;      out y  (over q);  prep u^ = k v
-  static constexpr int NT = 3, NP = 1, NS = 10, COLS = 16, NPREP = 4, NOUT = 1;
+  static constexpr int NT = 3, NP = 1, NS = 10, COLS = 16, NPREP = 4, NOUT = 1, NG = 2;
   static constexpr bool BWD = false, MIX = true;
 };
 template <>
 struct Cfg<3> {  // mix bwd: in q, k, v, dy;  out dq (over dy), dk (over k), dv (over v)
-  static constexpr int NT = 4, NP = 2, NS = 7, COLS = 32, NPREP = 4, NOUT = 3;
+  static constexpr int NT = 4, NP = 2, NS = 7, COLS = 32, NPREP = 4, NOUT = 3, NG = 2;
   static constexpr bool BWD = true, MIX = true;
 };
 
@@ -231,7 +232,7 @@ __device__ __forceinline__ void st_bf(uint8_t* base, uint32_t off, float x) {
 // ---------------------------------------------------------------------------
 // work list: CTA c owns blocks [g0, g1) of the flattened (line = b*H + h, t)
 // space, plus one left halo block (and, backward, one right halo block) when a
-// boundary falls inside a line.
+// boundary falls inside a line.  Items are walked with an incremental cursor.
 // ---------------------------------------------------------------------------
 struct Work {
   int64_t first, g0, g1, last;  // items are global block ids gi in [first, last)
@@ -247,18 +248,82 @@ __device__ __forceinline__ Work work_of(int64_t total, int64_t nb) {
   return w;
 }
 
+struct Cursor {
+  int64_t gi, t, line;
+  int b, h;
+  __device__ __forceinline__ void init(int64_t g, int64_t nb, int64_t H) {
+    gi = g;
+    line = g / nb;
+    t = g - line * nb;
+    b = (int)(line / H);
+    h = (int)(line - (int64_t)b * H);
+  }
+  __device__ __forceinline__ void next(int64_t nb, int64_t H) {
+    ++gi;
+    if (++t == nb) {
+      t = 0;
+      ++line;
+      if (++h == H) {
+        h = 0;
+        ++b;
+      }
+    }
+  }
+};
+
+// ring position of item j: stage s = j % NS, parity = (j / NS) & 1, advanced incrementally
+template <int NS>
+struct Ring {
+  int s;
+  uint32_t ph;
+  __device__ __forceinline__ void init(int64_t j) {
+    s = (int)(j % NS);
+    ph = (uint32_t)((j / NS) & 1);
+  }
+  __device__ __forceinline__ void next() {
+    if (++s == NS) {
+      s = 0;
+      ph ^= 1;
+    }
+  }
+};
+
+// pack two fp32 into bf16x2 (lo = first)
+__device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// Store 16 per-token values of this thread's channel c into a swizzled tile as
+// bf16 pairs: lanes (c, c^1) swap halves so every store is a 4-byte word and
+// the two rows of a warp instruction (i, i^4) fall in disjoint banks.
+__device__ __forceinline__ void store_col16(uint8_t* tile, int c, int lane, const float (&x)[16]) {
+  const bool odd = lane & 1;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    if (i & 4) continue;
+    const int i2 = i ^ 4;
+    const float send = odd ? x[i] : x[i2];
+    const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
+    if (!odd)
+      *reinterpret_cast<uint32_t*>(tile + tile_off(i, c)) = pack_bf2(x[i], recv);
+    else
+      *reinterpret_cast<uint32_t*>(tile + tile_off(i2, c - 1)) = pack_bf2(recv, x[i2]);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
 template <int OP>
-__global__ void __launch_bounds__((4 + Cfg<OP>::NPREP + 2) * 32, 1)
+__global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPREP + 2) * 32, 1)
     swr_tc_kernel(const __grid_constant__ Maps maps, const Params p) {
   using C = Cfg<OP>;
   using S = Stage<OP>;
-  constexpr int NS = C::NS;
+  constexpr int NS = C::NS, NG = C::NG;
   constexpr int kEpi = 128;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kPrepW0 = 4, kProdW = 4 + C::NPREP, kMmaW = kProdW + 1;
+  constexpr int kPrepW0 = 4 * NG, kProdW = kPrepW0 + C::NPREP, kMmaW = kProdW + 1;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -266,20 +331,25 @@ __global__ void __launch_bounds__((4 + Cfg<OP>::NPREP + 2) * 32, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(scratch);
   uint64_t* prepped = full + NS;
   uint64_t* mmad = prepped + NS;
-  uint64_t* empty = mmad + NS;
+  uint64_t* ready = mmad + NS;
+  uint64_t* empty = ready + NS;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(empty + NS);
-  float* red = reinterpret_cast<float*>(scratch + 2048);  // [2][4][16] da partials
+  float* red = reinterpret_cast<float*>(scratch + 2048);  // [NG][2][4][16] da partials
 
   constexpr int kTmemCols = (NS * C::COLS <= 32) ? 32 : (NS * C::COLS <= 64) ? 64
                           : (NS * C::COLS <= 128) ? 128 : (NS * C::COLS <= 256) ? 256 : 512;
   static_assert(NS * C::COLS <= 512, "TMEM budget");
+  // stage release: the item itself (after its store read SMEM) and the neighbour
+  // items that read its TMEM / g (next; backward also previous)
+  constexpr int kUsers = C::BWD ? 3 : 2;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&prepped[s], C::NPREP * 32);
       mbar_init(&mmad[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&ready[s], 1);
+      mbar_init(&empty[s], kUsers);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -297,84 +367,127 @@ __global__ void __launch_bounds__((4 + Cfg<OP>::NPREP + 2) * 32, 1)
   const int64_t nb = p.nb, H = p.H;
   const int64_t total = p.B * H * nb;
   const Work W = work_of<C::BWD>(total, nb);
+  const int64_t n_items = W.last - W.first;
 
   if (warp == kProdW) {
     // ===================== TMA producer =====================
-    if (lane == 0) {
-      for (int64_t gi = W.first; gi < W.last; ++gi) {
-        const int64_t j = gi - W.first;
-        const int s = (int)(j % NS);
-        const uint32_t use = (uint32_t)(j / NS);
-        mbar_wait(&empty[s], (use & 1) ^ 1);
-        const int64_t line = gi / nb, t = gi % nb;
-        const int b = (int)(line / H), h = (int)(line % H);
-        uint8_t* st = smem + s * S::kBytes;
-        mbar_expect_tx(&full[s], C::NT * kTile + 256);
+    if (lane == 0 && n_items > 0) {
+      Cursor cur;
+      cur.init(W.first, nb, H);
+      Ring<NS> rg;
+      rg.init(0);
+      for (int64_t j = 0; j < n_items; ++j) {
+        mbar_wait(&empty[rg.s], rg.ph ^ 1);
+        uint8_t* st = smem + rg.s * S::kBytes;
+        const int tt = (int)(cur.t * kEll);
+        mbar_expect_tx(&full[rg.s], C::NT * kTile + 256);
 #pragma unroll
         for (int x = 0; x < C::NT; ++x) {
-          tma_load_4d(st + x * kTile, &maps.in[x], &full[s], 0, h, (int)(t * kEll), b);
-          tma_load_4d(st + x * kTile + kHalf, &maps.in[x], &full[s], 64, h, (int)(t * kEll), b);
+          tma_load_4d(st + x * kTile, &maps.in[x], &full[rg.s], 0, cur.h, tt, cur.b);
+          tma_load_4d(st + x * kTile + kHalf, &maps.in[x], &full[rg.s], 64, cur.h, tt, cur.b);
         }
-        tma_load_3d(st + S::kA, &maps.a, &full[s], h & ~7, (int)(t * kEll), b);
+        tma_load_3d(st + S::kA, &maps.a, &full[rg.s], cur.h & ~7, tt, cur.b);
+        cur.next(nb, H);
+        rg.next();
       }
     }
   } else if (warp == kMmaW) {
-    // ===================== MMA issuer =====================
-    for (int64_t gi = W.first; gi < W.last; ++gi) {
-      const int64_t j = gi - W.first;
-      const int s = (int)(j % NS);
-      const uint32_t par = (uint32_t)(j / NS) & 1;
-      mbar_wait(&full[s], par);
-      mbar_wait(&prepped[s], par);
+    // ===================== MMA issuer + readiness =====================
+    // ready[j] is arrived once the MMAs of every item whose TMEM item j's
+    // epilogue reads are complete: j-1, j (and, backward, j+1).
+    Ring<NS> rg, r1, r2;  // item j, j-1, j-2
+    rg.init(0);
+    r1 = rg;
+    r2 = rg;
+    for (int64_t j = 0; j < n_items; ++j) {
+      mbar_wait(&full[rg.s], rg.ph);
+      mbar_wait(&prepped[rg.s], rg.ph);
       tc_fence_after();
       if (lane == 0) {
-        uint8_t* st = smem + s * S::kBytes;
-        const uint32_t d = tmem_base + (uint32_t)(s * C::COLS);
+        uint8_t* st = smem + rg.s * S::kBytes;
+        const uint32_t d = tmem_base + (uint32_t)(rg.s * C::COLS);
         const uint32_t aW = su32(st + (C::MIX ? C::NT * kTile : 0));  // u or u^ = k v
         umma_bf16(d, desc_A(aW), desc_B(su32(st + S::kLT)), kIdesc);
         if constexpr (C::BWD) {
           const uint32_t aG = su32(st + (C::MIX ? (C::NT + 1) * kTile : kTile));  // G or dy q
           umma_bf16(d + 16, desc_A(aG), desc_B(su32(st + S::kL)), kIdesc);
         }
-        umma_commit(&mmad[s]);
+        umma_commit(&mmad[rg.s]);
+      }
+      __syncwarp();
+      if (j >= 1) {
+        mbar_wait(&mmad[r1.s], r1.ph);  // item j-1 complete
+        tc_fence_before();
+        if (lane == 0) {
+          if constexpr (!C::BWD) mbar_arrive(&ready[r1.s]);
+          else if (j >= 2) mbar_arrive(&ready[r2.s]);
+        }
+        __syncwarp();
+      }
+      r2 = r1;
+      r1 = rg;
+      rg.next();
+    }
+    if (n_items > 0) {  // flush: r1 = last item, r2 = the one before
+      mbar_wait(&mmad[r1.s], r1.ph);
+      tc_fence_before();
+      if (lane == 0) {
+        if (C::BWD && n_items >= 2) mbar_arrive(&ready[r2.s]);
+        mbar_arrive(&ready[r1.s]);
       }
       __syncwarp();
     }
   } else if (warp >= kPrepW0) {
     // ===================== prep: L tiles (Alg. 3), g, r, pre-gates =====================
     const int pt = threadIdx.x - kPrepW0 * 32;  // 0 .. NPREP*32-1
-    for (int64_t gi = W.first; gi < W.last; ++gi) {
-      const int64_t j = gi - W.first;
-      const int s = (int)(j % NS);
-      mbar_wait(&full[s], (uint32_t)(j / NS) & 1);
-      uint8_t* st = smem + s * S::kBytes;
-      const int64_t line = gi / nb, t = gi % nb;
-      const int h = (int)(line % H);
-      if (pt < 32) {
-        // lane j < 16 owns column j of L_t: L[i][j] = a[j+1] ... a[i] (products only)
-        const int col = lane & 15;
-        const int64_t n = t * kEll + col;
-        const float acol = (n < p.L) ? bf(st + S::kA, (uint32_t)(col * 8 + (h & 7)) * 2) : 1.f;
-        // g_t = inclusive multiplicative scan of a over the 16 lanes (Alg. 1 line 8 pattern)
-        float g = acol;
+    Cursor cur;
+    if (n_items > 0) cur.init(W.first, nb, H);
+    Ring<NS> rg;
+    rg.init(0);
+    for (int64_t j = 0; j < n_items; ++j) {
+      mbar_wait(&full[rg.s], rg.ph);
+      uint8_t* st = smem + rg.s * S::kBytes;
+      if (pt < 16) {
+        // lane j owns column j of L_t.  Alg. 3: tile a down the columns, pre-mask
+        // the inclusive upper triangle with 1, column-wise cumulative product,
+        // zero the strict upper triangle.  Products only, never ratios.
+        const int col = pt;
+        const uint8_t* at = st + S::kA + (cur.h & 7) * 2;
+        float a[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          a[i] = (cur.t * kEll + i < p.L) ? __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(at + i * 16)) : 1.f;
+        float Lc[16];
+        float prod = 1.f;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          if (i > col) prod *= a[i];
+          Lc[i] = (i >= col) ? prod : 0.f;  // L[i][col]
+        }
+        // B of W (L_t^T, K-major): element (n = i, k = col)
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          *reinterpret_cast<__nv_bfloat16*>(st + S::kLT + btile_off(i, col)) = __float2bfloat16_rn(Lc[i]);
+        if constexpr (C::BWD) {
+          // B of lambda (L_t, K-major): element (n = col, k = i), contiguous along k
+          uint4 lo, hi;
+          lo.x = pack_bf2(Lc[0], Lc[1]);   lo.y = pack_bf2(Lc[2], Lc[3]);
+          lo.z = pack_bf2(Lc[4], Lc[5]);   lo.w = pack_bf2(Lc[6], Lc[7]);
+          hi.x = pack_bf2(Lc[8], Lc[9]);   hi.y = pack_bf2(Lc[10], Lc[11]);
+          hi.z = pack_bf2(Lc[12], Lc[13]); hi.w = pack_bf2(Lc[14], Lc[15]);
+          *reinterpret_cast<uint4*>(st + S::kL + btile_off(col, 0)) = lo;
+          *reinterpret_cast<uint4*>(st + S::kL + btile_off(col, 8)) = hi;
+          reinterpret_cast<float*>(st + S::kR)[col] = prod;  // r_t[j] = L[15][j]
+        }
+        // g_t[i] = a_t[0] ... a_t[i]: 16-lane multiplicative scan (pattern of Alg. 1 line 8)
+        float g = (cur.t * kEll + col < p.L)
+                      ? __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(at + col * 16)) : 1.f;
 #pragma unroll
         for (int d = 1; d < 16; d <<= 1) {
-          const float o = __shfl_up_sync(0xffffffffu, g, d, 16);
+          const float o = __shfl_up_sync(0x0000ffffu, g, d, 16);
           if (col >= d) g *= o;
         }
-        float prod = 1.f;
-        if (lane < 16) {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float ai = __shfl_sync(0x0000ffffu, acol, i, 16);
-            if (i > col) prod *= ai;
-            const float Lij = (i >= col) ? prod : 0.f;  // column cumprod, then tril (Alg. 3)
-            st_bf(st + S::kLT, btile_off(i, col), Lij);  // B of W:      B[k=j][n=i] = L[i][j]
-            if constexpr (C::BWD) st_bf(st + S::kL, btile_off(col, i), Lij);  // B of lambda: B[k=i][n=j] = L[i][j]
-          }
-          reinterpret_cast<float*>(st + S::kG)[col] = g;
-          if constexpr (C::BWD) reinterpret_cast<float*>(st + S::kR)[col] = prod;  // r_t[j] = L[15][j]
-        }
+        reinterpret_cast<float*>(st + S::kG)[col] = g;
       }
       if constexpr (C::MIX) {
         // pre-gates in the swizzled tile layout (elementwise, layout-agnostic):
@@ -392,8 +505,7 @@ __global__ void __launch_bounds__((4 + Cfg<OP>::NPREP + 2) * 32, 1)
           for (int e = 0; e < 4; ++e) {
             const float2 kf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ka[e]));
             const float2 vf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&va[e]));
-            const __nv_bfloat162 r = __floats2bfloat162_rn(kf.x * vf.x, kf.y * vf.y);
-            oa[e] = *reinterpret_cast<const uint32_t*>(&r);
+            oa[e] = pack_bf2(kf.x * vf.x, kf.y * vf.y);
           }
           U4[v] = o;
           if constexpr (C::BWD) {
@@ -407,146 +519,164 @@ __global__ void __launch_bounds__((4 + Cfg<OP>::NPREP + 2) * 32, 1)
             for (int e = 0; e < 4; ++e) {
               const float2 qf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&qa[e]));
               const float2 df = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&da[e]));
-              const __nv_bfloat162 r = __floats2bfloat162_rn(df.x * qf.x, df.y * qf.y);
-              oa[e] = *reinterpret_cast<const uint32_t*>(&r);
+              oa[e] = pack_bf2(df.x * qf.x, df.y * qf.y);
             }
             G4[v] = o;
           }
         }
       }
       fence_proxy_async();  // generic-proxy writes -> visible to the tensor core
-      mbar_arrive(&prepped[s]);
+      mbar_arrive(&prepped[rg.s]);
+      cur.next(nb, H);
+      rg.next();
     }
   } else {
-    // ===================== epilogue: thread = channel c =====================
-    const int c = threadIdx.x;  // 0..127 == TMEM lane
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-    float vcar = 0.f;  // carrier v_{t-1} of this channel
-    int64_t pending = -1;
+    // ===================== epilogue groups: thread = channel c =====================
+    const int grp = warp >> 2;                       // epilogue group, items j = grp mod NG
+    const int c = threadIdx.x & 127;                 // channel == TMEM lane
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    const bool leader = (threadIdx.x & 127) == 0;
+    float* red_g = red + grp * 128;                  // [2][4][16]
     int rbuf = 0;
-    for (int64_t gi = W.first; gi < W.last; ++gi) {
-      const int64_t j = gi - W.first;
-      const int s = (int)(j % NS);
-      const uint32_t par = (uint32_t)(j / NS) & 1;
-      const int64_t line = gi / nb, t = gi % nb;
-      const int b = (int)(line / H), h = (int)(line % H);
-      const bool halo = gi < W.g0 || gi >= W.g1;
-      uint8_t* st = smem + s * S::kBytes;
+    int pend = -1;                                   // stage of the last stored item (release lags its store)
+    Cursor cur;
+    if (grp < n_items) cur.init(W.first + grp, nb, H);
+    Ring<NS> rg, rp, rn;
+    rg.init(grp);
+    for (int64_t j = grp; j < n_items; j += NG) {
+      rp = rg;  // ring slots of items j-1 and j+1
+      if (rp.s == 0) { rp.s = NS - 1; rp.ph ^= 1; } else { --rp.s; }
+      rn = rg;
+      rn.next();
+      const int64_t t = cur.t;
+      const int b = cur.b, h = cur.h;
+      const bool halo = cur.gi < W.g0 || cur.gi >= W.g1;
+      uint8_t* st = smem + rg.s * S::kBytes;
       const float* g = reinterpret_cast<const float*>(st + S::kG);
-      const int64_t co = line * kD + c;
-      mbar_wait(&full[s], par);
-      mbar_wait(&prepped[s], par);
-      mbar_wait(&mmad[s], par);
+      const int64_t co = cur.line * kD + c;
+      mbar_wait(&ready[rg.s], rg.ph);
       tc_fence_after();
-      if (t == 0) vcar = p.carry_in ? p.carry_in[co] : 0.f;  // v_{-1}
-      const bool right_halo = C::BWD && gi >= W.g1;
       bool stored = false;
-      if (!right_halo) {
+      if (!halo) {
+        const uint32_t tslot = tmem_base + lane_base + (uint32_t)(rg.s * C::COLS);
         float w[16];
-        tmem_ld16(tmem_base + lane_base + (uint32_t)(s * C::COLS), w);
+        tmem_ld16(tslot, w);
+        // carrier v_{t-1} = w_{t-1}[15]: column 15 of the previous item's TMEM
+        float vprev;
+        if (t == 0) {
+          vprev = p.carry_in ? p.carry_in[co] : 0.f;  // v_{-1}
+        } else {
+          vprev = tmem_ld1(tmem_base + lane_base + (uint32_t)(rp.s * C::COLS + 15));
+        }
         if constexpr (!C::BWD) {
           tmem_wait_ld();
-          if (!halo) {
-            if constexpr (!C::MIX) {
+          float out[16];
 #pragma unroll
-              for (int i = 0; i < 16; ++i) st_bf(st, tile_off(i, c), fmaf(g[i], vcar, w[i]));
-            } else {
+          for (int i = 0; i < 16; ++i) out[i] = fmaf(g[i], vprev, w[i]);  // Pass II: x~ = w + g v
+          if constexpr (C::MIX) {
 #pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                const uint32_t o = tile_off(i, c);
-                const float x = fmaf(g[i], vcar, w[i]);           // Pass II
-                const float y = fmaf(bf(st, o), x, bf(st + 2 * kTile, o));  // y = q x~ + v
-                st_bf(st, o, y);
-              }
+            for (int i = 0; i < 16; ++i) {  // post-gate with residual: y = q x~ + v
+              const uint32_t o = tile_off(i, c);
+              out[i] = fmaf(bf(st, o), out[i], bf(st + 2 * kTile, o));
             }
-            stored = true;
           }
-          vcar = w[15];
-          if (!halo && t == nb - 1 && p.carry_out) p.carry_out[co] = vcar;
+          __syncwarp();
+          store_col16(st, c, lane, out);
+          if (t == nb - 1 && p.carry_out) p.carry_out[co] = w[15];
         } else {
           float lam[16];
-          tmem_ld16(tmem_base + lane_base + (uint32_t)(s * C::COLS + 16), lam);
+          tmem_ld16(tslot + 16, lam);
           float mu;
           if (t == nb - 1) {
             mu = p.mu_in ? p.mu_in[co] : 0.f;
             tmem_wait_ld();
-          } else {  // mu_t = a_{t+1}[0] lambda_{t+1}[0] from the next item (lookahead)
-            const int s1 = (int)((j + 1) % NS);
-            mbar_wait(&mmad[s1], (uint32_t)((j + 1) / NS) & 1);
-            mbar_wait(&prepped[s1], (uint32_t)((j + 1) / NS) & 1);
-            tc_fence_after();
-            const float l0 = tmem_ld1(tmem_base + lane_base + (uint32_t)(s1 * C::COLS + 16));
+          } else {  // mu_t = a_{t+1}[0] lambda_{t+1}[0] from the next item
+            const float l0 = tmem_ld1(tmem_base + lane_base + (uint32_t)(rn.s * C::COLS + 16));
             tmem_wait_ld();
-            mu = reinterpret_cast<const float*>(smem + s1 * S::kBytes + S::kG)[0] * l0;
+            mu = reinterpret_cast<const float*>(smem + rn.s * S::kBytes + S::kG)[0] * l0;
           }
-          if (!halo) {
-            const float* r = reinterpret_cast<const float*>(st + S::kR);
-            float part[16];
+          const float* r = reinterpret_cast<const float*>(st + S::kR);
+          float part[16], du[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float rmu = r[i] * mu;
+            du[i] = lam[i] + rmu;                                            // du = lambda + r mu
+            const float wp = (i > 0) ? w[i - 1] : 0.f;
+            const float xp = (i > 0) ? fmaf(g[i - 1], vprev, w[i - 1]) : vprev;  // x~[i-1]
+            part[i] = fmaf(lam[i], xp, rmu * wp);                              // da partial
+          }
+          __syncwarp();
+          if constexpr (!C::MIX) {
+            store_col16(st + kTile, c, lane, du);  // du over G
+          } else {
+            float dq[16], dk[16], dv[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-              const float rmu = r[i] * mu;
-              const float du = lam[i] + rmu;                                   // du = lambda + r mu
-              const float wp = (i > 0) ? w[i - 1] : 0.f;
-              const float xp = (i > 0) ? fmaf(g[i - 1], vcar, w[i - 1]) : vcar;  // x~[i-1]
-              part[i] = fmaf(lam[i], xp, rmu * wp);                              // da partial
               const uint32_t o = tile_off(i, c);
-              if constexpr (!C::MIX) {
-                st_bf(st + kTile, o, du);  // du over G
-              } else {
-                const float dy = bf(st + 3 * kTile, o), kk = bf(st + kTile, o), vv = bf(st + 2 * kTile, o);
-                const float x = fmaf(g[i], vcar, w[i]);
-                st_bf(st + 3 * kTile, o, dy * x);         // dq = dy x~
-                st_bf(st + kTile, o, du * vv);            // dk = du^ v
-                st_bf(st + 2 * kTile, o, fmaf(du, kk, dy));  // dv = du^ k + dy
-              }
+              const float dy = bf(st + 3 * kTile, o), kk = bf(st + kTile, o), vv = bf(st + 2 * kTile, o);
+              const float x = fmaf(g[i], vprev, w[i]);
+              dq[i] = dy * x;              // dq = dy x~
+              dk[i] = du[i] * vv;          // dk = du^ v
+              dv[i] = fmaf(du[i], kk, dy);  // dv = du^ k + dy
             }
-            if (t == 0 && p.mu_out) p.mu_out[co] = g[0] * lam[0];  // a_0[0] lambda_0[0]
-            // da: deterministic reduction over the 128 channels (4 warps)
-            int tok = 0;
-            GroupReduce<16, 16>::run(part, lane, tok);
-            float* rb = red + rbuf * 64;
-            if ((lane & 1) == 0) rb[warp * 16 + tok] = part[0];
-            named_bar(2, kEpi);
-            if (warp == 0 && lane < 16) {
-              const int64_t n = t * kEll + lane;
-              if (n < p.L) {
-                const float sum = ((rb[lane] + rb[16 + lane]) + rb[32 + lane]) + rb[48 + lane];
-                __nv_bfloat16* dA = (__nv_bfloat16*)p.da + (int64_t)b * p.sa_b + (int64_t)h * p.sa_h;
-                dA[n * p.sa_l] = __float2bfloat16_rn(sum);
-              }
-            }
-            rbuf ^= 1;
-            stored = true;
+            __syncwarp();
+            store_col16(st + 3 * kTile, c, lane, dq);
+            store_col16(st + 1 * kTile, c, lane, dk);
+            store_col16(st + 2 * kTile, c, lane, dv);
           }
-          vcar = w[15];
+          if (t == 0 && p.mu_out) p.mu_out[co] = g[0] * lam[0];  // a_0[0] lambda_0[0]
+          // da: deterministic reduction over the 128 channels (4 warps of this group)
+          int tok = 0;
+          GroupReduce<16, 16>::run(part, lane, tok);
+          float* rb = red_g + rbuf * 64;
+          if ((lane & 1) == 0) rb[(warp & 3) * 16 + tok] = part[0];
+          named_bar(1 + NG + grp, kEpi);
+          if ((warp & 3) == 0 && lane < 16) {
+            const int64_t n = t * kEll + lane;
+            if (n < p.L) {
+              const float sum = ((rb[lane] + rb[16 + lane]) + rb[32 + lane]) + rb[48 + lane];
+              __nv_bfloat16* dA = (__nv_bfloat16*)p.da + (int64_t)b * p.sa_b + (int64_t)h * p.sa_h;
+              dA[n * p.sa_l] = __float2bfloat16_rn(sum);
+            }
+          }
+          rbuf ^= 1;
         }
+        stored = true;
       }
-      // hand the stage back: outputs -> TMA store, then release after the store read SMEM
+      // hand back: outputs -> TMA store; release own stage once the store has read
+      // SMEM, and the neighbours' stages whose TMEM / g this item read
       tc_fence_before();
       if (stored) fence_proxy_async();
-      named_bar(1, kEpi);
-      if (threadIdx.x == 0) {
+      named_bar(1 + grp, kEpi);
+      if (leader) {
         if (stored) {
           const int tt = (int)(t * kEll);
 #pragma unroll
           for (int x = 0; x < C::NOUT; ++x) {
-            // output tile for output x (see Cfg comments)
             const int tile = (OP == 0) ? 0 : (OP == 1) ? 1 : (OP == 2) ? 0 : (x == 0 ? 3 : x);
             tma_store_4d(&maps.out[x], st + tile * kTile, 0, h, tt, b);
             tma_store_4d(&maps.out[x], st + tile * kTile + kHalf, 64, h, tt, b);
           }
           bulk_commit();
           bulk_wait_read<1>();
-          if (pending >= 0) mbar_arrive(&empty[pending]);
-          pending = s;
+          if (pend >= 0) mbar_arrive(&empty[pend]);
+          pend = rg.s;
         } else {
-          mbar_arrive(&empty[s]);
+          mbar_arrive(&empty[rg.s]);
         }
+        if (j >= 1) mbar_arrive(&empty[rp.s]);                       // as "next" of item j-1
+        if (C::BWD && j + 1 < n_items) mbar_arrive(&empty[rn.s]);  // as "previous" of item j+1
+        if (j == n_items - 1) mbar_arrive(&empty[rg.s]);           // no next item
+        if (C::BWD && j == 0) mbar_arrive(&empty[rg.s]);           // no previous item
+      }
+      for (int k = 0; k < NG; ++k) {
+        cur.next(nb, H);
+        rg.next();
       }
     }
-    if (threadIdx.x == 0) {
+    if (leader) {
       bulk_wait_all();
-      if (pending >= 0) mbar_arrive(&empty[pending]);
+      if (pend >= 0) mbar_arrive(&empty[pend]);
     }
   }
 
@@ -627,7 +757,7 @@ static cudaError_t launch_op(const Params& p, cudaStream_t st, int sms) {
   }
   const int64_t total = p.B * p.H * p.nb;
   const int grid = (int)std::min<int64_t>(sms, std::max<int64_t>(total, 1));
-  constexpr int threads = (4 + Cfg<OP>::NPREP + 2) * 32;
+  constexpr int threads = (4 * Cfg<OP>::NG + Cfg<OP>::NPREP + 2) * 32;
   swr_tc_kernel<OP><<<grid, threads, smem, st>>>(maps, p);
   return cudaGetLastError();
 }

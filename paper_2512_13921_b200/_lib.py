@@ -16,7 +16,8 @@ SWR_F32, SWR_BF16 = 0, 1
 SWR_PATH_AUTO, SWR_PATH_FFMA, SWR_PATH_TC = 0, 1, 2
 
 EXPORTS = ("swr_fwd", "swr_bwd", "phalanx_mix", "phalanx_mix_bwd", "swr_strerror",
-           "swr_last_cuda_error", "swr_set_path", "swr_launch_count", "swr_last_path")
+           "swr_last_cuda_error", "swr_set_path", "swr_launch_count", "swr_last_path",
+           "swr_set_trace")
 
 
 class SwrError(RuntimeError):
@@ -36,7 +37,7 @@ class swr_shape(ctypes.Structure):
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
-            f"{LIB_PATH} not found: build it with `python -m paper_2512_13921_b200.build` "
+            f"{LIB_PATH} not found: build it with `python paper_2512_13921_b200/build.py` "
             "(there is no CPU fallback)")
     lib = ctypes.CDLL(LIB_PATH)
     P = ctypes.c_void_p
@@ -58,6 +59,8 @@ def _load():
     lib.swr_launch_count.restype = ctypes.c_int64
     lib.swr_last_path.argtypes = []
     lib.swr_last_path.restype = I
+    lib.swr_set_trace.argtypes = [P, ctypes.c_int64]
+    lib.swr_set_trace.restype = None
     return lib
 
 
@@ -96,6 +99,11 @@ def launch_count() -> int:
 
 def last_path() -> int:
     return _lib.swr_last_path()
+
+
+def set_trace(ptr, n: int) -> None:
+    """Diagnostics: per-item pipeline timestamps of CTA 0 into device buffer `ptr`."""
+    _lib.swr_set_trace(ptr, n)
 
 
 def raw_status(fn: str, *args) -> int:

@@ -1,6 +1,6 @@
 """Build libswr.so in-tree with nvcc for sm_100a (B200).
 
-    python -m paper_2512_13921_b200.build        # or build() from __graft_entry__
+    python paper_2512_13921_b200/build.py        # or build() from __graft_entry__
 
 Compiles every csrc/*.cu into one shared library with the C ABI of include/swr.h.
 """

@@ -21,6 +21,8 @@ namespace {
 std::atomic<int64_t> g_launches{0};
 std::atomic<int> g_path{SWR_PATH_AUTO};
 std::atomic<int> g_last_path{0};
+std::atomic<unsigned long long*> g_trace{nullptr};
+std::atomic<int64_t> g_trace_n{0};
 thread_local char g_cuda_err[256] = "";
 
 constexpr int kMaxDev = 64;
@@ -94,6 +96,8 @@ swr::Params make_params(const swr_shape& s) {
   p.sa_l = s.sa_l;
   p.sa_h = s.sa_h;
   p.nb = (s.L + swr::kEll - 1) / swr::kEll;
+  p.trace = g_trace.load();
+  p.trace_n = g_trace_n.load();
   return p;
 }
 
@@ -248,5 +252,10 @@ swr_path swr_set_path(swr_path p) { return (swr_path)g_path.exchange((int)p); }
 int64_t swr_launch_count(void) { return g_launches.load(); }
 
 int swr_last_path(void) { return g_last_path.load(); }
+
+void swr_set_trace(unsigned long long* buf, int64_t n) {
+  g_trace_n.store(buf ? n : 0);
+  g_trace.store(buf);
+}
 
 }  // extern "C"

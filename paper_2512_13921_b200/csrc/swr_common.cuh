@@ -38,6 +38,8 @@ struct Params {
   int64_t sa_b, sa_l, sa_h;
   int64_t nb;  // number of 16-token blocks, ceil(L/16)
   int64_t K;   // blocks per walk (FFMA path)
+  unsigned long long* trace;  // diagnostics (swr_set_trace), NULL = off
+  int64_t trace_n;
 };
 
 // ---------------------------------------------------------------------------

@@ -21,8 +21,9 @@
 //     range boundary (and, backward, one on the right).
 //
 // Warp roles: 4*NG epilogue warps in NG groups of 4 (group g handles items
-// j = g mod NG; warp w reads TMEM lanes 32*(w%4)..+31), then prep warps (L tiles,
-// g/r, mixer pre-gates), then the producer (TMA), then the MMA issuer.
+// j = g mod NG; warp w reads TMEM lanes 32*(w%4)..+31), then NPW prep warps (L
+// tiles, g/r, mixer pre-gates; two items per pass), the producer (TMA loads),
+// the MMA issuer (one elected thread) and the store warp (TMA stores, release).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -39,45 +40,59 @@ constexpr int kTile = 4096;      // one 16 x 128 bf16 tile (two 64-channel halve
 constexpr int kHalf = 2048;      // one 64-channel half: 16 rows x 128 B, 128B-swizzled
 
 // ---------------------------------------------------------------------------
-// per-op configuration
-//   NT   TMA-loaded input tiles per item     NP  prep-computed A tiles
-//   NS   pipeline stages                     COLS TMEM columns per stage
+// per-op configuration.  A pipeline "item" is BPI consecutive 16-token blocks
+// of one (b, h) line (the last item of a line may be partial).
+//   NT   TMA-loaded input tiles per block    NP   extra prep-computed A tiles per block
+//   BPI  blocks per item                     NS   pipeline stages (items)
+//   COLS TMEM columns per block              NPW  prep warps (each owns whole items)
+//   NG   epilogue groups of 4 warps
+// Liveness: loading item x needs item x-NS released; that release needs the
+// store of the next item (store lag 1), the neighbours' epilogues and their
+// readiness (MMA of the next item backward), so NS >= BWD + 4 suffices; the
+// rings are sized deeper to cover latency.
 // ---------------------------------------------------------------------------
 template <int OP>
 struct Cfg;
 template <>
 struct Cfg<0> {  // swr_fwd: in u;            out x  (over u)
-  static constexpr int NT = 1, NP = 0, NS = 16, COLS = 16, NPREP = 1, NOUT = 1, NG = 2;
+  static constexpr int NT = 1, NP = 0, BPI = 4, NS = 8, COLS = 16, NPW = 2, NOUT = 1, NG = 3;
+  static constexpr int TU = 0, TG = 0;  // A-operand tiles of W and lambda
   static constexpr bool BWD = false, MIX = false;
 };
 template <>
 struct Cfg<1> {  // swr_bwd: in u, G;         out du (over G)
-  static constexpr int NT = 2, NP = 0, NS = 12, COLS = 32, NPREP = 1, NOUT = 1, NG = 2;
+  static constexpr int NT = 2, NP = 0, BPI = 2, NS = 8, COLS = 32, NPW = 2, NOUT = 1, NG = 4;
+  static constexpr int TU = 0, TG = 1;
   static constexpr bool BWD = true, MIX = false;
 };
 template <>
-struct Cfg<2> {  // mix fwd: in q, k, v;      out y  (over q);  prep u^ = k v
-  static constexpr int NT = 3, NP = 1, NS = 10, COLS = 16, NPREP = 4, NOUT = 1, NG = 2;
+struct Cfg<2> {  // mix fwd: in q, k, v;      out y  (over q);  prep u^ = k v (over k)
+  static constexpr int NT = 3, NP = 0, BPI = 2, NS = 7, COLS = 16, NPW = 4, NOUT = 1, NG = 3;
+  static constexpr int TU = 1, TG = 0;
   static constexpr bool BWD = false, MIX = true;
 };
 template <>
 struct Cfg<3> {  // mix bwd: in q, k, v, dy;  out dq (over dy), dk (over k), dv (over v)
-  static constexpr int NT = 4, NP = 2, NS = 7, COLS = 32, NPREP = 4, NOUT = 3, NG = 2;
+  //                prep u^ = k v (tile 4), G = dy q (over q)
+  static constexpr int NT = 4, NP = 1, BPI = 1, NS = 8, COLS = 32, NPW = 4, NOUT = 3, NG = 3;
+  static constexpr int TU = 4, TG = 0;
   static constexpr bool BWD = true, MIX = true;
 };
 
-// stage layout (bytes, every tile 1024-aligned for the 128B swizzle atoms)
+// stage layout (bytes; every 4 KiB tile 1024-aligned for the 128B swizzle atoms)
 template <int OP>
 struct Stage {
   using C = Cfg<OP>;
-  static constexpr int kTiles = 0;                                // NT input tiles, then NP prep tiles
-  static constexpr int kA = (C::NT + C::NP) * kTile;              // decay box [16 tokens][8 heads] bf16
-  static constexpr int kLT = kA + 256;                            // B operand of W:      L_t^T  (512 B)
-  static constexpr int kL = kLT + 512;                            // B operand of lambda: L_t    (512 B)
-  static constexpr int kG = kL + 512;                             // g_t[16] fp32
-  static constexpr int kR = kG + 64;                              // r_t[16] fp32
-  static constexpr int kRaw = kR + 64;
+  static constexpr int kTPB = C::NT + C::NP;                  // tiles per block
+  static constexpr int kA = C::BPI * kTPB * kTile;            // decay box [16*BPI tokens][8 heads] bf16
+  static constexpr int kL = kA + 256 * C::BPI;                // transfer tile L_t per block (512 B)
+  static constexpr int kG = kL + 512 * C::BPI;                // g_t[16] fp32 per block
+  static constexpr int kR = kG + 64 * C::BPI;                 // r_t[16] fp32 per block
+  static constexpr int kRaw = kR + 64 * C::BPI;
   static constexpr int kBytes = (kRaw + 1023) / 1024 * 1024;
+  static __device__ __forceinline__ uint8_t* tile(uint8_t* st, int k, int x) {
+    return st + (k * kTPB + x) * kTile;
+  }
 };
 
 template <int OP>
@@ -89,7 +104,7 @@ constexpr int smem_bytes() {
 struct Maps {
   CUtensorMap in[4];   // TMA load maps of the input d-tensors (op order above)
   CUtensorMap out[3];  // TMA store maps of the outputs
-  CUtensorMap a;       // decays, box [16 tokens][8 heads]
+  CUtensorMap a;       // decays, box [16*BPI tokens][8 heads]
 };
 
 // ---------------------------------------------------------------------------
@@ -116,6 +131,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "@!p bra SWR_WAIT_%=;\n\t}" ::"r"(su32(b)),
       "r"(parity)
       : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(su32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
 }
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0,
                                             int c1, int c2, int c3) {
@@ -192,6 +218,17 @@ __device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
   return __uint_as_float(r);
 }
+// diagnostics: %globaltimer stamp of event ev for item j of CTA 0 (swr_set_trace)
+// events: 0 producer got stage, 1 producer issued TMA, 2 prep saw full, 3 prep done,
+// 4 mma saw full+prepped, 5 mma issued, 6 mma marked ready, 7 epilogue saw ready,
+// 8 epilogue done (before store), 9 store committed, 10 own stage released
+__device__ __forceinline__ void trace(const Params& p, int64_t j, int ev) {
+  if (p.trace != nullptr && blockIdx.x == 0 && j < p.trace_n) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[j * 16 + ev] = t;
+  }
+}
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -205,21 +242,29 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
 // A = u_t^T from a TMA tile: MN-major, SWIZZLE_128B; 64-channel halves 2048 B apart
 // (LBO), 8-token row groups 1024 B apart (SBO).
 __device__ __forceinline__ uint64_t desc_A(uint32_t saddr) { return sdesc(saddr, kHalf, 1024, 2); }
-// B = 16x16 transfer tile: K-major, no swizzle; core matrices 8 (N) x 16 B (8 K),
-// K-halves 128 B apart (LBO), N-halves 256 B apart (SBO).
-__device__ __forceinline__ uint64_t desc_B(uint32_t saddr) { return sdesc(saddr, 128, 256, 0); }
-// instruction descriptor: D fp32, A/B bf16, A MN-major, B K-major, N = 16, M = 128
-constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (0u << 16) |
-                            ((16u >> 3) << 17) | ((128u >> 4) << 24);
+// The 16x16 transfer tile L_t is stored ONCE, column-major in 8x8 core matrices:
+// element L[i][j] at byte (j/8)*256 + (i/8)*128 + (j%8)*16 + (i%8)*2, i.e. each
+// column j is 32 contiguous-per-core-row bytes written by one lane.
+//  * lambda = L_t^T G needs B[k=i][n=j] = L[i][j]: K-major, no swizzle, core rows
+//    = n (16 B apart), K-halves 128 B apart (LBO), N-halves 256 B apart (SBO).
+//  * w = L_t u needs B[k=j][n=i] = L[i][j]: MN-major, no swizzle, core rows = k
+//    (16 B apart), N-halves 128 B apart (SBO), K-halves 256 B apart (LBO).
+// The same bytes serve both MMAs; only the descriptor (and the B-major bit) differ.
+__device__ __forceinline__ uint64_t desc_Bk(uint32_t saddr) { return sdesc(saddr, 128, 256, 0); }
+__device__ __forceinline__ uint64_t desc_Bmn(uint32_t saddr) { return sdesc(saddr, 256, 128, 0); }
+// instruction descriptors: D fp32, A/B bf16, A MN-major, N = 16, M = 128; B K- or MN-major
+constexpr uint32_t kIdescBk = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (0u << 16) |
+                              ((16u >> 3) << 17) | ((128u >> 4) << 24);
+constexpr uint32_t kIdescBmn = kIdescBk | (1u << 16);
 
 // byte offset of element (token i, channel c) inside a 4 KiB swizzled tile
 __device__ __forceinline__ uint32_t tile_off(int i, int c) {
   const int half = c >> 6, cc = c & 63;
   return half * kHalf + i * 128 + ((((cc >> 3) ^ (i & 7))) << 4) + ((cc & 7) << 1);
 }
-// byte offset of B-operand element (n, k) in the K-major no-swizzle 16x16 tile
-__device__ __forceinline__ uint32_t btile_off(int n, int k) {
-  return (n >> 3) * 256 + (k >> 3) * 128 + (n & 7) * 16 + (k & 7) * 2;
+// byte offset of L[i][j] in the transfer tile (see desc_Bk / desc_Bmn)
+__device__ __forceinline__ uint32_t ltile_off(int i, int j) {
+  return (j >> 3) * 256 + (i >> 3) * 128 + (j & 7) * 16 + (i & 7) * 2;
 }
 
 __device__ __forceinline__ float bf(const uint8_t* base, uint32_t off) {
@@ -230,38 +275,39 @@ __device__ __forceinline__ void st_bf(uint8_t* base, uint32_t off, float x) {
 }
 
 // ---------------------------------------------------------------------------
-// work list: CTA c owns blocks [g0, g1) of the flattened (line = b*H + h, t)
-// space, plus one left halo block (and, backward, one right halo block) when a
+// work list: items are BPI-block groups [BPI*m, BPI*m + BPI) of a line
+// (line = b*H + h).  CTA c owns items [g0, g1) of the flattened (line, m)
+// space, plus one left halo item (and, backward, one right halo item) when a
 // boundary falls inside a line.  Items are walked with an incremental cursor.
 // ---------------------------------------------------------------------------
 struct Work {
-  int64_t first, g0, g1, last;  // items are global block ids gi in [first, last)
+  int64_t first, g0, g1, last;  // global item ids gi in [first, last)
 };
 template <bool BWD>
-__device__ __forceinline__ Work work_of(int64_t total, int64_t nb) {
+__device__ __forceinline__ Work work_of(int64_t total, int64_t nbi) {
   Work w;
   w.g0 = (int64_t)blockIdx.x * total / gridDim.x;
   w.g1 = ((int64_t)blockIdx.x + 1) * total / gridDim.x;
-  w.first = w.g0 - ((w.g0 < w.g1 && w.g0 % nb != 0) ? 1 : 0);
-  w.last = w.g1 + ((BWD && w.g0 < w.g1 && w.g1 % nb != 0) ? 1 : 0);
+  w.first = w.g0 - ((w.g0 < w.g1 && w.g0 % nbi != 0) ? 1 : 0);
+  w.last = w.g1 + ((BWD && w.g0 < w.g1 && w.g1 % nbi != 0) ? 1 : 0);
   if (w.g0 >= w.g1) w.first = w.last = w.g0;
   return w;
 }
 
-struct Cursor {
-  int64_t gi, t, line;
+struct Cursor {  // item gi = line * nbi + m; t0 = first block of the item
+  int64_t gi, m, line;
   int b, h;
-  __device__ __forceinline__ void init(int64_t g, int64_t nb, int64_t H) {
+  __device__ __forceinline__ void init(int64_t g, int64_t nbi, int64_t H) {
     gi = g;
-    line = g / nb;
-    t = g - line * nb;
+    line = g / nbi;
+    m = g - line * nbi;
     b = (int)(line / H);
     h = (int)(line - (int64_t)b * H);
   }
-  __device__ __forceinline__ void next(int64_t nb, int64_t H) {
+  __device__ __forceinline__ void next(int64_t nbi, int64_t H) {
     ++gi;
-    if (++t == nb) {
-      t = 0;
+    if (++m == nbi) {
+      m = 0;
       ++line;
       if (++h == H) {
         h = 0;
@@ -286,7 +332,27 @@ struct Ring {
       ph ^= 1;
     }
   }
+  __device__ __forceinline__ void prev() {
+    if (s == 0) {
+      s = NS - 1;
+      ph ^= 1;
+    } else {
+      --s;
+    }
+  }
 };
+
+// 16 fp32 from 16-byte aligned shared memory as four 128-bit loads
+__device__ __forceinline__ void load16(const float4* src, float (&v)[16]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float4 x = src[q];
+    v[4 * q] = x.x;
+    v[4 * q + 1] = x.y;
+    v[4 * q + 2] = x.z;
+    v[4 * q + 3] = x.w;
+  }
+}
 
 // pack two fp32 into bf16x2 (lo = first)
 __device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
@@ -314,41 +380,56 @@ __device__ __forceinline__ void store_col16(uint8_t* tile, int c, int lane, cons
 
 // ---------------------------------------------------------------------------
 // the kernel
+//
+// Per item j (BPI blocks of one (b, h)) the barriers are
+//   full[s]     TMA bytes landed                      (producer, tx count)
+//   prepped[s]  L tiles, g, r, pre-gates in SMEM      (prep warp)
+//   mmad[s]     tcgen05 MMAs of item j complete        (tcgen05.commit)
+//   ready[s]    MMAs of every item whose TMEM item j's epilogue reads are done
+//               (j-1, j; backward also j+1)            (MMA warp)
+//   outready[s] outputs of item j written to SMEM     (epilogue group leader)
+//   empty[s]    stage free again: store read done (store warp) + the neighbour
+//               items that read its TMEM / g (next; backward also previous)
 // ---------------------------------------------------------------------------
 template <int OP>
-__global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPREP + 2) * 32, 1)
+__global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
     swr_tc_kernel(const __grid_constant__ Maps maps, const Params p) {
   using C = Cfg<OP>;
   using S = Stage<OP>;
-  constexpr int NS = C::NS, NG = C::NG;
+  constexpr int NS = C::NS, NG = C::NG, BPI = C::BPI;
   constexpr int kEpi = 128;
+  constexpr int kItemCols = BPI * C::COLS;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int kPrepW0 = 4 * NG, kProdW = kPrepW0 + C::NPREP, kMmaW = kProdW + 1;
+  constexpr int kPrepW0 = 4 * NG, kProdW = kPrepW0 + C::NPW, kMmaW = kProdW + 1, kStoreW = kMmaW + 1;
 
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-aligned stage base for the 128B-swizzle atoms.  Offset the __shared__
+  // array itself (not a uintptr_t round trip) so every access stays LDS/STS.
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   uint8_t* scratch = smem + NS * S::kBytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(scratch);
   uint64_t* prepped = full + NS;
   uint64_t* mmad = prepped + NS;
   uint64_t* ready = mmad + NS;
-  uint64_t* empty = ready + NS;
+  uint64_t* outready = ready + NS;
+  uint64_t* empty = outready + NS;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(empty + NS);
-  float* red = reinterpret_cast<float*>(scratch + 2048);  // [NG][2][4][16] da partials
+  float* red = reinterpret_cast<float*>(scratch + 1024);  // [NG][4 warps][16*BPI] da partials
 
-  constexpr int kTmemCols = (NS * C::COLS <= 32) ? 32 : (NS * C::COLS <= 64) ? 64
-                          : (NS * C::COLS <= 128) ? 128 : (NS * C::COLS <= 256) ? 256 : 512;
-  static_assert(NS * C::COLS <= 512, "TMEM budget");
-  // stage release: the item itself (after its store read SMEM) and the neighbour
-  // items that read its TMEM / g (next; backward also previous)
+  constexpr int kTmemCols = (NS * kItemCols <= 32) ? 32 : (NS * kItemCols <= 64) ? 64
+                          : (NS * kItemCols <= 128) ? 128 : (NS * kItemCols <= 256) ? 256 : 512;
+  static_assert(NS * kItemCols <= 512, "TMEM budget");
+  static_assert(NS >= (C::BWD ? 1 : 0) + 4, "pipeline depth (deadlock freedom)");
+  static_assert(6 * NS * 8 + 8 <= 1024 && NG * 4 * 16 * BPI * 4 <= 3072, "scratch budget");
   constexpr int kUsers = C::BWD ? 3 : 2;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&prepped[s], C::NPREP * 32);
+      mbar_init(&prepped[s], 1);
       mbar_init(&mmad[s], 1);
       mbar_init(&ready[s], 1);
+      mbar_init(&outready[s], 1);
       mbar_init(&empty[s], kUsers);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -365,318 +446,394 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPREP + 2) * 32, 1
   const uint32_t tmem_base = *tmem_slot;
 
   const int64_t nb = p.nb, H = p.H;
-  const int64_t total = p.B * H * nb;
-  const Work W = work_of<C::BWD>(total, nb);
+  const int64_t nbi = (nb + BPI - 1) / BPI;  // items per line
+  const int64_t total = p.B * H * nbi;
+  const Work W = work_of<C::BWD>(total, nbi);
   const int64_t n_items = W.last - W.first;
 
   if (warp == kProdW) {
     // ===================== TMA producer =====================
     if (lane == 0 && n_items > 0) {
       Cursor cur;
-      cur.init(W.first, nb, H);
+      cur.init(W.first, nbi, H);
       Ring<NS> rg;
       rg.init(0);
       for (int64_t j = 0; j < n_items; ++j) {
         mbar_wait(&empty[rg.s], rg.ph ^ 1);
+        trace(p, j, 0);
         uint8_t* st = smem + rg.s * S::kBytes;
-        const int tt = (int)(cur.t * kEll);
-        mbar_expect_tx(&full[rg.s], C::NT * kTile + 256);
+        const int tt = (int)(cur.m * BPI * kEll);
+        mbar_expect_tx(&full[rg.s], BPI * C::NT * kTile + 256 * BPI);
 #pragma unroll
-        for (int x = 0; x < C::NT; ++x) {
-          tma_load_4d(st + x * kTile, &maps.in[x], &full[rg.s], 0, cur.h, tt, cur.b);
-          tma_load_4d(st + x * kTile + kHalf, &maps.in[x], &full[rg.s], 64, cur.h, tt, cur.b);
+        for (int k = 0; k < BPI; ++k) {
+#pragma unroll
+          for (int x = 0; x < C::NT; ++x) {
+            uint8_t* dst = S::tile(st, k, x);
+            tma_load_4d(dst, &maps.in[x], &full[rg.s], 0, cur.h, tt + k * kEll, cur.b);
+            tma_load_4d(dst + kHalf, &maps.in[x], &full[rg.s], 64, cur.h, tt + k * kEll, cur.b);
+          }
         }
         tma_load_3d(st + S::kA, &maps.a, &full[rg.s], cur.h & ~7, tt, cur.b);
-        cur.next(nb, H);
+        trace(p, j, 1);
+        cur.next(nbi, H);
         rg.next();
       }
     }
   } else if (warp == kMmaW) {
     // ===================== MMA issuer + readiness =====================
-    // ready[j] is arrived once the MMAs of every item whose TMEM item j's
-    // epilogue reads are complete: j-1, j (and, backward, j+1).
-    Ring<NS> rg, r1, r2;  // item j, j-1, j-2
-    rg.init(0);
-    r1 = rg;
-    r2 = rg;
-    for (int64_t j = 0; j < n_items; ++j) {
-      mbar_wait(&full[rg.s], rg.ph);
-      mbar_wait(&prepped[rg.s], rg.ph);
-      tc_fence_after();
-      if (lane == 0) {
-        uint8_t* st = smem + rg.s * S::kBytes;
-        const uint32_t d = tmem_base + (uint32_t)(rg.s * C::COLS);
-        const uint32_t aW = su32(st + (C::MIX ? C::NT * kTile : 0));  // u or u^ = k v
-        umma_bf16(d, desc_A(aW), desc_B(su32(st + S::kLT)), kIdesc);
-        if constexpr (C::BWD) {
-          const uint32_t aG = su32(st + (C::MIX ? (C::NT + 1) * kTile : kTile));  // G or dy q
-          umma_bf16(d + 16, desc_A(aG), desc_B(su32(st + S::kL)), kIdesc);
+    // One thread polls two queues without blocking on either: issue the next
+    // item's MMAs once its operands have landed, and retire completed items in
+    // issue order (tcgen05 ops complete in order).  ready[j] is arrived once
+    // every MMA item j's epilogue reads is complete: j-1, j (backward also j+1).
+    // MMA latency therefore costs pipeline depth, not throughput.
+    if (lane == 0 && n_items > 0) {
+      constexpr int kBack = C::BWD ? 1 : 0;
+      Ring<NS> ri, rc, rr;  // next to issue, next to retire, next to mark ready
+      ri.init(0);
+      rc.init(0);
+      rr.init(0);
+      int64_t ji = 0, jc = 0, jr = 0;
+      while (jr < n_items) {
+        bool progressed = false;
+        if (ji < n_items && mbar_test(&full[ri.s], ri.ph) && mbar_test(&prepped[ri.s], ri.ph)) {
+          tc_fence_after();
+          trace(p, ji, 4);
+          uint8_t* st = smem + ri.s * S::kBytes;
+#pragma unroll
+          for (int k = 0; k < BPI; ++k) {
+            const uint32_t d = tmem_base + (uint32_t)(ri.s * kItemCols + k * C::COLS);
+            const uint32_t lt = su32(st + S::kL + 512 * k);
+            umma_bf16(d, desc_A(su32(S::tile(st, k, C::TU))), desc_Bmn(lt), kIdescBmn);  // w^T
+            if constexpr (C::BWD)  // lambda^T
+              umma_bf16(d + 16, desc_A(su32(S::tile(st, k, C::TG))), desc_Bk(lt), kIdescBk);
+          }
+          umma_commit(&mmad[ri.s]);
+          trace(p, ji, 5);
+          ri.next();
+          ++ji;
+          progressed = true;
         }
-        umma_commit(&mmad[rg.s]);
-      }
-      __syncwarp();
-      if (j >= 1) {
-        mbar_wait(&mmad[r1.s], r1.ph);  // item j-1 complete
-        tc_fence_before();
-        if (lane == 0) {
-          if constexpr (!C::BWD) mbar_arrive(&ready[r1.s]);
-          else if (j >= 2) mbar_arrive(&ready[r2.s]);
+        if (jc < ji && mbar_test(&mmad[rc.s], rc.ph)) {
+          rc.next();
+          ++jc;
+          progressed = true;
         }
-        __syncwarp();
+        // items whose dependencies are retired
+        while (jr < n_items && (jr + kBack < jc || (jc == n_items && jr < jc))) {
+          tc_fence_before();
+          mbar_arrive(&ready[rr.s]);
+          trace(p, jr, 6);
+          rr.next();
+          ++jr;
+          progressed = true;
+        }
+        if (!progressed) __nanosleep(20);
       }
-      r2 = r1;
-      r1 = rg;
-      rg.next();
     }
-    if (n_items > 0) {  // flush: r1 = last item, r2 = the one before
-      mbar_wait(&mmad[r1.s], r1.ph);
-      tc_fence_before();
-      if (lane == 0) {
-        if (C::BWD && n_items >= 2) mbar_arrive(&ready[r2.s]);
-        mbar_arrive(&ready[r1.s]);
-      }
-      __syncwarp();
-    }
-  } else if (warp >= kPrepW0) {
-    // ===================== prep: L tiles (Alg. 3), g, r, pre-gates =====================
-    const int pt = threadIdx.x - kPrepW0 * 32;  // 0 .. NPREP*32-1
-    Cursor cur;
-    if (n_items > 0) cur.init(W.first, nb, H);
-    Ring<NS> rg;
-    rg.init(0);
-    for (int64_t j = 0; j < n_items; ++j) {
-      mbar_wait(&full[rg.s], rg.ph);
-      uint8_t* st = smem + rg.s * S::kBytes;
-      if (pt < 16) {
-        // lane j owns column j of L_t.  Alg. 3: tile a down the columns, pre-mask
-        // the inclusive upper triangle with 1, column-wise cumulative product,
-        // zero the strict upper triangle.  Products only, never ratios.
-        const int col = pt;
-        const uint8_t* at = st + S::kA + (cur.h & 7) * 2;
-        float a[16];
+    __syncwarp();
+  } else if (warp == kStoreW) {
+    // ===================== TMA store + stage release =====================
+    if (lane == 0 && n_items > 0) {
+      Cursor cur;
+      cur.init(W.first, nbi, H);
+      Ring<NS> rg;
+      rg.init(0);
+      int pend = -1;  // stage whose store may still be reading SMEM
+      for (int64_t j = 0; j < n_items; ++j) {
+        mbar_wait(&outready[rg.s], rg.ph);
+        const bool halo = cur.gi < W.g0 || cur.gi >= W.g1;
+        if (!halo) {
+          uint8_t* st = smem + rg.s * S::kBytes;
+          const int64_t t0 = cur.m * BPI;
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-          a[i] = (cur.t * kEll + i < p.L) ? __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(at + i * 16)) : 1.f;
-        float Lc[16];
-        float prod = 1.f;
+          for (int k = 0; k < BPI; ++k) {
+            if (t0 + k >= nb) break;
+            const int tt = (int)((t0 + k) * kEll);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          if (i > col) prod *= a[i];
-          Lc[i] = (i >= col) ? prod : 0.f;  // L[i][col]
-        }
-        // B of W (L_t^T, K-major): element (n = i, k = col)
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-          *reinterpret_cast<__nv_bfloat16*>(st + S::kLT + btile_off(i, col)) = __float2bfloat16_rn(Lc[i]);
-        if constexpr (C::BWD) {
-          // B of lambda (L_t, K-major): element (n = col, k = i), contiguous along k
-          uint4 lo, hi;
-          lo.x = pack_bf2(Lc[0], Lc[1]);   lo.y = pack_bf2(Lc[2], Lc[3]);
-          lo.z = pack_bf2(Lc[4], Lc[5]);   lo.w = pack_bf2(Lc[6], Lc[7]);
-          hi.x = pack_bf2(Lc[8], Lc[9]);   hi.y = pack_bf2(Lc[10], Lc[11]);
-          hi.z = pack_bf2(Lc[12], Lc[13]); hi.w = pack_bf2(Lc[14], Lc[15]);
-          *reinterpret_cast<uint4*>(st + S::kL + btile_off(col, 0)) = lo;
-          *reinterpret_cast<uint4*>(st + S::kL + btile_off(col, 8)) = hi;
-          reinterpret_cast<float*>(st + S::kR)[col] = prod;  // r_t[j] = L[15][j]
-        }
-        // g_t[i] = a_t[0] ... a_t[i]: 16-lane multiplicative scan (pattern of Alg. 1 line 8)
-        float g = (cur.t * kEll + col < p.L)
-                      ? __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(at + col * 16)) : 1.f;
-#pragma unroll
-        for (int d = 1; d < 16; d <<= 1) {
-          const float o = __shfl_up_sync(0x0000ffffu, g, d, 16);
-          if (col >= d) g *= o;
-        }
-        reinterpret_cast<float*>(st + S::kG)[col] = g;
-      }
-      if constexpr (C::MIX) {
-        // pre-gates in the swizzled tile layout (elementwise, layout-agnostic):
-        //   u^ = k (.) v and, backward, G = dy (.) q; rounded once to bf16
-        const uint4* K4 = reinterpret_cast<const uint4*>(st + 1 * kTile);
-        const uint4* V4 = reinterpret_cast<const uint4*>(st + 2 * kTile);
-        uint4* U4 = reinterpret_cast<uint4*>(st + C::NT * kTile);
-        for (int v = pt; v < kTile / 16; v += C::NPREP * 32) {
-          const uint4 kk = K4[v], vv = V4[v];
-          uint4 o;
-          const uint32_t* ka = &kk.x;
-          const uint32_t* va = &vv.x;
-          uint32_t* oa = &o.x;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 kf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ka[e]));
-            const float2 vf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&va[e]));
-            oa[e] = pack_bf2(kf.x * vf.x, kf.y * vf.y);
-          }
-          U4[v] = o;
-          if constexpr (C::BWD) {
-            const uint4* Q4 = reinterpret_cast<const uint4*>(st + 0 * kTile);
-            const uint4* D4 = reinterpret_cast<const uint4*>(st + 3 * kTile);
-            uint4* G4 = reinterpret_cast<uint4*>(st + (C::NT + 1) * kTile);
-            const uint4 qq = Q4[v], dd = D4[v];
-            const uint32_t* qa = &qq.x;
-            const uint32_t* da = &dd.x;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 qf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&qa[e]));
-              const float2 df = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&da[e]));
-              oa[e] = pack_bf2(df.x * qf.x, df.y * qf.y);
+            for (int x = 0; x < C::NOUT; ++x) {
+              const int tile = (OP == 0) ? 0 : (OP == 1) ? 1 : (OP == 2) ? 0 : (x == 0 ? 3 : x);
+              tma_store_4d(&maps.out[x], S::tile(st, k, tile), 0, cur.h, tt, cur.b);
+              tma_store_4d(&maps.out[x], S::tile(st, k, tile) + kHalf, 64, cur.h, tt, cur.b);
             }
-            G4[v] = o;
-          }
-        }
-      }
-      fence_proxy_async();  // generic-proxy writes -> visible to the tensor core
-      mbar_arrive(&prepped[rg.s]);
-      cur.next(nb, H);
-      rg.next();
-    }
-  } else {
-    // ===================== epilogue groups: thread = channel c =====================
-    const int grp = warp >> 2;                       // epilogue group, items j = grp mod NG
-    const int c = threadIdx.x & 127;                 // channel == TMEM lane
-    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-    const bool leader = (threadIdx.x & 127) == 0;
-    float* red_g = red + grp * 128;                  // [2][4][16]
-    int rbuf = 0;
-    int pend = -1;                                   // stage of the last stored item (release lags its store)
-    Cursor cur;
-    if (grp < n_items) cur.init(W.first + grp, nb, H);
-    Ring<NS> rg, rp, rn;
-    rg.init(grp);
-    for (int64_t j = grp; j < n_items; j += NG) {
-      rp = rg;  // ring slots of items j-1 and j+1
-      if (rp.s == 0) { rp.s = NS - 1; rp.ph ^= 1; } else { --rp.s; }
-      rn = rg;
-      rn.next();
-      const int64_t t = cur.t;
-      const int b = cur.b, h = cur.h;
-      const bool halo = cur.gi < W.g0 || cur.gi >= W.g1;
-      uint8_t* st = smem + rg.s * S::kBytes;
-      const float* g = reinterpret_cast<const float*>(st + S::kG);
-      const int64_t co = cur.line * kD + c;
-      mbar_wait(&ready[rg.s], rg.ph);
-      tc_fence_after();
-      bool stored = false;
-      if (!halo) {
-        const uint32_t tslot = tmem_base + lane_base + (uint32_t)(rg.s * C::COLS);
-        float w[16];
-        tmem_ld16(tslot, w);
-        // carrier v_{t-1} = w_{t-1}[15]: column 15 of the previous item's TMEM
-        float vprev;
-        if (t == 0) {
-          vprev = p.carry_in ? p.carry_in[co] : 0.f;  // v_{-1}
-        } else {
-          vprev = tmem_ld1(tmem_base + lane_base + (uint32_t)(rp.s * C::COLS + 15));
-        }
-        if constexpr (!C::BWD) {
-          tmem_wait_ld();
-          float out[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) out[i] = fmaf(g[i], vprev, w[i]);  // Pass II: x~ = w + g v
-          if constexpr (C::MIX) {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {  // post-gate with residual: y = q x~ + v
-              const uint32_t o = tile_off(i, c);
-              out[i] = fmaf(bf(st, o), out[i], bf(st + 2 * kTile, o));
-            }
-          }
-          __syncwarp();
-          store_col16(st, c, lane, out);
-          if (t == nb - 1 && p.carry_out) p.carry_out[co] = w[15];
-        } else {
-          float lam[16];
-          tmem_ld16(tslot + 16, lam);
-          float mu;
-          if (t == nb - 1) {
-            mu = p.mu_in ? p.mu_in[co] : 0.f;
-            tmem_wait_ld();
-          } else {  // mu_t = a_{t+1}[0] lambda_{t+1}[0] from the next item
-            const float l0 = tmem_ld1(tmem_base + lane_base + (uint32_t)(rn.s * C::COLS + 16));
-            tmem_wait_ld();
-            mu = reinterpret_cast<const float*>(smem + rn.s * S::kBytes + S::kG)[0] * l0;
-          }
-          const float* r = reinterpret_cast<const float*>(st + S::kR);
-          float part[16], du[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float rmu = r[i] * mu;
-            du[i] = lam[i] + rmu;                                            // du = lambda + r mu
-            const float wp = (i > 0) ? w[i - 1] : 0.f;
-            const float xp = (i > 0) ? fmaf(g[i - 1], vprev, w[i - 1]) : vprev;  // x~[i-1]
-            part[i] = fmaf(lam[i], xp, rmu * wp);                              // da partial
-          }
-          __syncwarp();
-          if constexpr (!C::MIX) {
-            store_col16(st + kTile, c, lane, du);  // du over G
-          } else {
-            float dq[16], dk[16], dv[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const uint32_t o = tile_off(i, c);
-              const float dy = bf(st + 3 * kTile, o), kk = bf(st + kTile, o), vv = bf(st + 2 * kTile, o);
-              const float x = fmaf(g[i], vprev, w[i]);
-              dq[i] = dy * x;              // dq = dy x~
-              dk[i] = du[i] * vv;          // dk = du^ v
-              dv[i] = fmaf(du[i], kk, dy);  // dv = du^ k + dy
-            }
-            __syncwarp();
-            store_col16(st + 3 * kTile, c, lane, dq);
-            store_col16(st + 1 * kTile, c, lane, dk);
-            store_col16(st + 2 * kTile, c, lane, dv);
-          }
-          if (t == 0 && p.mu_out) p.mu_out[co] = g[0] * lam[0];  // a_0[0] lambda_0[0]
-          // da: deterministic reduction over the 128 channels (4 warps of this group)
-          int tok = 0;
-          GroupReduce<16, 16>::run(part, lane, tok);
-          float* rb = red_g + rbuf * 64;
-          if ((lane & 1) == 0) rb[(warp & 3) * 16 + tok] = part[0];
-          named_bar(1 + NG + grp, kEpi);
-          if ((warp & 3) == 0 && lane < 16) {
-            const int64_t n = t * kEll + lane;
-            if (n < p.L) {
-              const float sum = ((rb[lane] + rb[16 + lane]) + rb[32 + lane]) + rb[48 + lane];
-              __nv_bfloat16* dA = (__nv_bfloat16*)p.da + (int64_t)b * p.sa_b + (int64_t)h * p.sa_h;
-              dA[n * p.sa_l] = __float2bfloat16_rn(sum);
-            }
-          }
-          rbuf ^= 1;
-        }
-        stored = true;
-      }
-      // hand back: outputs -> TMA store; release own stage once the store has read
-      // SMEM, and the neighbours' stages whose TMEM / g this item read
-      tc_fence_before();
-      if (stored) fence_proxy_async();
-      named_bar(1 + grp, kEpi);
-      if (leader) {
-        if (stored) {
-          const int tt = (int)(t * kEll);
-#pragma unroll
-          for (int x = 0; x < C::NOUT; ++x) {
-            const int tile = (OP == 0) ? 0 : (OP == 1) ? 1 : (OP == 2) ? 0 : (x == 0 ? 3 : x);
-            tma_store_4d(&maps.out[x], st + tile * kTile, 0, h, tt, b);
-            tma_store_4d(&maps.out[x], st + tile * kTile + kHalf, 64, h, tt, b);
           }
           bulk_commit();
-          bulk_wait_read<1>();
+          trace(p, j, 9);
+          bulk_wait_read<1>();  // the previous item's store has read SMEM
           if (pend >= 0) mbar_arrive(&empty[pend]);
           pend = rg.s;
         } else {
           mbar_arrive(&empty[rg.s]);
         }
+        cur.next(nbi, H);
+        rg.next();
+      }
+      bulk_wait_all();
+      if (pend >= 0) mbar_arrive(&empty[pend]);
+    }
+  } else if (warp >= kPrepW0) {
+    // ===================== prep: L tiles (Alg. 3), g, r, pre-gates =====================
+    // prep warp pw owns items j = pw mod NPW; each 16-lane half builds one block
+    const int pw = warp - kPrepW0;
+    const int hf = lane >> 4, col = lane & 15;
+    Cursor cur;
+    if (pw < n_items) cur.init(W.first + pw, nbi, H);
+    Ring<NS> rg;
+    rg.init(pw);
+    for (int64_t j = pw; j < n_items; j += C::NPW) {
+      mbar_wait(&full[rg.s], rg.ph);
+      if (lane == 0) trace(p, j, 2);
+      uint8_t* st = smem + rg.s * S::kBytes;
+#pragma unroll
+      for (int kb = 0; kb < BPI; kb += 2) {
+        const int k = kb + hf;
+        if (k < BPI) {
+          const int64_t t = cur.m * BPI + k;
+          const int nval = (int)std::min<int64_t>(16, std::max<int64_t>(p.L - t * kEll, 0));  // valid tokens
+          // lane col owns column col of L_t.  Alg. 3: tile a down the columns, pre-mask
+          // the inclusive upper triangle with 1, column-wise cumulative product, zero
+          // the strict upper triangle.  Products only, never ratios.
+          const uint8_t* at = st + S::kA + (k * kEll) * 16 + (cur.h & 7) * 2;
+          float a[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            a[i] = (i < nval) ? __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(at + i * 16)) : 1.f;
+          float Lc[16];
+          float prod = 1.f;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            if (i > col) prod *= a[i];
+            Lc[i] = (i >= col) ? prod : 0.f;  // L[i][col]
+          }
+          // column col: two 16-byte stores (rows 0-7, rows 8-15), rounded once to bf16
+          uint8_t* l = st + S::kL + 512 * k;
+          uint4 lo, hi;
+          lo.x = pack_bf2(Lc[0], Lc[1]);   lo.y = pack_bf2(Lc[2], Lc[3]);
+          lo.z = pack_bf2(Lc[4], Lc[5]);   lo.w = pack_bf2(Lc[6], Lc[7]);
+          hi.x = pack_bf2(Lc[8], Lc[9]);   hi.y = pack_bf2(Lc[10], Lc[11]);
+          hi.z = pack_bf2(Lc[12], Lc[13]); hi.w = pack_bf2(Lc[14], Lc[15]);
+          *reinterpret_cast<uint4*>(l + ltile_off(0, col)) = lo;
+          *reinterpret_cast<uint4*>(l + ltile_off(8, col)) = hi;
+          if constexpr (C::BWD) reinterpret_cast<float*>(st + S::kR + 64 * k)[col] = prod;  // r_t[j] = L[15][j]
+          if (col == 0) {
+            // g_t[i] = a_t[0] L_t[i][0] = a_t[0] ... a_t[i], fp32
+            float4* gp = reinterpret_cast<float4*>(st + S::kG + 64 * k);
+            gp[0] = make_float4(a[0] * Lc[0], a[0] * Lc[1], a[0] * Lc[2], a[0] * Lc[3]);
+            gp[1] = make_float4(a[0] * Lc[4], a[0] * Lc[5], a[0] * Lc[6], a[0] * Lc[7]);
+            gp[2] = make_float4(a[0] * Lc[8], a[0] * Lc[9], a[0] * Lc[10], a[0] * Lc[11]);
+            gp[3] = make_float4(a[0] * Lc[12], a[0] * Lc[13], a[0] * Lc[14], a[0] * Lc[15]);
+          }
+        }
+      }
+      if constexpr (C::MIX) {
+        // pre-gates in the swizzled tile layout (elementwise, layout-agnostic), each
+        // rounded once to bf16: u^ = k (.) v; backward also G = dy (.) q
+#pragma unroll
+        for (int k = 0; k < BPI; ++k) {
+          const uint4* K4 = reinterpret_cast<const uint4*>(S::tile(st, k, 1));
+          const uint4* V4 = reinterpret_cast<const uint4*>(S::tile(st, k, 2));
+          uint4* U4 = reinterpret_cast<uint4*>(S::tile(st, k, C::TU));
+#pragma unroll 2
+          for (int v = lane; v < kTile / 16; v += 32) {
+            const uint4 kk = K4[v], vv = V4[v];
+            uint4 o;
+            const uint32_t* ka = &kk.x;
+            const uint32_t* va = &vv.x;
+            uint32_t* oa = &o.x;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 kf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ka[e]));
+              const float2 vf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&va[e]));
+              oa[e] = pack_bf2(kf.x * vf.x, kf.y * vf.y);
+            }
+            U4[v] = o;
+            if constexpr (C::BWD) {
+              uint4* Q4 = reinterpret_cast<uint4*>(S::tile(st, k, 0));  // G overwrites q
+              const uint4* D4 = reinterpret_cast<const uint4*>(S::tile(st, k, 3));
+              const uint4 qq = Q4[v], dd = D4[v];
+              const uint32_t* qa = &qq.x;
+              const uint32_t* da = &dd.x;
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 qf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&qa[e]));
+                const float2 df = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&da[e]));
+                oa[e] = pack_bf2(df.x * qf.x, df.y * qf.y);
+              }
+              Q4[v] = o;
+            }
+          }
+        }
+      }
+      fence_proxy_async();  // this lane's generic-proxy writes -> visible to the tensor core
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&prepped[rg.s]);
+        trace(p, j, 3);
+      }
+      for (int q = 0; q < C::NPW; ++q) {
+        cur.next(nbi, H);
+        rg.next();
+      }
+    }
+  } else {
+    // ===================== epilogue groups: thread = channel c =====================
+    const int grp = warp >> 2;                       // epilogue group, items j = grp mod NG
+    const int wq = warp & 3;                         // TMEM lane quarter
+    const int c = threadIdx.x & 127;                 // channel == TMEM lane
+    const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+    const bool leader = (threadIdx.x & 127) == 0;
+    float* rb = red + grp * (4 * 16 * BPI);          // [4 warps][16*BPI tokens]
+    Cursor cur;
+    if (grp < n_items) cur.init(W.first + grp, nbi, H);
+    Ring<NS> rg, rp, rn;
+    rg.init(grp);
+    for (int64_t j = grp; j < n_items; j += NG) {
+      rp = rg;
+      rp.prev();
+      rn = rg;
+      rn.next();
+      const int64_t t0 = cur.m * BPI;
+      const int b = cur.b, h = cur.h;
+      const bool halo = cur.gi < W.g0 || cur.gi >= W.g1;
+      const int nblk = (int)std::min<int64_t>(BPI, nb - t0);  // valid blocks of this item
+      uint8_t* st = smem + rg.s * S::kBytes;
+      const int64_t co = cur.line * kD + c;
+      const uint32_t tslot = tmem_base + lane_base + (uint32_t)(rg.s * kItemCols);
+      mbar_wait(&ready[rg.s], rg.ph);
+      tc_fence_after();
+      if (leader) trace(p, j, 7);
+      // 1) neighbour reads first, so the neighbours' stages are released early:
+      //    carrier entering block t0: v = w_{t0-1}[15], the last block of item j-1;
+      //    backward: mu of the item's last block from block 0 of item j+1
+      float vprev = 0.f, mu_last = 0.f;
+      if (!halo) {
+        if (t0 == 0) vprev = p.carry_in ? p.carry_in[co] : 0.f;  // v_{-1}
+        else vprev = tmem_ld1(tmem_base + lane_base + (uint32_t)(rp.s * kItemCols + (BPI - 1) * C::COLS + 15));
+        if constexpr (C::BWD) {
+          if (t0 + nblk == nb) {
+            mu_last = p.mu_in ? p.mu_in[co] : 0.f;
+          } else {  // mu_t = a_{t+1}[0] lambda_{t+1}[0]
+            const float l0 = tmem_ld1(tmem_base + lane_base + (uint32_t)(rn.s * kItemCols + 16));
+            tmem_wait_ld();
+            mu_last = reinterpret_cast<const float*>(smem + rn.s * S::kBytes + S::kG)[0] * l0;
+          }
+        }
+        tmem_wait_ld();
+      }
+      tc_fence_before();
+      named_bar(1 + grp, kEpi);
+      if (leader) {
         if (j >= 1) mbar_arrive(&empty[rp.s]);                       // as "next" of item j-1
         if (C::BWD && j + 1 < n_items) mbar_arrive(&empty[rn.s]);  // as "previous" of item j+1
         if (j == n_items - 1) mbar_arrive(&empty[rg.s]);           // no next item
         if (C::BWD && j == 0) mbar_arrive(&empty[rg.s]);           // no previous item
       }
-      for (int k = 0; k < NG; ++k) {
-        cur.next(nb, H);
+      // 2) the item's blocks, in order (the carrier passes block to block in a register)
+      if (!halo) {
+#pragma unroll 1
+        for (int k = 0; k < nblk; ++k) {
+          const int64_t t = t0 + k;
+          float g[16];
+          load16(reinterpret_cast<const float4*>(st + S::kG + 64 * k), g);
+          float w[16];
+          tmem_ld16(tslot + k * C::COLS, w);
+          if constexpr (!C::BWD) {
+            tmem_wait_ld();
+            float out[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) out[i] = fmaf(g[i], vprev, w[i]);  // Pass II: x~ = w + g v
+            uint8_t* t_out = S::tile(st, k, 0);
+            if constexpr (C::MIX) {
+              const uint8_t* t_v = S::tile(st, k, 2);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {  // post-gate with residual: y = q x~ + v
+                const uint32_t o = tile_off(i, c);
+                out[i] = fmaf(bf(t_out, o), out[i], bf(t_v, o));
+              }
+            }
+            __syncwarp();
+            store_col16(t_out, c, lane, out);
+            if (t == nb - 1 && p.carry_out) p.carry_out[co] = w[15];
+          } else {
+            float lam[16];
+            tmem_ld16(tslot + k * C::COLS + 16, lam);
+            float mu = mu_last;
+            if (k + 1 < nblk) {  // next block inside this item
+              const float l0 = tmem_ld1(tslot + (k + 1) * C::COLS + 16);
+              tmem_wait_ld();
+              mu = reinterpret_cast<const float*>(st + S::kG + 64 * (k + 1))[0] * l0;
+            }
+            tmem_wait_ld();
+            float r[16];
+            load16(reinterpret_cast<const float4*>(st + S::kR + 64 * k), r);
+            float part[16], du[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const float rmu = r[i] * mu;
+              du[i] = lam[i] + rmu;                                            // du = lambda + r mu
+              const float wp = (i > 0) ? w[i - 1] : 0.f;
+              const float xp = (i > 0) ? fmaf(g[i - 1], vprev, w[i - 1]) : vprev;  // x~[i-1]
+              part[i] = fmaf(lam[i], xp, rmu * wp);                              // da partial
+            }
+            if (t == 0 && p.mu_out) p.mu_out[co] = g[0] * lam[0];  // a_0[0] lambda_0[0]
+            __syncwarp();
+            if constexpr (!C::MIX) {
+              store_col16(S::tile(st, k, 1), c, lane, du);  // du over G
+            } else {
+              uint8_t* t_dy = S::tile(st, k, 3);
+              uint8_t* t_k = S::tile(st, k, 1);
+              uint8_t* t_v = S::tile(st, k, 2);
+              float o16[16], dyv[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {  // dq = dy x~
+                const uint32_t o = tile_off(i, c);
+                dyv[i] = bf(t_dy, o);
+                o16[i] = dyv[i] * fmaf(g[i], vprev, w[i]);
+              }
+              __syncwarp();
+              store_col16(t_dy, c, lane, o16);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {  // dv = du^ k + dy ; dk = du^ v
+                const uint32_t o = tile_off(i, c);
+                o16[i] = fmaf(du[i], bf(t_k, o), dyv[i]);
+                du[i] *= bf(t_v, o);
+              }
+              __syncwarp();
+              store_col16(t_v, c, lane, o16);
+              store_col16(t_k, c, lane, du);
+            }
+            // da: transpose-reduce over the warp's 32 channels, partials to SMEM
+            int tok = 0;
+            GroupReduce<16, 16>::run(part, lane, tok);
+            if ((lane & 1) == 0) rb[wq * (16 * BPI) + k * 16 + tok] = part[0];
+          }
+          vprev = w[15];
+        }
+        if constexpr (C::BWD) {  // da: sum the 4 warps' partials, fixed order
+          named_bar(1 + NG + grp, kEpi);
+          if (wq == 0) {
+            __nv_bfloat16* dA = (__nv_bfloat16*)p.da + (int64_t)b * p.sa_b + (int64_t)h * p.sa_h;
+            for (int q = lane; q < 16 * nblk; q += 32) {
+              const int64_t n = t0 * kEll + q;
+              if (n < p.L) {
+                const float sum = ((rb[q] + rb[16 * BPI + q]) + rb[32 * BPI + q]) + rb[48 * BPI + q];
+                dA[n * p.sa_l] = __float2bfloat16_rn(sum);
+              }
+            }
+          }
+        }
+      }
+      // 3) outputs are in SMEM: hand the item to the store warp
+      tc_fence_before();
+      fence_proxy_async();
+      named_bar(1 + grp, kEpi);
+      if (leader) {
+        trace(p, j, 8);
+        mbar_arrive(&outready[rg.s]);
+      }
+      for (int q = 0; q < NG; ++q) {
+        cur.next(nbi, H);
         rg.next();
       }
-    }
-    if (leader) {
-      bulk_wait_all();
-      if (pend >= 0) mbar_arrive(&empty[pend]);
     }
   }
 
@@ -717,10 +874,10 @@ static bool map_dtensor(CUtensorMap* m, const void* ptr, const Params& p) {
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-static bool map_decay(CUtensorMap* m, const void* ptr, const Params& p) {
+static bool map_decay(CUtensorMap* m, const void* ptr, const Params& p, int bpi) {
   cuuint64_t dims[3] = {(cuuint64_t)p.H, (cuuint64_t)p.L, (cuuint64_t)p.B};
   cuuint64_t strides[2] = {(cuuint64_t)p.sa_l * 2, (cuuint64_t)p.sa_b * 2};
-  cuuint32_t box[3] = {8, 16, 1};
+  cuuint32_t box[3] = {8, (cuuint32_t)(16 * bpi), 1};
   cuuint32_t es[3] = {1, 1, 1};
   return encoder()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -746,7 +903,7 @@ static cudaError_t launch_op(const Params& p, cudaStream_t st, int sms) {
     if (!map_dtensor(&maps.in[i], ins[i], p)) return cudaErrorNotSupported;
   for (int i = 0; i < nout; ++i)
     if (!map_dtensor(&maps.out[i], outs[i], p)) return cudaErrorNotSupported;
-  if (!map_decay(&maps.a, p.a, p)) return cudaErrorNotSupported;
+  if (!map_decay(&maps.a, p.a, p, Cfg<OP>::BPI)) return cudaErrorNotSupported;
 
   constexpr int smem = smem_bytes<OP>();
   static bool attr_set = false;
@@ -755,9 +912,9 @@ static cudaError_t launch_op(const Params& p, cudaStream_t st, int sms) {
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int64_t total = p.B * p.H * p.nb;
+  const int64_t total = p.B * p.H * ((p.nb + Cfg<OP>::BPI - 1) / Cfg<OP>::BPI);
   const int grid = (int)std::min<int64_t>(sms, std::max<int64_t>(total, 1));
-  constexpr int threads = (4 * Cfg<OP>::NG + Cfg<OP>::NPREP + 2) * 32;
+  constexpr int threads = (4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32;
   swr_tc_kernel<OP><<<grid, threads, smem, st>>>(maps, p);
   return cudaGetLastError();
 }

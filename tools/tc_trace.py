@@ -1,0 +1,49 @@
+"""Per-item pipeline timeline of CTA 0 of the TC kernels (diagnostics)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_2512_13921_b200 as P
+from paper_2512_13921_b200 import _lib
+from swr_inputs import swr_inputs, mix_inputs
+
+EV = ["prod_got", "prod_issued", "prep_full", "prep_done", "mma_full", "mma_issued", "ready",
+      "epi_ready", "epi_done", "store_commit", "released"]
+op = sys.argv[1] if len(sys.argv) > 1 else "fwd"
+N = 240
+P.set_path(P.SWR_PATH_TC)
+if op in ("fwd", "bwd"):
+    g = {k: v.cuda() for k, v in swr_inputs(8, 4096, 16, 128, seed=1).items()}
+    run = (lambda: P.swr_fwd(g["u"], g["a"])) if op == "fwd" else (lambda: P.swr_bwd(g["u"], g["a"], g["G"]))
+else:
+    g = {k: v.cuda() for k, v in mix_inputs(8, 4096, 16, 128, seed=1).items()}
+    run = (lambda: P.phalanx_mix(g["q"], g["k"], g["v"], g["a"])) if op == "mixf" else (
+        lambda: P.phalanx_mix_bwd(g["q"], g["k"], g["v"], g["a"], g["dy"]))
+for _ in range(5):
+    run()
+buf = torch.zeros(N * 16, dtype=torch.int64, device="cuda")
+_lib.set_trace(buf.data_ptr(), N)
+flush = torch.empty(64 << 20, device="cuda")
+flush.zero_()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record(); run(); e1.record()
+torch.cuda.synchronize()
+_lib.set_trace(None, 0)
+print(op, "kernel ms", e0.elapsed_time(e1))
+t = buf.cpu().numpy().reshape(N, 16)[:, :len(EV)].astype(np.int64)
+valid = t[:, 0] > 0
+t0 = t[valid][:, 0].min()
+rel = np.where(t > 0, t - t0, -1)
+print("item " + " ".join(f"{e[:10]:>10}" for e in EV))
+for j in list(range(0, 24)) + list(range(100, 112)) + list(range(200, 212)):
+    if j < N and valid[j]:
+        print(f"{j:4d} " + " ".join(f"{x:10d}" for x in rel[j]))
+# steady-state averages of stage-to-stage latencies (items 40..200)
+sl = slice(40, 200)
+def d(a, b):
+    m = (t[sl, a] > 0) & (t[sl, b] > 0)
+    return float(np.median(t[sl, b][m] - t[sl, a][m])) if m.any() else float("nan")
+print("median latencies (ns): prod_issued->prep_full", d(1, 2), " prep", d(2, 3), " prep_done->mma_full", d(3, 4),
+      " mma_issued->ready", d(5, 6), " ready->epi_ready", d(6, 7), " epi", d(7, 8), " epi_done->commit", d(8, 9),
+      " prod_got->released(own)", d(0, 10))
+per = np.diff(t[sl, 1])
+print("producer issue period ns (median)", float(np.median(per)), " epi_ready period", float(np.median(np.diff(t[sl, 7][t[sl,7]>0]))))

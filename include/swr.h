@@ -160,7 +160,7 @@ SWR_API int64_t swr_launch_count(void);
 SWR_API int swr_last_path(void);
 
 /* Diagnostics: when `buf` (device memory, >= 16 * n uint64) is non-NULL, the
- * tensor-core kernels of CTA 0 record a %globaltimer timestamp (ns) per pipeline
+ * tensor-core kernels of CTA 0 record a clock64 timestamp (SM cycles) per pipeline
  * event for each of their first n items (slot = 16 * item + event; events are
  * listed in paper_2512_13921_b200/csrc/swr_tc.cu).  NULL disables tracing. */
 SWR_API void swr_set_trace(unsigned long long* buf, int64_t n);

@@ -55,13 +55,13 @@ template <int OP>
 struct Cfg;
 template <>
 struct Cfg<0> {  // swr_fwd: in u;            out x  (over u)
-  static constexpr int NT = 1, NP = 0, BPI = 4, NS = 8, COLS = 16, NPW = 2, NOUT = 1, NG = 3;
+  static constexpr int NT = 1, NP = 0, BPI = 4, NS = 8, COLS = 16, NPW = 4, NOUT = 1, NG = 3;
   static constexpr int TU = 0, TG = 0;  // A-operand tiles of W and lambda
   static constexpr bool BWD = false, MIX = false;
 };
 template <>
 struct Cfg<1> {  // swr_bwd: in u, G;         out du (over G)
-  static constexpr int NT = 2, NP = 0, BPI = 2, NS = 8, COLS = 32, NPW = 2, NOUT = 1, NG = 4;
+  static constexpr int NT = 2, NP = 0, BPI = 2, NS = 8, COLS = 32, NPW = 2, NOUT = 1, NG = 3;
   static constexpr int TU = 0, TG = 1;
   static constexpr bool BWD = true, MIX = false;
 };
@@ -83,15 +83,19 @@ struct Cfg<3> {  // mix bwd: in q, k, v, dy;  out dq (over dy), dk (over k), dv 
 template <int OP>
 struct Stage {
   using C = Cfg<OP>;
-  static constexpr int kTPB = C::NT + C::NP;                  // tiles per block
+  // Each d-tensor of an item occupies one region [2 halves][16*BPI tokens][128 B]
+  // (one TMA box per 64-channel half); block k of it starts k*2 KiB into each half.
+  static constexpr int kTPB = C::NT + C::NP;                  // regions (tensors) per item
+  static constexpr int kHS = C::BPI * kHalf;                  // half stride inside a region
   static constexpr int kA = C::BPI * kTPB * kTile;            // decay box [16*BPI tokens][8 heads] bf16
   static constexpr int kL = kA + 256 * C::BPI;                // transfer tile L_t per block (512 B)
   static constexpr int kG = kL + 512 * C::BPI;                // g_t[16] fp32 per block
   static constexpr int kR = kG + 64 * C::BPI;                 // r_t[16] fp32 per block
   static constexpr int kRaw = kR + 64 * C::BPI;
   static constexpr int kBytes = (kRaw + 1023) / 1024 * 1024;
+  static __device__ __forceinline__ uint8_t* region(uint8_t* st, int x) { return st + x * (C::BPI * kTile); }
   static __device__ __forceinline__ uint8_t* tile(uint8_t* st, int k, int x) {
-    return st + (k * kTPB + x) * kTile;
+    return region(st, x) + k * kHalf;
   }
 };
 
@@ -218,15 +222,21 @@ __device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
   return __uint_as_float(r);
 }
-// diagnostics: %globaltimer stamp of event ev for item j of CTA 0 (swr_set_trace)
+// diagnostics: clock64 stamp (SM cycles) of event ev for item j of CTA 0 (swr_set_trace)
 // events: 0 producer got stage, 1 producer issued TMA, 2 prep saw full, 3 prep done,
 // 4 mma saw full+prepped, 5 mma issued, 6 mma marked ready, 7 epilogue saw ready,
 // 8 epilogue done (before store), 9 store committed, 10 own stage released
 __device__ __forceinline__ void trace(const Params& p, int64_t j, int ev) {
   if (p.trace != nullptr && blockIdx.x == 0 && j < p.trace_n) {
+    p.trace[j * 16 + ev] = clock64();  // SM cycles (all roles share the SM clock)
+  }
+}
+// diagnostics: per-CTA %globaltimer span (ns) after the per-item area: slot 16*n + 2*cta + e
+__device__ __forceinline__ void trace_cta(const Params& p, int e) {
+  if (p.trace != nullptr) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    p.trace[j * 16 + ev] = t;
+    p.trace[16 * p.trace_n + 2 * blockIdx.x + e] = t;
   }
 }
 __device__ __forceinline__ void tmem_wait_ld() {
@@ -239,9 +249,10 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
   return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
          ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (layout << 61);
 }
-// A = u_t^T from a TMA tile: MN-major, SWIZZLE_128B; 64-channel halves 2048 B apart
-// (LBO), 8-token row groups 1024 B apart (SBO).
-__device__ __forceinline__ uint64_t desc_A(uint32_t saddr) { return sdesc(saddr, kHalf, 1024, 2); }
+// A = u_t^T from a TMA tile: MN-major, SWIZZLE_128B; 64-channel halves HS bytes
+// apart (LBO), 8-token row groups 1024 B apart (SBO).
+template <int HS>
+__device__ __forceinline__ uint64_t desc_A(uint32_t saddr) { return sdesc(saddr, HS, 1024, 2); }
 // The 16x16 transfer tile L_t is stored ONCE, column-major in 8x8 core matrices:
 // element L[i][j] at byte (j/8)*256 + (i/8)*128 + (j%8)*16 + (i%8)*2, i.e. each
 // column j is 32 contiguous-per-core-row bytes written by one lane.
@@ -258,9 +269,10 @@ constexpr uint32_t kIdescBk = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | 
 constexpr uint32_t kIdescBmn = kIdescBk | (1u << 16);
 
 // byte offset of element (token i, channel c) inside a 4 KiB swizzled tile
+template <int HS>
 __device__ __forceinline__ uint32_t tile_off(int i, int c) {
   const int half = c >> 6, cc = c & 63;
-  return half * kHalf + i * 128 + ((((cc >> 3) ^ (i & 7))) << 4) + ((cc & 7) << 1);
+  return half * HS + i * 128 + ((((cc >> 3) ^ (i & 7))) << 4) + ((cc & 7) << 1);
 }
 // byte offset of L[i][j] in the transfer tile (see desc_Bk / desc_Bmn)
 __device__ __forceinline__ uint32_t ltile_off(int i, int j) {
@@ -363,6 +375,7 @@ __device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
 // Store 16 per-token values of this thread's channel c into a swizzled tile as
 // bf16 pairs: lanes (c, c^1) swap halves so every store is a 4-byte word and
 // the two rows of a warp instruction (i, i^4) fall in disjoint banks.
+template <int HS>
 __device__ __forceinline__ void store_col16(uint8_t* tile, int c, int lane, const float (&x)[16]) {
   const bool odd = lane & 1;
 #pragma unroll
@@ -372,9 +385,9 @@ __device__ __forceinline__ void store_col16(uint8_t* tile, int c, int lane, cons
     const float send = odd ? x[i] : x[i2];
     const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
     if (!odd)
-      *reinterpret_cast<uint32_t*>(tile + tile_off(i, c)) = pack_bf2(x[i], recv);
+      *reinterpret_cast<uint32_t*>(tile + tile_off<HS>(i, c)) = pack_bf2(x[i], recv);
     else
-      *reinterpret_cast<uint32_t*>(tile + tile_off(i2, c - 1)) = pack_bf2(recv, x[i2]);
+      *reinterpret_cast<uint32_t*>(tile + tile_off<HS>(i2, c - 1)) = pack_bf2(recv, x[i2]);
   }
 }
 
@@ -424,6 +437,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
   constexpr int kUsers = C::BWD ? 3 : 2;
 
   if (threadIdx.x == 0) {
+    trace_cta(p, 0);
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&prepped[s], 1);
@@ -465,13 +479,10 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
         const int tt = (int)(cur.m * BPI * kEll);
         mbar_expect_tx(&full[rg.s], BPI * C::NT * kTile + 256 * BPI);
 #pragma unroll
-        for (int k = 0; k < BPI; ++k) {
-#pragma unroll
-          for (int x = 0; x < C::NT; ++x) {
-            uint8_t* dst = S::tile(st, k, x);
-            tma_load_4d(dst, &maps.in[x], &full[rg.s], 0, cur.h, tt + k * kEll, cur.b);
-            tma_load_4d(dst + kHalf, &maps.in[x], &full[rg.s], 64, cur.h, tt + k * kEll, cur.b);
-          }
+        for (int x = 0; x < C::NT; ++x) {  // one box per 64-channel half: 16*BPI tokens
+          uint8_t* dst = S::region(st, x);
+          tma_load_4d(dst, &maps.in[x], &full[rg.s], 0, cur.h, tt, cur.b);
+          tma_load_4d(dst + S::kHS, &maps.in[x], &full[rg.s], 64, cur.h, tt, cur.b);
         }
         tma_load_3d(st + S::kA, &maps.a, &full[rg.s], cur.h & ~7, tt, cur.b);
         trace(p, j, 1);
@@ -503,9 +514,9 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
           for (int k = 0; k < BPI; ++k) {
             const uint32_t d = tmem_base + (uint32_t)(ri.s * kItemCols + k * C::COLS);
             const uint32_t lt = su32(st + S::kL + 512 * k);
-            umma_bf16(d, desc_A(su32(S::tile(st, k, C::TU))), desc_Bmn(lt), kIdescBmn);  // w^T
+            umma_bf16(d, desc_A<S::kHS>(su32(S::tile(st, k, C::TU))), desc_Bmn(lt), kIdescBmn);  // w^T
             if constexpr (C::BWD)  // lambda^T
-              umma_bf16(d + 16, desc_A(su32(S::tile(st, k, C::TG))), desc_Bk(lt), kIdescBk);
+              umma_bf16(d + 16, desc_A<S::kHS>(su32(S::tile(st, k, C::TG))), desc_Bk(lt), kIdescBk);
           }
           umma_commit(&mmad[ri.s]);
           trace(p, ji, 5);
@@ -544,17 +555,12 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
         const bool halo = cur.gi < W.g0 || cur.gi >= W.g1;
         if (!halo) {
           uint8_t* st = smem + rg.s * S::kBytes;
-          const int64_t t0 = cur.m * BPI;
+          const int tt = (int)(cur.m * BPI * kEll);
 #pragma unroll
-          for (int k = 0; k < BPI; ++k) {
-            if (t0 + k >= nb) break;
-            const int tt = (int)((t0 + k) * kEll);
-#pragma unroll
-            for (int x = 0; x < C::NOUT; ++x) {
-              const int tile = (OP == 0) ? 0 : (OP == 1) ? 1 : (OP == 2) ? 0 : (x == 0 ? 3 : x);
-              tma_store_4d(&maps.out[x], S::tile(st, k, tile), 0, cur.h, tt, cur.b);
-              tma_store_4d(&maps.out[x], S::tile(st, k, tile) + kHalf, 64, cur.h, tt, cur.b);
-            }
+          for (int x = 0; x < C::NOUT; ++x) {  // rows past L are clipped by TMA
+            const int reg = (OP == 0) ? 0 : (OP == 1) ? 1 : (OP == 2) ? 0 : (x == 0 ? 3 : x);
+            tma_store_4d(&maps.out[x], S::region(st, reg), 0, cur.h, tt, cur.b);
+            tma_store_4d(&maps.out[x], S::region(st, reg) + S::kHS, 64, cur.h, tt, cur.b);
           }
           bulk_commit();
           trace(p, j, 9);
@@ -627,13 +633,12 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
       if constexpr (C::MIX) {
         // pre-gates in the swizzled tile layout (elementwise, layout-agnostic), each
         // rounded once to bf16: u^ = k (.) v; backward also G = dy (.) q
-#pragma unroll
-        for (int k = 0; k < BPI; ++k) {
-          const uint4* K4 = reinterpret_cast<const uint4*>(S::tile(st, k, 1));
-          const uint4* V4 = reinterpret_cast<const uint4*>(S::tile(st, k, 2));
-          uint4* U4 = reinterpret_cast<uint4*>(S::tile(st, k, C::TU));
+        {
+          const uint4* K4 = reinterpret_cast<const uint4*>(S::region(st, 1));
+          const uint4* V4 = reinterpret_cast<const uint4*>(S::region(st, 2));
+          uint4* U4 = reinterpret_cast<uint4*>(S::region(st, C::TU));
 #pragma unroll 2
-          for (int v = lane; v < kTile / 16; v += 32) {
+          for (int v = lane; v < BPI * kTile / 16; v += 32) {
             const uint4 kk = K4[v], vv = V4[v];
             uint4 o;
             const uint32_t* ka = &kk.x;
@@ -647,8 +652,8 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
             }
             U4[v] = o;
             if constexpr (C::BWD) {
-              uint4* Q4 = reinterpret_cast<uint4*>(S::tile(st, k, 0));  // G overwrites q
-              const uint4* D4 = reinterpret_cast<const uint4*>(S::tile(st, k, 3));
+              uint4* Q4 = reinterpret_cast<uint4*>(S::region(st, 0));  // G overwrites q
+              const uint4* D4 = reinterpret_cast<const uint4*>(S::region(st, 3));
               const uint4 qq = Q4[v], dd = D4[v];
               const uint32_t* qa = &qq.x;
               const uint32_t* da = &dd.x;
@@ -746,12 +751,12 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
               const uint8_t* t_v = S::tile(st, k, 2);
 #pragma unroll
               for (int i = 0; i < 16; ++i) {  // post-gate with residual: y = q x~ + v
-                const uint32_t o = tile_off(i, c);
+                const uint32_t o = tile_off<S::kHS>(i, c);
                 out[i] = fmaf(bf(t_out, o), out[i], bf(t_v, o));
               }
             }
             __syncwarp();
-            store_col16(t_out, c, lane, out);
+            store_col16<S::kHS>(t_out, c, lane, out);
             if (t == nb - 1 && p.carry_out) p.carry_out[co] = w[15];
           } else {
             float lam[16];
@@ -777,7 +782,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
             if (t == 0 && p.mu_out) p.mu_out[co] = g[0] * lam[0];  // a_0[0] lambda_0[0]
             __syncwarp();
             if constexpr (!C::MIX) {
-              store_col16(S::tile(st, k, 1), c, lane, du);  // du over G
+              store_col16<S::kHS>(S::tile(st, k, 1), c, lane, du);  // du over G
             } else {
               uint8_t* t_dy = S::tile(st, k, 3);
               uint8_t* t_k = S::tile(st, k, 1);
@@ -785,21 +790,21 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
               float o16[16], dyv[16];
 #pragma unroll
               for (int i = 0; i < 16; ++i) {  // dq = dy x~
-                const uint32_t o = tile_off(i, c);
+                const uint32_t o = tile_off<S::kHS>(i, c);
                 dyv[i] = bf(t_dy, o);
                 o16[i] = dyv[i] * fmaf(g[i], vprev, w[i]);
               }
               __syncwarp();
-              store_col16(t_dy, c, lane, o16);
+              store_col16<S::kHS>(t_dy, c, lane, o16);
 #pragma unroll
               for (int i = 0; i < 16; ++i) {  // dv = du^ k + dy ; dk = du^ v
-                const uint32_t o = tile_off(i, c);
+                const uint32_t o = tile_off<S::kHS>(i, c);
                 o16[i] = fmaf(du[i], bf(t_k, o), dyv[i]);
                 du[i] *= bf(t_v, o);
               }
               __syncwarp();
-              store_col16(t_v, c, lane, o16);
-              store_col16(t_k, c, lane, du);
+              store_col16<S::kHS>(t_v, c, lane, o16);
+              store_col16<S::kHS>(t_k, c, lane, du);
             }
             // da: transpose-reduce over the warp's 32 channels, partials to SMEM
             int tok = 0;
@@ -840,6 +845,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (threadIdx.x == 0) trace_cta(p, 1);
   if (warp == kMmaW) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "r"(kTmemCols)
@@ -864,10 +870,10 @@ static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   return fn;
 }
 
-static bool map_dtensor(CUtensorMap* m, const void* ptr, const Params& p) {
+static bool map_dtensor(CUtensorMap* m, const void* ptr, const Params& p, int rows) {
   cuuint64_t dims[4] = {(cuuint64_t)p.D, (cuuint64_t)p.H, (cuuint64_t)p.L, (cuuint64_t)p.B};
   cuuint64_t strides[3] = {(cuuint64_t)p.sx_h * 2, (cuuint64_t)p.sx_l * 2, (cuuint64_t)p.sx_b * 2};
-  cuuint32_t box[4] = {64, 1, 16, 1};
+  cuuint32_t box[4] = {64, 1, (cuuint32_t)rows, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return encoder()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -900,9 +906,9 @@ static cudaError_t launch_op(const Params& p, cudaStream_t st, int sms) {
       outs[0] = p.dq; outs[1] = p.dk; outs[2] = p.dv; nin = 4; nout = 3;
   }
   for (int i = 0; i < nin; ++i)
-    if (!map_dtensor(&maps.in[i], ins[i], p)) return cudaErrorNotSupported;
+    if (!map_dtensor(&maps.in[i], ins[i], p, 16 * Cfg<OP>::BPI)) return cudaErrorNotSupported;
   for (int i = 0; i < nout; ++i)
-    if (!map_dtensor(&maps.out[i], outs[i], p)) return cudaErrorNotSupported;
+    if (!map_dtensor(&maps.out[i], outs[i], p, 16 * Cfg<OP>::BPI)) return cudaErrorNotSupported;
   if (!map_decay(&maps.a, p.a, p, Cfg<OP>::BPI)) return cudaErrorNotSupported;
 
   constexpr int smem = smem_bytes<OP>();

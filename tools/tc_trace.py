@@ -9,7 +9,7 @@ from swr_inputs import swr_inputs, mix_inputs
 EV = ["prod_got", "prod_issued", "prep_full", "prep_done", "mma_full", "mma_issued", "ready",
       "epi_ready", "epi_done", "store_commit", "released"]
 op = sys.argv[1] if len(sys.argv) > 1 else "fwd"
-N = 240
+N = 64
 P.set_path(P.SWR_PATH_TC)
 if op in ("fwd", "bwd"):
     g = {k: v.cuda() for k, v in swr_inputs(8, 4096, 16, 128, seed=1).items()}
@@ -20,7 +20,7 @@ else:
         lambda: P.phalanx_mix_bwd(g["q"], g["k"], g["v"], g["a"], g["dy"]))
 for _ in range(5):
     run()
-buf = torch.zeros(N * 16, dtype=torch.int64, device="cuda")
+buf = torch.zeros(N * 16 + 2 * 160, dtype=torch.int64, device="cuda")
 _lib.set_trace(buf.data_ptr(), N)
 flush = torch.empty(64 << 20, device="cuda")
 flush.zero_()
@@ -29,21 +29,27 @@ e0.record(); run(); e1.record()
 torch.cuda.synchronize()
 _lib.set_trace(None, 0)
 print(op, "kernel ms", e0.elapsed_time(e1))
-t = buf.cpu().numpy().reshape(N, 16)[:, :len(EV)].astype(np.int64)
+allb = buf.cpu().numpy()
+span = allb[N * 16:].reshape(-1, 2)
+span = span[span[:, 0] > 0]
+st0 = span[:, 0].min()
+dur = (span[:, 1] - span[:, 0]) / 1e3
+print(f"CTAs {len(span)}: start spread {(span[:,0].max()-st0)/1e3:.1f} us, span min/med/max {dur.min():.1f}/{np.median(dur):.1f}/{dur.max():.1f} us, last end {(span[:,1].max()-st0)/1e3:.1f} us")
+t = allb[:N * 16].reshape(N, 16)[:, :len(EV)].astype(np.int64)
 valid = t[:, 0] > 0
 t0 = t[valid][:, 0].min()
 rel = np.where(t > 0, t - t0, -1)
 print("item " + " ".join(f"{e[:10]:>10}" for e in EV))
-for j in list(range(0, 24)) + list(range(100, 112)) + list(range(200, 212)):
+for j in range(0, 0):
     if j < N and valid[j]:
         print(f"{j:4d} " + " ".join(f"{x:10d}" for x in rel[j]))
 # steady-state averages of stage-to-stage latencies (items 40..200)
-sl = slice(40, 200)
+sl = slice(8, 48)
 def d(a, b):
     m = (t[sl, a] > 0) & (t[sl, b] > 0)
     return float(np.median(t[sl, b][m] - t[sl, a][m])) if m.any() else float("nan")
-print("median latencies (ns): prod_issued->prep_full", d(1, 2), " prep", d(2, 3), " prep_done->mma_full", d(3, 4),
+print("median latencies (cycles): prod_issued->prep_full", d(1, 2), " prep", d(2, 3), " prep_done->mma_full", d(3, 4),
       " mma_issued->ready", d(5, 6), " ready->epi_ready", d(6, 7), " epi", d(7, 8), " epi_done->commit", d(8, 9),
       " prod_got->released(own)", d(0, 10))
 per = np.diff(t[sl, 1])
-print("producer issue period ns (median)", float(np.median(per)), " epi_ready period", float(np.median(np.diff(t[sl, 7][t[sl,7]>0]))))
+print("producer issue period cycles (median)", float(np.median(per)), " epi_ready period", float(np.median(np.diff(t[sl, 7][t[sl,7]>0]))))

@@ -41,59 +41,68 @@ constexpr int kHalf = 2048;      // one 64-channel half: 16 rows x 128 B, 128B-s
 
 // ---------------------------------------------------------------------------
 // per-op configuration.  A pipeline "item" is BPI consecutive 16-token blocks
-// of one (b, h) line (the last item of a line may be partial).
-//   NT   TMA-loaded input tiles per block    NP   extra prep-computed A tiles per block
-//   BPI  blocks per item                     NS   pipeline stages (items)
-//   COLS TMEM columns per block              NPW  prep warps (each owns whole items)
+// of one (b, h) line (the last item of a line may be partial).  Three rings:
+//   input  (NI stages, SMEM): TMA load -> prep -> MMA.  For the SWR ops the
+//          input tiles are consumed by the MMA alone, so a stage is released
+//          when its MMAs complete; the mixer epilogue also reads q/k/v/dy, so
+//          there the epilogue releases it.
+//   work   (NW slots): the item's TMEM accumulators + g_t/r_t, held from prep
+//          until the epilogues of the item and of its neighbours have read them.
+//   output (NO slots, SMEM): epilogue -> TMA store.
+//   NT   TMA-loaded input regions (d-tensors)  NP   extra prep-computed A regions
+//   COLS TMEM columns per block                NPW  prep warps (each owns whole items)
 //   NG   epilogue groups of 4 warps
-// Liveness: loading item x needs item x-NS released; that release needs the
-// store of the next item (store lag 1), the neighbours' epilogues and their
-// readiness (MMA of the next item backward), so NS >= BWD + 4 suffices; the
-// rings are sized deeper to cover latency.
 // ---------------------------------------------------------------------------
 template <int OP>
 struct Cfg;
 template <>
-struct Cfg<0> {  // swr_fwd: in u;            out x  (over u)
-  static constexpr int NT = 1, NP = 0, BPI = 4, NS = 8, COLS = 16, NPW = 4, NOUT = 1, NG = 3;
-  static constexpr int TU = 0, TG = 0;  // A-operand tiles of W and lambda
+struct Cfg<0> {  // swr_fwd: in u;  out x
+  static constexpr int NT = 1, NP = 0, BPI = 4, NI = 7, NW = 8, NO = 4, COLS = 16, NPW = 4, NOUT = 1, NG = 3;
+  static constexpr int TU = 0, TG = 0;  // A-operand regions of W and lambda
   static constexpr bool BWD = false, MIX = false;
 };
 template <>
-struct Cfg<1> {  // swr_bwd: in u, G;         out du (over G)
-  static constexpr int NT = 2, NP = 0, BPI = 2, NS = 8, COLS = 32, NPW = 2, NOUT = 1, NG = 3;
+struct Cfg<1> {  // swr_bwd: in u, G;  out du
+  static constexpr int NT = 2, NP = 0, BPI = 2, NI = 9, NW = 8, NO = 4, COLS = 32, NPW = 2, NOUT = 1, NG = 3;
   static constexpr int TU = 0, TG = 1;
   static constexpr bool BWD = true, MIX = false;
 };
 template <>
-struct Cfg<2> {  // mix fwd: in q, k, v;      out y  (over q);  prep u^ = k v (over k)
-  static constexpr int NT = 3, NP = 0, BPI = 2, NS = 7, COLS = 16, NPW = 4, NOUT = 1, NG = 3;
+struct Cfg<2> {  // mix fwd: in q, k, v;  out y;  prep u^ = k v (over k)
+  static constexpr int NT = 3, NP = 0, BPI = 2, NI = 6, NW = 8, NO = 4, COLS = 16, NPW = 4, NOUT = 1, NG = 3;
   static constexpr int TU = 1, TG = 0;
   static constexpr bool BWD = false, MIX = true;
 };
 template <>
-struct Cfg<3> {  // mix bwd: in q, k, v, dy;  out dq (over dy), dk (over k), dv (over v)
-  //                prep u^ = k v (tile 4), G = dy q (over q)
-  static constexpr int NT = 4, NP = 1, BPI = 1, NS = 8, COLS = 32, NPW = 4, NOUT = 3, NG = 3;
+struct Cfg<3> {  // mix bwd: in q, k, v, dy;  out dq, dk, dv;  prep u^ = k v (region 4), G = dy q (over q)
+  static constexpr int NT = 4, NP = 1, BPI = 1, NI = 7, NW = 8, NO = 3, COLS = 32, NPW = 4, NOUT = 3, NG = 3;
   static constexpr int TU = 4, TG = 0;
   static constexpr bool BWD = true, MIX = true;
 };
 
-// stage layout (bytes; every 4 KiB tile 1024-aligned for the 128B swizzle atoms)
+// SMEM layout (bytes; every 4 KiB tile 1024-aligned for the 128B swizzle atoms).
+// A d-tensor of an item occupies one region [2 halves][16*BPI tokens][128 B] (one
+// TMA box per 64-channel half); block k of it starts k*2 KiB into each half.
 template <int OP>
 struct Stage {
   using C = Cfg<OP>;
-  // Each d-tensor of an item occupies one region [2 halves][16*BPI tokens][128 B]
-  // (one TMA box per 64-channel half); block k of it starts k*2 KiB into each half.
-  static constexpr int kTPB = C::NT + C::NP;                  // regions (tensors) per item
-  static constexpr int kHS = C::BPI * kHalf;                  // half stride inside a region
-  static constexpr int kA = C::BPI * kTPB * kTile;            // decay box [16*BPI tokens][8 heads] bf16
-  static constexpr int kL = kA + 256 * C::BPI;                // transfer tile L_t per block (512 B)
-  static constexpr int kG = kL + 512 * C::BPI;                // g_t[16] fp32 per block
-  static constexpr int kR = kG + 64 * C::BPI;                 // r_t[16] fp32 per block
-  static constexpr int kRaw = kR + 64 * C::BPI;
-  static constexpr int kBytes = (kRaw + 1023) / 1024 * 1024;
-  static __device__ __forceinline__ uint8_t* region(uint8_t* st, int x) { return st + x * (C::BPI * kTile); }
+  static constexpr int kRegion = C::BPI * kTile;
+  static constexpr int kHS = C::BPI * kHalf;                   // half stride inside a region
+  // input stage
+  static constexpr int kA = (C::NT + C::NP) * kRegion;         // decay box [16*BPI tokens][8 heads] bf16
+  static constexpr int kL = kA + 256 * C::BPI;                 // transfer tile L_t per block (512 B)
+  static constexpr int kInRaw = kL + 512 * C::BPI;
+  static constexpr int kIn = (kInRaw + 1023) / 1024 * 1024;
+  // output slot
+  static constexpr int kOut = C::NOUT * kRegion;
+  // work-slot aux: g_t[16], r_t[16] fp32 per block
+  static constexpr int kAux = C::BPI * 128;
+  static constexpr int kInBase = 0;
+  static constexpr int kOutBase = C::NI * kIn;
+  static constexpr int kAuxBase = kOutBase + C::NO * kOut;
+  static constexpr int kScratch = kAuxBase + C::NW * kAux;     // barriers + da partials (4 KiB)
+  static constexpr int kBytes = kScratch + 4096;
+  static __device__ __forceinline__ uint8_t* region(uint8_t* st, int x) { return st + x * kRegion; }
   static __device__ __forceinline__ uint8_t* tile(uint8_t* st, int k, int x) {
     return region(st, x) + k * kHalf;
   }
@@ -101,8 +110,7 @@ struct Stage {
 
 template <int OP>
 constexpr int smem_bytes() {
-  // stages + barriers/scratch (4 KiB) + 1 KiB alignment slack
-  return Cfg<OP>::NS * Stage<OP>::kBytes + 4096 + 1024;
+  return Stage<OP>::kBytes + 1024;  // + alignment slack
 }
 
 struct Maps {
@@ -374,77 +382,94 @@ __device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
 
 // Store 16 per-token values of this thread's channel c into a swizzled tile as
 // bf16 pairs: lanes (c, c^1) swap halves so every store is a 4-byte word and
-// the two rows of a warp instruction (i, i^4) fall in disjoint banks.
+// the two rows of a warp instruction (i, i^4) fall in disjoint banks.  Even
+// lanes write (row i, channels c, c+1), odd lanes (row i^4, channels c-1, c);
+// branch-free (selects), so the warp issues each store once.
 template <int HS>
 __device__ __forceinline__ void store_col16(uint8_t* tile, int c, int lane, const float (&x)[16]) {
   const bool odd = lane & 1;
+  const int ce = c & ~1;  // even channel of the pair
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     if (i & 4) continue;
     const int i2 = i ^ 4;
     const float send = odd ? x[i] : x[i2];
     const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
-    if (!odd)
-      *reinterpret_cast<uint32_t*>(tile + tile_off<HS>(i, c)) = pack_bf2(x[i], recv);
-    else
-      *reinterpret_cast<uint32_t*>(tile + tile_off<HS>(i2, c - 1)) = pack_bf2(recv, x[i2]);
+    const float lo = odd ? recv : x[i];
+    const float hi = odd ? x[i2] : recv;
+    const uint32_t off = odd ? tile_off<HS>(i2, ce) : tile_off<HS>(i, ce);
+    *reinterpret_cast<uint32_t*>(tile + off) = pack_bf2(lo, hi);
   }
 }
 
 // ---------------------------------------------------------------------------
 // the kernel
 //
-// Per item j (BPI blocks of one (b, h)) the barriers are
-//   full[s]     TMA bytes landed                      (producer, tx count)
-//   prepped[s]  L tiles, g, r, pre-gates in SMEM      (prep warp)
-//   mmad[s]     tcgen05 MMAs of item j complete        (tcgen05.commit)
-//   ready[s]    MMAs of every item whose TMEM item j's epilogue reads are done
-//               (j-1, j; backward also j+1)            (MMA warp)
-//   outready[s] outputs of item j written to SMEM     (epilogue group leader)
-//   empty[s]    stage free again: store read done (store warp) + the neighbour
-//               items that read its TMEM / g (next; backward also previous)
+// Barriers (ring sizes in Cfg):
+//   full[NI]     TMA bytes of the input stage landed            (producer, tx count)
+//   prepped[NI]  L tiles (input stage) + g/r (work slot) + pre-gates written (prep)
+//   inempty[NI]  input stage free: MMAs retired (SWR) / epilogue done (mixer)
+//   mmad[NW]     tcgen05 MMAs of the item complete               (tcgen05.commit)
+//   ready[NW]    MMAs of every item whose TMEM the epilogue reads are complete:
+//                j-1, j (backward also j+1)                      (MMA warp)
+//   wfree[NW]    work slot free: the item's epilogue and the neighbours that read
+//                its TMEM / g are done (next; backward also previous)
+//   ofull[NO]    outputs in the output slot                      (epilogue leader)
+//   oempty[NO]   output slot free: TMA store has read it         (store warp)
 // ---------------------------------------------------------------------------
 template <int OP>
 __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
     swr_tc_kernel(const __grid_constant__ Maps maps, const Params p) {
   using C = Cfg<OP>;
   using S = Stage<OP>;
-  constexpr int NS = C::NS, NG = C::NG, BPI = C::BPI;
+  constexpr int NI = C::NI, NW = C::NW, NO = C::NO, NG = C::NG, BPI = C::BPI;
   constexpr int kEpi = 128;
   constexpr int kItemCols = BPI * C::COLS;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int kPrepW0 = 4 * NG, kProdW = kPrepW0 + C::NPW, kMmaW = kProdW + 1, kStoreW = kMmaW + 1;
 
-  // 1024-aligned stage base for the 128B-swizzle atoms.  Offset the __shared__
-  // array itself (not a uintptr_t round trip) so every access stays LDS/STS.
+  // 1024-aligned base for the 128B-swizzle atoms.  Offset the __shared__ array
+  // itself (not a uintptr_t round trip) so every access stays LDS/STS.
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* scratch = smem + NS * S::kBytes;
+  uint8_t* sin = smem + S::kInBase;
+  uint8_t* sout = smem + S::kOutBase;
+  uint8_t* aux = smem + S::kAuxBase;
+  uint8_t* scratch = smem + S::kScratch;
   uint64_t* full = reinterpret_cast<uint64_t*>(scratch);
-  uint64_t* prepped = full + NS;
-  uint64_t* mmad = prepped + NS;
-  uint64_t* ready = mmad + NS;
-  uint64_t* outready = ready + NS;
-  uint64_t* empty = outready + NS;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(empty + NS);
+  uint64_t* prepped = full + NI;
+  uint64_t* inempty = prepped + NI;
+  uint64_t* mmad = inempty + NI;
+  uint64_t* ready = mmad + NW;
+  uint64_t* wfree = ready + NW;
+  uint64_t* ofull = wfree + NW;
+  uint64_t* oempty = ofull + NO;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(oempty + NO);
   float* red = reinterpret_cast<float*>(scratch + 1024);  // [NG][4 warps][16*BPI] da partials
 
-  constexpr int kTmemCols = (NS * kItemCols <= 32) ? 32 : (NS * kItemCols <= 64) ? 64
-                          : (NS * kItemCols <= 128) ? 128 : (NS * kItemCols <= 256) ? 256 : 512;
-  static_assert(NS * kItemCols <= 512, "TMEM budget");
-  static_assert(NS >= (C::BWD ? 1 : 0) + 4, "pipeline depth (deadlock freedom)");
-  static_assert(6 * NS * 8 + 8 <= 1024 && NG * 4 * 16 * BPI * 4 <= 3072, "scratch budget");
+  constexpr int kTmemCols = (NW * kItemCols <= 32) ? 32 : (NW * kItemCols <= 64) ? 64
+                          : (NW * kItemCols <= 128) ? 128 : (NW * kItemCols <= 256) ? 256 : 512;
+  static_assert(NW * kItemCols <= 512, "TMEM budget");
+  static_assert(NW >= 4 && NI >= 3 && NO >= 2, "ring depth (deadlock freedom)");
+  static_assert((3 * NI + 3 * NW + 2 * NO) * 8 + 8 <= 1024 && NG * 4 * 16 * BPI * 4 <= 3072, "scratch budget");
+  static_assert(S::kBytes + 1024 <= 227 * 1024, "shared memory budget");
   constexpr int kUsers = C::BWD ? 3 : 2;
 
   if (threadIdx.x == 0) {
     trace_cta(p, 0);
-    for (int s = 0; s < NS; ++s) {
+    for (int s = 0; s < NI; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&prepped[s], 1);
+      mbar_init(&inempty[s], 1);
+    }
+    for (int s = 0; s < NW; ++s) {
       mbar_init(&mmad[s], 1);
       mbar_init(&ready[s], 1);
-      mbar_init(&outready[s], 1);
-      mbar_init(&empty[s], kUsers);
+      mbar_init(&wfree[s], kUsers);
+    }
+    for (int s = 0; s < NO; ++s) {
+      mbar_init(&ofull[s], 1);
+      mbar_init(&oempty[s], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -470,38 +495,40 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
     if (lane == 0 && n_items > 0) {
       Cursor cur;
       cur.init(W.first, nbi, H);
-      Ring<NS> rg;
-      rg.init(0);
+      Ring<NI> ri;
+      ri.init(0);
       for (int64_t j = 0; j < n_items; ++j) {
-        mbar_wait(&empty[rg.s], rg.ph ^ 1);
+        mbar_wait(&inempty[ri.s], ri.ph ^ 1);
         trace(p, j, 0);
-        uint8_t* st = smem + rg.s * S::kBytes;
+        uint8_t* st = sin + ri.s * S::kIn;
         const int tt = (int)(cur.m * BPI * kEll);
-        mbar_expect_tx(&full[rg.s], BPI * C::NT * kTile + 256 * BPI);
+        mbar_expect_tx(&full[ri.s], C::NT * S::kRegion + 256 * BPI);
 #pragma unroll
         for (int x = 0; x < C::NT; ++x) {  // one box per 64-channel half: 16*BPI tokens
           uint8_t* dst = S::region(st, x);
-          tma_load_4d(dst, &maps.in[x], &full[rg.s], 0, cur.h, tt, cur.b);
-          tma_load_4d(dst + S::kHS, &maps.in[x], &full[rg.s], 64, cur.h, tt, cur.b);
+          tma_load_4d(dst, &maps.in[x], &full[ri.s], 0, cur.h, tt, cur.b);
+          tma_load_4d(dst + S::kHS, &maps.in[x], &full[ri.s], 64, cur.h, tt, cur.b);
         }
-        tma_load_3d(st + S::kA, &maps.a, &full[rg.s], cur.h & ~7, tt, cur.b);
+        tma_load_3d(st + S::kA, &maps.a, &full[ri.s], cur.h & ~7, tt, cur.b);
         trace(p, j, 1);
         cur.next(nbi, H);
-        rg.next();
+        ri.next();
       }
     }
   } else if (warp == kMmaW) {
-    // ===================== MMA issuer + readiness =====================
-    // One thread polls two queues without blocking on either: issue the next
-    // item's MMAs once its operands have landed, and retire completed items in
-    // issue order (tcgen05 ops complete in order).  ready[j] is arrived once
-    // every MMA item j's epilogue reads is complete: j-1, j (backward also j+1).
-    // MMA latency therefore costs pipeline depth, not throughput.
+    // ===================== MMA issuer + retire + readiness =====================
+    // One thread polls without blocking: issue the next item's MMAs once its
+    // operands landed, retire completed items in issue order (tcgen05 ops complete
+    // in order) -- which frees their input stage for the SWR ops -- and mark items
+    // ready once every MMA their epilogue reads is retired.
     if (lane == 0 && n_items > 0) {
       constexpr int kBack = C::BWD ? 1 : 0;
-      Ring<NS> ri, rc, rr;  // next to issue, next to retire, next to mark ready
+      Ring<NI> ri, rci;     // input stage of the next item to issue / to retire
+      Ring<NW> rw, rcw, rr;  // work slot of the next item to issue / to retire / to mark ready
       ri.init(0);
-      rc.init(0);
+      rci.init(0);
+      rw.init(0);
+      rcw.init(0);
       rr.init(0);
       int64_t ji = 0, jc = 0, jr = 0;
       while (jr < n_items) {
@@ -509,27 +536,29 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
         if (ji < n_items && mbar_test(&full[ri.s], ri.ph) && mbar_test(&prepped[ri.s], ri.ph)) {
           tc_fence_after();
           trace(p, ji, 4);
-          uint8_t* st = smem + ri.s * S::kBytes;
+          uint8_t* st = sin + ri.s * S::kIn;
 #pragma unroll
           for (int k = 0; k < BPI; ++k) {
-            const uint32_t d = tmem_base + (uint32_t)(ri.s * kItemCols + k * C::COLS);
+            const uint32_t d = tmem_base + (uint32_t)(rw.s * kItemCols + k * C::COLS);
             const uint32_t lt = su32(st + S::kL + 512 * k);
             umma_bf16(d, desc_A<S::kHS>(su32(S::tile(st, k, C::TU))), desc_Bmn(lt), kIdescBmn);  // w^T
             if constexpr (C::BWD)  // lambda^T
               umma_bf16(d + 16, desc_A<S::kHS>(su32(S::tile(st, k, C::TG))), desc_Bk(lt), kIdescBk);
           }
-          umma_commit(&mmad[ri.s]);
+          umma_commit(&mmad[rw.s]);
           trace(p, ji, 5);
           ri.next();
+          rw.next();
           ++ji;
           progressed = true;
         }
-        if (jc < ji && mbar_test(&mmad[rc.s], rc.ph)) {
-          rc.next();
+        if (jc < ji && mbar_test(&mmad[rcw.s], rcw.ph)) {
+          if constexpr (!C::MIX) mbar_arrive(&inempty[rci.s]);  // operands consumed
+          rci.next();
+          rcw.next();
           ++jc;
           progressed = true;
         }
-        // items whose dependencies are retired
         while (jr < n_items && (jr + kBack < jc || (jc == n_items && jr < jc))) {
           tc_fence_before();
           mbar_arrive(&ready[rr.s]);
@@ -543,38 +572,32 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
     }
     __syncwarp();
   } else if (warp == kStoreW) {
-    // ===================== TMA store + stage release =====================
+    // ===================== TMA store + output-slot release =====================
     if (lane == 0 && n_items > 0) {
       Cursor cur;
       cur.init(W.first, nbi, H);
-      Ring<NS> rg;
-      rg.init(0);
-      int pend = -1;  // stage whose store may still be reading SMEM
+      Ring<NO> ro;
+      ro.init(0);
       for (int64_t j = 0; j < n_items; ++j) {
-        mbar_wait(&outready[rg.s], rg.ph);
+        mbar_wait(&ofull[ro.s], ro.ph);
         const bool halo = cur.gi < W.g0 || cur.gi >= W.g1;
         if (!halo) {
-          uint8_t* st = smem + rg.s * S::kBytes;
+          uint8_t* ot = sout + ro.s * S::kOut;
           const int tt = (int)(cur.m * BPI * kEll);
 #pragma unroll
           for (int x = 0; x < C::NOUT; ++x) {  // rows past L are clipped by TMA
-            const int reg = (OP == 0) ? 0 : (OP == 1) ? 1 : (OP == 2) ? 0 : (x == 0 ? 3 : x);
-            tma_store_4d(&maps.out[x], S::region(st, reg), 0, cur.h, tt, cur.b);
-            tma_store_4d(&maps.out[x], S::region(st, reg) + S::kHS, 64, cur.h, tt, cur.b);
+            tma_store_4d(&maps.out[x], S::region(ot, x), 0, cur.h, tt, cur.b);
+            tma_store_4d(&maps.out[x], S::region(ot, x) + S::kHS, 64, cur.h, tt, cur.b);
           }
           bulk_commit();
           trace(p, j, 9);
-          bulk_wait_read<1>();  // the previous item's store has read SMEM
-          if (pend >= 0) mbar_arrive(&empty[pend]);
-          pend = rg.s;
-        } else {
-          mbar_arrive(&empty[rg.s]);
+          bulk_wait_read<0>();
         }
+        mbar_arrive(&oempty[ro.s]);
         cur.next(nbi, H);
-        rg.next();
+        ro.next();
       }
       bulk_wait_all();
-      if (pend >= 0) mbar_arrive(&empty[pend]);
     }
   } else if (warp >= kPrepW0) {
     // ===================== prep: L tiles (Alg. 3), g, r, pre-gates =====================
@@ -583,12 +606,16 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
     const int hf = lane >> 4, col = lane & 15;
     Cursor cur;
     if (pw < n_items) cur.init(W.first + pw, nbi, H);
-    Ring<NS> rg;
-    rg.init(pw);
+    Ring<NI> ri;
+    Ring<NW> rw;
+    ri.init(pw);
+    rw.init(pw);
     for (int64_t j = pw; j < n_items; j += C::NPW) {
-      mbar_wait(&full[rg.s], rg.ph);
+      mbar_wait(&full[ri.s], ri.ph);
+      mbar_wait(&wfree[rw.s], rw.ph ^ 1);
       if (lane == 0) trace(p, j, 2);
-      uint8_t* st = smem + rg.s * S::kBytes;
+      uint8_t* st = sin + ri.s * S::kIn;
+      float* gr = reinterpret_cast<float*>(aux + rw.s * S::kAux);  // [BPI][g 16 | r 16]
 #pragma unroll
       for (int kb = 0; kb < BPI; kb += 2) {
         const int k = kb + hf;
@@ -619,10 +646,10 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
           hi.z = pack_bf2(Lc[12], Lc[13]); hi.w = pack_bf2(Lc[14], Lc[15]);
           *reinterpret_cast<uint4*>(l + ltile_off(0, col)) = lo;
           *reinterpret_cast<uint4*>(l + ltile_off(8, col)) = hi;
-          if constexpr (C::BWD) reinterpret_cast<float*>(st + S::kR + 64 * k)[col] = prod;  // r_t[j] = L[15][j]
+          if constexpr (C::BWD) gr[32 * k + 16 + col] = prod;  // r_t[j] = L[15][j]
           if (col == 0) {
             // g_t[i] = a_t[0] L_t[i][0] = a_t[0] ... a_t[i], fp32
-            float4* gp = reinterpret_cast<float4*>(st + S::kG + 64 * k);
+            float4* gp = reinterpret_cast<float4*>(gr + 32 * k);
             gp[0] = make_float4(a[0] * Lc[0], a[0] * Lc[1], a[0] * Lc[2], a[0] * Lc[3]);
             gp[1] = make_float4(a[0] * Lc[4], a[0] * Lc[5], a[0] * Lc[6], a[0] * Lc[7]);
             gp[2] = make_float4(a[0] * Lc[8], a[0] * Lc[9], a[0] * Lc[10], a[0] * Lc[11]);
@@ -633,50 +660,49 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
       if constexpr (C::MIX) {
         // pre-gates in the swizzled tile layout (elementwise, layout-agnostic), each
         // rounded once to bf16: u^ = k (.) v; backward also G = dy (.) q
-        {
-          const uint4* K4 = reinterpret_cast<const uint4*>(S::region(st, 1));
-          const uint4* V4 = reinterpret_cast<const uint4*>(S::region(st, 2));
-          uint4* U4 = reinterpret_cast<uint4*>(S::region(st, C::TU));
+        const uint4* K4 = reinterpret_cast<const uint4*>(S::region(st, 1));
+        const uint4* V4 = reinterpret_cast<const uint4*>(S::region(st, 2));
+        uint4* U4 = reinterpret_cast<uint4*>(S::region(st, C::TU));
 #pragma unroll 2
-          for (int v = lane; v < BPI * kTile / 16; v += 32) {
-            const uint4 kk = K4[v], vv = V4[v];
-            uint4 o;
-            const uint32_t* ka = &kk.x;
-            const uint32_t* va = &vv.x;
-            uint32_t* oa = &o.x;
+        for (int v = lane; v < S::kRegion / 16; v += 32) {
+          const uint4 kk = K4[v], vv = V4[v];
+          uint4 o;
+          const uint32_t* ka = &kk.x;
+          const uint32_t* va = &vv.x;
+          uint32_t* oa = &o.x;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 kf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ka[e]));
+            const float2 vf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&va[e]));
+            oa[e] = pack_bf2(kf.x * vf.x, kf.y * vf.y);
+          }
+          U4[v] = o;
+          if constexpr (C::BWD) {
+            uint4* Q4 = reinterpret_cast<uint4*>(S::region(st, 0));  // G overwrites q
+            const uint4* D4 = reinterpret_cast<const uint4*>(S::region(st, 3));
+            const uint4 qq = Q4[v], dd = D4[v];
+            const uint32_t* qa = &qq.x;
+            const uint32_t* da = &dd.x;
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              const float2 kf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ka[e]));
-              const float2 vf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&va[e]));
-              oa[e] = pack_bf2(kf.x * vf.x, kf.y * vf.y);
+              const float2 qf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&qa[e]));
+              const float2 df = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&da[e]));
+              oa[e] = pack_bf2(df.x * qf.x, df.y * qf.y);
             }
-            U4[v] = o;
-            if constexpr (C::BWD) {
-              uint4* Q4 = reinterpret_cast<uint4*>(S::region(st, 0));  // G overwrites q
-              const uint4* D4 = reinterpret_cast<const uint4*>(S::region(st, 3));
-              const uint4 qq = Q4[v], dd = D4[v];
-              const uint32_t* qa = &qq.x;
-              const uint32_t* da = &dd.x;
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 qf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&qa[e]));
-                const float2 df = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&da[e]));
-                oa[e] = pack_bf2(df.x * qf.x, df.y * qf.y);
-              }
-              Q4[v] = o;
-            }
+            Q4[v] = o;
           }
         }
       }
       fence_proxy_async();  // this lane's generic-proxy writes -> visible to the tensor core
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(&prepped[rg.s]);
+        mbar_arrive(&prepped[ri.s]);
         trace(p, j, 3);
       }
       for (int q = 0; q < C::NPW; ++q) {
         cur.next(nbi, H);
-        rg.next();
+        ri.next();
+        rw.next();
       }
     }
   } else {
@@ -689,24 +715,29 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
     float* rb = red + grp * (4 * 16 * BPI);          // [4 warps][16*BPI tokens]
     Cursor cur;
     if (grp < n_items) cur.init(W.first + grp, nbi, H);
-    Ring<NS> rg, rp, rn;
-    rg.init(grp);
+    Ring<NI> ri;
+    Ring<NW> rw;
+    Ring<NO> ro;
+    ri.init(grp);
+    rw.init(grp);
+    ro.init(grp);
     for (int64_t j = grp; j < n_items; j += NG) {
-      rp = rg;
+      Ring<NW> rp = rw, rn = rw;  // work slots of items j-1 and j+1
       rp.prev();
-      rn = rg;
       rn.next();
       const int64_t t0 = cur.m * BPI;
       const int b = cur.b, h = cur.h;
       const bool halo = cur.gi < W.g0 || cur.gi >= W.g1;
       const int nblk = (int)std::min<int64_t>(BPI, nb - t0);  // valid blocks of this item
-      uint8_t* st = smem + rg.s * S::kBytes;
+      uint8_t* st = sin + ri.s * S::kIn;
+      uint8_t* ot = sout + ro.s * S::kOut;
+      const float* gr = reinterpret_cast<const float*>(aux + rw.s * S::kAux);
       const int64_t co = cur.line * kD + c;
-      const uint32_t tslot = tmem_base + lane_base + (uint32_t)(rg.s * kItemCols);
-      mbar_wait(&ready[rg.s], rg.ph);
+      const uint32_t tslot = tmem_base + lane_base + (uint32_t)(rw.s * kItemCols);
+      mbar_wait(&ready[rw.s], rw.ph);
       tc_fence_after();
       if (leader) trace(p, j, 7);
-      // 1) neighbour reads first, so the neighbours' stages are released early:
+      // 1) neighbour reads first, so the neighbours' work slots are released early:
       //    carrier entering block t0: v = w_{t0-1}[15], the last block of item j-1;
       //    backward: mu of the item's last block from block 0 of item j+1
       float vprev = 0.f, mu_last = 0.f;
@@ -719,7 +750,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
           } else {  // mu_t = a_{t+1}[0] lambda_{t+1}[0]
             const float l0 = tmem_ld1(tmem_base + lane_base + (uint32_t)(rn.s * kItemCols + 16));
             tmem_wait_ld();
-            mu_last = reinterpret_cast<const float*>(smem + rn.s * S::kBytes + S::kG)[0] * l0;
+            mu_last = reinterpret_cast<const float*>(aux + rn.s * S::kAux)[0] * l0;
           }
         }
         tmem_wait_ld();
@@ -727,18 +758,17 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
       tc_fence_before();
       named_bar(1 + grp, kEpi);
       if (leader) {
-        if (j >= 1) mbar_arrive(&empty[rp.s]);                       // as "next" of item j-1
-        if (C::BWD && j + 1 < n_items) mbar_arrive(&empty[rn.s]);  // as "previous" of item j+1
-        if (j == n_items - 1) mbar_arrive(&empty[rg.s]);           // no next item
-        if (C::BWD && j == 0) mbar_arrive(&empty[rg.s]);           // no previous item
+        if (j >= 1) mbar_arrive(&wfree[rp.s]);                       // as "next" of item j-1
+        if (C::BWD && j + 1 < n_items) mbar_arrive(&wfree[rn.s]);  // as "previous" of item j+1
       }
+      mbar_wait(&oempty[ro.s], ro.ph ^ 1);
       // 2) the item's blocks, in order (the carrier passes block to block in a register)
       if (!halo) {
 #pragma unroll 1
         for (int k = 0; k < nblk; ++k) {
           const int64_t t = t0 + k;
           float g[16];
-          load16(reinterpret_cast<const float4*>(st + S::kG + 64 * k), g);
+          load16(reinterpret_cast<const float4*>(gr + 32 * k), g);
           float w[16];
           tmem_ld16(tslot + k * C::COLS, w);
           if constexpr (!C::BWD) {
@@ -746,17 +776,17 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
             float out[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) out[i] = fmaf(g[i], vprev, w[i]);  // Pass II: x~ = w + g v
-            uint8_t* t_out = S::tile(st, k, 0);
             if constexpr (C::MIX) {
+              const uint8_t* t_q = S::tile(st, k, 0);
               const uint8_t* t_v = S::tile(st, k, 2);
 #pragma unroll
               for (int i = 0; i < 16; ++i) {  // post-gate with residual: y = q x~ + v
                 const uint32_t o = tile_off<S::kHS>(i, c);
-                out[i] = fmaf(bf(t_out, o), out[i], bf(t_v, o));
+                out[i] = fmaf(bf(t_q, o), out[i], bf(t_v, o));
               }
             }
             __syncwarp();
-            store_col16<S::kHS>(t_out, c, lane, out);
+            store_col16<S::kHS>(S::tile(ot, k, 0), c, lane, out);
             if (t == nb - 1 && p.carry_out) p.carry_out[co] = w[15];
           } else {
             float lam[16];
@@ -765,11 +795,11 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
             if (k + 1 < nblk) {  // next block inside this item
               const float l0 = tmem_ld1(tslot + (k + 1) * C::COLS + 16);
               tmem_wait_ld();
-              mu = reinterpret_cast<const float*>(st + S::kG + 64 * (k + 1))[0] * l0;
+              mu = gr[32 * (k + 1)] * l0;
             }
             tmem_wait_ld();
             float r[16];
-            load16(reinterpret_cast<const float4*>(st + S::kR + 64 * k), r);
+            load16(reinterpret_cast<const float4*>(gr + 32 * k + 16), r);
             float part[16], du[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
@@ -782,11 +812,11 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
             if (t == 0 && p.mu_out) p.mu_out[co] = g[0] * lam[0];  // a_0[0] lambda_0[0]
             __syncwarp();
             if constexpr (!C::MIX) {
-              store_col16<S::kHS>(S::tile(st, k, 1), c, lane, du);  // du over G
+              store_col16<S::kHS>(S::tile(ot, k, 0), c, lane, du);
             } else {
-              uint8_t* t_dy = S::tile(st, k, 3);
-              uint8_t* t_k = S::tile(st, k, 1);
-              uint8_t* t_v = S::tile(st, k, 2);
+              const uint8_t* t_dy = S::tile(st, k, 3);
+              const uint8_t* t_k = S::tile(st, k, 1);
+              const uint8_t* t_v = S::tile(st, k, 2);
               float o16[16], dyv[16];
 #pragma unroll
               for (int i = 0; i < 16; ++i) {  // dq = dy x~
@@ -795,7 +825,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
                 o16[i] = dyv[i] * fmaf(g[i], vprev, w[i]);
               }
               __syncwarp();
-              store_col16<S::kHS>(t_dy, c, lane, o16);
+              store_col16<S::kHS>(S::tile(ot, k, 0), c, lane, o16);
 #pragma unroll
               for (int i = 0; i < 16; ++i) {  // dv = du^ k + dy ; dk = du^ v
                 const uint32_t o = tile_off<S::kHS>(i, c);
@@ -803,8 +833,8 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
                 du[i] *= bf(t_v, o);
               }
               __syncwarp();
-              store_col16<S::kHS>(t_v, c, lane, o16);
-              store_col16<S::kHS>(t_k, c, lane, du);
+              store_col16<S::kHS>(S::tile(ot, k, 2), c, lane, o16);
+              store_col16<S::kHS>(S::tile(ot, k, 1), c, lane, du);
             }
             // da: transpose-reduce over the warp's 32 channels, partials to SMEM
             int tok = 0;
@@ -827,17 +857,24 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
           }
         }
       }
-      // 3) outputs are in SMEM: hand the item to the store warp
+      // 3) outputs are in the output slot: hand them to the store warp; release the
+      //    work slot (and, mixer, the input stage)
       tc_fence_before();
       fence_proxy_async();
       named_bar(1 + grp, kEpi);
       if (leader) {
         trace(p, j, 8);
-        mbar_arrive(&outready[rg.s]);
+        mbar_arrive(&ofull[ro.s]);
+        mbar_arrive(&wfree[rw.s]);                                 // self
+        if (j == n_items - 1) mbar_arrive(&wfree[rw.s]);           // no next item
+        if (C::BWD && j == 0) mbar_arrive(&wfree[rw.s]);           // no previous item
+        if constexpr (C::MIX) mbar_arrive(&inempty[ri.s]);
       }
       for (int q = 0; q < NG; ++q) {
         cur.next(nbi, H);
-        rg.next();
+        ri.next();
+        rw.next();
+        ro.next();
       }
     }
   }

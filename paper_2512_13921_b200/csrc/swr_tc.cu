@@ -95,8 +95,9 @@ struct Stage {
   static constexpr int kIn = (kInRaw + 1023) / 1024 * 1024;
   // output slot
   static constexpr int kOut = C::NOUT * kRegion;
-  // work-slot aux: g_t[16], r_t[16] fp32 per block
-  static constexpr int kAux = C::BPI * 128;
+  // work-slot aux per block: g_t[16], r_t[16], gs[16] = g_t shifted by one (gs[0] = 1), fp32
+  static constexpr int kAuxBlk = 48;  // floats
+  static constexpr int kAux = C::BPI * kAuxBlk * 4;
   static constexpr int kInBase = 0;
   static constexpr int kOutBase = C::NI * kIn;
   static constexpr int kAuxBase = kOutBase + C::NO * kOut;
@@ -135,13 +136,16 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
                : "memory");
 }
+// Blocking wait.  The suspend-time hint (ns) lets the waiting warp sleep until
+// the phase completes instead of re-polling on the default short timeout, so
+// idle roles do not consume issue slots.
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "SWR_WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra SWR_WAIT_%=;\n\t}" ::"r"(su32(b)),
-      "r"(parity)
+      "r"(parity), "r"(1000000)
       : "memory");
 }
 __device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
@@ -362,6 +366,21 @@ struct Ring {
   }
 };
 
+// packed fp32x2 arithmetic (sm_100 FFMA2 / FMUL2 / FADD2): one instruction for two lanes of work
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d)
+      : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)),
+        "l"(*reinterpret_cast<uint64_t*>(&c)));
+  return *reinterpret_cast<float2*>(&d);
+}
+__device__ __forceinline__ float2 f2mul(float2 a, float2 b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d)
+      : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)));
+  return *reinterpret_cast<float2*>(&d);
+}
+
 // 16 fp32 from 16-byte aligned shared memory as four 128-bit loads
 __device__ __forceinline__ void load16(const float4* src, float (&v)[16]) {
 #pragma unroll
@@ -384,21 +403,31 @@ __device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
 // bf16 pairs: lanes (c, c^1) swap halves so every store is a 4-byte word and
 // the two rows of a warp instruction (i, i^4) fall in disjoint banks.  Even
 // lanes write (row i, channels c, c+1), odd lanes (row i^4, channels c-1, c);
-// branch-free (selects), so the warp issues each store once.
+// branch-free (selects), so the warp issues each store once.  The four row
+// offsets of the thread are computed once (ColMap); rows i+8 add 1024 B.
+struct ColMap {
+  uint32_t off[4];
+  bool odd;
+};
 template <int HS>
-__device__ __forceinline__ void store_col16(uint8_t* tile, int c, int lane, const float (&x)[16]) {
-  const bool odd = lane & 1;
+__device__ __forceinline__ ColMap col_map(int c, int lane) {
+  ColMap m;
+  m.odd = lane & 1;
   const int ce = c & ~1;  // even channel of the pair
+#pragma unroll
+  for (int q = 0; q < 4; ++q) m.off[q] = m.odd ? tile_off<HS>(q + 4, ce) : tile_off<HS>(q, ce);
+  return m;
+}
+__device__ __forceinline__ void store_col16(uint8_t* tile, const ColMap& m, const float (&x)[16]) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     if (i & 4) continue;
     const int i2 = i ^ 4;
-    const float send = odd ? x[i] : x[i2];
+    const float send = m.odd ? x[i] : x[i2];
     const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
-    const float lo = odd ? recv : x[i];
-    const float hi = odd ? x[i2] : recv;
-    const uint32_t off = odd ? tile_off<HS>(i2, ce) : tile_off<HS>(i, ce);
-    *reinterpret_cast<uint32_t*>(tile + off) = pack_bf2(lo, hi);
+    const float lo = m.odd ? recv : x[i];
+    const float hi = m.odd ? x[i2] : recv;
+    *reinterpret_cast<uint32_t*>(tile + m.off[i & 3] + (i & 8) * 128) = pack_bf2(lo, hi);
   }
 }
 
@@ -567,7 +596,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
           ++jr;
           progressed = true;
         }
-        if (!progressed) __nanosleep(20);
+        if (!progressed) __nanosleep(128);
       }
     }
     __syncwarp();
@@ -615,7 +644,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
       mbar_wait(&wfree[rw.s], rw.ph ^ 1);
       if (lane == 0) trace(p, j, 2);
       uint8_t* st = sin + ri.s * S::kIn;
-      float* gr = reinterpret_cast<float*>(aux + rw.s * S::kAux);  // [BPI][g 16 | r 16]
+      float* gr = reinterpret_cast<float*>(aux + rw.s * S::kAux);  // [BPI][g 16 | r 16 | gs 16]
 #pragma unroll
       for (int kb = 0; kb < BPI; kb += 2) {
         const int k = kb + hf;
@@ -646,14 +675,21 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
           hi.z = pack_bf2(Lc[12], Lc[13]); hi.w = pack_bf2(Lc[14], Lc[15]);
           *reinterpret_cast<uint4*>(l + ltile_off(0, col)) = lo;
           *reinterpret_cast<uint4*>(l + ltile_off(8, col)) = hi;
-          if constexpr (C::BWD) gr[32 * k + 16 + col] = prod;  // r_t[j] = L[15][j]
+          if constexpr (C::BWD) gr[S::kAuxBlk * k + 16 + col] = prod;  // r_t[j] = L[15][j]
           if (col == 0) {
             // g_t[i] = a_t[0] L_t[i][0] = a_t[0] ... a_t[i], fp32
-            float4* gp = reinterpret_cast<float4*>(gr + 32 * k);
-            gp[0] = make_float4(a[0] * Lc[0], a[0] * Lc[1], a[0] * Lc[2], a[0] * Lc[3]);
-            gp[1] = make_float4(a[0] * Lc[4], a[0] * Lc[5], a[0] * Lc[6], a[0] * Lc[7]);
-            gp[2] = make_float4(a[0] * Lc[8], a[0] * Lc[9], a[0] * Lc[10], a[0] * Lc[11]);
-            gp[3] = make_float4(a[0] * Lc[12], a[0] * Lc[13], a[0] * Lc[14], a[0] * Lc[15]);
+            float g[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) g[i] = a[0] * Lc[i];
+            float4* gp = reinterpret_cast<float4*>(gr + S::kAuxBlk * k);
+            gp[0] = make_float4(g[0], g[1], g[2], g[3]);
+            gp[1] = make_float4(g[4], g[5], g[6], g[7]);
+            gp[2] = make_float4(g[8], g[9], g[10], g[11]);
+            gp[3] = make_float4(g[12], g[13], g[14], g[15]);
+            gp[8] = make_float4(1.f, g[0], g[1], g[2]);  // gs: g shifted by one token
+            gp[9] = make_float4(g[3], g[4], g[5], g[6]);
+            gp[10] = make_float4(g[7], g[8], g[9], g[10]);
+            gp[11] = make_float4(g[11], g[12], g[13], g[14]);
           }
         }
       }
@@ -712,6 +748,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
     const int c = threadIdx.x & 127;                 // channel == TMEM lane
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
     const bool leader = (threadIdx.x & 127) == 0;
+    const ColMap cmap = col_map<S::kHS>(c, lane);
     float* rb = red + grp * (4 * 16 * BPI);          // [4 warps][16*BPI tokens]
     Cursor cur;
     if (grp < n_items) cur.init(W.first + grp, nbi, H);
@@ -750,7 +787,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
           } else {  // mu_t = a_{t+1}[0] lambda_{t+1}[0]
             const float l0 = tmem_ld1(tmem_base + lane_base + (uint32_t)(rn.s * kItemCols + 16));
             tmem_wait_ld();
-            mu_last = reinterpret_cast<const float*>(aux + rn.s * S::kAux)[0] * l0;
+            mu_last = reinterpret_cast<const float*>(aux + rn.s * S::kAux)[0] * l0;  // g[0] = a[0]
           }
         }
         tmem_wait_ld();
@@ -768,14 +805,19 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
         for (int k = 0; k < nblk; ++k) {
           const int64_t t = t0 + k;
           float g[16];
-          load16(reinterpret_cast<const float4*>(gr + 32 * k), g);
+          load16(reinterpret_cast<const float4*>(gr + S::kAuxBlk * k), g);
           float w[16];
           tmem_ld16(tslot + k * C::COLS, w);
           if constexpr (!C::BWD) {
             tmem_wait_ld();
             float out[16];
+            const float2 v2 = make_float2(vprev, vprev);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) out[i] = fmaf(g[i], vprev, w[i]);  // Pass II: x~ = w + g v
+            for (int i = 0; i < 16; i += 2) {  // Pass II: x~ = w + g v (packed pairs)
+              const float2 o = f2fma(make_float2(g[i], g[i + 1]), v2, make_float2(w[i], w[i + 1]));
+              out[i] = o.x;
+              out[i + 1] = o.y;
+            }
             if constexpr (C::MIX) {
               const uint8_t* t_q = S::tile(st, k, 0);
               const uint8_t* t_v = S::tile(st, k, 2);
@@ -786,7 +828,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
               }
             }
             __syncwarp();
-            store_col16<S::kHS>(S::tile(ot, k, 0), c, lane, out);
+            store_col16(S::tile(ot, k, 0), cmap, out);
             if (t == nb - 1 && p.carry_out) p.carry_out[co] = w[15];
           } else {
             float lam[16];
@@ -795,24 +837,32 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
             if (k + 1 < nblk) {  // next block inside this item
               const float l0 = tmem_ld1(tslot + (k + 1) * C::COLS + 16);
               tmem_wait_ld();
-              mu = gr[32 * (k + 1)] * l0;
+              mu = gr[S::kAuxBlk * (k + 1)] * l0;
             }
             tmem_wait_ld();
             float r[16];
-            load16(reinterpret_cast<const float4*>(gr + 32 * k + 16), r);
+            load16(reinterpret_cast<const float4*>(gr + S::kAuxBlk * k + 16), r);
+            float gs[16];
+            load16(reinterpret_cast<const float4*>(gr + S::kAuxBlk * k + 32), gs);  // gs[i] = g[i-1]
             float part[16], du[16];
+            const float2 v2 = make_float2(vprev, vprev), mu2 = make_float2(mu, mu);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const float rmu = r[i] * mu;
-              du[i] = lam[i] + rmu;                                            // du = lambda + r mu
-              const float wp = (i > 0) ? w[i - 1] : 0.f;
-              const float xp = (i > 0) ? fmaf(g[i - 1], vprev, w[i - 1]) : vprev;  // x~[i-1]
-              part[i] = fmaf(lam[i], xp, rmu * wp);                              // da partial
+            for (int i = 0; i < 16; i += 2) {  // packed token pairs (i, i+1)
+              const float2 lam2 = make_float2(lam[i], lam[i + 1]);
+              const float2 rmu = f2mul(make_float2(r[i], r[i + 1]), mu2);        // r mu
+              const float2 d2 = f2fma(make_float2(r[i], r[i + 1]), mu2, lam2);   // du = lambda + r mu
+              const float2 wp = make_float2(i > 0 ? w[i - 1] : 0.f, w[i]);       // w~[i-1]
+              const float2 xp = f2fma(make_float2(gs[i], gs[i + 1]), v2, wp);    // x~[i-1] = w[i-1] + g[i-1] v
+              const float2 pt = f2fma(lam2, xp, f2mul(rmu, wp));                 // da partial
+              du[i] = d2.x;
+              du[i + 1] = d2.y;
+              part[i] = pt.x;
+              part[i + 1] = pt.y;
             }
             if (t == 0 && p.mu_out) p.mu_out[co] = g[0] * lam[0];  // a_0[0] lambda_0[0]
             __syncwarp();
             if constexpr (!C::MIX) {
-              store_col16<S::kHS>(S::tile(ot, k, 0), c, lane, du);
+              store_col16(S::tile(ot, k, 0), cmap, du);
             } else {
               const uint8_t* t_dy = S::tile(st, k, 3);
               const uint8_t* t_k = S::tile(st, k, 1);
@@ -825,7 +875,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
                 o16[i] = dyv[i] * fmaf(g[i], vprev, w[i]);
               }
               __syncwarp();
-              store_col16<S::kHS>(S::tile(ot, k, 0), c, lane, o16);
+              store_col16(S::tile(ot, k, 0), cmap, o16);
 #pragma unroll
               for (int i = 0; i < 16; ++i) {  // dv = du^ k + dy ; dk = du^ v
                 const uint32_t o = tile_off<S::kHS>(i, c);
@@ -833,8 +883,8 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
                 du[i] *= bf(t_v, o);
               }
               __syncwarp();
-              store_col16<S::kHS>(S::tile(ot, k, 2), c, lane, o16);
-              store_col16<S::kHS>(S::tile(ot, k, 1), c, lane, du);
+              store_col16(S::tile(ot, k, 2), cmap, o16);
+              store_col16(S::tile(ot, k, 1), cmap, du);
             }
             // da: transpose-reduce over the warp's 32 channels, partials to SMEM
             int tok = 0;

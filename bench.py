@@ -41,7 +41,9 @@ CONFIGS = {
     "bxh": (8, 8192, 16, 128, "bf16"),        # BJ configs[3] per-GPU shard at 8 GPUs
     "paper_d16": (8, 8192, 128, 16, "bf16"),  # the paper's head shape d=16, h=128
     "tiny": (1, 64, 1, 16, "f32"),            # BJ configs[0]
+    "sp131k": (1, 131072, 16, 128, "bf16"),   # BJ configs[4]: sequence-parallel across ranks
 }
+SP_CONFIGS = {"sp131k"}
 METRIC = "SWR fwd+bwd tokens/s and achieved HBM GB/s vs B200 peak at 4K-32K, 1/2/4/8 GPUs"
 
 
@@ -69,7 +71,7 @@ def load_peaks():
 class ClockSampler:
     """NVML sampling of SM clock and throttle reasons during the timed region."""
 
-    def __init__(self, index, period=0.005):
+    def __init__(self, index, period=0.001):
         self.index, self.period = index, period
         self.samples, self.reasons = [], set()
         self.max_mhz = None
@@ -240,12 +242,36 @@ def main():
     import paper_2512_13921_b200 as P
     P.set_path({"auto": P.SWR_PATH_AUTO, "ffma": P.SWR_PATH_FFMA, "tc": P.SWR_PATH_TC}[args.path])
 
-    # per-rank shard of the batch (batch x head sharding): seed by global batch offset
-    inp_host = make_host_inputs(args.op, B, L, H, D, dt, seed=1 + 1000 * rank)
+    sp = args.config in SP_CONFIGS
+    if sp:
+        # sequence parallel: one L-shard per rank (multiples of 16), carrier halo over NCCL
+        from paper_2512_13921_b200 import dist as sdist
+        if args.op != "swr":
+            raise SystemExit("sequence-parallel bench supports --op swr")
+        full = make_host_inputs("swr", B, L, H, D, dt, seed=3)
+        lens = sdist.sp_shard_lengths(L, world)
+        lo = sum(lens[:rank])
+        inp_host = {k: (v[:, lo:lo + lens[rank]].contiguous() if v.dim() >= 3 else v)
+                    for k, v in full.items()}
+        Ls = lens[rank]
+        grp = dist.group.WORLD if world > 1 else None
+    else:
+        # per-rank shard of the batch (batch x head sharding): seed by global batch offset
+        inp_host = make_host_inputs(args.op, B, L, H, D, dt, seed=1 + 1000 * rank)
+        Ls = L
     g = {k: v.to(dev) for k, v in inp_host.items()}
     stream = torch.cuda.current_stream()
 
-    if args.op == "swr":
+    if sp and world > 1:
+        state = {}
+
+        def fwd():
+            x, state["cin"] = sdist.swr_sp_fwd(g["u"], g["a"], group=grp)
+            return x
+
+        def bwd():
+            return sdist.swr_sp_bwd(g["u"], g["a"], g["G"], carry_in=state.get("cin"), group=grp)
+    elif args.op == "swr":
         def fwd():
             return P.swr_fwd(g["u"], g["a"])
 
@@ -291,10 +317,10 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_per_step = t.item() / args.steps
-    tokens_per_step = B * L * world
+    tokens_per_step = B * L if sp else B * L * world
     value = tokens_per_step / (ms_per_step / 1e3)
 
-    bytes_ = algo_bytes(args.op, B, L, H, D, dt)
+    bytes_ = algo_bytes(args.op, B, Ls, H, D, dt)
     mf, mb = statistics.mean(t_fwd), statistics.mean(t_bwd)
     dom = "bwd" if mb >= mf else "fwd"
     peak, peak_kind = load_peaks()
@@ -310,11 +336,13 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if sp else "weak", "vs_baseline": None,
         "dtype": dt, "data": "synthetic",
         "config": {"workload": args.config, "B": B, "L": L, "H": H, "d_head": D, "op": args.op,
-                   "global_batch": B * world, "seq_len": L,
-                   "parallelism": f"dp{world} (batch x head shards, no collective)",
+                   "global_batch": B if sp else B * world, "seq_len": L,
+                   "parallelism": (f"sp{world} (sequence shards, one-block carrier halo via "
+                                   f"{'NCCL send/recv' if world > 1 else 'none'})") if sp else
+                                  f"dp{world} (batch x head shards, no collective)",
                    "l2_flush": f"{flush.numel() * 4 >> 20} MiB write between timed steps",
                    "path": args.path, "last_path": {0: "none", 1: "ffma", 2: "tc"}[P.last_path()]},
         "fwd_ms": mf, "bwd_ms": mb,
@@ -329,7 +357,7 @@ def main():
     }
 
     # end to end through the public API with host buffers (pinned), copies timed
-    if not args.no_e2e:
+    if not args.no_e2e and not (sp and world > 1):
         pin = {k: v.pin_memory() for k, v in inp_host.items()}
         outs_host = None
         ne = min(args.steps, 10)
@@ -359,7 +387,7 @@ def main():
                        "ms_per_step": te.item(), "steps": ne}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args.op, inp_host, B, L)
+        line["cpu_baseline"] = cpu_baseline(args.op, inp_host, B, Ls, rows=1)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -10,7 +10,8 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libswr.so")
+# SWR_LIB: an alternative in-tree build of the same library (kernel A/B experiments)
+LIB_PATH = os.environ.get("SWR_LIB") or os.path.join(_PKG, "libswr.so")
 
 SWR_F32, SWR_BF16 = 0, 1
 SWR_PATH_AUTO, SWR_PATH_FFMA, SWR_PATH_TC = 0, 1, 2

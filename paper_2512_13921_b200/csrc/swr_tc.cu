@@ -53,29 +53,46 @@ constexpr int kHalf = 2048;      // one 64-channel half: 16 rows x 128 B, 128B-s
 //   COLS TMEM columns per block                NPW  prep warps (each owns whole items)
 //   NG   epilogue groups of 4 warps
 // ---------------------------------------------------------------------------
+// ring depths / prep warps: compile-time tuning knobs (tools/build_var.sh -D...)
+#ifndef SWR_F_NI
+#define SWR_F_NI 8
+#define SWR_F_NO 3
+#define SWR_F_NPW 4
+#endif
+#ifndef SWR_B_NI
+#define SWR_B_NI 8
+#define SWR_B_NPW 2
+#endif
+#ifndef SWR_MF_NPW
+#define SWR_MF_NPW 3
+#define SWR_MF_NW 6
+#endif
+#ifndef SWR_MB_NI
+#define SWR_MB_NI 8
+#endif
 template <int OP>
 struct Cfg;
 template <>
 struct Cfg<0> {  // swr_fwd: in u;  out x
-  static constexpr int NT = 1, NP = 0, BPI = 4, NI = 7, NW = 8, NO = 4, COLS = 16, NPW = 4, NOUT = 1, NG = 3;
+  static constexpr int NT = 1, NP = 0, BPI = 4, NI = SWR_F_NI, NW = 8, NO = SWR_F_NO, COLS = 16, NPW = SWR_F_NPW, NOUT = 1, NG = 3;
   static constexpr int TU = 0, TG = 0;  // A-operand regions of W and lambda
   static constexpr bool BWD = false, MIX = false;
 };
 template <>
 struct Cfg<1> {  // swr_bwd: in u, G;  out du
-  static constexpr int NT = 2, NP = 0, BPI = 2, NI = 9, NW = 8, NO = 4, COLS = 32, NPW = 2, NOUT = 1, NG = 3;
+  static constexpr int NT = 2, NP = 0, BPI = 2, NI = SWR_B_NI, NW = 8, NO = 4, COLS = 32, NPW = SWR_B_NPW, NOUT = 1, NG = 3;
   static constexpr int TU = 0, TG = 1;
   static constexpr bool BWD = true, MIX = false;
 };
 template <>
 struct Cfg<2> {  // mix fwd: in q, k, v;  out y;  prep u^ = k v (over k)
-  static constexpr int NT = 3, NP = 0, BPI = 2, NI = 6, NW = 8, NO = 4, COLS = 16, NPW = 4, NOUT = 1, NG = 3;
+  static constexpr int NT = 3, NP = 0, BPI = 2, NI = 6, NW = SWR_MF_NW, NO = 4, COLS = 16, NPW = SWR_MF_NPW, NOUT = 1, NG = 3;
   static constexpr int TU = 1, TG = 0;
   static constexpr bool BWD = false, MIX = true;
 };
 template <>
 struct Cfg<3> {  // mix bwd: in q, k, v, dy;  out dq, dk, dv;  prep u^ = k v (region 4), G = dy q (over q)
-  static constexpr int NT = 4, NP = 1, BPI = 1, NI = 7, NW = 8, NO = 3, COLS = 32, NPW = 4, NOUT = 3, NG = 3;
+  static constexpr int NT = 4, NP = 1, BPI = 1, NI = SWR_MB_NI, NW = 8, NO = 3, COLS = 32, NPW = 4, NOUT = 3, NG = 3;
   static constexpr int TU = 4, TG = 0;
   static constexpr bool BWD = true, MIX = true;
 };
@@ -446,16 +463,23 @@ __device__ __forceinline__ void store_col16(uint8_t* tile, const ColMap& m, cons
 //   ofull[NO]    outputs in the output slot                      (epilogue leader)
 //   oempty[NO]   output slot free: TMA store has read it         (store warp)
 // ---------------------------------------------------------------------------
+#ifndef SWR_VAR
+#define SWR_VAR 0
+#endif
 template <int OP>
-__global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
+__global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
     swr_tc_kernel(const __grid_constant__ Maps maps, const Params p) {
   using C = Cfg<OP>;
   using S = Stage<OP>;
   constexpr int NI = C::NI, NW = C::NW, NO = C::NO, NG = C::NG, BPI = C::BPI;
   constexpr int kEpi = 128;
   constexpr int kItemCols = BPI * C::COLS;
+  // TMEM columns of a block: forward [w 0..15]; backward [lambda 0..15 | w 16..31], so
+  // w is preceded by a valid column and can also be read shifted by one (w[i-1]).
+  constexpr int kWo = C::BWD ? 16 : 0, kLo = 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int kPrepW0 = 4 * NG, kProdW = kPrepW0 + C::NPW, kMmaW = kProdW + 1, kStoreW = kMmaW + 1;
+  constexpr int kPrepW0 = 4 * NG, kProdW = kPrepW0 + C::NPW, kMmaW = kProdW + 1, kStoreW = kMmaW + 1,
+                kRetW = kStoreW + 1;
 
   // 1024-aligned base for the 128B-swizzle atoms.  Offset the __shared__ array
   // itself (not a uintptr_t round trip) so every access stays LDS/STS.
@@ -480,6 +504,15 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
                           : (NW * kItemCols <= 128) ? 128 : (NW * kItemCols <= 256) ? 256 : 512;
   static_assert(NW * kItemCols <= 512, "TMEM budget");
   static_assert(NW >= 4 && NI >= 3 && NO >= 2, "ring depth (deadlock freedom)");
+  // mbarrier waits are by phase parity, so a waiter must never be two phases ahead
+  // of a barrier.  Prep warp j mod NPW waits full[j mod NI] / wfree[j mod NW] and
+  // arrives prepped[j mod NI]; those phases complete out of item order (TMA loads
+  // finish out of order), so each stage and slot must always belong to the same
+  // prep warp, which then sees its phases in order.  The epilogue's ready/oempty
+  // phases are produced in item order by one thread; NO >= NG keeps a group (items
+  // j - NG, j) within one phase of oempty.
+  static_assert(NI % C::NPW == 0 && NW % C::NPW == 0, "prep warp <-> stage/slot ownership");
+  static_assert(NO >= NG && NW >= NG, "epilogue group within one phase");
   static_assert((3 * NI + 3 * NW + 2 * NO) * 8 + 8 <= 1024 && NG * 4 * 16 * BPI * 4 <= 3072, "scratch budget");
   static_assert(S::kBytes + 1024 <= 227 * 1024, "shared memory budget");
   constexpr int kUsers = C::BWD ? 3 : 2;
@@ -545,58 +578,68 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
       }
     }
   } else if (warp == kMmaW) {
-    // ===================== MMA issuer + retire + readiness =====================
-    // One thread polls without blocking: issue the next item's MMAs once its
-    // operands landed, retire completed items in issue order (tcgen05 ops complete
-    // in order) -- which frees their input stage for the SWR ops -- and mark items
-    // ready once every MMA their epilogue reads is retired.
+    // ===================== MMA issuer =====================
+    // Blocks on prepped[] (which the prep arrives only after observing full[]),
+    // issues the item's MMAs into its work slot's TMEM columns and commits them.
+    if (lane == 0 && n_items > 0) {
+      Ring<NI> ri;
+      Ring<NW> rw;
+      ri.init(0);
+      rw.init(0);
+      for (int64_t j = 0; j < n_items; ++j) {
+#if SWR_VAR == 1
+        mbar_wait(&full[ri.s], ri.ph);
+#endif
+#if SWR_VAR == 2
+        while (!mbar_test(&prepped[ri.s], ri.ph)) {}
+#else
+        mbar_wait(&prepped[ri.s], ri.ph);
+#endif
+        tc_fence_after();
+        trace(p, j, 4);
+        uint8_t* st = sin + ri.s * S::kIn;
+#pragma unroll
+        for (int k = 0; k < BPI; ++k) {
+          const uint32_t d = tmem_base + (uint32_t)(rw.s * kItemCols + k * C::COLS);
+          const uint32_t lt = su32(st + S::kL + 512 * k);
+          umma_bf16(d + kWo, desc_A<S::kHS>(su32(S::tile(st, k, C::TU))), desc_Bmn(lt), kIdescBmn);  // w^T
+          if constexpr (C::BWD)  // lambda^T
+            umma_bf16(d + kLo, desc_A<S::kHS>(su32(S::tile(st, k, C::TG))), desc_Bk(lt), kIdescBk);
+        }
+        umma_commit(&mmad[rw.s]);
+        trace(p, j, 5);
+        ri.next();
+        rw.next();
+      }
+    }
+    __syncwarp();
+  } else if (warp == kRetW) {
+    // ===================== MMA retire + readiness =====================
+    // tcgen05 ops complete in issue order: retire items in order, which frees their
+    // input stage (SWR: the operands are consumed), and mark an item ready once every
+    // MMA its epilogue reads is complete: j-1, j (backward also j+1).
     if (lane == 0 && n_items > 0) {
       constexpr int kBack = C::BWD ? 1 : 0;
-      Ring<NI> ri, rci;     // input stage of the next item to issue / to retire
-      Ring<NW> rw, rcw, rr;  // work slot of the next item to issue / to retire / to mark ready
+      Ring<NI> ri;
+      Ring<NW> rw, rr;
       ri.init(0);
-      rci.init(0);
       rw.init(0);
-      rcw.init(0);
       rr.init(0);
-      int64_t ji = 0, jc = 0, jr = 0;
-      while (jr < n_items) {
-        bool progressed = false;
-        if (ji < n_items && mbar_test(&full[ri.s], ri.ph) && mbar_test(&prepped[ri.s], ri.ph)) {
-          tc_fence_after();
-          trace(p, ji, 4);
-          uint8_t* st = sin + ri.s * S::kIn;
-#pragma unroll
-          for (int k = 0; k < BPI; ++k) {
-            const uint32_t d = tmem_base + (uint32_t)(rw.s * kItemCols + k * C::COLS);
-            const uint32_t lt = su32(st + S::kL + 512 * k);
-            umma_bf16(d, desc_A<S::kHS>(su32(S::tile(st, k, C::TU))), desc_Bmn(lt), kIdescBmn);  // w^T
-            if constexpr (C::BWD)  // lambda^T
-              umma_bf16(d + 16, desc_A<S::kHS>(su32(S::tile(st, k, C::TG))), desc_Bk(lt), kIdescBk);
-          }
-          umma_commit(&mmad[rw.s]);
-          trace(p, ji, 5);
-          ri.next();
-          rw.next();
-          ++ji;
-          progressed = true;
-        }
-        if (jc < ji && mbar_test(&mmad[rcw.s], rcw.ph)) {
-          if constexpr (!C::MIX) mbar_arrive(&inempty[rci.s]);  // operands consumed
-          rci.next();
-          rcw.next();
-          ++jc;
-          progressed = true;
-        }
-        while (jr < n_items && (jr + kBack < jc || (jc == n_items && jr < jc))) {
-          tc_fence_before();
+      for (int64_t j = 0; j < n_items; ++j) {
+        mbar_wait(&mmad[rw.s], rw.ph);
+        tc_fence_before();
+        if constexpr (!C::MIX) mbar_arrive(&inempty[ri.s]);  // operands consumed
+        if (j - kBack >= 0) {
           mbar_arrive(&ready[rr.s]);
-          trace(p, jr, 6);
+          trace(p, j - kBack, 6);
           rr.next();
-          ++jr;
-          progressed = true;
         }
-        if (!progressed) __nanosleep(128);
+        ri.next();
+        rw.next();
+      }
+      for (int64_t jr = std::max<int64_t>(n_items - kBack, 0); jr < n_items; ++jr) {
+        mbar_arrive(&ready[rr.s]);
+        rr.next();
       }
     }
     __syncwarp();
@@ -780,12 +823,12 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
       float vprev = 0.f, mu_last = 0.f;
       if (!halo) {
         if (t0 == 0) vprev = p.carry_in ? p.carry_in[co] : 0.f;  // v_{-1}
-        else vprev = tmem_ld1(tmem_base + lane_base + (uint32_t)(rp.s * kItemCols + (BPI - 1) * C::COLS + 15));
+        else vprev = tmem_ld1(tmem_base + lane_base + (uint32_t)(rp.s * kItemCols + (BPI - 1) * C::COLS + kWo + 15));
         if constexpr (C::BWD) {
           if (t0 + nblk == nb) {
             mu_last = p.mu_in ? p.mu_in[co] : 0.f;
           } else {  // mu_t = a_{t+1}[0] lambda_{t+1}[0]
-            const float l0 = tmem_ld1(tmem_base + lane_base + (uint32_t)(rn.s * kItemCols + 16));
+            const float l0 = tmem_ld1(tmem_base + lane_base + (uint32_t)(rn.s * kItemCols + kLo));
             tmem_wait_ld();
             mu_last = reinterpret_cast<const float*>(aux + rn.s * S::kAux)[0] * l0;  // g[0] = a[0]
           }
@@ -804,10 +847,13 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
 #pragma unroll 1
         for (int k = 0; k < nblk; ++k) {
           const int64_t t = t0 + k;
-          float g[16];
-          load16(reinterpret_cast<const float4*>(gr + S::kAuxBlk * k), g);
-          float w[16];
-          tmem_ld16(tslot + k * C::COLS, w);
+          float g[16], w[16];
+          if constexpr (!C::BWD || C::MIX) {  // SWR backward needs only w[i-1] (wsh) and w[15]
+            load16(reinterpret_cast<const float4*>(gr + S::kAuxBlk * k), g);
+            tmem_ld16(tslot + k * C::COLS + kWo, w);
+          } else {
+            w[15] = tmem_ld1(tslot + k * C::COLS + kWo + 15);
+          }
           if constexpr (!C::BWD) {
             tmem_wait_ld();
             float out[16];
@@ -832,10 +878,12 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
             if (t == nb - 1 && p.carry_out) p.carry_out[co] = w[15];
           } else {
             float lam[16];
-            tmem_ld16(tslot + k * C::COLS + 16, lam);
+            tmem_ld16(tslot + k * C::COLS + kLo, lam);
+            float wsh[16];  // wsh[j] = w[j-1] (column kWo-1 = lambda[15] lands in wsh[0], unused)
+            tmem_ld16(tslot + k * C::COLS + kWo - 1, wsh);
             float mu = mu_last;
             if (k + 1 < nblk) {  // next block inside this item
-              const float l0 = tmem_ld1(tslot + (k + 1) * C::COLS + 16);
+              const float l0 = tmem_ld1(tslot + (k + 1) * C::COLS + kLo);
               tmem_wait_ld();
               mu = gr[S::kAuxBlk * (k + 1)] * l0;
             }
@@ -851,7 +899,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
               const float2 lam2 = make_float2(lam[i], lam[i + 1]);
               const float2 rmu = f2mul(make_float2(r[i], r[i + 1]), mu2);        // r mu
               const float2 d2 = f2fma(make_float2(r[i], r[i + 1]), mu2, lam2);   // du = lambda + r mu
-              const float2 wp = make_float2(i > 0 ? w[i - 1] : 0.f, w[i]);       // w~[i-1]
+              const float2 wp = make_float2(i > 0 ? wsh[i] : 0.f, wsh[i + 1]);  // w[i-1], w[i]
               const float2 xp = f2fma(make_float2(gs[i], gs[i + 1]), v2, wp);    // x~[i-1] = w[i-1] + g[i-1] v
               const float2 pt = f2fma(lam2, xp, f2mul(rmu, wp));                 // da partial
               du[i] = d2.x;
@@ -859,7 +907,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32, 1)
               part[i] = pt.x;
               part[i + 1] = pt.y;
             }
-            if (t == 0 && p.mu_out) p.mu_out[co] = g[0] * lam[0];  // a_0[0] lambda_0[0]
+            if (t == 0 && p.mu_out) p.mu_out[co] = gr[S::kAuxBlk * k] * lam[0];  // a_0[0] lambda_0[0]
             __syncwarp();
             if constexpr (!C::MIX) {
               store_col16(S::tile(ot, k, 0), cmap, du);
@@ -1007,7 +1055,7 @@ static cudaError_t launch_op(const Params& p, cudaStream_t st, int sms) {
   }
   const int64_t total = p.B * p.H * ((p.nb + Cfg<OP>::BPI - 1) / Cfg<OP>::BPI);
   const int grid = (int)std::min<int64_t>(sms, std::max<int64_t>(total, 1));
-  constexpr int threads = (4 * Cfg<OP>::NG + Cfg<OP>::NPW + 3) * 32;
+  constexpr int threads = (4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32;
   swr_tc_kernel<OP><<<grid, threads, smem, st>>>(maps, p);
   return cudaGetLastError();
 }

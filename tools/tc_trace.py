@@ -40,7 +40,7 @@ valid = t[:, 0] > 0
 t0 = t[valid][:, 0].min()
 rel = np.where(t > 0, t - t0, -1)
 print("item " + " ".join(f"{e[:10]:>10}" for e in EV))
-for j in range(0, 0):
+for j in list(range(20, 36)):
     if j < N and valid[j]:
         print(f"{j:4d} " + " ".join(f"{x:10d}" for x in rel[j]))
 # steady-state averages of stage-to-stage latencies (items 40..200)

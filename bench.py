@@ -12,9 +12,11 @@ mixer forward + backward -- on inputs already resident in HBM.  Metric
 kernel against the measured copy peak (MEASURED_PEAKS.json).
 
 Timing: W untimed warm-up steps; then K steps, each bracketed by CUDA events on
-the launching stream with an L2 flush (a write of 2x the L2 size) between
-steps, outside the events; barrier + synchronize around the loop; per-rank sum
-of step times, max over ranks.  Multi-GPU (torchrun): every rank runs the same
+the launching stream with an L2 flush between steps, outside the events (a
+write of 2x the L2 size, then a read of another 2x-L2 buffer so the flush's own
+dirty lines are written back before the step: a clean L2 holding no step data);
+barrier + synchronize around the loop; per-rank sum of step times, max over
+ranks.  Multi-GPU (torchrun): every rank runs the same
 per-GPU workload on its own batch shard (batch x head sharding, no collective;
 weak scaling).
 """
@@ -286,9 +288,19 @@ def main():
 
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = torch.empty(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=dev)
+    flush_rd = torch.zeros_like(flush)
+    flush_sink = torch.empty(1, dtype=torch.float32, device=dev)
+
+    def l2_flush():
+        # write > 2x L2, then read another > 2x L2 buffer: the write evicts every line
+        # of the previous step, the read pushes the flush's own dirty lines back to HBM,
+        # so the step starts with a clean L2 holding nothing it will read (the state
+        # ncu's --cache-control all gives a kernel) and pays no stray write-back
+        flush.zero_()
+        flush_sink.copy_(flush_rd.sum())
 
     for _ in range(args.warmup):
-        flush.zero_()
+        l2_flush()
         fwd()
         bwd()
     torch.cuda.synchronize()
@@ -300,7 +312,7 @@ def main():
     launches0 = P.launch_count()
     with ClockSampler(dev.index if world == 1 else local) as clk:
         for s in range(args.steps):
-            flush.zero_()
+            l2_flush()
             ev[s][0].record(stream)
             fwd()
             ev[s][1].record(stream)
@@ -343,7 +355,8 @@ def main():
                    "parallelism": (f"sp{world} (sequence shards, one-block carrier halo via "
                                    f"{'NCCL send/recv' if world > 1 else 'none'})") if sp else
                                   f"dp{world} (batch x head shards, no collective)",
-                   "l2_flush": f"{flush.numel() * 4 >> 20} MiB write between timed steps",
+                   "l2_flush": (f"{flush.numel() * 4 >> 20} MiB write + {flush_rd.numel() * 4 >> 20} MiB read "
+                                "between timed steps (L2 clean, holds no step data)"),
                    "path": args.path, "last_path": {0: "none", 1: "ffma", 2: "tc"}[P.last_path()]},
         "fwd_ms": mf, "bwd_ms": mb,
         "hbm_gbs": {"fwd": bytes_["fwd"] / mf / 1e6, "bwd": bytes_["bwd"] / mb / 1e6,
@@ -365,7 +378,7 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         times = []
         for s in range(ne + 2):
-            flush.zero_()
+            l2_flush()
             e0.record(stream)
             for k, v in pin.items():
                 g[k].copy_(v, non_blocking=True)

@@ -63,6 +63,9 @@ constexpr int kHalf = 2048;      // one 64-channel half: 16 rows x 128 B, 128B-s
 #define SWR_B_NI 8
 #define SWR_B_NPW 2
 #endif
+#ifndef SWR_B_NG
+#define SWR_B_NG 3
+#endif
 #ifndef SWR_MF_NPW
 #define SWR_MF_NPW 3
 #define SWR_MF_NW 6
@@ -80,7 +83,7 @@ struct Cfg<0> {  // swr_fwd: in u;  out x
 };
 template <>
 struct Cfg<1> {  // swr_bwd: in u, G;  out du
-  static constexpr int NT = 2, NP = 0, BPI = 2, NI = SWR_B_NI, NW = 8, NO = 4, COLS = 32, NPW = SWR_B_NPW, NOUT = 1, NG = 3;
+  static constexpr int NT = 2, NP = 0, BPI = 2, NI = SWR_B_NI, NW = 8, NO = 4, COLS = 32, NPW = SWR_B_NPW, NOUT = 1, NG = SWR_B_NG;
   static constexpr int TU = 0, TG = 1;
   static constexpr bool BWD = true, MIX = false;
 };
@@ -356,6 +359,18 @@ struct Cursor {  // item gi = line * nbi + m; t0 = first block of the item
       }
     }
   }
+  __device__ __forceinline__ void step(int n, int64_t nbi, int64_t H) {  // n items forward
+    gi += n;
+    m += n;
+    while (m >= nbi) {
+      m -= nbi;
+      ++line;
+      if (++h == H) {
+        h = 0;
+        ++b;
+      }
+    }
+  }
 };
 
 // ring position of item j: stage s = j % NS, parity = (j / NS) & 1, advanced incrementally
@@ -370,6 +385,15 @@ struct Ring {
   __device__ __forceinline__ void next() {
     if (++s == NS) {
       s = 0;
+      ph ^= 1;
+    }
+  }
+  template <int N>  // N <= NS items forward
+  __device__ __forceinline__ void step() {
+    static_assert(N <= NS, "one wrap at most");
+    s += N;
+    if (s >= NS) {
+      s -= NS;
       ph ^= 1;
     }
   }
@@ -459,9 +483,12 @@ __device__ __forceinline__ void store_col16(uint8_t* tile, const ColMap& m, cons
 //   ready[NW]    MMAs of every item whose TMEM the epilogue reads are complete:
 //                j-1, j (backward also j+1)                      (MMA warp)
 //   wfree[NW]    work slot free: the item's epilogue and the neighbours that read
-//                its TMEM / g are done (next; backward also previous)
-//   ofull[NO]    outputs in the output slot                      (epilogue leader)
-//   oempty[NO]   output slot free: TMA store has read it         (store warp)
+//                its TMEM / g are done (next; backward also previous) -- one
+//                arrival per epilogue warp and user
+//   ofull[NO]    outputs (and da partials) in the output slot    (each epilogue warp)
+//   oempty[NO]   output slot free: TMA store has read it, da summed (store warp)
+// The 4 warps of an epilogue group never synchronise with each other: each owns
+// 32 channels (a TMEM lane quarter) and arrives on the barriers itself.
 // ---------------------------------------------------------------------------
 #ifndef SWR_VAR
 #define SWR_VAR 0
@@ -472,7 +499,6 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
   using C = Cfg<OP>;
   using S = Stage<OP>;
   constexpr int NI = C::NI, NW = C::NW, NO = C::NO, NG = C::NG, BPI = C::BPI;
-  constexpr int kEpi = 128;
   constexpr int kItemCols = BPI * C::COLS;
   // TMEM columns of a block: forward [w 0..15]; backward [lambda 0..15 | w 16..31], so
   // w is preceded by a valid column and can also be read shifted by one (w[i-1]).
@@ -498,7 +524,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
   uint64_t* ofull = wfree + NW;
   uint64_t* oempty = ofull + NO;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(oempty + NO);
-  float* red = reinterpret_cast<float*>(scratch + 1024);  // [NG][4 warps][16*BPI] da partials
+  float* red = reinterpret_cast<float*>(scratch + 1024);  // [NO][4 warps][16*BPI] da partials
 
   constexpr int kTmemCols = (NW * kItemCols <= 32) ? 32 : (NW * kItemCols <= 64) ? 64
                           : (NW * kItemCols <= 128) ? 128 : (NW * kItemCols <= 256) ? 256 : 512;
@@ -513,16 +539,16 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
   // j - NG, j) within one phase of oempty.
   static_assert(NI % C::NPW == 0 && NW % C::NPW == 0, "prep warp <-> stage/slot ownership");
   static_assert(NO >= NG && NW >= NG, "epilogue group within one phase");
-  static_assert((3 * NI + 3 * NW + 2 * NO) * 8 + 8 <= 1024 && NG * 4 * 16 * BPI * 4 <= 3072, "scratch budget");
+  static_assert((3 * NI + 3 * NW + 2 * NO) * 8 + 8 <= 1024 && NO * 4 * 16 * BPI * 4 <= 3072, "scratch budget");
   static_assert(S::kBytes + 1024 <= 227 * 1024, "shared memory budget");
-  constexpr int kUsers = C::BWD ? 3 : 2;
+  constexpr int kUsers = (C::BWD ? 3 : 2) * 4;  // users x epilogue warps
 
   if (threadIdx.x == 0) {
     trace_cta(p, 0);
     for (int s = 0; s < NI; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&prepped[s], 1);
-      mbar_init(&inempty[s], 1);
+      mbar_init(&inempty[s], C::MIX ? 4 : 1);
     }
     for (int s = 0; s < NW; ++s) {
       mbar_init(&mmad[s], 1);
@@ -530,7 +556,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
       mbar_init(&wfree[s], kUsers);
     }
     for (int s = 0; s < NO; ++s) {
-      mbar_init(&ofull[s], 1);
+      mbar_init(&ofull[s], 4);
       mbar_init(&oempty[s], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -644,8 +670,10 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
     }
     __syncwarp();
   } else if (warp == kStoreW) {
-    // ===================== TMA store + output-slot release =====================
-    if (lane == 0 && n_items > 0) {
+    // ===================== TMA store, da sum, output-slot release =====================
+    // lane 0 issues the TMA stores; backward: the warp sums the 4 epilogue warps'
+    // da partials of the slot in a fixed order (deterministic) and writes da
+    if (n_items > 0) {
       Cursor cur;
       cur.init(W.first, nbi, H);
       Ring<NO> ro;
@@ -654,22 +682,38 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
         mbar_wait(&ofull[ro.s], ro.ph);
         const bool halo = cur.gi < W.g0 || cur.gi >= W.g1;
         if (!halo) {
-          uint8_t* ot = sout + ro.s * S::kOut;
-          const int tt = (int)(cur.m * BPI * kEll);
+          if (lane == 0) {
+            uint8_t* ot = sout + ro.s * S::kOut;
+            const int tt = (int)(cur.m * BPI * kEll);
 #pragma unroll
-          for (int x = 0; x < C::NOUT; ++x) {  // rows past L are clipped by TMA
-            tma_store_4d(&maps.out[x], S::region(ot, x), 0, cur.h, tt, cur.b);
-            tma_store_4d(&maps.out[x], S::region(ot, x) + S::kHS, 64, cur.h, tt, cur.b);
+            for (int x = 0; x < C::NOUT; ++x) {  // rows past L are clipped by TMA
+              tma_store_4d(&maps.out[x], S::region(ot, x), 0, cur.h, tt, cur.b);
+              tma_store_4d(&maps.out[x], S::region(ot, x) + S::kHS, 64, cur.h, tt, cur.b);
+            }
+            bulk_commit();
+            trace(p, j, 9);
           }
-          bulk_commit();
-          trace(p, j, 9);
-          bulk_wait_read<0>();
+          if constexpr (C::BWD) {
+            const float* rb = red + ro.s * (4 * 16 * BPI);
+            __nv_bfloat16* dA = (__nv_bfloat16*)p.da + (int64_t)cur.b * p.sa_b + (int64_t)cur.h * p.sa_h;
+#pragma unroll
+            for (int q0 = 0; q0 < 16 * BPI; q0 += 32) {
+              const int q = q0 + lane;
+              const int64_t n = cur.m * BPI * kEll + q;
+              if (q < 16 * BPI && n < p.L) {
+                const float sum = ((rb[q] + rb[16 * BPI + q]) + rb[32 * BPI + q]) + rb[48 * BPI + q];
+                dA[n * p.sa_l] = __float2bfloat16_rn(sum);
+              }
+            }
+          }
+          if (lane == 0) bulk_wait_read<0>();
         }
-        mbar_arrive(&oempty[ro.s]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&oempty[ro.s]);
         cur.next(nbi, H);
         ro.next();
       }
-      bulk_wait_all();
+      if (lane == 0) bulk_wait_all();
     }
   } else if (warp >= kPrepW0) {
     // ===================== prep: L tiles (Alg. 3), g, r, pre-gates =====================
@@ -778,11 +822,9 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
         mbar_arrive(&prepped[ri.s]);
         trace(p, j, 3);
       }
-      for (int q = 0; q < C::NPW; ++q) {
-        cur.next(nbi, H);
-        ri.next();
-        rw.next();
-      }
+      cur.step(C::NPW, nbi, H);
+      ri.template step<C::NPW>();
+      rw.template step<C::NPW>();
     }
   } else {
     // ===================== epilogue groups: thread = channel c =====================
@@ -790,9 +832,8 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
     const int wq = warp & 3;                         // TMEM lane quarter
     const int c = threadIdx.x & 127;                 // channel == TMEM lane
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
-    const bool leader = (threadIdx.x & 127) == 0;
+    const bool leader = (threadIdx.x & 127) == 0;   // trace only
     const ColMap cmap = col_map<S::kHS>(c, lane);
-    float* rb = red + grp * (4 * 16 * BPI);          // [4 warps][16*BPI tokens]
     Cursor cur;
     if (grp < n_items) cur.init(W.first + grp, nbi, H);
     Ring<NI> ri;
@@ -806,7 +847,6 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
       rp.prev();
       rn.next();
       const int64_t t0 = cur.m * BPI;
-      const int b = cur.b, h = cur.h;
       const bool halo = cur.gi < W.g0 || cur.gi >= W.g1;
       const int nblk = (int)std::min<int64_t>(BPI, nb - t0);  // valid blocks of this item
       uint8_t* st = sin + ri.s * S::kIn;
@@ -836,12 +876,13 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
         tmem_wait_ld();
       }
       tc_fence_before();
-      named_bar(1 + grp, kEpi);
-      if (leader) {
+      __syncwarp();
+      if (lane == 0) {
         if (j >= 1) mbar_arrive(&wfree[rp.s]);                       // as "next" of item j-1
         if (C::BWD && j + 1 < n_items) mbar_arrive(&wfree[rn.s]);  // as "previous" of item j+1
       }
       mbar_wait(&oempty[ro.s], ro.ph ^ 1);
+      float* rb = red + ro.s * (4 * 16 * BPI);  // this slot's da partials [4 warps][16*BPI tokens]
       // 2) the item's blocks, in order (the carrier passes block to block in a register)
       if (!halo) {
 #pragma unroll 1
@@ -941,39 +982,24 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
           }
           vprev = w[15];
         }
-        if constexpr (C::BWD) {  // da: sum the 4 warps' partials, fixed order
-          named_bar(1 + NG + grp, kEpi);
-          if (wq == 0) {
-            __nv_bfloat16* dA = (__nv_bfloat16*)p.da + (int64_t)b * p.sa_b + (int64_t)h * p.sa_h;
-            for (int q = lane; q < 16 * nblk; q += 32) {
-              const int64_t n = t0 * kEll + q;
-              if (n < p.L) {
-                const float sum = ((rb[q] + rb[16 * BPI + q]) + rb[32 * BPI + q]) + rb[48 * BPI + q];
-                dA[n * p.sa_l] = __float2bfloat16_rn(sum);
-              }
-            }
-          }
-        }
       }
-      // 3) outputs are in the output slot: hand them to the store warp; release the
-      //    work slot (and, mixer, the input stage)
+      // 3) this warp's outputs (and da partials) are in the output slot: hand them to
+      //    the store warp; release the work slot (and, mixer, the input stage)
       tc_fence_before();
       fence_proxy_async();
-      named_bar(1 + grp, kEpi);
-      if (leader) {
-        trace(p, j, 8);
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) trace(p, j, 8);
         mbar_arrive(&ofull[ro.s]);
         mbar_arrive(&wfree[rw.s]);                                 // self
         if (j == n_items - 1) mbar_arrive(&wfree[rw.s]);           // no next item
         if (C::BWD && j == 0) mbar_arrive(&wfree[rw.s]);           // no previous item
         if constexpr (C::MIX) mbar_arrive(&inempty[ri.s]);
       }
-      for (int q = 0; q < NG; ++q) {
-        cur.next(nbi, H);
-        ri.next();
-        rw.next();
-        ro.next();
-      }
+      cur.step(NG, nbi, H);
+      ri.template step<NG>();
+      rw.template step<NG>();
+      ro.template step<NG>();
     }
   }
 

@@ -17,12 +17,14 @@ fn = {"fwd": lambda: P.swr_fwd(s["u"], s["a"]),
       "mixf": lambda: P.phalanx_mix(m["q"], m["k"], m["v"], m["a"]),
       "mixb": lambda: P.phalanx_mix_bwd(m["q"], m["k"], m["v"], m["a"], m["dy"])}
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+flush_rd = torch.zeros(64 << 20, device="cuda")
+sink = torch.empty(1, device="cuda")
 out = []
 for op in ops:
     for _ in range(3): fn[op]()
     ts = []
     for _ in range(25):
-        flush.zero_()
+        flush.zero_(); sink.copy_(flush_rd.sum())  # clean L2 (bench.py's flush)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(); fn[op](); e1.record(); torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1) * 1e3)

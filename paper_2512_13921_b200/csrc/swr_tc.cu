@@ -237,18 +237,6 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                    su32(bar))
                : "memory");
 }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-  uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15},"
-      " [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-        "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
 __device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
   uint32_t r;
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
@@ -258,21 +246,30 @@ __device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
 // events: 0 producer got stage, 1 producer issued TMA, 2 prep saw full, 3 prep done,
 // 4 mma saw full+prepped, 5 mma issued, 6 mma marked ready, 7 epilogue saw ready,
 // 8 epilogue done (before store), 9 store committed, 10 own stage released
+// Compiled in only with -DSWR_TRACE=1 (tools/build_var.sh); the product build has none.
+#ifndef SWR_TRACE
+#define SWR_TRACE 0
+#endif
 __device__ __forceinline__ void trace(const Params& p, int64_t j, int ev) {
+#if SWR_TRACE
   if (p.trace != nullptr && blockIdx.x == 0 && j < p.trace_n) {
     p.trace[j * 16 + ev] = clock64();  // SM cycles (all roles share the SM clock)
   }
+#endif
 }
 // diagnostics: per-CTA %globaltimer span (ns) after the per-item area: slot 16*n + 2*cta + e
 __device__ __forceinline__ void trace_cta(const Params& p, int e) {
+#if SWR_TRACE
   if (p.trace != nullptr) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     p.trace[16 * p.trace_n + 2 * blockIdx.x + e] = t;
   }
+#endif
 }
-__device__ __forceinline__ void tmem_wait_ld() {
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+// wait with the loaded value bound as an operand (no use can move above the wait)
+__device__ __forceinline__ void tmem_wait_f(float& x) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" : "+f"(x) : : "memory");
 }
 
 // UMMA shared-memory descriptor (sm_100: version 1 at bit 46, layout type at 61..63)
@@ -300,23 +297,11 @@ constexpr uint32_t kIdescBk = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | 
                               ((16u >> 3) << 17) | ((128u >> 4) << 24);
 constexpr uint32_t kIdescBmn = kIdescBk | (1u << 16);
 
-// byte offset of element (token i, channel c) inside a 4 KiB swizzled tile
-template <int HS>
-__device__ __forceinline__ uint32_t tile_off(int i, int c) {
-  const int half = c >> 6, cc = c & 63;
-  return half * HS + i * 128 + ((((cc >> 3) ^ (i & 7))) << 4) + ((cc & 7) << 1);
-}
 // byte offset of L[i][j] in the transfer tile (see desc_Bk / desc_Bmn)
 __device__ __forceinline__ uint32_t ltile_off(int i, int j) {
   return (j >> 3) * 256 + (i >> 3) * 128 + (j & 7) * 16 + (i & 7) * 2;
 }
 
-__device__ __forceinline__ float bf(const uint8_t* base, uint32_t off) {
-  return __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(base + off));
-}
-__device__ __forceinline__ void st_bf(uint8_t* base, uint32_t off, float x) {
-  *reinterpret_cast<__nv_bfloat16*>(base + off) = __float2bfloat16_rn(x);
-}
 
 // ---------------------------------------------------------------------------
 // work list: items are BPI-block groups [BPI*m, BPI*m + BPI) of a line
@@ -422,17 +407,6 @@ __device__ __forceinline__ float2 f2mul(float2 a, float2 b) {
   return *reinterpret_cast<float2*>(&d);
 }
 
-// 16 fp32 from 16-byte aligned shared memory as four 128-bit loads
-__device__ __forceinline__ void load16(const float4* src, float (&v)[16]) {
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const float4 x = src[q];
-    v[4 * q] = x.x;
-    v[4 * q + 1] = x.y;
-    v[4 * q + 2] = x.z;
-    v[4 * q + 3] = x.w;
-  }
-}
 
 // pack two fp32 into bf16x2 (lo = first)
 __device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
@@ -440,37 +414,92 @@ __device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-// Store 16 per-token values of this thread's channel c into a swizzled tile as
-// bf16 pairs: lanes (c, c^1) swap halves so every store is a 4-byte word and
-// the two rows of a warp instruction (i, i^4) fall in disjoint banks.  Even
-// lanes write (row i, channels c, c+1), odd lanes (row i^4, channels c-1, c);
-// branch-free (selects), so the warp issues each store once.  The four row
-// offsets of the thread are computed once (ColMap); rows i+8 add 1024 B.
-struct ColMap {
-  uint32_t off[4];
-  bool odd;
-};
-template <int HS>
-__device__ __forceinline__ ColMap col_map(int c, int lane) {
-  ColMap m;
-  m.odd = lane & 1;
-  const int ce = c & ~1;  // even channel of the pair
+// ---------------------------------------------------------------------------
+// Epilogue fragment layout.  An epilogue warp (TMEM lane quarter wq) reads a
+// block's 128 x 16 accumulator [channel lane][token column] in the m16n8
+// fragment layout of tcgen05.ld.16x256b: lane l = 4 rr + qd holds
+//     channels  c_k = 32 wq + rr + 8 k           (k = 0..3)
+//     tokens    tk_m = 8 (m >> 1) + 2 qd + (m & 1)  (m = 0..3)
+// as x[k][m].  Token pairs (m, m+1) of one channel pack into one bf16x2 word,
+// which is exactly the element pair of an 8x8 b16 matrix fragment whose rows
+// are channels: stmatrix/ldmatrix .trans move it to/from the swizzled token-row
+// tile with no shuffles (matrix k = channels 32 wq + 8 k .. +7, tokens 8 tg ..
+// +7; lane l supplies the address of row l & 7 of matrix l >> 3).
+// ---------------------------------------------------------------------------
+// x[k][m] <- TMEM columns col .. col+15 of lanes 32 wq .. 32 wq + 31 (taddr = lane
+// quarter base | col).  Completes at tmem_wait_frag.
+__device__ __forceinline__ void tmem_ld_frag(uint32_t taddr, float (&x)[4][4]) {
+  uint32_t r[16];
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                 "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+                 "=r"(r[14]), "=r"(r[15])
+               : "r"(taddr + (16u << 16)));
 #pragma unroll
-  for (int q = 0; q < 4; ++q) m.off[q] = m.odd ? tile_off<HS>(q + 4, ce) : tile_off<HS>(q, ce);
-  return m;
-}
-__device__ __forceinline__ void store_col16(uint8_t* tile, const ColMap& m, const float (&x)[16]) {
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    if (i & 4) continue;
-    const int i2 = i ^ 4;
-    const float send = m.odd ? x[i] : x[i2];
-    const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
-    const float lo = m.odd ? recv : x[i];
-    const float hi = m.odd ? x[i2] : recv;
-    *reinterpret_cast<uint32_t*>(tile + m.off[i & 3] + (i & 8) * 128) = pack_bf2(lo, hi);
+  for (int h = 0; h < 2; ++h) {  // registers: (lane, col) = (rr, 2qd) (rr, 2qd+1) (rr+8, ..) x 2 col halves
+    x[2 * h][0] = __uint_as_float(r[8 * h + 0]);
+    x[2 * h][1] = __uint_as_float(r[8 * h + 1]);
+    x[2 * h + 1][0] = __uint_as_float(r[8 * h + 2]);
+    x[2 * h + 1][1] = __uint_as_float(r[8 * h + 3]);
+    x[2 * h][2] = __uint_as_float(r[8 * h + 4]);
+    x[2 * h][3] = __uint_as_float(r[8 * h + 5]);
+    x[2 * h + 1][2] = __uint_as_float(r[8 * h + 6]);
+    x[2 * h + 1][3] = __uint_as_float(r[8 * h + 7]);
   }
 }
+// wait for this thread's tcgen05.ld; the fragment is bound as an operand so no use
+// of it can be scheduled above the wait
+__device__ __forceinline__ void tmem_wait_frag(float (&x)[4][4]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+f"(x[0][0]), "+f"(x[0][1]), "+f"(x[0][2]), "+f"(x[0][3]), "+f"(x[1][0]), "+f"(x[1][1]),
+                 "+f"(x[1][2]), "+f"(x[1][3]), "+f"(x[2][0]), "+f"(x[2][1]), "+f"(x[2][2]), "+f"(x[2][3]),
+                 "+f"(x[3][0]), "+f"(x[3][1]), "+f"(x[3][2]), "+f"(x[3][3])
+               :
+               : "memory");
+}
+// byte offset of this lane's stmatrix/ldmatrix row address inside a swizzled 4 KiB
+// tile, token group tg = 0 (tg = 1 adds 1024 B): row (l & 7) of matrix k = l >> 3
+template <int HS>
+__device__ __forceinline__ uint32_t frag_row_off(int wq, int lane) {
+  const int r = lane & 7, k = lane >> 3;
+  return (uint32_t)((wq >> 1) * HS + r * 128 + (((4 * (wq & 1) + k) ^ r) << 4));
+}
+__device__ __forceinline__ void stsm_t(uint8_t* p, uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
+  asm volatile("stmatrix.sync.aligned.m8n8.x4.trans.shared.b16 [%0], {%1, %2, %3, %4};" ::"r"(su32(p)), "r"(r0),
+               "r"(r1), "r"(r2), "r"(r3)
+               : "memory");
+}
+__device__ __forceinline__ void ldsm_t(const uint8_t* p, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(su32(p))
+               : "memory");
+}
+// store x[k][m] (rounded once to bf16) into a swizzled tile; ro = frag_row_off
+__device__ __forceinline__ void store_frag(uint8_t* tile, uint32_t ro, const float (&x)[4][4]) {
+#pragma unroll
+  for (int tg = 0; tg < 2; ++tg)
+    stsm_t(tile + ro + 1024 * tg, pack_bf2(x[0][2 * tg], x[0][2 * tg + 1]), pack_bf2(x[1][2 * tg], x[1][2 * tg + 1]),
+           pack_bf2(x[2][2 * tg], x[2][2 * tg + 1]), pack_bf2(x[3][2 * tg], x[3][2 * tg + 1]));
+}
+// load a bf16 tile's elements in fragment order: t[k][tg] = bf16x2 (tokens 2qd+8tg, +1; channel c_k)
+__device__ __forceinline__ void load_frag(const uint8_t* tile, uint32_t ro, uint32_t (&t)[2][4]) {
+  ldsm_t(tile + ro, t[0]);
+  ldsm_t(tile + ro + 1024, t[1]);
+}
+__device__ __forceinline__ float2 bf2f(uint32_t w) {
+  return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
+}
+// the value v held by lane (rr + 8k) for k = 0..3 (channel c_k of a 32x32b TMEM read)
+__device__ __forceinline__ void chan4(float v, int rr, float (&o)[4]) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) o[k] = __shfl_sync(0xffffffffu, v, rr + 8 * k);
+}
+// aux arrays (g, r, gs) are stored per block in fragment token order: [qd][m]
+__device__ __forceinline__ int aux_perm(int i) { return 4 * ((i & 7) >> 1) + 2 * (i >> 3) + (i & 1); }
 
 // ---------------------------------------------------------------------------
 // the kernel
@@ -762,21 +791,21 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
           hi.z = pack_bf2(Lc[12], Lc[13]); hi.w = pack_bf2(Lc[14], Lc[15]);
           *reinterpret_cast<uint4*>(l + ltile_off(0, col)) = lo;
           *reinterpret_cast<uint4*>(l + ltile_off(8, col)) = hi;
-          if constexpr (C::BWD) gr[S::kAuxBlk * k + 16 + col] = prod;  // r_t[j] = L[15][j]
+          // aux arrays in the epilogue's fragment token order (aux_perm)
+          if constexpr (C::BWD) gr[S::kAuxBlk * k + 16 + aux_perm(col)] = prod;  // r_t[j] = L[15][j]
           if (col == 0) {
-            // g_t[i] = a_t[0] L_t[i][0] = a_t[0] ... a_t[i], fp32
-            float g[16];
+            // g_t[i] = a_t[0] L_t[i][0] = a_t[0] ... a_t[i], fp32;
+            // gs[i] = g_t[i-1] (gs[0] = 1)
+            float g[17];
+            g[0] = 1.f;
 #pragma unroll
-            for (int i = 0; i < 16; ++i) g[i] = a[0] * Lc[i];
+            for (int i = 0; i < 16; ++i) g[i + 1] = a[0] * Lc[i];
             float4* gp = reinterpret_cast<float4*>(gr + S::kAuxBlk * k);
-            gp[0] = make_float4(g[0], g[1], g[2], g[3]);
-            gp[1] = make_float4(g[4], g[5], g[6], g[7]);
-            gp[2] = make_float4(g[8], g[9], g[10], g[11]);
-            gp[3] = make_float4(g[12], g[13], g[14], g[15]);
-            gp[8] = make_float4(1.f, g[0], g[1], g[2]);  // gs: g shifted by one token
-            gp[9] = make_float4(g[3], g[4], g[5], g[6]);
-            gp[10] = make_float4(g[7], g[8], g[9], g[10]);
-            gp[11] = make_float4(g[11], g[12], g[13], g[14]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              gp[q] = make_float4(g[2 * q + 1], g[2 * q + 2], g[2 * q + 9], g[2 * q + 10]);
+              gp[8 + q] = make_float4(g[2 * q], g[2 * q + 1], g[2 * q + 8], g[2 * q + 9]);
+            }
           }
         }
       }
@@ -827,13 +856,15 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
       rw.template step<C::NPW>();
     }
   } else {
-    // ===================== epilogue groups: thread = channel c =====================
+    // ===================== epilogue groups: fragment layout (see tmem_ld_frag) =====================
+    // lane l = 4 rr + qd owns channels c_k = 32 wq + rr + 8k and tokens tk_m of every block
     const int grp = warp >> 2;                       // epilogue group, items j = grp mod NG
     const int wq = warp & 3;                         // TMEM lane quarter
-    const int c = threadIdx.x & 127;                 // channel == TMEM lane
+    const int qd = lane & 3, rr = lane >> 2;
+    const int cb = 32 * wq + rr;                     // channel c_0
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+    const uint32_t fro = frag_row_off<S::kHS>(wq, lane);
     const bool leader = (threadIdx.x & 127) == 0;   // trace only
-    const ColMap cmap = col_map<S::kHS>(c, lane);
     Cursor cur;
     if (grp < n_items) cur.init(W.first + grp, nbi, H);
     Ring<NI> ri;
@@ -852,7 +883,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
       uint8_t* st = sin + ri.s * S::kIn;
       uint8_t* ot = sout + ro.s * S::kOut;
       const float* gr = reinterpret_cast<const float*>(aux + rw.s * S::kAux);
-      const int64_t co = cur.line * kD + c;
+      const int64_t co = cur.line * kD + cb;          // carry / mu index of c_0
       const uint32_t tslot = tmem_base + lane_base + (uint32_t)(rw.s * kItemCols);
       mbar_wait(&ready[rw.s], rw.ph);
       tc_fence_after();
@@ -860,20 +891,30 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
       // 1) neighbour reads first, so the neighbours' work slots are released early:
       //    carrier entering block t0: v = w_{t0-1}[15], the last block of item j-1;
       //    backward: mu of the item's last block from block 0 of item j+1
-      float vprev = 0.f, mu_last = 0.f;
+      float v[4] = {0.f, 0.f, 0.f, 0.f}, mu_last[4] = {0.f, 0.f, 0.f, 0.f};
       if (!halo) {
-        if (t0 == 0) vprev = p.carry_in ? p.carry_in[co] : 0.f;  // v_{-1}
-        else vprev = tmem_ld1(tmem_base + lane_base + (uint32_t)(rp.s * kItemCols + (BPI - 1) * C::COLS + kWo + 15));
+        if (t0 == 0) {  // v_{-1}
+          if (p.carry_in) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[k] = p.carry_in[co + 8 * k];
+          }
+        } else {
+          float x = tmem_ld1(tmem_base + lane_base + (uint32_t)(rp.s * kItemCols + (BPI - 1) * C::COLS + kWo + 15));
+          tmem_wait_f(x);
+          chan4(x, rr, v);
+        }
         if constexpr (C::BWD) {
           if (t0 + nblk == nb) {
-            mu_last = p.mu_in ? p.mu_in[co] : 0.f;
+            if (p.mu_in) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k) mu_last[k] = p.mu_in[co + 8 * k];
+            }
           } else {  // mu_t = a_{t+1}[0] lambda_{t+1}[0]
-            const float l0 = tmem_ld1(tmem_base + lane_base + (uint32_t)(rn.s * kItemCols + kLo));
-            tmem_wait_ld();
-            mu_last = reinterpret_cast<const float*>(aux + rn.s * S::kAux)[0] * l0;  // g[0] = a[0]
+            float l0 = tmem_ld1(tmem_base + lane_base + (uint32_t)(rn.s * kItemCols + kLo));
+            tmem_wait_f(l0);
+            chan4(reinterpret_cast<const float*>(aux + rn.s * S::kAux)[0] * l0, rr, mu_last);  // g[0] = a[0]
           }
         }
-        tmem_wait_ld();
       }
       tc_fence_before();
       __syncwarp();
@@ -883,104 +924,148 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
       }
       mbar_wait(&oempty[ro.s], ro.ph ^ 1);
       float* rb = red + ro.s * (4 * 16 * BPI);  // this slot's da partials [4 warps][16*BPI tokens]
-      // 2) the item's blocks, in order (the carrier passes block to block in a register)
+      // 2) the item's blocks, in order (the carrier passes block to block in registers)
       if (!halo) {
 #pragma unroll 1
-        for (int k = 0; k < nblk; ++k) {
-          const int64_t t = t0 + k;
-          float g[16], w[16];
-          if constexpr (!C::BWD || C::MIX) {  // SWR backward needs only w[i-1] (wsh) and w[15]
-            load16(reinterpret_cast<const float4*>(gr + S::kAuxBlk * k), g);
-            tmem_ld16(tslot + k * C::COLS + kWo, w);
-          } else {
-            w[15] = tmem_ld1(tslot + k * C::COLS + kWo + 15);
-          }
+        for (int kb = 0; kb < nblk; ++kb) {
+          const int64_t t = t0 + kb;
+          const float* ga = gr + S::kAuxBlk * kb;  // [g 16 | r 16 | gs 16], fragment order
           if constexpr (!C::BWD) {
-            tmem_wait_ld();
-            float out[16];
-            const float2 v2 = make_float2(vprev, vprev);
+            float w[4][4];
+            tmem_ld_frag(tslot + kb * C::COLS + kWo, w);
+            const float4 g4 = reinterpret_cast<const float4*>(ga)[qd];
+            tmem_wait_frag(w);
+            const float2 gA = make_float2(g4.x, g4.y), gB = make_float2(g4.z, g4.w);
+            float out[4][4];
 #pragma unroll
-            for (int i = 0; i < 16; i += 2) {  // Pass II: x~ = w + g v (packed pairs)
-              const float2 o = f2fma(make_float2(g[i], g[i + 1]), v2, make_float2(w[i], w[i + 1]));
-              out[i] = o.x;
-              out[i + 1] = o.y;
+            for (int k = 0; k < 4; ++k) {  // Pass II: x~ = w + g v, packed token pairs
+              const float2 v2 = make_float2(v[k], v[k]);
+              const float2 o0 = f2fma(gA, v2, make_float2(w[k][0], w[k][1]));
+              const float2 o1 = f2fma(gB, v2, make_float2(w[k][2], w[k][3]));
+              out[k][0] = o0.x; out[k][1] = o0.y; out[k][2] = o1.x; out[k][3] = o1.y;
             }
-            if constexpr (C::MIX) {
-              const uint8_t* t_q = S::tile(st, k, 0);
-              const uint8_t* t_v = S::tile(st, k, 2);
+            if constexpr (C::MIX) {  // post-gate with residual: y = q x~ + v
+              uint32_t tq[2][4], tv[2][4];
+              load_frag(S::tile(st, kb, 0), fro, tq);
+              load_frag(S::tile(st, kb, 2), fro, tv);
 #pragma unroll
-              for (int i = 0; i < 16; ++i) {  // post-gate with residual: y = q x~ + v
-                const uint32_t o = tile_off<S::kHS>(i, c);
-                out[i] = fmaf(bf(t_q, o), out[i], bf(t_v, o));
-              }
+              for (int k = 0; k < 4; ++k)
+#pragma unroll
+                for (int tg = 0; tg < 2; ++tg) {
+                  const float2 o = f2fma(bf2f(tq[tg][k]), make_float2(out[k][2 * tg], out[k][2 * tg + 1]),
+                                         bf2f(tv[tg][k]));
+                  out[k][2 * tg] = o.x;
+                  out[k][2 * tg + 1] = o.y;
+                }
             }
-            __syncwarp();
-            store_col16(S::tile(ot, k, 0), cmap, out);
-            if (t == nb - 1 && p.carry_out) p.carry_out[co] = w[15];
+            store_frag(S::tile(ot, kb, 0), fro, out);
+            if (t == nb - 1 && p.carry_out && qd == 3) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k) p.carry_out[co + 8 * k] = w[k][3];  // w_t[15]
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[k] = __shfl_sync(0xffffffffu, w[k][3], lane | 3);  // v_t = w_t[15]
           } else {
-            float lam[16];
-            tmem_ld16(tslot + k * C::COLS + kLo, lam);
-            float wsh[16];  // wsh[j] = w[j-1] (column kWo-1 = lambda[15] lands in wsh[0], unused)
-            tmem_ld16(tslot + k * C::COLS + kWo - 1, wsh);
-            float mu = mu_last;
-            if (k + 1 < nblk) {  // next block inside this item
-              const float l0 = tmem_ld1(tslot + (k + 1) * C::COLS + kLo);
-              tmem_wait_ld();
-              mu = gr[S::kAuxBlk * (k + 1)] * l0;
+            // lambda and w of the block; tcgen05.ld.16x256b needs 8-column alignment, so
+            // w[i-1] is formed by shuffles inside the lane quad (the token order of tk_m)
+            float lam[4][4], w[4][4];
+            tmem_ld_frag(tslot + kb * C::COLS + kLo, lam);
+            tmem_ld_frag(tslot + kb * C::COLS + kWo, w);
+            float mu[4] = {mu_last[0], mu_last[1], mu_last[2], mu_last[3]};
+            if (kb + 1 < nblk) {  // next block inside this item: mu_t = a_{t+1}[0] lambda_{t+1}[0]
+              float l0 = tmem_ld1(tslot + (kb + 1) * C::COLS + kLo);
+              tmem_wait_f(l0);
+              chan4(ga[S::kAuxBlk] * l0, rr, mu);
             }
-            tmem_wait_ld();
-            float r[16];
-            load16(reinterpret_cast<const float4*>(gr + S::kAuxBlk * k + 16), r);
-            float gs[16];
-            load16(reinterpret_cast<const float4*>(gr + S::kAuxBlk * k + 32), gs);  // gs[i] = g[i-1]
-            float part[16], du[16];
-            const float2 v2 = make_float2(vprev, vprev), mu2 = make_float2(mu, mu);
+            tmem_wait_frag(lam);
+            tmem_wait_frag(w);
+            float wsh[4][4];  // wsh[k][m] = w[tk_m - 1], w[-1] = 0
+            const int src = (lane & ~3) | ((lane + 3) & 3);  // lane - 1 inside the quad (qd 0 <- qd 3)
 #pragma unroll
-            for (int i = 0; i < 16; i += 2) {  // packed token pairs (i, i+1)
-              const float2 lam2 = make_float2(lam[i], lam[i + 1]);
-              const float2 rmu = f2mul(make_float2(r[i], r[i + 1]), mu2);        // r mu
-              const float2 d2 = f2fma(make_float2(r[i], r[i + 1]), mu2, lam2);   // du = lambda + r mu
-              const float2 wp = make_float2(i > 0 ? wsh[i] : 0.f, wsh[i + 1]);  // w[i-1], w[i]
-              const float2 xp = f2fma(make_float2(gs[i], gs[i + 1]), v2, wp);    // x~[i-1] = w[i-1] + g[i-1] v
-              const float2 pt = f2fma(lam2, xp, f2mul(rmu, wp));                 // da partial
-              du[i] = d2.x;
-              du[i + 1] = d2.y;
-              part[i] = pt.x;
-              part[i + 1] = pt.y;
+            for (int k = 0; k < 4; ++k) {
+              const float x0 = __shfl_sync(0xffffffffu, w[k][1], src);                    // token 2qd - 1
+              const float x2 = __shfl_sync(0xffffffffu, qd == 3 ? w[k][1] : w[k][3], src);  // token 7 + 2qd
+              wsh[k][0] = qd == 0 ? 0.f : x0;
+              wsh[k][1] = w[k][0];
+              wsh[k][2] = x2;
+              wsh[k][3] = w[k][2];
             }
-            if (t == 0 && p.mu_out) p.mu_out[co] = gr[S::kAuxBlk * k] * lam[0];  // a_0[0] lambda_0[0]
-            __syncwarp();
+            const float4 r4 = reinterpret_cast<const float4*>(ga + 16)[qd];
+            const float4 s4 = reinterpret_cast<const float4*>(ga + 32)[qd];  // gs = g shifted by one
+            const float2 rA = make_float2(r4.x, r4.y), rB = make_float2(r4.z, r4.w);
+            const float2 sA = make_float2(s4.x, s4.y), sB = make_float2(s4.z, s4.w);
+            float du[4][4], part[4][4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float2 v2 = make_float2(v[k], v[k]), mu2 = make_float2(mu[k], mu[k]);
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {  // token pairs (m, m+1) = (2h, 2h+1)
+                const float2 r2 = h ? rB : rA, s2 = h ? sB : sA;
+                const float2 lam2 = make_float2(lam[k][2 * h], lam[k][2 * h + 1]);
+                const float2 wp = make_float2(wsh[k][2 * h], wsh[k][2 * h + 1]);  // w[i-1]
+                const float2 rmu = f2mul(r2, mu2);                          // r mu
+                const float2 d2 = f2fma(r2, mu2, lam2);                     // du = lambda + r mu
+                const float2 xp = f2fma(s2, v2, wp);                        // x~[i-1] = w[i-1] + g[i-1] v
+                const float2 pt = f2fma(lam2, xp, f2mul(rmu, wp));          // da partial
+                du[k][2 * h] = d2.x; du[k][2 * h + 1] = d2.y;
+                part[k][2 * h] = pt.x; part[k][2 * h + 1] = pt.y;
+              }
+            }
+            if (t == 0 && p.mu_out && qd == 0) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k) p.mu_out[co + 8 * k] = ga[0] * lam[k][0];  // a_0[0] lambda_0[0]
+            }
             if constexpr (!C::MIX) {
-              store_col16(S::tile(ot, k, 0), cmap, du);
+              store_frag(S::tile(ot, kb, 0), fro, du);
             } else {
-              const uint8_t* t_dy = S::tile(st, k, 3);
-              const uint8_t* t_k = S::tile(st, k, 1);
-              const uint8_t* t_v = S::tile(st, k, 2);
-              float o16[16], dyv[16];
+              const float4 g4 = reinterpret_cast<const float4*>(ga)[qd];
+              const float2 gA = make_float2(g4.x, g4.y), gB = make_float2(g4.z, g4.w);
+              uint32_t tdy[2][4], tk[2][4], tv[2][4];
+              load_frag(S::tile(st, kb, 3), fro, tdy);
+              load_frag(S::tile(st, kb, 1), fro, tk);
+              load_frag(S::tile(st, kb, 2), fro, tv);
+              float o[4][4];
 #pragma unroll
-              for (int i = 0; i < 16; ++i) {  // dq = dy x~
-                const uint32_t o = tile_off<S::kHS>(i, c);
-                dyv[i] = bf(t_dy, o);
-                o16[i] = dyv[i] * fmaf(g[i], vprev, w[i]);
-              }
-              __syncwarp();
-              store_col16(S::tile(ot, k, 0), cmap, o16);
+              for (int k = 0; k < 4; ++k) {  // dq = dy x~,  x~ = w + g v
+                const float2 v2 = make_float2(v[k], v[k]);
 #pragma unroll
-              for (int i = 0; i < 16; ++i) {  // dv = du^ k + dy ; dk = du^ v
-                const uint32_t o = tile_off<S::kHS>(i, c);
-                o16[i] = fmaf(du[i], bf(t_k, o), dyv[i]);
-                du[i] *= bf(t_v, o);
+                for (int h = 0; h < 2; ++h) {
+                  const float2 x2 = f2fma(h ? gB : gA, v2, make_float2(w[k][2 * h], w[k][2 * h + 1]));
+                  const float2 q2 = f2mul(bf2f(tdy[h][k]), x2);
+                  o[k][2 * h] = q2.x; o[k][2 * h + 1] = q2.y;
+                }
               }
-              __syncwarp();
-              store_col16(S::tile(ot, k, 2), cmap, o16);
-              store_col16(S::tile(ot, k, 1), cmap, du);
+              store_frag(S::tile(ot, kb, 0), fro, o);
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {  // dv = du^ k + dy ; dk = du^ v
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                  const float2 d2 = make_float2(du[k][2 * h], du[k][2 * h + 1]);
+                  const float2 dv2 = f2fma(d2, bf2f(tk[h][k]), bf2f(tdy[h][k]));
+                  const float2 dk2 = f2mul(d2, bf2f(tv[h][k]));
+                  o[k][2 * h] = dv2.x; o[k][2 * h + 1] = dv2.y;
+                  du[k][2 * h] = dk2.x; du[k][2 * h + 1] = dk2.y;
+                }
+              }
+              store_frag(S::tile(ot, kb, 2), fro, o);
+              store_frag(S::tile(ot, kb, 1), fro, du);
             }
-            // da: transpose-reduce over the warp's 32 channels, partials to SMEM
-            int tok = 0;
-            GroupReduce<16, 16>::run(part, lane, tok);
-            if ((lane & 1) == 0) rb[wq * (16 * BPI) + k * 16 + tok] = part[0];
+            // da: sum the thread's 4 channels, then a transpose-reduce of the 4 token
+            // sums over the 8 lanes sharing qd (lane bits 2..4); fixed order, no atomics
+            float s[4];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) s[m] = ((part[0][m] + part[1][m]) + part[2][m]) + part[3][m];
+            const bool u16 = lane & 16, u8 = lane & 8;
+            const float a0 = (u16 ? s[2] : s[0]) + __shfl_xor_sync(0xffffffffu, u16 ? s[0] : s[2], 16);
+            const float a1 = (u16 ? s[3] : s[1]) + __shfl_xor_sync(0xffffffffu, u16 ? s[1] : s[3], 16);
+            float b = (u8 ? a1 : a0) + __shfl_xor_sync(0xffffffffu, u8 ? a0 : a1, 8);
+            b += __shfl_xor_sync(0xffffffffu, b, 4);
+            if ((lane & 4) == 0) {  // lane holds m = 2 u16 + u8: token 8 u16 + 2 qd + u8
+              rb[wq * (16 * BPI) + kb * 16 + (u16 ? 8 : 0) + 2 * qd + (u8 ? 1 : 0)] = b;
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[k] = __shfl_sync(0xffffffffu, w[k][3], lane | 3);  // v_t = w_t[15]
           }
-          vprev = w[15];
         }
       }
       // 3) this warp's outputs (and da partials) are in the output slot: hand them to

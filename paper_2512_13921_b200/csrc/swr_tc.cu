@@ -73,30 +73,40 @@ constexpr int kHalf = 2048;      // one 64-channel half: 16 rows x 128 B, 128B-s
 #ifndef SWR_MB_NI
 #define SWR_MB_NI 8
 #endif
+#ifndef SWR_B_TS
+#define SWR_B_TS 1
+#endif
+#ifndef SWR_MB_TS
+#define SWR_MB_TS 1
+#endif
 template <int OP>
 struct Cfg;
 template <>
 struct Cfg<0> {  // swr_fwd: in u;  out x
   static constexpr int NT = 1, NP = 0, BPI = 4, NI = SWR_F_NI, NW = 8, NO = SWR_F_NO, COLS = 16, NPW = SWR_F_NPW, NOUT = 1, NG = 3;
   static constexpr int TU = 0, TG = 0;  // A-operand regions of W and lambda
+  static constexpr int TS = 1;          // epilogue token split (warps per lane quarter)
   static constexpr bool BWD = false, MIX = false;
 };
 template <>
 struct Cfg<1> {  // swr_bwd: in u, G;  out du
   static constexpr int NT = 2, NP = 0, BPI = 2, NI = SWR_B_NI, NW = 8, NO = 4, COLS = 32, NPW = SWR_B_NPW, NOUT = 1, NG = SWR_B_NG;
   static constexpr int TU = 0, TG = 1;
+  static constexpr int TS = SWR_B_TS;
   static constexpr bool BWD = true, MIX = false;
 };
 template <>
 struct Cfg<2> {  // mix fwd: in q, k, v;  out y;  prep u^ = k v (over k)
   static constexpr int NT = 3, NP = 0, BPI = 2, NI = 6, NW = SWR_MF_NW, NO = 4, COLS = 16, NPW = SWR_MF_NPW, NOUT = 1, NG = 3;
   static constexpr int TU = 1, TG = 0;
+  static constexpr int TS = 1;
   static constexpr bool BWD = false, MIX = true;
 };
 template <>
 struct Cfg<3> {  // mix bwd: in q, k, v, dy;  out dq, dk, dv;  prep u^ = k v (region 4), G = dy q (over q)
   static constexpr int NT = 4, NP = 1, BPI = 1, NI = SWR_MB_NI, NW = 8, NO = 3, COLS = 32, NPW = 4, NOUT = 3, NG = 3;
   static constexpr int TU = 4, TG = 0;
+  static constexpr int TS = SWR_MB_TS;
   static constexpr bool BWD = true, MIX = true;
 };
 
@@ -257,17 +267,22 @@ __device__ __forceinline__ void trace(const Params& p, int64_t j, int ev) {
   }
 #endif
 }
-// diagnostics: per-CTA %globaltimer span (ns) after the per-item area: slot 16*n + 2*cta + e
+// diagnostics: per-CTA %globaltimer span (ns) and SM id after the per-item area:
+// slot 16*n + 4*cta + {0: start, 1: end, 2: smid}
 __device__ __forceinline__ void trace_cta(const Params& p, int e) {
 #if SWR_TRACE
   if (p.trace != nullptr) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    p.trace[16 * p.trace_n + 2 * blockIdx.x + e] = t;
+    p.trace[16 * p.trace_n + 4 * blockIdx.x + e] = t;
+    if (e == 0) {
+      uint32_t sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      p.trace[16 * p.trace_n + 4 * blockIdx.x + 2] = sm;
+    }
   }
 #endif
 }
-// wait with the loaded value bound as an operand (no use can move above the wait)
 __device__ __forceinline__ void tmem_wait_f(float& x) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" : "+f"(x) : : "memory");
 }
@@ -392,20 +407,10 @@ struct Ring {
   }
 };
 
-// packed fp32x2 arithmetic (sm_100 FFMA2 / FMUL2 / FADD2): one instruction for two lanes of work
-__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
-  uint64_t d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d)
-      : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)),
-        "l"(*reinterpret_cast<uint64_t*>(&c)));
-  return *reinterpret_cast<float2*>(&d);
-}
-__device__ __forceinline__ float2 f2mul(float2 a, float2 b) {
-  uint64_t d;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d)
-      : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)));
-  return *reinterpret_cast<float2*>(&d);
-}
+// packed fp32x2 arithmetic (sm_100 FFMA2 / FMUL2): one instruction for two lanes of
+// work; the builtins leave register pairing to ptxas
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 f2mul(float2 a, float2 b) { return __fmul2_rn(a, b); }
 
 
 // pack two fp32 into bf16x2 (lo = first)
@@ -479,14 +484,14 @@ __device__ __forceinline__ void ldsm_t(const uint8_t* p, uint32_t (&r)[4]) {
                : "memory");
 }
 // store x[k][m] (rounded once to bf16) into a swizzled tile; ro = frag_row_off
-__device__ __forceinline__ void store_frag(uint8_t* tile, uint32_t ro, const float (&x)[4][4]) {
+__device__ __forceinline__ void store_frag(uint8_t* tile, uint32_t ro, const float (&x)[4][4], int = 0) {
 #pragma unroll
   for (int tg = 0; tg < 2; ++tg)
     stsm_t(tile + ro + 1024 * tg, pack_bf2(x[0][2 * tg], x[0][2 * tg + 1]), pack_bf2(x[1][2 * tg], x[1][2 * tg + 1]),
            pack_bf2(x[2][2 * tg], x[2][2 * tg + 1]), pack_bf2(x[3][2 * tg], x[3][2 * tg + 1]));
 }
 // load a bf16 tile's elements in fragment order: t[k][tg] = bf16x2 (tokens 2qd+8tg, +1; channel c_k)
-__device__ __forceinline__ void load_frag(const uint8_t* tile, uint32_t ro, uint32_t (&t)[2][4]) {
+__device__ __forceinline__ void load_frag(const uint8_t* tile, uint32_t ro, uint32_t (&t)[2][4], int = 0) {
   ldsm_t(tile + ro, t[0]);
   ldsm_t(tile + ro + 1024, t[1]);
 }
@@ -498,7 +503,49 @@ __device__ __forceinline__ void chan4(float v, int rr, float (&o)[4]) {
 #pragma unroll
   for (int k = 0; k < 4; ++k) o[k] = __shfl_sync(0xffffffffu, v, rr + 8 * k);
 }
+// Half-block variants (token split TS = 2: two warps per lane quarter, each owning
+// the 8 tokens 8 ts .. 8 ts + 7): x[k][m] = (channel c_k, token 8 ts + 2 qd + m), m = 0, 1.
+// taddr already points at column col + 8 ts.
+__device__ __forceinline__ void tmem_ld_frag(uint32_t taddr, float (&x)[4][2]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x1.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x1.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr + (16u << 16)));
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    x[2 * h][0] = __uint_as_float(r[4 * h + 0]);
+    x[2 * h][1] = __uint_as_float(r[4 * h + 1]);
+    x[2 * h + 1][0] = __uint_as_float(r[4 * h + 2]);
+    x[2 * h + 1][1] = __uint_as_float(r[4 * h + 3]);
+  }
+}
+__device__ __forceinline__ void tmem_wait_frag(float (&x)[4][2]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+f"(x[0][0]), "+f"(x[0][1]), "+f"(x[1][0]), "+f"(x[1][1]), "+f"(x[2][0]), "+f"(x[2][1]),
+                 "+f"(x[3][0]), "+f"(x[3][1])
+               :
+               : "memory");
+}
+// store / load the token group tg of a half-block fragment
+__device__ __forceinline__ void store_frag(uint8_t* tile, uint32_t ro, const float (&x)[4][2], int tg) {
+  stsm_t(tile + ro + 1024 * tg, pack_bf2(x[0][0], x[0][1]), pack_bf2(x[1][0], x[1][1]), pack_bf2(x[2][0], x[2][1]),
+         pack_bf2(x[3][0], x[3][1]));
+}
+__device__ __forceinline__ void load_frag(const uint8_t* tile, uint32_t ro, uint32_t (&t)[1][4], int tg) {
+  ldsm_t(tile + ro + 1024 * tg, t[0]);
+}
 // aux arrays (g, r, gs) are stored per block in fragment token order: [qd][m]
+__device__ __forceinline__ void load_aux(const float* p, float (&o)[4]) {
+  const float4 x = *reinterpret_cast<const float4*>(p);
+  o[0] = x.x; o[1] = x.y; o[2] = x.z; o[3] = x.w;
+}
+__device__ __forceinline__ void load_aux(const float* p, float (&o)[2]) {
+  const float2 x = *reinterpret_cast<const float2*>(p);
+  o[0] = x.x; o[1] = x.y;
+}
 __device__ __forceinline__ int aux_perm(int i) { return 4 * ((i & 7) >> 1) + 2 * (i >> 3) + (i & 1); }
 
 // ---------------------------------------------------------------------------
@@ -522,8 +569,12 @@ __device__ __forceinline__ int aux_perm(int i) { return 4 * ((i & 7) >> 1) + 2 *
 #ifndef SWR_VAR
 #define SWR_VAR 0
 #endif
+#ifndef SWR_EPI_UNROLL
+#define SWR_EPI_UNROLL 1
+#endif
+constexpr int kEpiUnroll = SWR_EPI_UNROLL;
 template <int OP>
-__global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
+__global__ void __launch_bounds__((4 * Cfg<OP>::NG * Cfg<OP>::TS + Cfg<OP>::NPW + 4) * 32, 1)
     swr_tc_kernel(const __grid_constant__ Maps maps, const Params p) {
   using C = Cfg<OP>;
   using S = Stage<OP>;
@@ -533,7 +584,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
   // w is preceded by a valid column and can also be read shifted by one (w[i-1]).
   constexpr int kWo = C::BWD ? 16 : 0, kLo = 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int kPrepW0 = 4 * NG, kProdW = kPrepW0 + C::NPW, kMmaW = kProdW + 1, kStoreW = kMmaW + 1,
+  constexpr int kPrepW0 = 4 * NG * C::TS, kProdW = kPrepW0 + C::NPW, kMmaW = kProdW + 1, kStoreW = kMmaW + 1,
                 kRetW = kStoreW + 1;
 
   // 1024-aligned base for the 128B-swizzle atoms.  Offset the __shared__ array
@@ -570,14 +621,14 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
   static_assert(NO >= NG && NW >= NG, "epilogue group within one phase");
   static_assert((3 * NI + 3 * NW + 2 * NO) * 8 + 8 <= 1024 && NO * 4 * 16 * BPI * 4 <= 3072, "scratch budget");
   static_assert(S::kBytes + 1024 <= 227 * 1024, "shared memory budget");
-  constexpr int kUsers = (C::BWD ? 3 : 2) * 4;  // users x epilogue warps
+  constexpr int kUsers = (C::BWD ? 3 : 2) * 4 * C::TS;  // users x epilogue warps
 
   if (threadIdx.x == 0) {
     trace_cta(p, 0);
     for (int s = 0; s < NI; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&prepped[s], 1);
-      mbar_init(&inempty[s], C::MIX ? 4 : 1);
+      mbar_init(&inempty[s], C::MIX ? 4 * C::TS : 1);
     }
     for (int s = 0; s < NW; ++s) {
       mbar_init(&mmad[s], 1);
@@ -585,7 +636,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
       mbar_init(&wfree[s], kUsers);
     }
     for (int s = 0; s < NO; ++s) {
-      mbar_init(&ofull[s], 4);
+      mbar_init(&ofull[s], 4 * C::TS);
       mbar_init(&oempty[s], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -701,17 +752,20 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
   } else if (warp == kStoreW) {
     // ===================== TMA store, da sum, output-slot release =====================
     // lane 0 issues the TMA stores; backward: the warp sums the 4 epilogue warps'
-    // da partials of the slot in a fixed order (deterministic) and writes da
+    // da partials of the slot in a fixed order (deterministic) and writes da.  One
+    // bulk group per item (empty for halo items); a slot is released once the NEXT
+    // item's stores are issued and its own group has been read (wait_group.read 1),
+    // so consecutive stores overlap instead of serialising on the SMEM read.
     if (n_items > 0) {
       Cursor cur;
       cur.init(W.first, nbi, H);
-      Ring<NO> ro;
+      Ring<NO> ro, rprev;
       ro.init(0);
       for (int64_t j = 0; j < n_items; ++j) {
         mbar_wait(&ofull[ro.s], ro.ph);
         const bool halo = cur.gi < W.g0 || cur.gi >= W.g1;
-        if (!halo) {
-          if (lane == 0) {
+        if (lane == 0) {
+          if (!halo) {
             uint8_t* ot = sout + ro.s * S::kOut;
             const int tt = (int)(cur.m * BPI * kEll);
 #pragma unroll
@@ -719,10 +773,12 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
               tma_store_4d(&maps.out[x], S::region(ot, x), 0, cur.h, tt, cur.b);
               tma_store_4d(&maps.out[x], S::region(ot, x) + S::kHS, 64, cur.h, tt, cur.b);
             }
-            bulk_commit();
-            trace(p, j, 9);
           }
-          if constexpr (C::BWD) {
+          bulk_commit();
+          trace(p, j, 9);
+        }
+        if constexpr (C::BWD) {
+          if (!halo) {
             const float* rb = red + ro.s * (4 * 16 * BPI);
             __nv_bfloat16* dA = (__nv_bfloat16*)p.da + (int64_t)cur.b * p.sa_b + (int64_t)cur.h * p.sa_h;
 #pragma unroll
@@ -735,10 +791,13 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
               }
             }
           }
-          if (lane == 0) bulk_wait_read<0>();
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&oempty[ro.s]);
+        if (j >= 1) {  // release the previous item's slot once its stores have read it
+          if (lane == 0) bulk_wait_read<1>();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&oempty[rprev.s]);
+        }
+        rprev = ro;
         cur.next(nbi, H);
         ro.next();
       }
@@ -857,14 +916,21 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
     }
   } else {
     // ===================== epilogue groups: fragment layout (see tmem_ld_frag) =====================
-    // lane l = 4 rr + qd owns channels c_k = 32 wq + rr + 8k and tokens tk_m of every block
-    const int grp = warp >> 2;                       // epilogue group, items j = grp mod NG
+    // A group is 4 TS warps: lane quarter wq = warp & 3, token split ts = (warp >> 2) % TS.
+    // Lane l = 4 rr + qd owns channels c_k = 32 wq + rr + 8k and MT = 4 / TS tokens of every
+    // block: TS = 1: tk_m = 8 (m >> 1) + 2 qd + (m & 1);  TS = 2: tk_m = 8 ts + 2 qd + m.
+    // Token pairs (m, m+1) are packed fp32x2 lanes and one bf16x2 word of a fragment.
+    constexpr int TS = C::TS, MT = 4 / TS, NTG = 2 / TS;
+    const int grp = warp / (4 * TS);                 // epilogue group, items j = grp mod NG
     const int wq = warp & 3;                         // TMEM lane quarter
+    const int ts = (warp >> 2) & (TS - 1);           // token half (TS = 2)
     const int qd = lane & 3, rr = lane >> 2;
     const int cb = 32 * wq + rr;                     // channel c_0
+    const int col0 = 8 * ts;                         // first TMEM column (token) of this warp
+    const int am = 4 * qd + 2 * ts;                  // aux offset of this thread's tokens (aux_perm)
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
     const uint32_t fro = frag_row_off<S::kHS>(wq, lane);
-    const bool leader = (threadIdx.x & 127) == 0;   // trace only
+    const bool leader = (threadIdx.x % (128 * TS)) == 0;  // trace only
     Cursor cur;
     if (grp < n_items) cur.init(W.first + grp, nbi, H);
     Ring<NI> ri;
@@ -885,6 +951,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
       const float* gr = reinterpret_cast<const float*>(aux + rw.s * S::kAux);
       const int64_t co = cur.line * kD + cb;          // carry / mu index of c_0
       const uint32_t tslot = tmem_base + lane_base + (uint32_t)(rw.s * kItemCols);
+      const bool first_item = t0 == 0, last_item = t0 + nblk == nb;
       mbar_wait(&ready[rw.s], rw.ph);
       tc_fence_after();
       if (leader) trace(p, j, 7);
@@ -893,7 +960,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
       //    backward: mu of the item's last block from block 0 of item j+1
       float v[4] = {0.f, 0.f, 0.f, 0.f}, mu_last[4] = {0.f, 0.f, 0.f, 0.f};
       if (!halo) {
-        if (t0 == 0) {  // v_{-1}
+        if (first_item) {  // v_{-1}
           if (p.carry_in) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) v[k] = p.carry_in[co + 8 * k];
@@ -904,7 +971,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
           chan4(x, rr, v);
         }
         if constexpr (C::BWD) {
-          if (t0 + nblk == nb) {
+          if (last_item) {
             if (p.mu_in) {
 #pragma unroll
               for (int k = 0; k < 4; ++k) mu_last[k] = p.mu_in[co + 8 * k];
@@ -923,54 +990,69 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
         if (C::BWD && j + 1 < n_items) mbar_arrive(&wfree[rn.s]);  // as "previous" of item j+1
       }
       mbar_wait(&oempty[ro.s], ro.ph ^ 1);
-      float* rb = red + ro.s * (4 * 16 * BPI);  // this slot's da partials [4 warps][16*BPI tokens]
+      float* rb = red + ro.s * (4 * 16 * BPI);  // this slot's da partials [4 lane quarters][16*BPI tokens]
       // 2) the item's blocks, in order (the carrier passes block to block in registers)
       if (!halo) {
-#pragma unroll 1
+#pragma unroll kEpiUnroll
         for (int kb = 0; kb < nblk; ++kb) {
-          const int64_t t = t0 + kb;
           const float* ga = gr + S::kAuxBlk * kb;  // [g 16 | r 16 | gs 16], fragment order
+          const uint32_t tb = tslot + kb * C::COLS + col0;
           if constexpr (!C::BWD) {
-            float w[4][4];
-            tmem_ld_frag(tslot + kb * C::COLS + kWo, w);
-            const float4 g4 = reinterpret_cast<const float4*>(ga)[qd];
+            float w[4][MT];
+            tmem_ld_frag(tb + kWo, w);
+            float w15 = 0.f;
+            if constexpr (TS == 2) w15 = tmem_ld1(tslot + kb * C::COLS + kWo + 15);
+            float gg[MT];
+            load_aux(ga + am, gg);
             tmem_wait_frag(w);
-            const float2 gA = make_float2(g4.x, g4.y), gB = make_float2(g4.z, g4.w);
-            float out[4][4];
+            if constexpr (TS == 2) tmem_wait_f(w15);
+            float out[4][MT];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {  // Pass II: x~ = w + g v, packed token pairs
               const float2 v2 = make_float2(v[k], v[k]);
-              const float2 o0 = f2fma(gA, v2, make_float2(w[k][0], w[k][1]));
-              const float2 o1 = f2fma(gB, v2, make_float2(w[k][2], w[k][3]));
-              out[k][0] = o0.x; out[k][1] = o0.y; out[k][2] = o1.x; out[k][3] = o1.y;
+#pragma unroll
+              for (int h = 0; h < NTG; ++h) {
+                const float2 o = f2fma(make_float2(gg[2 * h], gg[2 * h + 1]), v2, make_float2(w[k][2 * h], w[k][2 * h + 1]));
+                out[k][2 * h] = o.x;
+                out[k][2 * h + 1] = o.y;
+              }
             }
             if constexpr (C::MIX) {  // post-gate with residual: y = q x~ + v
-              uint32_t tq[2][4], tv[2][4];
-              load_frag(S::tile(st, kb, 0), fro, tq);
-              load_frag(S::tile(st, kb, 2), fro, tv);
+              uint32_t tq[NTG][4], tv[NTG][4];
+              load_frag(S::tile(st, kb, 0), fro, tq, ts);
+              load_frag(S::tile(st, kb, 2), fro, tv, ts);
 #pragma unroll
               for (int k = 0; k < 4; ++k)
 #pragma unroll
-                for (int tg = 0; tg < 2; ++tg) {
-                  const float2 o = f2fma(bf2f(tq[tg][k]), make_float2(out[k][2 * tg], out[k][2 * tg + 1]),
-                                         bf2f(tv[tg][k]));
-                  out[k][2 * tg] = o.x;
-                  out[k][2 * tg + 1] = o.y;
+                for (int h = 0; h < NTG; ++h) {
+                  const float2 o = f2fma(bf2f(tq[h][k]), make_float2(out[k][2 * h], out[k][2 * h + 1]), bf2f(tv[h][k]));
+                  out[k][2 * h] = o.x;
+                  out[k][2 * h + 1] = o.y;
                 }
             }
-            store_frag(S::tile(ot, kb, 0), fro, out);
-            if (t == nb - 1 && p.carry_out && qd == 3) {
+            store_frag(S::tile(ot, kb, 0), fro, out, ts);
+            if (t0 + kb == nb - 1 && p.carry_out && qd == 3 && ts == TS - 1) {
 #pragma unroll
-              for (int k = 0; k < 4; ++k) p.carry_out[co + 8 * k] = w[k][3];  // w_t[15]
+              for (int k = 0; k < 4; ++k) p.carry_out[co + 8 * k] = w[k][MT - 1];  // w_t[15]
             }
+            if constexpr (TS == 1) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) v[k] = __shfl_sync(0xffffffffu, w[k][3], lane | 3);  // v_t = w_t[15]
+              for (int k = 0; k < 4; ++k) v[k] = __shfl_sync(0xffffffffu, w[k][3], lane | 3);  // v_t = w_t[15]
+            } else {
+              chan4(w15, rr, v);
+            }
           } else {
-            // lambda and w of the block; tcgen05.ld.16x256b needs 8-column alignment, so
-            // w[i-1] is formed by shuffles inside the lane quad (the token order of tk_m)
-            float lam[4][4], w[4][4];
-            tmem_ld_frag(tslot + kb * C::COLS + kLo, lam);
-            tmem_ld_frag(tslot + kb * C::COLS + kWo, w);
+            // lambda and w of the block.  tcgen05.ld.16x256b needs 8-column alignment, so
+            // w[i-1] is formed by shuffles inside the lane quad (and, for the second token
+            // half, w[7] from a 32x32b read)
+            float lam[4][MT], w[4][MT];
+            tmem_ld_frag(tb + kLo, lam);
+            tmem_ld_frag(tb + kWo, w);
+            float w15 = 0.f, w7 = 0.f;
+            if constexpr (TS == 2) {
+              w15 = tmem_ld1(tslot + kb * C::COLS + kWo + 15);
+              if (ts == 1) w7 = tmem_ld1(tslot + kb * C::COLS + kWo + 7);
+            }
             float mu[4] = {mu_last[0], mu_last[1], mu_last[2], mu_last[3]};
             if (kb + 1 < nblk) {  // next block inside this item: mu_t = a_{t+1}[0] lambda_{t+1}[0]
               float l0 = tmem_ld1(tslot + (kb + 1) * C::COLS + kLo);
@@ -979,67 +1061,81 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
             }
             tmem_wait_frag(lam);
             tmem_wait_frag(w);
-            float wsh[4][4];  // wsh[k][m] = w[tk_m - 1], w[-1] = 0
+            float wsh[4][MT];  // wsh[k][m] = w[tk_m - 1], w[-1] = 0
             const int src = (lane & ~3) | ((lane + 3) & 3);  // lane - 1 inside the quad (qd 0 <- qd 3)
+            if constexpr (TS == 1) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const float x0 = __shfl_sync(0xffffffffu, w[k][1], src);                    // token 2qd - 1
-              const float x2 = __shfl_sync(0xffffffffu, qd == 3 ? w[k][1] : w[k][3], src);  // token 7 + 2qd
-              wsh[k][0] = qd == 0 ? 0.f : x0;
-              wsh[k][1] = w[k][0];
-              wsh[k][2] = x2;
-              wsh[k][3] = w[k][2];
+              for (int k = 0; k < 4; ++k) {
+                const float x0 = __shfl_sync(0xffffffffu, w[k][1], src);                    // token 2qd - 1
+                const float x2 = __shfl_sync(0xffffffffu, qd == 3 ? w[k][1] : w[k][3], src);  // token 7 + 2qd
+                wsh[k][0] = qd == 0 ? 0.f : x0;
+                wsh[k][1] = w[k][0];
+                wsh[k][2] = x2;
+                wsh[k][3] = w[k][2];
+              }
+            } else {
+              tmem_wait_f(w15);
+              float w7c[4] = {0.f, 0.f, 0.f, 0.f};  // w[7] of c_k (first token of half 1 needs it)
+              if (ts == 1) {
+                tmem_wait_f(w7);
+                chan4(w7, rr, w7c);
+              }
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const float x0 = __shfl_sync(0xffffffffu, w[k][1], src);  // token 8ts + 2qd - 1
+                wsh[k][0] = qd == 0 ? w7c[k] : x0;
+                wsh[k][1] = w[k][0];
+              }
             }
-            const float4 r4 = reinterpret_cast<const float4*>(ga + 16)[qd];
-            const float4 s4 = reinterpret_cast<const float4*>(ga + 32)[qd];  // gs = g shifted by one
-            const float2 rA = make_float2(r4.x, r4.y), rB = make_float2(r4.z, r4.w);
-            const float2 sA = make_float2(s4.x, s4.y), sB = make_float2(s4.z, s4.w);
-            float du[4][4], part[4][4];
+            float rv[MT], sv[MT];
+            load_aux(ga + 16 + am, rv);
+            load_aux(ga + 32 + am, sv);  // gs = g shifted by one
+            float du[4][MT], part[4][MT];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const float2 v2 = make_float2(v[k], v[k]), mu2 = make_float2(mu[k], mu[k]);
 #pragma unroll
-              for (int h = 0; h < 2; ++h) {  // token pairs (m, m+1) = (2h, 2h+1)
-                const float2 r2 = h ? rB : rA, s2 = h ? sB : sA;
+              for (int h = 0; h < NTG; ++h) {  // token pairs (2h, 2h+1)
+                const float2 r2 = make_float2(rv[2 * h], rv[2 * h + 1]), s2 = make_float2(sv[2 * h], sv[2 * h + 1]);
                 const float2 lam2 = make_float2(lam[k][2 * h], lam[k][2 * h + 1]);
                 const float2 wp = make_float2(wsh[k][2 * h], wsh[k][2 * h + 1]);  // w[i-1]
-                const float2 rmu = f2mul(r2, mu2);                          // r mu
-                const float2 d2 = f2fma(r2, mu2, lam2);                     // du = lambda + r mu
-                const float2 xp = f2fma(s2, v2, wp);                        // x~[i-1] = w[i-1] + g[i-1] v
-                const float2 pt = f2fma(lam2, xp, f2mul(rmu, wp));          // da partial
+                // du = lambda + r mu;  da partial = lambda x~[i-1] + r mu w[i-1]
+                //                                 = du w[i-1] + g[i-1] (lambda v)
+                const float2 d2 = f2fma(r2, mu2, lam2);
+                const float2 pt = f2fma(s2, f2mul(lam2, v2), f2mul(d2, wp));
                 du[k][2 * h] = d2.x; du[k][2 * h + 1] = d2.y;
                 part[k][2 * h] = pt.x; part[k][2 * h + 1] = pt.y;
               }
             }
-            if (t == 0 && p.mu_out && qd == 0) {
+            if (t0 + kb == 0 && p.mu_out && qd == 0 && ts == 0) {
 #pragma unroll
               for (int k = 0; k < 4; ++k) p.mu_out[co + 8 * k] = ga[0] * lam[k][0];  // a_0[0] lambda_0[0]
             }
             if constexpr (!C::MIX) {
-              store_frag(S::tile(ot, kb, 0), fro, du);
+              store_frag(S::tile(ot, kb, 0), fro, du, ts);
             } else {
-              const float4 g4 = reinterpret_cast<const float4*>(ga)[qd];
-              const float2 gA = make_float2(g4.x, g4.y), gB = make_float2(g4.z, g4.w);
-              uint32_t tdy[2][4], tk[2][4], tv[2][4];
-              load_frag(S::tile(st, kb, 3), fro, tdy);
-              load_frag(S::tile(st, kb, 1), fro, tk);
-              load_frag(S::tile(st, kb, 2), fro, tv);
-              float o[4][4];
+              float gg[MT];
+              load_aux(ga + am, gg);
+              uint32_t tdy[NTG][4], tk[NTG][4], tv[NTG][4];
+              load_frag(S::tile(st, kb, 3), fro, tdy, ts);
+              load_frag(S::tile(st, kb, 1), fro, tk, ts);
+              load_frag(S::tile(st, kb, 2), fro, tv, ts);
+              float o[4][MT];
 #pragma unroll
               for (int k = 0; k < 4; ++k) {  // dq = dy x~,  x~ = w + g v
                 const float2 v2 = make_float2(v[k], v[k]);
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                  const float2 x2 = f2fma(h ? gB : gA, v2, make_float2(w[k][2 * h], w[k][2 * h + 1]));
+                for (int h = 0; h < NTG; ++h) {
+                  const float2 x2 = f2fma(make_float2(gg[2 * h], gg[2 * h + 1]), v2, make_float2(w[k][2 * h], w[k][2 * h + 1]));
                   const float2 q2 = f2mul(bf2f(tdy[h][k]), x2);
                   o[k][2 * h] = q2.x; o[k][2 * h + 1] = q2.y;
                 }
               }
-              store_frag(S::tile(ot, kb, 0), fro, o);
+              store_frag(S::tile(ot, kb, 0), fro, o, ts);
 #pragma unroll
               for (int k = 0; k < 4; ++k) {  // dv = du^ k + dy ; dk = du^ v
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
+                for (int h = 0; h < NTG; ++h) {
                   const float2 d2 = make_float2(du[k][2 * h], du[k][2 * h + 1]);
                   const float2 dv2 = f2fma(d2, bf2f(tk[h][k]), bf2f(tdy[h][k]));
                   const float2 dk2 = f2mul(d2, bf2f(tv[h][k]));
@@ -1047,24 +1143,35 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
                   du[k][2 * h] = dk2.x; du[k][2 * h + 1] = dk2.y;
                 }
               }
-              store_frag(S::tile(ot, kb, 2), fro, o);
-              store_frag(S::tile(ot, kb, 1), fro, du);
+              store_frag(S::tile(ot, kb, 2), fro, o, ts);
+              store_frag(S::tile(ot, kb, 1), fro, du, ts);
             }
-            // da: sum the thread's 4 channels, then a transpose-reduce of the 4 token
+            // da: sum the thread's 4 channels, then a transpose-reduce of the MT token
             // sums over the 8 lanes sharing qd (lane bits 2..4); fixed order, no atomics
-            float s[4];
+            float s[MT];
 #pragma unroll
-            for (int m = 0; m < 4; ++m) s[m] = ((part[0][m] + part[1][m]) + part[2][m]) + part[3][m];
+            for (int m = 0; m < MT; ++m) s[m] = ((part[0][m] + part[1][m]) + part[2][m]) + part[3][m];
             const bool u16 = lane & 16, u8 = lane & 8;
-            const float a0 = (u16 ? s[2] : s[0]) + __shfl_xor_sync(0xffffffffu, u16 ? s[0] : s[2], 16);
-            const float a1 = (u16 ? s[3] : s[1]) + __shfl_xor_sync(0xffffffffu, u16 ? s[1] : s[3], 16);
-            float b = (u8 ? a1 : a0) + __shfl_xor_sync(0xffffffffu, u8 ? a0 : a1, 8);
-            b += __shfl_xor_sync(0xffffffffu, b, 4);
-            if ((lane & 4) == 0) {  // lane holds m = 2 u16 + u8: token 8 u16 + 2 qd + u8
-              rb[wq * (16 * BPI) + kb * 16 + (u16 ? 8 : 0) + 2 * qd + (u8 ? 1 : 0)] = b;
+            if constexpr (TS == 1) {
+              const float a0 = (u16 ? s[2] : s[0]) + __shfl_xor_sync(0xffffffffu, u16 ? s[0] : s[2], 16);
+              const float a1 = (u16 ? s[3] : s[1]) + __shfl_xor_sync(0xffffffffu, u16 ? s[1] : s[3], 16);
+              float b = (u8 ? a1 : a0) + __shfl_xor_sync(0xffffffffu, u8 ? a0 : a1, 8);
+              b += __shfl_xor_sync(0xffffffffu, b, 4);
+              if ((lane & 4) == 0)  // lane holds m = 2 u16 + u8: token 8 u16 + 2 qd + u8
+                rb[wq * (16 * BPI) + kb * 16 + (u16 ? 8 : 0) + 2 * qd + (u8 ? 1 : 0)] = b;
+            } else {
+              float b = (u16 ? s[1] : s[0]) + __shfl_xor_sync(0xffffffffu, u16 ? s[0] : s[1], 16);
+              b += __shfl_xor_sync(0xffffffffu, b, 8);
+              b += __shfl_xor_sync(0xffffffffu, b, 4);
+              if ((lane & 12) == 0)  // lane holds m = u16: token 8 ts + 2 qd + u16
+                rb[wq * (16 * BPI) + kb * 16 + col0 + 2 * qd + (u16 ? 1 : 0)] = b;
             }
+            if constexpr (TS == 1) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) v[k] = __shfl_sync(0xffffffffu, w[k][3], lane | 3);  // v_t = w_t[15]
+              for (int k = 0; k < 4; ++k) v[k] = __shfl_sync(0xffffffffu, w[k][3], lane | 3);  // v_t = w_t[15]
+            } else {
+              chan4(w15, rr, v);
+            }
           }
         }
       }
@@ -1166,7 +1273,7 @@ static cudaError_t launch_op(const Params& p, cudaStream_t st, int sms) {
   }
   const int64_t total = p.B * p.H * ((p.nb + Cfg<OP>::BPI - 1) / Cfg<OP>::BPI);
   const int grid = (int)std::min<int64_t>(sms, std::max<int64_t>(total, 1));
-  constexpr int threads = (4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32;
+  constexpr int threads = (4 * Cfg<OP>::NG * Cfg<OP>::TS + Cfg<OP>::NPW + 4) * 32;
   swr_tc_kernel<OP><<<grid, threads, smem, st>>>(maps, p);
   return cudaGetLastError();
 }

@@ -20,7 +20,7 @@ else:
         lambda: P.phalanx_mix_bwd(g["q"], g["k"], g["v"], g["a"], g["dy"]))
 for _ in range(5):
     run()
-buf = torch.zeros(N * 16 + 2 * 160, dtype=torch.int64, device="cuda")
+buf = torch.zeros(N * 16 + 4 * 160, dtype=torch.int64, device="cuda")
 _lib.set_trace(buf.data_ptr(), N)
 flush = torch.empty(64 << 20, device="cuda")
 flush.zero_()
@@ -30,8 +30,11 @@ torch.cuda.synchronize()
 _lib.set_trace(None, 0)
 print(op, "kernel ms", e0.elapsed_time(e1))
 allb = buf.cpu().numpy()
-span = allb[N * 16:].reshape(-1, 2)
+span = allb[N * 16:].reshape(-1, 4)
 span = span[span[:, 0] > 0]
+order = np.argsort(span[:, 2])
+d_sm = (span[order, 1] - span[order, 0]) / 1e3
+print("span (us) by SM id:", " ".join(f"{int(span[i,2])}:{x:.0f}" for i, x in zip(order, d_sm)))
 st0 = span[:, 0].min()
 dur = (span[:, 1] - span[:, 0]) / 1e3
 print(f"CTAs {len(span)}: start spread {(span[:,0].max()-st0)/1e3:.1f} us, span min/med/max {dur.min():.1f}/{np.median(dur):.1f}/{dur.max():.1f} us, last end {(span[:,1].max()-st0)/1e3:.1f} us")

@@ -137,6 +137,9 @@ struct Stage {
   static __device__ __forceinline__ uint8_t* tile(uint8_t* st, int k, int x) {
     return region(st, x) + k * kHalf;
   }
+  static __device__ __forceinline__ uint32_t tile(uint32_t st, int k, int x) {  // shared-window address
+    return st + x * kRegion + k * kHalf;
+  }
 };
 
 template <int OP>
@@ -260,7 +263,7 @@ __device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
 #ifndef SWR_TRACE
 #define SWR_TRACE 0
 #endif
-__device__ __forceinline__ void trace(const Params& p, int64_t j, int ev) {
+__device__ __forceinline__ void trace(const Params& p, int j, int ev) {
 #if SWR_TRACE
   if (p.trace != nullptr && blockIdx.x == 0 && j < p.trace_n) {
     p.trace[j * 16 + ev] = clock64();  // SM cycles (all roles share the SM clock)
@@ -325,13 +328,13 @@ __device__ __forceinline__ uint32_t ltile_off(int i, int j) {
 // boundary falls inside a line.  Items are walked with an incremental cursor.
 // ---------------------------------------------------------------------------
 struct Work {
-  int64_t first, g0, g1, last;  // global item ids gi in [first, last)
+  int first, g0, g1, last;  // global item ids gi in [first, last) (< 2^31, tc_supported)
 };
 template <bool BWD>
-__device__ __forceinline__ Work work_of(int64_t total, int64_t nbi) {
+__device__ __forceinline__ Work work_of(int total, int nbi) {
   Work w;
-  w.g0 = (int64_t)blockIdx.x * total / gridDim.x;
-  w.g1 = ((int64_t)blockIdx.x + 1) * total / gridDim.x;
+  w.g0 = (int)((int64_t)blockIdx.x * total / gridDim.x);
+  w.g1 = (int)(((int64_t)blockIdx.x + 1) * total / gridDim.x);
   w.first = w.g0 - ((w.g0 < w.g1 && w.g0 % nbi != 0) ? 1 : 0);
   w.last = w.g1 + ((BWD && w.g0 < w.g1 && w.g1 % nbi != 0) ? 1 : 0);
   if (w.g0 >= w.g1) w.first = w.last = w.g0;
@@ -339,16 +342,16 @@ __device__ __forceinline__ Work work_of(int64_t total, int64_t nbi) {
 }
 
 struct Cursor {  // item gi = line * nbi + m; t0 = first block of the item
-  int64_t gi, m, line;
+  int gi, m, line;
   int b, h;
-  __device__ __forceinline__ void init(int64_t g, int64_t nbi, int64_t H) {
+  __device__ __forceinline__ void init(int g, int nbi, int H) {
     gi = g;
     line = g / nbi;
     m = g - line * nbi;
-    b = (int)(line / H);
-    h = (int)(line - (int64_t)b * H);
+    b = line / H;
+    h = line - b * H;
   }
-  __device__ __forceinline__ void next(int64_t nbi, int64_t H) {
+  __device__ __forceinline__ void next(int nbi, int H) {
     ++gi;
     if (++m == nbi) {
       m = 0;
@@ -359,7 +362,7 @@ struct Cursor {  // item gi = line * nbi + m; t0 = first block of the item
       }
     }
   }
-  __device__ __forceinline__ void step(int n, int64_t nbi, int64_t H) {  // n items forward
+  __device__ __forceinline__ void step(int n, int nbi, int H) {  // n items forward
     gi += n;
     m += n;
     while (m >= nbi) {
@@ -378,7 +381,7 @@ template <int NS>
 struct Ring {
   int s;
   uint32_t ph;
-  __device__ __forceinline__ void init(int64_t j) {
+  __device__ __forceinline__ void init(int j) {
     s = (int)(j % NS);
     ph = (uint32_t)((j / NS) & 1);
   }
@@ -472,26 +475,26 @@ __device__ __forceinline__ uint32_t frag_row_off(int wq, int lane) {
   const int r = lane & 7, k = lane >> 3;
   return (uint32_t)((wq >> 1) * HS + r * 128 + (((4 * (wq & 1) + k) ^ r) << 4));
 }
-__device__ __forceinline__ void stsm_t(uint8_t* p, uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
-  asm volatile("stmatrix.sync.aligned.m8n8.x4.trans.shared.b16 [%0], {%1, %2, %3, %4};" ::"r"(su32(p)), "r"(r0),
+__device__ __forceinline__ void stsm_t(uint32_t p, uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
+  asm volatile("stmatrix.sync.aligned.m8n8.x4.trans.shared.b16 [%0], {%1, %2, %3, %4};" ::"r"(p), "r"(r0),
                "r"(r1), "r"(r2), "r"(r3)
                : "memory");
 }
-__device__ __forceinline__ void ldsm_t(const uint8_t* p, uint32_t (&r)[4]) {
+__device__ __forceinline__ void ldsm_t(uint32_t p, uint32_t (&r)[4]) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-               : "r"(su32(p))
+               : "r"(p)
                : "memory");
 }
 // store x[k][m] (rounded once to bf16) into a swizzled tile; ro = frag_row_off
-__device__ __forceinline__ void store_frag(uint8_t* tile, uint32_t ro, const float (&x)[4][4], int = 0) {
+__device__ __forceinline__ void store_frag(uint32_t tile, uint32_t ro, const float (&x)[4][4], int = 0) {
 #pragma unroll
   for (int tg = 0; tg < 2; ++tg)
     stsm_t(tile + ro + 1024 * tg, pack_bf2(x[0][2 * tg], x[0][2 * tg + 1]), pack_bf2(x[1][2 * tg], x[1][2 * tg + 1]),
            pack_bf2(x[2][2 * tg], x[2][2 * tg + 1]), pack_bf2(x[3][2 * tg], x[3][2 * tg + 1]));
 }
 // load a bf16 tile's elements in fragment order: t[k][tg] = bf16x2 (tokens 2qd+8tg, +1; channel c_k)
-__device__ __forceinline__ void load_frag(const uint8_t* tile, uint32_t ro, uint32_t (&t)[2][4], int = 0) {
+__device__ __forceinline__ void load_frag(uint32_t tile, uint32_t ro, uint32_t (&t)[2][4], int = 0) {
   ldsm_t(tile + ro, t[0]);
   ldsm_t(tile + ro + 1024, t[1]);
 }
@@ -530,11 +533,11 @@ __device__ __forceinline__ void tmem_wait_frag(float (&x)[4][2]) {
                : "memory");
 }
 // store / load the token group tg of a half-block fragment
-__device__ __forceinline__ void store_frag(uint8_t* tile, uint32_t ro, const float (&x)[4][2], int tg) {
+__device__ __forceinline__ void store_frag(uint32_t tile, uint32_t ro, const float (&x)[4][2], int tg) {
   stsm_t(tile + ro + 1024 * tg, pack_bf2(x[0][0], x[0][1]), pack_bf2(x[1][0], x[1][1]), pack_bf2(x[2][0], x[2][1]),
          pack_bf2(x[3][0], x[3][1]));
 }
-__device__ __forceinline__ void load_frag(const uint8_t* tile, uint32_t ro, uint32_t (&t)[1][4], int tg) {
+__device__ __forceinline__ void load_frag(uint32_t tile, uint32_t ro, uint32_t (&t)[1][4], int tg) {
   ldsm_t(tile + ro + 1024 * tg, t[0]);
 }
 // aux arrays (g, r, gs) are stored per block in fragment token order: [qd][m]
@@ -595,6 +598,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG * Cfg<OP>::TS + Cfg<OP>::NPW 
   uint8_t* sout = smem + S::kOutBase;
   uint8_t* aux = smem + S::kAuxBase;
   uint8_t* scratch = smem + S::kScratch;
+  const uint32_t smem_s = su32(smem);
   uint64_t* full = reinterpret_cast<uint64_t*>(scratch);
   uint64_t* prepped = full + NI;
   uint64_t* inempty = prepped + NI;
@@ -652,11 +656,11 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG * Cfg<OP>::TS + Cfg<OP>::NPW 
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int64_t nb = p.nb, H = p.H;
-  const int64_t nbi = (nb + BPI - 1) / BPI;  // items per line
-  const int64_t total = p.B * H * nbi;
+  const int nb = (int)p.nb, H = (int)p.H;   // sizes < 2^31 (tc_supported)
+  const int nbi = (nb + BPI - 1) / BPI;       // items per line
+  const int total = (int)p.B * H * nbi;
   const Work W = work_of<C::BWD>(total, nbi);
-  const int64_t n_items = W.last - W.first;
+  const int n_items = W.last - W.first;
 
   if (warp == kProdW) {
     // ===================== TMA producer =====================
@@ -665,7 +669,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG * Cfg<OP>::TS + Cfg<OP>::NPW 
       cur.init(W.first, nbi, H);
       Ring<NI> ri;
       ri.init(0);
-      for (int64_t j = 0; j < n_items; ++j) {
+      for (int j = 0; j < n_items; ++j) {
         mbar_wait(&inempty[ri.s], ri.ph ^ 1);
         trace(p, j, 0);
         uint8_t* st = sin + ri.s * S::kIn;
@@ -692,7 +696,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG * Cfg<OP>::TS + Cfg<OP>::NPW 
       Ring<NW> rw;
       ri.init(0);
       rw.init(0);
-      for (int64_t j = 0; j < n_items; ++j) {
+      for (int j = 0; j < n_items; ++j) {
 #if SWR_VAR == 1
         mbar_wait(&full[ri.s], ri.ph);
 #endif
@@ -731,7 +735,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG * Cfg<OP>::TS + Cfg<OP>::NPW 
       ri.init(0);
       rw.init(0);
       rr.init(0);
-      for (int64_t j = 0; j < n_items; ++j) {
+      for (int j = 0; j < n_items; ++j) {
         mbar_wait(&mmad[rw.s], rw.ph);
         tc_fence_before();
         if constexpr (!C::MIX) mbar_arrive(&inempty[ri.s]);  // operands consumed
@@ -743,7 +747,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG * Cfg<OP>::TS + Cfg<OP>::NPW 
         ri.next();
         rw.next();
       }
-      for (int64_t jr = std::max<int64_t>(n_items - kBack, 0); jr < n_items; ++jr) {
+      for (int jr = max(n_items - kBack, 0); jr < n_items; ++jr) {
         mbar_arrive(&ready[rr.s]);
         rr.next();
       }
@@ -761,7 +765,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG * Cfg<OP>::TS + Cfg<OP>::NPW 
       cur.init(W.first, nbi, H);
       Ring<NO> ro, rprev;
       ro.init(0);
-      for (int64_t j = 0; j < n_items; ++j) {
+      for (int j = 0; j < n_items; ++j) {
         mbar_wait(&ofull[ro.s], ro.ph);
         const bool halo = cur.gi < W.g0 || cur.gi >= W.g1;
         if (lane == 0) {
@@ -784,7 +788,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG * Cfg<OP>::TS + Cfg<OP>::NPW 
 #pragma unroll
             for (int q0 = 0; q0 < 16 * BPI; q0 += 32) {
               const int q = q0 + lane;
-              const int64_t n = cur.m * BPI * kEll + q;
+              const int64_t n = (int64_t)cur.m * BPI * kEll + q;
               if (q < 16 * BPI && n < p.L) {
                 const float sum = ((rb[q] + rb[16 * BPI + q]) + rb[32 * BPI + q]) + rb[48 * BPI + q];
                 dA[n * p.sa_l] = __float2bfloat16_rn(sum);
@@ -814,7 +818,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG * Cfg<OP>::TS + Cfg<OP>::NPW 
     Ring<NW> rw;
     ri.init(pw);
     rw.init(pw);
-    for (int64_t j = pw; j < n_items; j += C::NPW) {
+    for (int j = pw; j < n_items; j += C::NPW) {
       mbar_wait(&full[ri.s], ri.ph);
       mbar_wait(&wfree[rw.s], rw.ph ^ 1);
       if (lane == 0) trace(p, j, 2);
@@ -824,8 +828,8 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG * Cfg<OP>::TS + Cfg<OP>::NPW 
       for (int kb = 0; kb < BPI; kb += 2) {
         const int k = kb + hf;
         if (k < BPI) {
-          const int64_t t = cur.m * BPI + k;
-          const int nval = (int)std::min<int64_t>(16, std::max<int64_t>(p.L - t * kEll, 0));  // valid tokens
+          const int t = cur.m * BPI + k;
+          const int nval = (int)std::min<int64_t>(16, std::max<int64_t>(p.L - (int64_t)t * kEll, 0));  // valid tokens
           // lane col owns column col of L_t.  Alg. 3: tile a down the columns, pre-mask
           // the inclusive upper triangle with 1, column-wise cumulative product, zero
           // the strict upper triangle.  Products only, never ratios.
@@ -939,17 +943,17 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG * Cfg<OP>::TS + Cfg<OP>::NPW 
     ri.init(grp);
     rw.init(grp);
     ro.init(grp);
-    for (int64_t j = grp; j < n_items; j += NG) {
+    for (int j = grp; j < n_items; j += NG) {
       Ring<NW> rp = rw, rn = rw;  // work slots of items j-1 and j+1
       rp.prev();
       rn.next();
-      const int64_t t0 = cur.m * BPI;
+      const int t0 = cur.m * BPI;
       const bool halo = cur.gi < W.g0 || cur.gi >= W.g1;
-      const int nblk = (int)std::min<int64_t>(BPI, nb - t0);  // valid blocks of this item
-      uint8_t* st = sin + ri.s * S::kIn;
-      uint8_t* ot = sout + ro.s * S::kOut;
+      const int nblk = min(BPI, nb - t0);  // valid blocks of this item
+      const uint32_t st = smem_s + S::kInBase + ri.s * S::kIn;   // shared-window addresses
+      const uint32_t ot = smem_s + S::kOutBase + ro.s * S::kOut;
       const float* gr = reinterpret_cast<const float*>(aux + rw.s * S::kAux);
-      const int64_t co = cur.line * kD + cb;          // carry / mu index of c_0
+      const int co = cur.line * kD + cb;              // carry / mu index of c_0 (< 2^31)
       const uint32_t tslot = tmem_base + lane_base + (uint32_t)(rw.s * kItemCols);
       const bool first_item = t0 == 0, last_item = t0 + nblk == nb;
       mbar_wait(&ready[rw.s], rw.ph);
@@ -1287,7 +1291,8 @@ bool tc_supported(int op, bool bf16, const Params& p) {
   auto a16 = [](const void* q) { return q == nullptr || (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
   // decays must be TMA-addressable: heads contiguous, 16-byte token/batch strides
   if (p.sa_h != 1 || (p.sa_l * 2) % 16 != 0 || (p.sa_b * 2) % 16 != 0 || !a16(p.a)) return false;
-  if (p.H > (1 << 30) || p.L > (1 << 30) || p.B > (1 << 30)) return false;
+  // 32-bit item / carry indexing in the kernel
+  if (p.B * p.H > (1 << 22) || p.B * p.H * p.nb >= (int64_t(1) << 31) || p.L > (1 << 30)) return false;
   return true;
 }
 

@@ -73,40 +73,34 @@ constexpr int kHalf = 2048;      // one 64-channel half: 16 rows x 128 B, 128B-s
 #ifndef SWR_MB_NI
 #define SWR_MB_NI 8
 #endif
-#ifndef SWR_B_TS
-#define SWR_B_TS 1
-#endif
-#ifndef SWR_MB_TS
-#define SWR_MB_TS 1
-#endif
 template <int OP>
 struct Cfg;
 template <>
 struct Cfg<0> {  // swr_fwd: in u;  out x
   static constexpr int NT = 1, NP = 0, BPI = 4, NI = SWR_F_NI, NW = 8, NO = SWR_F_NO, COLS = 16, NPW = SWR_F_NPW, NOUT = 1, NG = 3;
   static constexpr int TU = 0, TG = 0;  // A-operand regions of W and lambda
-  static constexpr int TS = 1;          // epilogue token split (warps per lane quarter)
+  static constexpr bool CYC = false;    // w MMA through the row-rotated tile (see Stage::kLc)
   static constexpr bool BWD = false, MIX = false;
 };
 template <>
 struct Cfg<1> {  // swr_bwd: in u, G;  out du
   static constexpr int NT = 2, NP = 0, BPI = 2, NI = SWR_B_NI, NW = 8, NO = 4, COLS = 32, NPW = SWR_B_NPW, NOUT = 1, NG = SWR_B_NG;
   static constexpr int TU = 0, TG = 1;
-  static constexpr int TS = SWR_B_TS;
+  static constexpr bool CYC = true;
   static constexpr bool BWD = true, MIX = false;
 };
 template <>
 struct Cfg<2> {  // mix fwd: in q, k, v;  out y;  prep u^ = k v (over k)
   static constexpr int NT = 3, NP = 0, BPI = 2, NI = 6, NW = SWR_MF_NW, NO = 4, COLS = 16, NPW = SWR_MF_NPW, NOUT = 1, NG = 3;
   static constexpr int TU = 1, TG = 0;
-  static constexpr int TS = 1;
+  static constexpr bool CYC = false;
   static constexpr bool BWD = false, MIX = true;
 };
 template <>
 struct Cfg<3> {  // mix bwd: in q, k, v, dy;  out dq, dk, dv;  prep u^ = k v (region 4), G = dy q (over q)
   static constexpr int NT = 4, NP = 1, BPI = 1, NI = SWR_MB_NI, NW = 8, NO = 3, COLS = 32, NPW = 4, NOUT = 3, NG = 3;
   static constexpr int TU = 4, TG = 0;
-  static constexpr int TS = SWR_MB_TS;
+  static constexpr bool CYC = false;
   static constexpr bool BWD = true, MIX = true;
 };
 
@@ -121,7 +115,11 @@ struct Stage {
   // input stage
   static constexpr int kA = (C::NT + C::NP) * kRegion;         // decay box [16*BPI tokens][8 heads] bf16
   static constexpr int kL = kA + 256 * C::BPI;                 // transfer tile L_t per block (512 B)
-  static constexpr int kInRaw = kL + 512 * C::BPI;
+  // CYC: a second tile per block with the rows of L_t rotated by one,
+  // Lc[i][j] = L[(i - 1) mod 16][j], so the w MMA yields [w_15, w_0, ..., w_14]:
+  // w[i-1] for i >= 1 and the carrier w[15] in column 0 (SWR backward)
+  static constexpr int kLc = kL + 512 * C::BPI;
+  static constexpr int kInRaw = kLc + (C::CYC ? 512 * C::BPI : 0);
   static constexpr int kIn = (kInRaw + 1023) / 1024 * 1024;
   // output slot
   static constexpr int kOut = C::NOUT * kRegion;
@@ -487,14 +485,14 @@ __device__ __forceinline__ void ldsm_t(uint32_t p, uint32_t (&r)[4]) {
                : "memory");
 }
 // store x[k][m] (rounded once to bf16) into a swizzled tile; ro = frag_row_off
-__device__ __forceinline__ void store_frag(uint32_t tile, uint32_t ro, const float (&x)[4][4], int = 0) {
+__device__ __forceinline__ void store_frag(uint32_t tile, uint32_t ro, const float (&x)[4][4]) {
 #pragma unroll
   for (int tg = 0; tg < 2; ++tg)
     stsm_t(tile + ro + 1024 * tg, pack_bf2(x[0][2 * tg], x[0][2 * tg + 1]), pack_bf2(x[1][2 * tg], x[1][2 * tg + 1]),
            pack_bf2(x[2][2 * tg], x[2][2 * tg + 1]), pack_bf2(x[3][2 * tg], x[3][2 * tg + 1]));
 }
 // load a bf16 tile's elements in fragment order: t[k][tg] = bf16x2 (tokens 2qd+8tg, +1; channel c_k)
-__device__ __forceinline__ void load_frag(uint32_t tile, uint32_t ro, uint32_t (&t)[2][4], int = 0) {
+__device__ __forceinline__ void load_frag(uint32_t tile, uint32_t ro, uint32_t (&t)[2][4]) {
   ldsm_t(tile + ro, t[0]);
   ldsm_t(tile + ro + 1024, t[1]);
 }
@@ -506,48 +504,10 @@ __device__ __forceinline__ void chan4(float v, int rr, float (&o)[4]) {
 #pragma unroll
   for (int k = 0; k < 4; ++k) o[k] = __shfl_sync(0xffffffffu, v, rr + 8 * k);
 }
-// Half-block variants (token split TS = 2: two warps per lane quarter, each owning
-// the 8 tokens 8 ts .. 8 ts + 7): x[k][m] = (channel c_k, token 8 ts + 2 qd + m), m = 0, 1.
-// taddr already points at column col + 8 ts.
-__device__ __forceinline__ void tmem_ld_frag(uint32_t taddr, float (&x)[4][2]) {
-  uint32_t r[8];
-  asm volatile("tcgen05.ld.sync.aligned.16x256b.x1.b32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-               : "r"(taddr));
-  asm volatile("tcgen05.ld.sync.aligned.16x256b.x1.b32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-               : "r"(taddr + (16u << 16)));
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    x[2 * h][0] = __uint_as_float(r[4 * h + 0]);
-    x[2 * h][1] = __uint_as_float(r[4 * h + 1]);
-    x[2 * h + 1][0] = __uint_as_float(r[4 * h + 2]);
-    x[2 * h + 1][1] = __uint_as_float(r[4 * h + 3]);
-  }
-}
-__device__ __forceinline__ void tmem_wait_frag(float (&x)[4][2]) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;"
-               : "+f"(x[0][0]), "+f"(x[0][1]), "+f"(x[1][0]), "+f"(x[1][1]), "+f"(x[2][0]), "+f"(x[2][1]),
-                 "+f"(x[3][0]), "+f"(x[3][1])
-               :
-               : "memory");
-}
-// store / load the token group tg of a half-block fragment
-__device__ __forceinline__ void store_frag(uint32_t tile, uint32_t ro, const float (&x)[4][2], int tg) {
-  stsm_t(tile + ro + 1024 * tg, pack_bf2(x[0][0], x[0][1]), pack_bf2(x[1][0], x[1][1]), pack_bf2(x[2][0], x[2][1]),
-         pack_bf2(x[3][0], x[3][1]));
-}
-__device__ __forceinline__ void load_frag(uint32_t tile, uint32_t ro, uint32_t (&t)[1][4], int tg) {
-  ldsm_t(tile + ro + 1024 * tg, t[0]);
-}
 // aux arrays (g, r, gs) are stored per block in fragment token order: [qd][m]
 __device__ __forceinline__ void load_aux(const float* p, float (&o)[4]) {
   const float4 x = *reinterpret_cast<const float4*>(p);
   o[0] = x.x; o[1] = x.y; o[2] = x.z; o[3] = x.w;
-}
-__device__ __forceinline__ void load_aux(const float* p, float (&o)[2]) {
-  const float2 x = *reinterpret_cast<const float2*>(p);
-  o[0] = x.x; o[1] = x.y;
 }
 __device__ __forceinline__ int aux_perm(int i) { return 4 * ((i & 7) >> 1) + 2 * (i >> 3) + (i & 1); }
 
@@ -577,7 +537,7 @@ __device__ __forceinline__ int aux_perm(int i) { return 4 * ((i & 7) >> 1) + 2 *
 #endif
 constexpr int kEpiUnroll = SWR_EPI_UNROLL;
 template <int OP>
-__global__ void __launch_bounds__((4 * Cfg<OP>::NG * Cfg<OP>::TS + Cfg<OP>::NPW + 4) * 32, 1)
+__global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
     swr_tc_kernel(const __grid_constant__ Maps maps, const Params p) {
   using C = Cfg<OP>;
   using S = Stage<OP>;
@@ -587,7 +547,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG * Cfg<OP>::TS + Cfg<OP>::NPW 
   // w is preceded by a valid column and can also be read shifted by one (w[i-1]).
   constexpr int kWo = C::BWD ? 16 : 0, kLo = 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int kPrepW0 = 4 * NG * C::TS, kProdW = kPrepW0 + C::NPW, kMmaW = kProdW + 1, kStoreW = kMmaW + 1,
+  constexpr int kPrepW0 = 4 * NG, kProdW = kPrepW0 + C::NPW, kMmaW = kProdW + 1, kStoreW = kMmaW + 1,
                 kRetW = kStoreW + 1;
 
   // 1024-aligned base for the 128B-swizzle atoms.  Offset the __shared__ array
@@ -625,14 +585,14 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG * Cfg<OP>::TS + Cfg<OP>::NPW 
   static_assert(NO >= NG && NW >= NG, "epilogue group within one phase");
   static_assert((3 * NI + 3 * NW + 2 * NO) * 8 + 8 <= 1024 && NO * 4 * 16 * BPI * 4 <= 3072, "scratch budget");
   static_assert(S::kBytes + 1024 <= 227 * 1024, "shared memory budget");
-  constexpr int kUsers = (C::BWD ? 3 : 2) * 4 * C::TS;  // users x epilogue warps
+  constexpr int kUsers = (C::BWD ? 3 : 2) * 4;  // users x epilogue warps
 
   if (threadIdx.x == 0) {
     trace_cta(p, 0);
     for (int s = 0; s < NI; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&prepped[s], 1);
-      mbar_init(&inempty[s], C::MIX ? 4 * C::TS : 1);
+      mbar_init(&inempty[s], C::MIX ? 4 : 1);
     }
     for (int s = 0; s < NW; ++s) {
       mbar_init(&mmad[s], 1);
@@ -640,7 +600,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG * Cfg<OP>::TS + Cfg<OP>::NPW 
       mbar_init(&wfree[s], kUsers);
     }
     for (int s = 0; s < NO; ++s) {
-      mbar_init(&ofull[s], 4 * C::TS);
+      mbar_init(&ofull[s], 4);
       mbar_init(&oempty[s], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -712,7 +672,8 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG * Cfg<OP>::TS + Cfg<OP>::NPW 
         for (int k = 0; k < BPI; ++k) {
           const uint32_t d = tmem_base + (uint32_t)(rw.s * kItemCols + k * C::COLS);
           const uint32_t lt = su32(st + S::kL + 512 * k);
-          umma_bf16(d + kWo, desc_A<S::kHS>(su32(S::tile(st, k, C::TU))), desc_Bmn(lt), kIdescBmn);  // w^T
+          const uint32_t lw = C::CYC ? su32(st + S::kLc + 512 * k) : lt;
+          umma_bf16(d + kWo, desc_A<S::kHS>(su32(S::tile(st, k, C::TU))), desc_Bmn(lw), kIdescBmn);  // w^T
           if constexpr (C::BWD)  // lambda^T
             umma_bf16(d + kLo, desc_A<S::kHS>(su32(S::tile(st, k, C::TG))), desc_Bk(lt), kIdescBk);
         }
@@ -854,6 +815,16 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG * Cfg<OP>::TS + Cfg<OP>::NPW 
           hi.z = pack_bf2(Lc[12], Lc[13]); hi.w = pack_bf2(Lc[14], Lc[15]);
           *reinterpret_cast<uint4*>(l + ltile_off(0, col)) = lo;
           *reinterpret_cast<uint4*>(l + ltile_off(8, col)) = hi;
+          if constexpr (C::CYC) {  // rows rotated by one: Lc[i][col] = L[(i-1) mod 16][col]
+            uint8_t* lc = st + S::kLc + 512 * k;
+            uint4 clo, chi;
+            clo.x = pack_bf2(Lc[15], Lc[0]); clo.y = pack_bf2(Lc[1], Lc[2]);
+            clo.z = pack_bf2(Lc[3], Lc[4]);  clo.w = pack_bf2(Lc[5], Lc[6]);
+            chi.x = pack_bf2(Lc[7], Lc[8]);  chi.y = pack_bf2(Lc[9], Lc[10]);
+            chi.z = pack_bf2(Lc[11], Lc[12]); chi.w = pack_bf2(Lc[13], Lc[14]);
+            *reinterpret_cast<uint4*>(lc + ltile_off(0, col)) = clo;
+            *reinterpret_cast<uint4*>(lc + ltile_off(8, col)) = chi;
+          }
           // aux arrays in the epilogue's fragment token order (aux_perm)
           if constexpr (C::BWD) gr[S::kAuxBlk * k + 16 + aux_perm(col)] = prod;  // r_t[j] = L[15][j]
           if (col == 0) {
@@ -920,21 +891,15 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG * Cfg<OP>::TS + Cfg<OP>::NPW 
     }
   } else {
     // ===================== epilogue groups: fragment layout (see tmem_ld_frag) =====================
-    // A group is 4 TS warps: lane quarter wq = warp & 3, token split ts = (warp >> 2) % TS.
-    // Lane l = 4 rr + qd owns channels c_k = 32 wq + rr + 8k and MT = 4 / TS tokens of every
-    // block: TS = 1: tk_m = 8 (m >> 1) + 2 qd + (m & 1);  TS = 2: tk_m = 8 ts + 2 qd + m.
-    // Token pairs (m, m+1) are packed fp32x2 lanes and one bf16x2 word of a fragment.
-    constexpr int TS = C::TS, MT = 4 / TS, NTG = 2 / TS;
-    const int grp = warp / (4 * TS);                 // epilogue group, items j = grp mod NG
+    // lane l = 4 rr + qd owns channels c_k = 32 wq + rr + 8k and tokens tk_m of every block;
+    // token pairs (m, m+1) are packed fp32x2 lanes and one bf16x2 word of a fragment
+    const int grp = warp >> 2;                       // epilogue group, items j = grp mod NG
     const int wq = warp & 3;                         // TMEM lane quarter
-    const int ts = (warp >> 2) & (TS - 1);           // token half (TS = 2)
     const int qd = lane & 3, rr = lane >> 2;
     const int cb = 32 * wq + rr;                     // channel c_0
-    const int col0 = 8 * ts;                         // first TMEM column (token) of this warp
-    const int am = 4 * qd + 2 * ts;                  // aux offset of this thread's tokens (aux_perm)
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
     const uint32_t fro = frag_row_off<S::kHS>(wq, lane);
-    const bool leader = (threadIdx.x % (128 * TS)) == 0;  // trace only
+    const bool leader = (threadIdx.x & 127) == 0;   // trace only
     Cursor cur;
     if (grp < n_items) cur.init(W.first + grp, nbi, H);
     Ring<NI> ri;
@@ -970,7 +935,9 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG * Cfg<OP>::TS + Cfg<OP>::NPW 
             for (int k = 0; k < 4; ++k) v[k] = p.carry_in[co + 8 * k];
           }
         } else {
-          float x = tmem_ld1(tmem_base + lane_base + (uint32_t)(rp.s * kItemCols + (BPI - 1) * C::COLS + kWo + 15));
+          // w[15] of the previous item's last block (CYC: stored in its column 0)
+          float x = tmem_ld1(tmem_base + lane_base +
+                             (uint32_t)(rp.s * kItemCols + (BPI - 1) * C::COLS + kWo + (C::CYC ? 0 : 15)));
           tmem_wait_f(x);
           chan4(x, rr, v);
         }
@@ -1000,74 +967,74 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG * Cfg<OP>::TS + Cfg<OP>::NPW 
 #pragma unroll kEpiUnroll
         for (int kb = 0; kb < nblk; ++kb) {
           const float* ga = gr + S::kAuxBlk * kb;  // [g 16 | r 16 | gs 16], fragment order
-          const uint32_t tb = tslot + kb * C::COLS + col0;
+          const uint32_t tb = tslot + kb * C::COLS;
           if constexpr (!C::BWD) {
-            float w[4][MT];
+            float w[4][4];
             tmem_ld_frag(tb + kWo, w);
-            float w15 = 0.f;
-            if constexpr (TS == 2) w15 = tmem_ld1(tslot + kb * C::COLS + kWo + 15);
-            float gg[MT];
-            load_aux(ga + am, gg);
+            float gg[4];
+            load_aux(ga + 4 * qd, gg);
             tmem_wait_frag(w);
-            if constexpr (TS == 2) tmem_wait_f(w15);
-            float out[4][MT];
+            float out[4][4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {  // Pass II: x~ = w + g v, packed token pairs
               const float2 v2 = make_float2(v[k], v[k]);
 #pragma unroll
-              for (int h = 0; h < NTG; ++h) {
+              for (int h = 0; h < 2; ++h) {
                 const float2 o = f2fma(make_float2(gg[2 * h], gg[2 * h + 1]), v2, make_float2(w[k][2 * h], w[k][2 * h + 1]));
                 out[k][2 * h] = o.x;
                 out[k][2 * h + 1] = o.y;
               }
             }
             if constexpr (C::MIX) {  // post-gate with residual: y = q x~ + v
-              uint32_t tq[NTG][4], tv[NTG][4];
-              load_frag(S::tile(st, kb, 0), fro, tq, ts);
-              load_frag(S::tile(st, kb, 2), fro, tv, ts);
+              uint32_t tq[2][4], tv[2][4];
+              load_frag(S::tile(st, kb, 0), fro, tq);
+              load_frag(S::tile(st, kb, 2), fro, tv);
 #pragma unroll
               for (int k = 0; k < 4; ++k)
 #pragma unroll
-                for (int h = 0; h < NTG; ++h) {
+                for (int h = 0; h < 2; ++h) {
                   const float2 o = f2fma(bf2f(tq[h][k]), make_float2(out[k][2 * h], out[k][2 * h + 1]), bf2f(tv[h][k]));
                   out[k][2 * h] = o.x;
                   out[k][2 * h + 1] = o.y;
                 }
             }
-            store_frag(S::tile(ot, kb, 0), fro, out, ts);
-            if (t0 + kb == nb - 1 && p.carry_out && qd == 3 && ts == TS - 1) {
+            store_frag(S::tile(ot, kb, 0), fro, out);
+            if (t0 + kb == nb - 1 && p.carry_out && qd == 3) {
 #pragma unroll
-              for (int k = 0; k < 4; ++k) p.carry_out[co + 8 * k] = w[k][MT - 1];  // w_t[15]
+              for (int k = 0; k < 4; ++k) p.carry_out[co + 8 * k] = w[k][3];  // w_t[15]
             }
-            if constexpr (TS == 1) {
 #pragma unroll
-              for (int k = 0; k < 4; ++k) v[k] = __shfl_sync(0xffffffffu, w[k][3], lane | 3);  // v_t = w_t[15]
-            } else {
-              chan4(w15, rr, v);
-            }
+            for (int k = 0; k < 4; ++k) v[k] = __shfl_sync(0xffffffffu, w[k][3], lane | 3);  // v_t = w_t[15]
           } else {
-            // lambda and w of the block.  tcgen05.ld.16x256b needs 8-column alignment, so
-            // w[i-1] is formed by shuffles inside the lane quad (and, for the second token
-            // half, w[7] from a 32x32b read)
-            float lam[4][MT], w[4][MT];
+            // lambda and w[i-1] of the block.  SWR (CYC): the rotated tile puts w[i-1] at
+            // token i and w[15] at token 0.  Mixer: w[i] in place (needed for dq), w[i-1]
+            // by shuffles inside the lane quad (tcgen05.ld.16x256b needs 8-column alignment).
+            float lam[4][4], w[4][4];
             tmem_ld_frag(tb + kLo, lam);
             tmem_ld_frag(tb + kWo, w);
-            float w15 = 0.f, w7 = 0.f;
-            if constexpr (TS == 2) {
-              w15 = tmem_ld1(tslot + kb * C::COLS + kWo + 15);
-              if (ts == 1) w7 = tmem_ld1(tslot + kb * C::COLS + kWo + 7);
-            }
             float mu[4] = {mu_last[0], mu_last[1], mu_last[2], mu_last[3]};
             if (kb + 1 < nblk) {  // next block inside this item: mu_t = a_{t+1}[0] lambda_{t+1}[0]
-              float l0 = tmem_ld1(tslot + (kb + 1) * C::COLS + kLo);
+              float l0 = tmem_ld1(tb + C::COLS + kLo);
               tmem_wait_f(l0);
               chan4(ga[S::kAuxBlk] * l0, rr, mu);
             }
+            float rv[4], sv[4];
+            load_aux(ga + 16 + 4 * qd, rv);
+            load_aux(ga + 32 + 4 * qd, sv);  // gs = g shifted by one
             tmem_wait_frag(lam);
             tmem_wait_frag(w);
-            float wsh[4][MT];  // wsh[k][m] = w[tk_m - 1], w[-1] = 0
-            const int src = (lane & ~3) | ((lane + 3) & 3);  // lane - 1 inside the quad (qd 0 <- qd 3)
-            if constexpr (TS == 1) {
+            float wsh[4][4], vnext[4] = {0.f, 0.f, 0.f, 0.f};  // wsh[k][m] = w[tk_m - 1], w[-1] = 0
+            if constexpr (C::CYC) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                vnext[k] = __shfl_sync(0xffffffffu, w[k][0], lane & ~3);  // token 0 of qd 0: w[15]
+                wsh[k][0] = qd == 0 ? 0.f : w[k][0];
+                wsh[k][1] = w[k][1];
+                wsh[k][2] = w[k][2];
+                wsh[k][3] = w[k][3];
+              }
+            } else {
+              const int src = (lane & ~3) | ((lane + 3) & 3);  // lane - 1 inside the quad (qd 0 <- qd 3)
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
                 const float x0 = __shfl_sync(0xffffffffu, w[k][1], src);                    // token 2qd - 1
@@ -1077,69 +1044,71 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG * Cfg<OP>::TS + Cfg<OP>::NPW 
                 wsh[k][2] = x2;
                 wsh[k][3] = w[k][2];
               }
-            } else {
-              tmem_wait_f(w15);
-              float w7c[4] = {0.f, 0.f, 0.f, 0.f};  // w[7] of c_k (first token of half 1 needs it)
-              if (ts == 1) {
-                tmem_wait_f(w7);
-                chan4(w7, rr, w7c);
-              }
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const float x0 = __shfl_sync(0xffffffffu, w[k][1], src);  // token 8ts + 2qd - 1
-                wsh[k][0] = qd == 0 ? w7c[k] : x0;
-                wsh[k][1] = w[k][0];
-              }
             }
-            float rv[MT], sv[MT];
-            load_aux(ga + 16 + am, rv);
-            load_aux(ga + 32 + am, sv);  // gs = g shifted by one
-            float du[4][MT], part[4][MT];
+            // du = lambda + r mu;  da[i] = sum_c lambda x~[i-1] + r mu w[i-1]
+            //                           = sum_c du w[i-1] + g[i-1] sum_c lambda v
+            // (both channel sums of the thread as packed FMA chains over k)
+            float du[4][4];
+            float2 dw[2], lv[2];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const float2 v2 = make_float2(v[k], v[k]), mu2 = make_float2(mu[k], mu[k]);
 #pragma unroll
-              for (int h = 0; h < NTG; ++h) {  // token pairs (2h, 2h+1)
-                const float2 r2 = make_float2(rv[2 * h], rv[2 * h + 1]), s2 = make_float2(sv[2 * h], sv[2 * h + 1]);
+              for (int h = 0; h < 2; ++h) {  // token pairs (2h, 2h+1)
                 const float2 lam2 = make_float2(lam[k][2 * h], lam[k][2 * h + 1]);
-                const float2 wp = make_float2(wsh[k][2 * h], wsh[k][2 * h + 1]);  // w[i-1]
-                // du = lambda + r mu;  da partial = lambda x~[i-1] + r mu w[i-1]
-                //                                 = du w[i-1] + g[i-1] (lambda v)
-                const float2 d2 = f2fma(r2, mu2, lam2);
-                const float2 pt = f2fma(s2, f2mul(lam2, v2), f2mul(d2, wp));
-                du[k][2 * h] = d2.x; du[k][2 * h + 1] = d2.y;
-                part[k][2 * h] = pt.x; part[k][2 * h + 1] = pt.y;
+                const float2 wp = make_float2(wsh[k][2 * h], wsh[k][2 * h + 1]);
+                const float2 d2 = f2fma(make_float2(rv[2 * h], rv[2 * h + 1]), mu2, lam2);
+                dw[h] = k == 0 ? f2mul(d2, wp) : f2fma(d2, wp, dw[h]);
+                lv[h] = k == 0 ? f2mul(lam2, v2) : f2fma(lam2, v2, lv[h]);
+                du[k][2 * h] = d2.x;
+                du[k][2 * h + 1] = d2.y;
               }
             }
-            if (t0 + kb == 0 && p.mu_out && qd == 0 && ts == 0) {
+            if (t0 + kb == 0 && p.mu_out && qd == 0) {
 #pragma unroll
               for (int k = 0; k < 4; ++k) p.mu_out[co + 8 * k] = ga[0] * lam[k][0];  // a_0[0] lambda_0[0]
             }
+            // da: the thread's 4-channel sums per token, then a transpose-reduce over the
+            // 8 lanes sharing qd (lane bits 2..4); fixed order, no atomics
+            float s[4];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const float2 s2 = f2fma(make_float2(sv[2 * h], sv[2 * h + 1]), lv[h], dw[h]);
+              s[2 * h] = s2.x;
+              s[2 * h + 1] = s2.y;
+            }
+            const bool u16 = lane & 16, u8 = lane & 8;
+            const float a0 = (u16 ? s[2] : s[0]) + __shfl_xor_sync(0xffffffffu, u16 ? s[0] : s[2], 16);
+            const float a1 = (u16 ? s[3] : s[1]) + __shfl_xor_sync(0xffffffffu, u16 ? s[1] : s[3], 16);
+            float b = (u8 ? a1 : a0) + __shfl_xor_sync(0xffffffffu, u8 ? a0 : a1, 8);
+            b += __shfl_xor_sync(0xffffffffu, b, 4);
+            if ((lane & 4) == 0)  // lane holds m = 2 u16 + u8: token 8 u16 + 2 qd + u8
+              rb[wq * (16 * BPI) + kb * 16 + (u16 ? 8 : 0) + 2 * qd + (u8 ? 1 : 0)] = b;
             if constexpr (!C::MIX) {
-              store_frag(S::tile(ot, kb, 0), fro, du, ts);
+              store_frag(S::tile(ot, kb, 0), fro, du);
             } else {
-              float gg[MT];
-              load_aux(ga + am, gg);
-              uint32_t tdy[NTG][4], tk[NTG][4], tv[NTG][4];
-              load_frag(S::tile(st, kb, 3), fro, tdy, ts);
-              load_frag(S::tile(st, kb, 1), fro, tk, ts);
-              load_frag(S::tile(st, kb, 2), fro, tv, ts);
-              float o[4][MT];
+              float gg[4];
+              load_aux(ga + 4 * qd, gg);
+              uint32_t tdy[2][4], tk[2][4], tv[2][4];
+              load_frag(S::tile(st, kb, 3), fro, tdy);
+              load_frag(S::tile(st, kb, 1), fro, tk);
+              load_frag(S::tile(st, kb, 2), fro, tv);
+              float o[4][4];
 #pragma unroll
               for (int k = 0; k < 4; ++k) {  // dq = dy x~,  x~ = w + g v
                 const float2 v2 = make_float2(v[k], v[k]);
 #pragma unroll
-                for (int h = 0; h < NTG; ++h) {
+                for (int h = 0; h < 2; ++h) {
                   const float2 x2 = f2fma(make_float2(gg[2 * h], gg[2 * h + 1]), v2, make_float2(w[k][2 * h], w[k][2 * h + 1]));
                   const float2 q2 = f2mul(bf2f(tdy[h][k]), x2);
                   o[k][2 * h] = q2.x; o[k][2 * h + 1] = q2.y;
                 }
               }
-              store_frag(S::tile(ot, kb, 0), fro, o, ts);
+              store_frag(S::tile(ot, kb, 0), fro, o);
 #pragma unroll
               for (int k = 0; k < 4; ++k) {  // dv = du^ k + dy ; dk = du^ v
 #pragma unroll
-                for (int h = 0; h < NTG; ++h) {
+                for (int h = 0; h < 2; ++h) {
                   const float2 d2 = make_float2(du[k][2 * h], du[k][2 * h + 1]);
                   const float2 dv2 = f2fma(d2, bf2f(tk[h][k]), bf2f(tdy[h][k]));
                   const float2 dk2 = f2mul(d2, bf2f(tv[h][k]));
@@ -1147,35 +1116,12 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG * Cfg<OP>::TS + Cfg<OP>::NPW 
                   du[k][2 * h] = dk2.x; du[k][2 * h + 1] = dk2.y;
                 }
               }
-              store_frag(S::tile(ot, kb, 2), fro, o, ts);
-              store_frag(S::tile(ot, kb, 1), fro, du, ts);
+              store_frag(S::tile(ot, kb, 2), fro, o);
+              store_frag(S::tile(ot, kb, 1), fro, du);
             }
-            // da: sum the thread's 4 channels, then a transpose-reduce of the MT token
-            // sums over the 8 lanes sharing qd (lane bits 2..4); fixed order, no atomics
-            float s[MT];
 #pragma unroll
-            for (int m = 0; m < MT; ++m) s[m] = ((part[0][m] + part[1][m]) + part[2][m]) + part[3][m];
-            const bool u16 = lane & 16, u8 = lane & 8;
-            if constexpr (TS == 1) {
-              const float a0 = (u16 ? s[2] : s[0]) + __shfl_xor_sync(0xffffffffu, u16 ? s[0] : s[2], 16);
-              const float a1 = (u16 ? s[3] : s[1]) + __shfl_xor_sync(0xffffffffu, u16 ? s[1] : s[3], 16);
-              float b = (u8 ? a1 : a0) + __shfl_xor_sync(0xffffffffu, u8 ? a0 : a1, 8);
-              b += __shfl_xor_sync(0xffffffffu, b, 4);
-              if ((lane & 4) == 0)  // lane holds m = 2 u16 + u8: token 8 u16 + 2 qd + u8
-                rb[wq * (16 * BPI) + kb * 16 + (u16 ? 8 : 0) + 2 * qd + (u8 ? 1 : 0)] = b;
-            } else {
-              float b = (u16 ? s[1] : s[0]) + __shfl_xor_sync(0xffffffffu, u16 ? s[0] : s[1], 16);
-              b += __shfl_xor_sync(0xffffffffu, b, 8);
-              b += __shfl_xor_sync(0xffffffffu, b, 4);
-              if ((lane & 12) == 0)  // lane holds m = u16: token 8 ts + 2 qd + u16
-                rb[wq * (16 * BPI) + kb * 16 + col0 + 2 * qd + (u16 ? 1 : 0)] = b;
-            }
-            if constexpr (TS == 1) {
-#pragma unroll
-              for (int k = 0; k < 4; ++k) v[k] = __shfl_sync(0xffffffffu, w[k][3], lane | 3);  // v_t = w_t[15]
-            } else {
-              chan4(w15, rr, v);
-            }
+            for (int k = 0; k < 4; ++k)  // v_t = w_t[15]
+              v[k] = C::CYC ? vnext[k] : __shfl_sync(0xffffffffu, w[k][3], lane | 3);
           }
         }
       }
@@ -1277,7 +1223,7 @@ static cudaError_t launch_op(const Params& p, cudaStream_t st, int sms) {
   }
   const int64_t total = p.B * p.H * ((p.nb + Cfg<OP>::BPI - 1) / Cfg<OP>::BPI);
   const int grid = (int)std::min<int64_t>(sms, std::max<int64_t>(total, 1));
-  constexpr int threads = (4 * Cfg<OP>::NG * Cfg<OP>::TS + Cfg<OP>::NPW + 4) * 32;
+  constexpr int threads = (4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32;
   swr_tc_kernel<OP><<<grid, threads, smem, st>>>(maps, p);
   return cudaGetLastError();
 }

@@ -56,11 +56,17 @@ constexpr int kHalf = 2048;      // one 64-channel half: 16 rows x 128 B, 128B-s
 // ring depths / prep warps: compile-time tuning knobs (tools/build_var.sh -D...)
 #ifndef SWR_F_NI
 #define SWR_F_NI 8
+#endif
+#ifndef SWR_F_NO
 #define SWR_F_NO 3
+#endif
+#ifndef SWR_F_NPW
 #define SWR_F_NPW 4
 #endif
 #ifndef SWR_B_NI
 #define SWR_B_NI 8
+#endif
+#ifndef SWR_B_NPW
 #define SWR_B_NPW 2
 #endif
 #ifndef SWR_B_NG
@@ -68,6 +74,8 @@ constexpr int kHalf = 2048;      // one 64-channel half: 16 rows x 128 B, 128B-s
 #endif
 #ifndef SWR_MF_NPW
 #define SWR_MF_NPW 3
+#endif
+#ifndef SWR_MF_NW
 #define SWR_MF_NW 6
 #endif
 #ifndef SWR_MB_NI
@@ -77,28 +85,28 @@ template <int OP>
 struct Cfg;
 template <>
 struct Cfg<0> {  // swr_fwd: in u;  out x
-  static constexpr int NT = 1, NP = 0, BPI = 4, NI = SWR_F_NI, NW = 8, NO = SWR_F_NO, COLS = 16, NPW = SWR_F_NPW, NOUT = 1, NG = 3;
+  static constexpr int NT = 1, NP = 0, BPI = 4, NI = SWR_F_NI, NA = 8, NW = 8, NO = SWR_F_NO, COLS = 16, NPW = SWR_F_NPW, NOUT = 1, NG = 3;
   static constexpr int TU = 0, TG = 0;  // A-operand regions of W and lambda
   static constexpr bool CYC = false;    // w MMA through the row-rotated tile (see Stage::kLc)
   static constexpr bool BWD = false, MIX = false;
 };
 template <>
 struct Cfg<1> {  // swr_bwd: in u, G;  out du
-  static constexpr int NT = 2, NP = 0, BPI = 2, NI = SWR_B_NI, NW = 8, NO = 4, COLS = 32, NPW = SWR_B_NPW, NOUT = 1, NG = SWR_B_NG;
+  static constexpr int NT = 2, NP = 0, BPI = 2, NI = SWR_B_NI, NA = 8, NW = 8, NO = 4, COLS = 32, NPW = SWR_B_NPW, NOUT = 1, NG = SWR_B_NG;
   static constexpr int TU = 0, TG = 1;
   static constexpr bool CYC = true;
   static constexpr bool BWD = true, MIX = false;
 };
 template <>
 struct Cfg<2> {  // mix fwd: in q, k, v;  out y;  prep u^ = k v (over k)
-  static constexpr int NT = 3, NP = 0, BPI = 2, NI = 6, NW = SWR_MF_NW, NO = 4, COLS = 16, NPW = SWR_MF_NPW, NOUT = 1, NG = 3;
+  static constexpr int NT = 3, NP = 0, BPI = 2, NI = 6, NA = 6, NW = SWR_MF_NW, NO = 4, COLS = 16, NPW = SWR_MF_NPW, NOUT = 1, NG = 3;
   static constexpr int TU = 1, TG = 0;
   static constexpr bool CYC = false;
   static constexpr bool BWD = false, MIX = true;
 };
 template <>
 struct Cfg<3> {  // mix bwd: in q, k, v, dy;  out dq, dk, dv;  prep u^ = k v (region 4), G = dy q (over q)
-  static constexpr int NT = 4, NP = 1, BPI = 1, NI = SWR_MB_NI, NW = 8, NO = 3, COLS = 32, NPW = 4, NOUT = 3, NG = 3;
+  static constexpr int NT = 4, NP = 1, BPI = 1, NI = SWR_MB_NI, NA = 8, NW = 8, NO = 3, COLS = 32, NPW = 4, NOUT = 3, NG = 3;
   static constexpr int TU = 4, TG = 0;
   static constexpr bool CYC = false;
   static constexpr bool BWD = true, MIX = true;
@@ -107,29 +115,35 @@ struct Cfg<3> {  // mix bwd: in q, k, v, dy;  out dq, dk, dv;  prep u^ = k v (re
 // SMEM layout (bytes; every 4 KiB tile 1024-aligned for the 128B swizzle atoms).
 // A d-tensor of an item occupies one region [2 halves][16*BPI tokens][128 B] (one
 // TMA box per 64-channel half); block k of it starts k*2 KiB into each half.
+// Four rings: input stages (the item's d-tensor tiles), decay stages (its decay
+// box, loaded ahead by its own producer so the transfer tiles are built while the
+// d-tensor tiles are still in flight), work slots (transfer tiles + g/r/gs + TMEM
+// columns) and output slots.
 template <int OP>
 struct Stage {
   using C = Cfg<OP>;
   static constexpr int kRegion = C::BPI * kTile;
   static constexpr int kHS = C::BPI * kHalf;                   // half stride inside a region
-  // input stage
-  static constexpr int kA = (C::NT + C::NP) * kRegion;         // decay box [16*BPI tokens][8 heads] bf16
-  static constexpr int kL = kA + 256 * C::BPI;                 // transfer tile L_t per block (512 B)
-  // CYC: a second tile per block with the rows of L_t rotated by one,
-  // Lc[i][j] = L[(i - 1) mod 16][j], so the w MMA yields [w_15, w_0, ..., w_14]:
-  // w[i-1] for i >= 1 and the carrier w[15] in column 0 (SWR backward)
-  static constexpr int kLc = kL + 512 * C::BPI;
-  static constexpr int kInRaw = kLc + (C::CYC ? 512 * C::BPI : 0);
-  static constexpr int kIn = (kInRaw + 1023) / 1024 * 1024;
+  // input stage: NT loaded d-tensors + NP prep-computed A operands
+  static constexpr int kIn = (C::NT + C::NP) * kRegion;
+  // decay stage: box [16*BPI tokens][8 heads] bf16
+  static constexpr int kAD = 256 * C::BPI;
+  // work slot: transfer tile L_t per block (512 B); CYC: a second tile per block with
+  // the rows of L_t rotated by one, Lc[i][j] = L[(i - 1) mod 16][j], so the w MMA
+  // yields [w_15, w_0, ..., w_14]: w[i-1] for i >= 1 and the carrier w[15] in column 0
+  // (SWR backward); then aux per block: g_t[16], r_t[16], gs[16] = g_t shifted by one
+  // (gs[0] = 1), fp32, in fragment token order
+  static constexpr int kLc = 512 * C::BPI;                     // offset of the CYC tiles
+  static constexpr int kAuxOff = kLc + (C::CYC ? 512 * C::BPI : 0);
+  static constexpr int kAuxBlk = 48;  // floats
+  static constexpr int kWork = kAuxOff + C::BPI * kAuxBlk * 4;
   // output slot
   static constexpr int kOut = C::NOUT * kRegion;
-  // work-slot aux per block: g_t[16], r_t[16], gs[16] = g_t shifted by one (gs[0] = 1), fp32
-  static constexpr int kAuxBlk = 48;  // floats
-  static constexpr int kAux = C::BPI * kAuxBlk * 4;
   static constexpr int kInBase = 0;
   static constexpr int kOutBase = C::NI * kIn;
-  static constexpr int kAuxBase = kOutBase + C::NO * kOut;
-  static constexpr int kScratch = kAuxBase + C::NW * kAux;     // barriers + da partials (4 KiB)
+  static constexpr int kWorkBase = kOutBase + C::NO * kOut;
+  static constexpr int kADBase = kWorkBase + C::NW * kWork;
+  static constexpr int kScratch = kADBase + C::NA * kAD;       // barriers + da partials (4 KiB)
   static constexpr int kBytes = kScratch + 4096;
   static __device__ __forceinline__ uint8_t* region(uint8_t* st, int x) { return st + x * kRegion; }
   static __device__ __forceinline__ uint8_t* tile(uint8_t* st, int k, int x) {
@@ -529,15 +543,12 @@ __device__ __forceinline__ int aux_perm(int i) { return 4 * ((i & 7) >> 1) + 2 *
 // The 4 warps of an epilogue group never synchronise with each other: each owns
 // 32 channels (a TMEM lane quarter) and arrives on the barriers itself.
 // ---------------------------------------------------------------------------
-#ifndef SWR_VAR
-#define SWR_VAR 0
-#endif
 #ifndef SWR_EPI_UNROLL
 #define SWR_EPI_UNROLL 1
 #endif
 constexpr int kEpiUnroll = SWR_EPI_UNROLL;
 template <int OP>
-__global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
+__global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MIX ? 4 : 5)) * 32, 1)
     swr_tc_kernel(const __grid_constant__ Maps maps, const Params p) {
   using C = Cfg<OP>;
   using S = Stage<OP>;
@@ -548,7 +559,8 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
   constexpr int kWo = C::BWD ? 16 : 0, kLo = 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int kPrepW0 = 4 * NG, kProdW = kPrepW0 + C::NPW, kMmaW = kProdW + 1, kStoreW = kMmaW + 1,
-                kRetW = kStoreW + 1;
+                kRetW = kStoreW + 1, kAProdW = C::MIX ? -1 : kRetW + 1;
+  constexpr int NA = C::NA;
 
   // 1024-aligned base for the 128B-swizzle atoms.  Offset the __shared__ array
   // itself (not a uintptr_t round trip) so every access stays LDS/STS.
@@ -556,13 +568,18 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
   uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sin = smem + S::kInBase;
   uint8_t* sout = smem + S::kOutBase;
-  uint8_t* aux = smem + S::kAuxBase;
+  uint8_t* work = smem + S::kWorkBase;
+  uint8_t* sad = smem + S::kADBase;
   uint8_t* scratch = smem + S::kScratch;
   const uint32_t smem_s = su32(smem);
+  // work slot s: transfer tiles at work + s*kWork, aux floats at auxf(s)
+  auto auxf = [&](int s) { return reinterpret_cast<float*>(work + s * S::kWork + S::kAuxOff); };
   uint64_t* full = reinterpret_cast<uint64_t*>(scratch);
-  uint64_t* prepped = full + NI;
-  uint64_t* inempty = prepped + NI;
-  uint64_t* mmad = inempty + NI;
+  uint64_t* inempty = full + NI;
+  uint64_t* afull = inempty + NI;
+  uint64_t* aempty = afull + NA;
+  uint64_t* prepped = aempty + NA;
+  uint64_t* mmad = prepped + NW;
   uint64_t* ready = mmad + NW;
   uint64_t* wfree = ready + NW;
   uint64_t* ofull = wfree + NW;
@@ -575,15 +592,17 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
   static_assert(NW * kItemCols <= 512, "TMEM budget");
   static_assert(NW >= 4 && NI >= 3 && NO >= 2, "ring depth (deadlock freedom)");
   // mbarrier waits are by phase parity, so a waiter must never be two phases ahead
-  // of a barrier.  Prep warp j mod NPW waits full[j mod NI] / wfree[j mod NW] and
-  // arrives prepped[j mod NI]; those phases complete out of item order (TMA loads
-  // finish out of order), so each stage and slot must always belong to the same
-  // prep warp, which then sees its phases in order.  The epilogue's ready/oempty
-  // phases are produced in item order by one thread; NO >= NG keeps a group (items
-  // j - NG, j) within one phase of oempty.
-  static_assert(NI % C::NPW == 0 && NW % C::NPW == 0, "prep warp <-> stage/slot ownership");
+  // of a barrier.  Prep warp j mod NPW waits afull[j mod NA] / wfree[j mod NW] (and,
+  // mixer, full[j mod NI]) and arrives aempty[j mod NA] / prepped[j mod NW]; those
+  // phases complete out of item order (TMA loads finish out of order), so each
+  // stage and slot must always belong to the same prep warp, which then sees its
+  // phases in order.  The epilogue's ready/oempty phases are produced in item order
+  // by one thread; NO >= NG keeps a group (items j - NG, j) within one phase of oempty.
+  static_assert(NA % C::NPW == 0 && NW % C::NPW == 0 && (!C::MIX || NI % C::NPW == 0),
+                "prep warp <-> stage/slot ownership");
   static_assert(NO >= NG && NW >= NG, "epilogue group within one phase");
-  static_assert((3 * NI + 3 * NW + 2 * NO) * 8 + 8 <= 1024 && NO * 4 * 16 * BPI * 4 <= 3072, "scratch budget");
+  static_assert((2 * NI + 2 * NA + 4 * NW + 2 * NO) * 8 + 8 <= 1024 && NO * 4 * 16 * BPI * 4 <= 3072,
+                "scratch budget");
   static_assert(S::kBytes + 1024 <= 227 * 1024, "shared memory budget");
   constexpr int kUsers = (C::BWD ? 3 : 2) * 4;  // users x epilogue warps
 
@@ -591,10 +610,14 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
     trace_cta(p, 0);
     for (int s = 0; s < NI; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&prepped[s], 1);
       mbar_init(&inempty[s], C::MIX ? 4 : 1);
     }
+    for (int s = 0; s < NA; ++s) {
+      mbar_init(&afull[s], 1);
+      mbar_init(&aempty[s], 1);
+    }
     for (int s = 0; s < NW; ++s) {
+      mbar_init(&prepped[s], 1);
       mbar_init(&mmad[s], 1);
       mbar_init(&ready[s], 1);
       mbar_init(&wfree[s], kUsers);
@@ -624,27 +647,54 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
 
   if (warp == kProdW) {
     // ===================== TMA producer =====================
+    // SWR ops: the decay boxes come from their own producer warp, up to NA items
+    // ahead, so the prep builds the transfer tiles while the d-tensor tiles are in
+    // flight.  Mixer: the prep needs the tiles anyway; the decays are issued here,
+    // just before the item's tiles.
     if (lane == 0 && n_items > 0) {
       Cursor cur;
       cur.init(W.first, nbi, H);
       Ring<NI> ri;
+      Ring<NA> ra;
       ri.init(0);
+      ra.init(0);
       for (int j = 0; j < n_items; ++j) {
+        const int tt = (int)(cur.m * BPI * kEll);
+        if constexpr (C::MIX) {
+          mbar_wait(&aempty[ra.s], ra.ph ^ 1);
+          mbar_expect_tx(&afull[ra.s], S::kAD);
+          tma_load_3d(sad + ra.s * S::kAD, &maps.a, &afull[ra.s], cur.h & ~7, tt, cur.b);
+          ra.next();
+        }
         mbar_wait(&inempty[ri.s], ri.ph ^ 1);
         trace(p, j, 0);
         uint8_t* st = sin + ri.s * S::kIn;
-        const int tt = (int)(cur.m * BPI * kEll);
-        mbar_expect_tx(&full[ri.s], C::NT * S::kRegion + 256 * BPI);
+        mbar_expect_tx(&full[ri.s], C::NT * S::kRegion);
 #pragma unroll
         for (int x = 0; x < C::NT; ++x) {  // one box per 64-channel half: 16*BPI tokens
           uint8_t* dst = S::region(st, x);
           tma_load_4d(dst, &maps.in[x], &full[ri.s], 0, cur.h, tt, cur.b);
           tma_load_4d(dst + S::kHS, &maps.in[x], &full[ri.s], 64, cur.h, tt, cur.b);
         }
-        tma_load_3d(st + S::kA, &maps.a, &full[ri.s], cur.h & ~7, tt, cur.b);
         trace(p, j, 1);
         cur.next(nbi, H);
         ri.next();
+      }
+    }
+  } else if (warp == kAProdW) {
+    // ===================== decay producer (SWR ops) =====================
+    if (lane == 0 && n_items > 0) {
+      Cursor cur;
+      cur.init(W.first, nbi, H);
+      Ring<NA> ra;
+      ra.init(0);
+      for (int j = 0; j < n_items; ++j) {
+        mbar_wait(&aempty[ra.s], ra.ph ^ 1);
+        trace(p, j, 11);
+        mbar_expect_tx(&afull[ra.s], S::kAD);
+        tma_load_3d(sad + ra.s * S::kAD, &maps.a, &afull[ra.s], cur.h & ~7, (int)(cur.m * BPI * kEll), cur.b);
+        cur.next(nbi, H);
+        ra.next();
       }
     }
   } else if (warp == kMmaW) {
@@ -657,22 +707,16 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
       ri.init(0);
       rw.init(0);
       for (int j = 0; j < n_items; ++j) {
-#if SWR_VAR == 1
-        mbar_wait(&full[ri.s], ri.ph);
-#endif
-#if SWR_VAR == 2
-        while (!mbar_test(&prepped[ri.s], ri.ph)) {}
-#else
-        mbar_wait(&prepped[ri.s], ri.ph);
-#endif
+        mbar_wait(&prepped[rw.s], rw.ph);                  // transfer tiles (mixer: and pre-gates)
+        if constexpr (!C::MIX) mbar_wait(&full[ri.s], ri.ph);  // operand tiles landed
         tc_fence_after();
         trace(p, j, 4);
         uint8_t* st = sin + ri.s * S::kIn;
 #pragma unroll
         for (int k = 0; k < BPI; ++k) {
           const uint32_t d = tmem_base + (uint32_t)(rw.s * kItemCols + k * C::COLS);
-          const uint32_t lt = su32(st + S::kL + 512 * k);
-          const uint32_t lw = C::CYC ? su32(st + S::kLc + 512 * k) : lt;
+          const uint32_t lt = su32(work + rw.s * S::kWork + 512 * k);
+          const uint32_t lw = C::CYC ? lt + S::kLc : lt;
           umma_bf16(d + kWo, desc_A<S::kHS>(su32(S::tile(st, k, C::TU))), desc_Bmn(lw), kIdescBmn);  // w^T
           if constexpr (C::BWD)  // lambda^T
             umma_bf16(d + kLo, desc_A<S::kHS>(su32(S::tile(st, k, C::TG))), desc_Bk(lt), kIdescBk);
@@ -700,6 +744,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
         mbar_wait(&mmad[rw.s], rw.ph);
         tc_fence_before();
         if constexpr (!C::MIX) mbar_arrive(&inempty[ri.s]);  // operands consumed
+        trace(p, j, 10);
         if (j - kBack >= 0) {
           mbar_arrive(&ready[rr.s]);
           trace(p, j - kBack, 6);
@@ -776,15 +821,19 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
     Cursor cur;
     if (pw < n_items) cur.init(W.first + pw, nbi, H);
     Ring<NI> ri;
+    Ring<NA> ra;
     Ring<NW> rw;
     ri.init(pw);
+    ra.init(pw);
     rw.init(pw);
     for (int j = pw; j < n_items; j += C::NPW) {
-      mbar_wait(&full[ri.s], ri.ph);
+      // the transfer tiles need only the decays (loaded ahead) and a free work slot
+      mbar_wait(&afull[ra.s], ra.ph);
       mbar_wait(&wfree[rw.s], rw.ph ^ 1);
       if (lane == 0) trace(p, j, 2);
       uint8_t* st = sin + ri.s * S::kIn;
-      float* gr = reinterpret_cast<float*>(aux + rw.s * S::kAux);  // [BPI][g 16 | r 16 | gs 16]
+      uint8_t* wt = work + rw.s * S::kWork;  // transfer tiles of this work slot
+      float* gr = auxf(rw.s);               // [BPI][g 16 | r 16 | gs 16]
 #pragma unroll
       for (int kb = 0; kb < BPI; kb += 2) {
         const int k = kb + hf;
@@ -794,7 +843,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
           // lane col owns column col of L_t.  Alg. 3: tile a down the columns, pre-mask
           // the inclusive upper triangle with 1, column-wise cumulative product, zero
           // the strict upper triangle.  Products only, never ratios.
-          const uint8_t* at = st + S::kA + (k * kEll) * 16 + (cur.h & 7) * 2;
+          const uint8_t* at = sad + ra.s * S::kAD + (k * kEll) * 16 + (cur.h & 7) * 2;
           float a[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i)
@@ -807,7 +856,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
             Lc[i] = (i >= col) ? prod : 0.f;  // L[i][col]
           }
           // column col: two 16-byte stores (rows 0-7, rows 8-15), rounded once to bf16
-          uint8_t* l = st + S::kL + 512 * k;
+          uint8_t* l = wt + 512 * k;
           uint4 lo, hi;
           lo.x = pack_bf2(Lc[0], Lc[1]);   lo.y = pack_bf2(Lc[2], Lc[3]);
           lo.z = pack_bf2(Lc[4], Lc[5]);   lo.w = pack_bf2(Lc[6], Lc[7]);
@@ -816,7 +865,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
           *reinterpret_cast<uint4*>(l + ltile_off(0, col)) = lo;
           *reinterpret_cast<uint4*>(l + ltile_off(8, col)) = hi;
           if constexpr (C::CYC) {  // rows rotated by one: Lc[i][col] = L[(i-1) mod 16][col]
-            uint8_t* lc = st + S::kLc + 512 * k;
+            uint8_t* lc = wt + S::kLc + 512 * k;
             uint4 clo, chi;
             clo.x = pack_bf2(Lc[15], Lc[0]); clo.y = pack_bf2(Lc[1], Lc[2]);
             clo.z = pack_bf2(Lc[3], Lc[4]);  clo.w = pack_bf2(Lc[5], Lc[6]);
@@ -843,7 +892,10 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
           }
         }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&aempty[ra.s]);  // decays read
       if constexpr (C::MIX) {
+        mbar_wait(&full[ri.s], ri.ph);
         // pre-gates in the swizzled tile layout (elementwise, layout-agnostic), each
         // rounded once to bf16: u^ = k (.) v; backward also G = dy (.) q
         const uint4* K4 = reinterpret_cast<const uint4*>(S::region(st, 1));
@@ -882,11 +934,12 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
       fence_proxy_async();  // this lane's generic-proxy writes -> visible to the tensor core
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(&prepped[ri.s]);
+        mbar_arrive(&prepped[rw.s]);
         trace(p, j, 3);
       }
       cur.step(C::NPW, nbi, H);
       ri.template step<C::NPW>();
+      ra.template step<C::NPW>();
       rw.template step<C::NPW>();
     }
   } else {
@@ -917,7 +970,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
       const int nblk = min(BPI, nb - t0);  // valid blocks of this item
       const uint32_t st = smem_s + S::kInBase + ri.s * S::kIn;   // shared-window addresses
       const uint32_t ot = smem_s + S::kOutBase + ro.s * S::kOut;
-      const float* gr = reinterpret_cast<const float*>(aux + rw.s * S::kAux);
+      const float* gr = auxf(rw.s);
       const int co = cur.line * kD + cb;              // carry / mu index of c_0 (< 2^31)
       const uint32_t tslot = tmem_base + lane_base + (uint32_t)(rw.s * kItemCols);
       const bool first_item = t0 == 0, last_item = t0 + nblk == nb;
@@ -950,7 +1003,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32, 1)
           } else {  // mu_t = a_{t+1}[0] lambda_{t+1}[0]
             float l0 = tmem_ld1(tmem_base + lane_base + (uint32_t)(rn.s * kItemCols + kLo));
             tmem_wait_f(l0);
-            chan4(reinterpret_cast<const float*>(aux + rn.s * S::kAux)[0] * l0, rr, mu_last);  // g[0] = a[0]
+            chan4(auxf(rn.s)[0] * l0, rr, mu_last);  // g[0] = a[0]
           }
         }
       }
@@ -1223,7 +1276,7 @@ static cudaError_t launch_op(const Params& p, cudaStream_t st, int sms) {
   }
   const int64_t total = p.B * p.H * ((p.nb + Cfg<OP>::BPI - 1) / Cfg<OP>::BPI);
   const int grid = (int)std::min<int64_t>(sms, std::max<int64_t>(total, 1));
-  constexpr int threads = (4 * Cfg<OP>::NG + Cfg<OP>::NPW + 4) * 32;
+  constexpr int threads = (4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MIX ? 4 : 5)) * 32;
   swr_tc_kernel<OP><<<grid, threads, smem, st>>>(maps, p);
   return cudaGetLastError();
 }

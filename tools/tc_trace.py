@@ -38,7 +38,7 @@ print("span (us) by SM id:", " ".join(f"{int(span[i,2])}:{x:.0f}" for i, x in zi
 st0 = span[:, 0].min()
 dur = (span[:, 1] - span[:, 0]) / 1e3
 print(f"CTAs {len(span)}: start spread {(span[:,0].max()-st0)/1e3:.1f} us, span min/med/max {dur.min():.1f}/{np.median(dur):.1f}/{dur.max():.1f} us, last end {(span[:,1].max()-st0)/1e3:.1f} us")
-t = allb[:N * 16].reshape(N, 16)[:, :len(EV)].astype(np.int64)
+t = allb[:N * 16].reshape(N, 16).astype(np.int64)
 valid = t[:, 0] > 0
 t0 = t[valid][:, 0].min()
 rel = np.where(t > 0, t - t0, -1)
@@ -56,3 +56,9 @@ print("median latencies (cycles): prod_issued->prep_full", d(1, 2), " prep", d(2
       " prod_got->released(own)", d(0, 10))
 per = np.diff(t[sl, 1])
 print("producer issue period cycles (median)", float(np.median(per)), " epi_ready period", float(np.median(np.diff(t[sl, 7][t[sl,7]>0]))))
+# full timeline of CTA 0: item, producer got-stage time (us), prep_full latency, epi_done (us)
+if os.environ.get("TIMELINE"):
+    clk = 1.965e3  # cycles per us at the max SM clock
+    for j in range(N):
+        if not valid[j]: break
+        print(f"tl {j:3d} got {rel[j,0]/clk:6.2f} issued {rel[j,1]/clk:6.2f} landed {rel[j,2]/clk:6.2f} prepped {rel[j,3]/clk:6.2f} mma {rel[j,5]/clk:6.2f} epi_in {rel[j,7]/clk:6.2f} epi_out {rel[j,8]/clk:6.2f} store {rel[j,9]/clk:6.2f} retired {rel[j,10]/clk:6.2f} dec_issue {rel[j,11]/clk:6.2f}")

@@ -40,6 +40,7 @@ struct Params {
   int64_t K;   // blocks per walk (FFMA path)
   unsigned long long* trace;  // diagnostics (swr_set_trace), NULL = off
   int64_t trace_n;
+  uint32_t epoch;  // TC path: launch ticket of the range claims (set by launch_tc)
 };
 
 // ---------------------------------------------------------------------------

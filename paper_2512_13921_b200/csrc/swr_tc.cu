@@ -28,7 +28,11 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
+#include <cmath>
 #include <cstring>
+#include <mutex>
+#include <vector>
 
 #include "swr_common.cuh"
 
@@ -60,6 +64,9 @@ constexpr int kHalf = 2048;      // one 64-channel half: 16 rows x 128 B, 128B-s
 #ifndef SWR_F_NO
 #define SWR_F_NO 3
 #endif
+#ifndef SWR_F_NA
+#define SWR_F_NA 8
+#endif
 #ifndef SWR_F_NPW
 #define SWR_F_NPW 4
 #endif
@@ -85,7 +92,7 @@ template <int OP>
 struct Cfg;
 template <>
 struct Cfg<0> {  // swr_fwd: in u;  out x
-  static constexpr int NT = 1, NP = 0, BPI = 4, NI = SWR_F_NI, NA = 8, NW = 8, NO = SWR_F_NO, COLS = 16, NPW = SWR_F_NPW, NOUT = 1, NG = 3;
+  static constexpr int NT = 1, NP = 0, BPI = 4, NI = SWR_F_NI, NA = SWR_F_NA, NW = 8, NO = SWR_F_NO, COLS = 16, NPW = SWR_F_NPW, NOUT = 1, NG = 3;
   static constexpr int TU = 0, TG = 0;  // A-operand regions of W and lambda
   static constexpr bool CYC = false;    // w MMA through the row-rotated tile (see Stage::kLc)
   static constexpr bool BWD = false, MIX = false;
@@ -342,11 +349,41 @@ __device__ __forceinline__ uint32_t ltile_off(int i, int j) {
 struct Work {
   int first, g0, g1, last;  // global item ids gi in [first, last) (< 2^31, tc_supported)
 };
+// Range split of the item space.  SMs of a B200 differ by up to +-15% in sustained
+// streaming rate, in a fixed pattern, so equal ranges finish when the
+// slowest SM does.  When `weighted`, range r is sized for SM r (feedback from the
+// per-SM item times of earlier launches of the op, g_spi) and a CTA claims the range
+// of the SM it runs on (first free range if that is taken: every range is claimed
+// exactly once, whatever the placement); results do not depend on the split.
+constexpr int kMaxSM = 256;
+struct Split {
+  int weighted;
+  int bnd[kMaxSM + 1];  // range r = items [bnd[r], bnd[r+1])
+};
+constexpr int kClaimSlots = 256;
+__device__ unsigned g_claim[kClaimSlots][kMaxSM];  // {launch epoch} of the claimer, per range
+__device__ float g_spi[4][kMaxSM];                 // ns per item of the last CTA on each SM, per op
+__device__ __forceinline__ int claim_range(const Split& sp, uint32_t epoch) {
+  if (!sp.weighted) return (int)blockIdx.x;
+  uint32_t sm;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+  unsigned* cl = g_claim[epoch % kClaimSlots];
+  const int n = (int)gridDim.x;
+  if ((int)sm < n && atomicExch(&cl[sm], epoch) != epoch) return (int)sm;
+  for (int r = 0; r < n; ++r)
+    if (atomicExch(&cl[r], epoch) != epoch) return r;
+  return -1;  // unreachable: as many ranges as CTAs
+}
 template <bool BWD>
-__device__ __forceinline__ Work work_of(int total, int nbi) {
+__device__ __forceinline__ Work work_of(const Split& sp, int r, int total, int nbi) {
   Work w;
-  w.g0 = (int)((int64_t)blockIdx.x * total / gridDim.x);
-  w.g1 = (int)(((int64_t)blockIdx.x + 1) * total / gridDim.x);
+  if (sp.weighted) {
+    w.g0 = sp.bnd[r];
+    w.g1 = sp.bnd[r + 1];
+  } else {
+    w.g0 = (int)((int64_t)r * total / gridDim.x);
+    w.g1 = (int)(((int64_t)r + 1) * total / gridDim.x);
+  }
   w.first = w.g0 - ((w.g0 < w.g1 && w.g0 % nbi != 0) ? 1 : 0);
   w.last = w.g1 + ((BWD && w.g0 < w.g1 && w.g1 % nbi != 0) ? 1 : 0);
   if (w.g0 >= w.g1) w.first = w.last = w.g0;
@@ -549,7 +586,7 @@ __device__ __forceinline__ int aux_perm(int i) { return 4 * ((i & 7) >> 1) + 2 *
 constexpr int kEpiUnroll = SWR_EPI_UNROLL;
 template <int OP>
 __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MIX ? 4 : 5)) * 32, 1)
-    swr_tc_kernel(const __grid_constant__ Maps maps, const Params p) {
+    swr_tc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Split split, const Params p) {
   using C = Cfg<OP>;
   using S = Stage<OP>;
   constexpr int NI = C::NI, NW = C::NW, NO = C::NO, NG = C::NG, BPI = C::BPI;
@@ -585,6 +622,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
   uint64_t* ofull = wfree + NW;
   uint64_t* oempty = ofull + NO;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(oempty + NO);
+  int* range_slot = reinterpret_cast<int*>(tmem_slot + 1);
   float* red = reinterpret_cast<float*>(scratch + 1024);  // [NO][4 warps][16*BPI] da partials
 
   constexpr int kTmemCols = (NW * kItemCols <= 32) ? 32 : (NW * kItemCols <= 64) ? 64
@@ -601,7 +639,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
   static_assert(NA % C::NPW == 0 && NW % C::NPW == 0 && (!C::MIX || NI % C::NPW == 0),
                 "prep warp <-> stage/slot ownership");
   static_assert(NO >= NG && NW >= NG, "epilogue group within one phase");
-  static_assert((2 * NI + 2 * NA + 4 * NW + 2 * NO) * 8 + 8 <= 1024 && NO * 4 * 16 * BPI * 4 <= 3072,
+  static_assert((2 * NI + 2 * NA + 4 * NW + 2 * NO) * 8 + 16 <= 1024 && NO * 4 * 16 * BPI * 4 <= 3072,
                 "scratch budget");
   static_assert(S::kBytes + 1024 <= 227 * 1024, "shared memory budget");
   constexpr int kUsers = (C::BWD ? 3 : 2) * 4;  // users x epilogue warps
@@ -627,6 +665,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
       mbar_init(&oempty[s], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    *range_slot = claim_range(split, p.epoch);
   }
   if (warp == kMmaW) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
@@ -642,7 +681,9 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
   const int nb = (int)p.nb, H = (int)p.H;   // sizes < 2^31 (tc_supported)
   const int nbi = (nb + BPI - 1) / BPI;       // items per line
   const int total = (int)p.B * H * nbi;
-  const Work W = work_of<C::BWD>(total, nbi);
+  const Work W = work_of<C::BWD>(split, *range_slot, total, nbi);
+  unsigned long long t_begin = 0;
+  if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
   const int n_items = W.last - W.first;
 
   if (warp == kProdW) {
@@ -1201,7 +1242,19 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (threadIdx.x == 0) trace_cta(p, 1);
+  if (threadIdx.x == 0) {
+    trace_cta(p, 1);
+#if SWR_TRACE
+    if (p.trace != nullptr) p.trace[16 * p.trace_n + 4 * blockIdx.x + 3] = (unsigned long long)(W.g1 - W.g0);
+#endif
+    if (split.weighted && W.g1 > W.g0) {  // this SM's time per item, for the next split
+      unsigned long long t_end;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+      uint32_t sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      if (sm < kMaxSM) g_spi[OP][sm] = (float)(t_end - t_begin) / (float)(W.g1 - W.g0);
+    }
+  }
   if (warp == kMmaW) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "r"(kTmemCols)
@@ -1212,6 +1265,83 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
+// Host side of the weighted split (see Split): per op, the SM rates learned from
+// g_spi.  After a launch, g_spi[op] is copied to pinned memory on a private stream
+// that waits for the launch (so the caller's stream never waits for the copy); a
+// later launch folds the copy in once it has completed (never a host sync).  Skipped
+// while the caller's stream is being captured into a graph.
+struct Balance {
+  std::mutex mu;
+  std::vector<float> rate;  // items per ns, per SM (0 = unknown)
+  float* host = nullptr;    // pinned readback buffer
+  cudaEvent_t ev = nullptr, done = nullptr;
+  cudaStream_t side = nullptr;
+  bool pending = false;
+  uint64_t launches = 0;
+
+  // fills q.epoch and the split for this launch; true if a readback should follow it
+  bool plan(Params& q, Split& sp, int grid, int sms, int64_t total, cudaStream_t st) {
+    static std::atomic<uint32_t> epoch{0};
+    do {
+      q.epoch = epoch.fetch_add(1, std::memory_order_relaxed) + 1;
+    } while (q.epoch == 0);
+    sp.weighted = 0;
+    if (grid != sms || sms > kMaxSM) return false;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cap) != cudaSuccess) cap = cudaStreamCaptureStatusActive;
+    std::lock_guard<std::mutex> lock(mu);
+    if ((int)rate.size() != sms) rate.assign(sms, 0.f);
+    if (pending && cudaEventQuery(ev) == cudaSuccess) {
+      for (int s = 0; s < sms; ++s)
+        if (host[s] > 0.f) rate[s] = rate[s] > 0.f ? 0.7f * rate[s] + 0.3f / host[s] : 1.f / host[s];
+      pending = false;
+    }
+    double sum = 0.0;
+    bool known = true;
+    for (int s = 0; s < sms; ++s) {
+      known = known && rate[s] > 0.f;
+      sum += rate[s];
+    }
+    if (known) {
+      sp.weighted = 1;
+      double acc = 0.0;
+      sp.bnd[0] = 0;
+      for (int s = 0; s < sms; ++s) {
+        acc += rate[s];
+        sp.bnd[s + 1] = (int)std::llround(acc / sum * (double)total);
+        if (sp.bnd[s + 1] < sp.bnd[s]) sp.bnd[s + 1] = sp.bnd[s];
+      }
+      sp.bnd[sms] = (int)total;
+    } else {
+      // uniform ranges by SM id until every SM has reported (CTA placement then learns)
+      sp.weighted = 1;
+      for (int s = 0; s <= sms; ++s) sp.bnd[s] = (int)((int64_t)s * total / sms);
+    }
+    ++launches;
+    return cap == cudaStreamCaptureStatusNone && !pending;
+  }
+  void request(int op, int sms, cudaStream_t st) {
+    std::lock_guard<std::mutex> lock(mu);
+    if (pending) return;
+    if (host == nullptr && cudaMallocHost(reinterpret_cast<void**>(&host), kMaxSM * sizeof(float)) != cudaSuccess) {
+      host = nullptr;
+      return;
+    }
+    if (ev == nullptr && (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess ||
+                          cudaEventCreateWithFlags(&done, cudaEventDisableTiming) != cudaSuccess ||
+                          cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) != cudaSuccess)) {
+      ev = nullptr;
+      return;
+    }
+    if (cudaEventRecord(done, st) != cudaSuccess || cudaStreamWaitEvent(side, done, 0) != cudaSuccess) return;
+    if (cudaMemcpyFromSymbolAsync(host, g_spi, sms * sizeof(float), (size_t)op * kMaxSM * sizeof(float),
+                                  cudaMemcpyDeviceToHost, side) != cudaSuccess)
+      return;
+    if (cudaEventRecord(ev, side) == cudaSuccess) pending = true;
+  }
+};
+static Balance g_balance[4];
+
 static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static bool tried = false;
@@ -1277,8 +1407,13 @@ static cudaError_t launch_op(const Params& p, cudaStream_t st, int sms) {
   const int64_t total = p.B * p.H * ((p.nb + Cfg<OP>::BPI - 1) / Cfg<OP>::BPI);
   const int grid = (int)std::min<int64_t>(sms, std::max<int64_t>(total, 1));
   constexpr int threads = (4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MIX ? 4 : 5)) * 32;
-  swr_tc_kernel<OP><<<grid, threads, smem, st>>>(maps, p);
-  return cudaGetLastError();
+  Params q = p;
+  Split sp;
+  const bool readback = g_balance[OP].plan(q, sp, grid, sms, total, st);
+  swr_tc_kernel<OP><<<grid, threads, smem, st>>>(maps, sp, q);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && readback) g_balance[OP].request(OP, sms, st);
+  return e;
 }
 
 }  // namespace tc

@@ -18,7 +18,7 @@ else:
     g = {k: v.cuda() for k, v in mix_inputs(8, 4096, 16, 128, seed=1).items()}
     run = (lambda: P.phalanx_mix(g["q"], g["k"], g["v"], g["a"])) if op == "mixf" else (
         lambda: P.phalanx_mix_bwd(g["q"], g["k"], g["v"], g["a"], g["dy"]))
-for _ in range(5):
+for _ in range(int(os.environ.get("WARM", "5"))):
     run()
 buf = torch.zeros(N * 16 + 4 * 160, dtype=torch.int64, device="cuda")
 _lib.set_trace(buf.data_ptr(), N)
@@ -34,7 +34,7 @@ span = allb[N * 16:].reshape(-1, 4)
 span = span[span[:, 0] > 0]
 order = np.argsort(span[:, 2])
 d_sm = (span[order, 1] - span[order, 0]) / 1e3
-print("span (us) by SM id:", " ".join(f"{int(span[i,2])}:{x:.0f}" for i, x in zip(order, d_sm)))
+print("span (us) / items by SM id:", " ".join(f"{int(span[i,2])}:{x:.0f}/{int(span[i,3])}" for i, x in zip(order, d_sm)))
 st0 = span[:, 0].min()
 dur = (span[:, 1] - span[:, 0]) / 1e3
 print(f"CTAs {len(span)}: start spread {(span[:,0].max()-st0)/1e3:.1f} us, span min/med/max {dur.min():.1f}/{np.median(dur):.1f}/{dur.max():.1f} us, last end {(span[:,1].max()-st0)/1e3:.1f} us")

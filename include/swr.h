@@ -35,9 +35,15 @@
  * Conventions shared by every entry point
  * ------------------------------------------------------------------------
  * Pointers  : DEVICE pointers owned by the caller.  The library never
- *             allocates, frees or keeps device memory and holds no state other
- *             than the process-global path selector and launch counter below;
- *             it is thread-safe.
+ *             allocates or frees device memory the caller sees.  Process-global
+ *             state: the path selector and launch counter below, and for the
+ *             tensor-core kernels (bf16, D = 128) a per-op table of per-SM
+ *             item rates that sizes each SM's share of the work (module-static
+ *             device arrays; refreshed by an asynchronous device->pinned-host
+ *             copy on a library-private stream that waits on the caller's
+ *             stream, never blocking it).  Results do not depend on that table
+ *             (bit-identical for any split).  Thread-safe.  Up to 256 launches
+ *             may be in flight concurrently (per-launch claim slots).
  * Layout    : every "d-tensor" (u, x, dx, du, q, k, v, y, dy, dq, dk, dv) is
  *             [B, L, H, D] with D contiguous (stride 1) and element strides
  *             (sx_b, sx_l, sx_h); all d-tensors of one call share those strides.

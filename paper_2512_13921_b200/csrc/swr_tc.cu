@@ -580,6 +580,9 @@ __device__ __forceinline__ int aux_perm(int i) { return 4 * ((i & 7) >> 1) + 2 *
 // The 4 warps of an epilogue group never synchronise with each other: each owns
 // 32 channels (a TMEM lane quarter) and arrives on the barriers itself.
 // ---------------------------------------------------------------------------
+#ifndef SWR_PDL
+#define SWR_PDL 0  // programmatic dependent launch: measured 2% slower on the SWR step (bwd CTAs start early on freed SMs), off
+#endif
 #ifndef SWR_EPI_UNROLL
 #define SWR_EPI_UNROLL 1
 #endif
@@ -677,6 +680,14 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Programmatic dependent launch: everything above (barrier init, TMEM allocation,
+  // range claim) overlapped the previous kernel's tail; no global memory it may
+  // write is touched before this wait.  The next kernel may start its own prologue
+  // on SMs this grid frees (it waits for this grid's completion the same way).
+#if SWR_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
 
   const int nb = (int)p.nb, H = (int)p.H;   // sizes < 2^31 (tc_supported)
   const int nbi = (nb + BPI - 1) / BPI;       // items per line
@@ -1410,8 +1421,18 @@ static cudaError_t launch_op(const Params& p, cudaStream_t st, int sms) {
   Params q = p;
   Split sp;
   const bool readback = g_balance[OP].plan(q, sp, grid, sms, total, st);
-  swr_tc_kernel<OP><<<grid, threads, smem, st>>>(maps, sp, q);
-  cudaError_t e = cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = SWR_PDL ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, swr_tc_kernel<OP>, maps, sp, q);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e == cudaSuccess && readback) g_balance[OP].request(OP, sms, st);
   return e;
 }

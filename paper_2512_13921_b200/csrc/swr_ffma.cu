@@ -108,8 +108,11 @@ __device__ __forceinline__ void load_G(const Params& p, int64_t xo, int64_t n0,
 // ---------------------------------------------------------------------------
 // forward
 // ---------------------------------------------------------------------------
+#ifndef SWR_FFMA_FWD_MINB
+#define SWR_FFMA_FWD_MINB 3
+#endif
 template <typename T, int TPH, bool MIX>
-__global__ void __launch_bounds__(128) fwd_ffma(const Params p) {
+__global__ void __launch_bounds__(128, SWR_FFMA_FWD_MINB) fwd_ffma(const Params p) {
   using io = IO<T>;
   constexpr int HPC = 128 / TPH;  // heads per CTA
   const int tid = threadIdx.x;
@@ -187,8 +190,11 @@ __global__ void __launch_bounds__(128) fwd_ffma(const Params p) {
 //   da_t[i] = sum_c lambda_t[i] x~_t[i-1] + r_t[i] mu_t w_t[i-1]
 //            (x~_t[-1] = v_{t-1}, w_t[-1] = 0)
 // ---------------------------------------------------------------------------
+#ifndef SWR_FFMA_BWD_MINB
+#define SWR_FFMA_BWD_MINB 4  // caps registers at 128: occupancy beats the spills (bwd 936 -> 642 us at d=16)
+#endif
 template <typename T, int TPH, bool MIX>
-__global__ void __launch_bounds__(128) bwd_ffma(const Params p) {
+__global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma(const Params p) {
   using io = IO<T>;
   constexpr int HPC = 128 / TPH;
   constexpr int GS = TPH < 32 ? TPH : 32;

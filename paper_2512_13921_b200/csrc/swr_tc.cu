@@ -465,6 +465,15 @@ __device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) { return _
 __device__ __forceinline__ float2 f2mul(float2 a, float2 b) { return __fmul2_rn(a, b); }
 
 
+// 8 bf16 products, elementwise, one RNE rounding each (mul.rn.bf16x2)
+__device__ __forceinline__ uint4 bmul8(const uint4& a, const uint4& b) {
+  uint4 o;
+  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(o.x) : "r"(a.x), "r"(b.x));
+  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(o.y) : "r"(a.y), "r"(b.y));
+  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(o.z) : "r"(a.z), "r"(b.z));
+  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(o.w) : "r"(a.w), "r"(b.w));
+  return o;
+}
 // pack two fp32 into bf16x2 (lo = first)
 __device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
@@ -949,37 +958,19 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
       if constexpr (C::MIX) {
         mbar_wait(&full[ri.s], ri.ph);
         // pre-gates in the swizzled tile layout (elementwise, layout-agnostic), each
-        // rounded once to bf16: u^ = k (.) v; backward also G = dy (.) q
+        // rounded once to bf16: u^ = k (.) v; backward also G = dy (.) q.
+        // A bf16 x bf16 product is exact in fp32, so the packed bf16x2 multiply (one
+        // rounding of the exact product) equals fp32 multiply + one RNE rounding.
         const uint4* K4 = reinterpret_cast<const uint4*>(S::region(st, 1));
         const uint4* V4 = reinterpret_cast<const uint4*>(S::region(st, 2));
         uint4* U4 = reinterpret_cast<uint4*>(S::region(st, C::TU));
-#pragma unroll 2
+#pragma unroll 4
         for (int v = lane; v < S::kRegion / 16; v += 32) {
-          const uint4 kk = K4[v], vv = V4[v];
-          uint4 o;
-          const uint32_t* ka = &kk.x;
-          const uint32_t* va = &vv.x;
-          uint32_t* oa = &o.x;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 kf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ka[e]));
-            const float2 vf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&va[e]));
-            oa[e] = pack_bf2(kf.x * vf.x, kf.y * vf.y);
-          }
-          U4[v] = o;
+          U4[v] = bmul8(K4[v], V4[v]);
           if constexpr (C::BWD) {
             uint4* Q4 = reinterpret_cast<uint4*>(S::region(st, 0));  // G overwrites q
             const uint4* D4 = reinterpret_cast<const uint4*>(S::region(st, 3));
-            const uint4 qq = Q4[v], dd = D4[v];
-            const uint32_t* qa = &qq.x;
-            const uint32_t* da = &dd.x;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 qf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&qa[e]));
-              const float2 df = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&da[e]));
-              oa[e] = pack_bf2(df.x * qf.x, df.y * qf.y);
-            }
-            Q4[v] = o;
+            Q4[v] = bmul8(D4[v], Q4[v]);
           }
         }
       }

@@ -1342,7 +1342,8 @@ struct Balance {
     if (cudaEventRecord(ev, side) == cudaSuccess) pending = true;
   }
 };
-static Balance g_balance[4];
+constexpr int kMaxDev = 64;
+static Balance g_balance[kMaxDev][4];  // per device (SM rates are a property of the GPU), per op
 
 static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -1411,7 +1412,17 @@ static cudaError_t launch_op(const Params& p, cudaStream_t st, int sms) {
   constexpr int threads = (4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MIX ? 4 : 5)) * 32;
   Params q = p;
   Split sp;
-  const bool readback = g_balance[OP].plan(q, sp, grid, sms, total, st);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) dev = -1;
+  Balance* bal = dev >= 0 ? &g_balance[dev][OP] : nullptr;
+  bool readback = false;
+  if (bal != nullptr) {
+    readback = bal->plan(q, sp, grid, sms, total, st);
+  } else {
+    static std::atomic<uint32_t> epoch{0};
+    q.epoch = epoch.fetch_add(1, std::memory_order_relaxed) | 0x80000000u;  // never 0
+    sp.weighted = 0;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3((unsigned)threads);
@@ -1424,7 +1435,10 @@ static cudaError_t launch_op(const Params& p, cudaStream_t st, int sms) {
   cfg.numAttrs = SWR_PDL ? 1 : 0;
   cudaError_t e = cudaLaunchKernelEx(&cfg, swr_tc_kernel<OP>, maps, sp, q);
   if (e == cudaSuccess) e = cudaGetLastError();
-  if (e == cudaSuccess && readback) g_balance[OP].request(OP, sms, st);
+  if (e == cudaSuccess && readback) {
+    bal->request(OP, sms, st);
+    (void)cudaGetLastError();  // a failed readback only skips a table refresh; keep it out of the error state
+  }
   return e;
 }
 

@@ -112,7 +112,7 @@ __device__ __forceinline__ void load_G(const Params& p, int64_t xo, int64_t n0,
 #define SWR_FFMA_FWD_MINB 3
 #endif
 template <typename T, int TPH, bool MIX>
-__global__ void __launch_bounds__(128, SWR_FFMA_FWD_MINB) fwd_ffma(const Params p) {
+__global__ void __launch_bounds__(128, MIX ? 1 : SWR_FFMA_FWD_MINB) fwd_ffma(const Params p) {
   using io = IO<T>;
   constexpr int HPC = 128 / TPH;  // heads per CTA
   const int tid = threadIdx.x;
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(128, SWR_FFMA_FWD_MINB) fwd_ffma(const Params 
 #define SWR_FFMA_BWD_MINB 4  // caps registers at 128: occupancy beats the spills (bwd 936 -> 642 us at d=16)
 #endif
 template <typename T, int TPH, bool MIX>
-__global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma(const Params p) {
+__global__ void __launch_bounds__(128, MIX ? 1 : SWR_FFMA_BWD_MINB) bwd_ffma(const Params p) {
   using io = IO<T>;
   constexpr int HPC = 128 / TPH;
   constexpr int GS = TPH < 32 ? TPH : 32;

@@ -1,4 +1,5 @@
-"""Quick TC-path check: each op once on small bf16 D=128 inputs vs the oracle."""
+"""Quick TC-path parity probe (test infrastructure: it calls oracle/): each op once on
+bf16 D=128 inputs vs the fp64 oracle.  python tests/tc_check.py [B] [L] [ops]"""
 import sys, os, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch

@@ -190,11 +190,173 @@ __global__ void __launch_bounds__(128, MIX ? 1 : SWR_FFMA_FWD_MINB) fwd_ffma(con
 //   da_t[i] = sum_c lambda_t[i] x~_t[i-1] + r_t[i] mu_t w_t[i-1]
 //            (x~_t[-1] = v_{t-1}, w_t[-1] = 0)
 // ---------------------------------------------------------------------------
-#ifndef SWR_FFMA_BWD_MINB
-#define SWR_FFMA_BWD_MINB 4  // caps registers at 128: occupancy beats the spills (bwd 936 -> 642 us at d=16)
+#ifndef SWR_FFMA_C_UNROLL
+#define SWR_FFMA_C_UNROLL 4
 #endif
-template <typename T, int TPH, bool MIX>
-__global__ void __launch_bounds__(128, MIX ? 1 : SWR_FFMA_BWD_MINB) bwd_ffma(const Params p) {
+constexpr int kCUnroll = SWR_FFMA_C_UNROLL;  // pass C unroll (register pressure vs load ILP)
+
+#ifndef SWR_FFMA_BWD_MINB
+#define SWR_FFMA_BWD_MINB 4  // 128 registers: with pass C unrolled by 4, d=16 bwd 936 -> 481 us
+#endif
+// Three passes per block t (walked in reverse, carrying mu from block t+1), so a
+// thread never holds two blocks of per-channel arrays (the registers that capped
+// occupancy): A) Pass I of block t-1 streamed for its carrier v_{t-1} = w_{t-1}[15]
+// (its tiles are read again as block t-1 on the next step, from L2); B) the
+// adjoint recurrence lambda_t = L_t^T G_t in reverse, staged in shared memory
+// ([token][thread], conflict-free), with r_t = suffix products of a_t; C) Pass I of
+// block t forward, pairing w[i-1] with lambda[i]:
+//   du[i] = lambda[i] + r[i] mu,  da[i] = sum_c du[i] w[i-1] + g[i-1] (lambda[i] v)
+// (the same sums as the reverse-mode definition; g[-1] = 1, w[-1] = 0).
+template <typename T, int TPH>
+__global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma(const Params p) {
+  constexpr bool MIX = false;  // SWR only (the mixer uses bwd_ffma_mix)
+  using io = IO<T>;
+  constexpr int HPC = 128 / TPH;
+  constexpr int GS = TPH < 32 ? TPH : 32;
+  __shared__ float red[2][HPC][kEll];
+  __shared__ float2 slam[kEll][128];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int hh = tid / TPH;
+  const int c = 2 * (tid % TPH);
+  const int64_t b = blockIdx.z;
+  const int64_t h = (int64_t)blockIdx.y * HPC + hh;
+  const bool act = h < p.H;
+  const int64_t hc = act ? h : p.H - 1;  // inactive threads read a valid head, store nothing
+  const int64_t t_lo = (int64_t)blockIdx.x * p.K;
+  const int64_t t_hi = min(t_lo + p.K, p.nb);
+  const T* A = (const T*)p.a + b * p.sa_b + hc * p.sa_h;
+  T* dA = (T*)p.da + b * p.sa_b + hc * p.sa_h;
+  const int64_t xo = b * p.sx_b + hc * p.sx_h + c;
+  const int64_t co = (b * p.H + hc) * p.D + c;
+
+  // mu for block t_hi - 1: from the right halo block, or mu_in at the end of the sequence
+  float2 mu = make_float2(0.f, 0.f);
+  if (t_hi == p.nb) {
+    if (p.mu_in) mu = *reinterpret_cast<const float2*>(p.mu_in + co);
+  } else {
+    float a[kEll];
+    float2 G[kEll];
+    load_decays<T>(A, p.sa_l, t_hi * kEll, p.L, a);
+    load_G<T, MIX>(p, xo, t_hi * kEll, G);
+    float2 l = G[kEll - 1];
+#pragma unroll
+    for (int i = kEll - 2; i >= 0; --i) l = lambda_step(a[i + 1], l, G[i]);
+    mu = make_float2(a[0] * l.x, a[0] * l.y);
+  }
+
+  int buf = 0;
+  for (int64_t t = t_hi - 1; t >= t_lo; --t) {
+    const int64_t n0 = t * kEll;
+    // A) carrier v_{t-1}
+    float2 vprev = make_float2(0.f, 0.f);
+    if (t > 0) {
+      float a[kEll];
+      float2 u[kEll];
+      load_decays<T>(A, p.sa_l, n0 - kEll, p.L, a);
+      load_u<T, MIX>(p, xo, n0 - kEll, u);
+      float w0 = u[0].x, w1 = u[0].y;
+#pragma unroll
+      for (int i = 1; i < kEll; ++i) {
+        w0 = fmaf(a[i], w0, u[i].x);
+        w1 = fmaf(a[i], w1, u[i].y);
+      }
+      vprev = make_float2(w0, w1);
+    } else if (p.carry_in) {
+      vprev = *reinterpret_cast<const float2*>(p.carry_in + co);
+    }
+    // B) lambda_t in reverse (same op order as lambda_step above), r_t
+    float acur[kEll], r[kEll];
+    load_decays<T>(A, p.sa_l, n0, p.L, acur);
+    {
+      float2 G[kEll];
+      load_G<T, MIX>(p, xo, n0, G);
+      float2 lam = G[kEll - 1];
+      float rr = 1.f;
+      r[kEll - 1] = 1.f;
+      slam[kEll - 1][tid] = lam;
+#pragma unroll
+      for (int i = kEll - 2; i >= 0; --i) {
+        lam = lambda_step(acur[i + 1], lam, G[i]);
+        rr *= acur[i + 1];
+        r[i] = rr;  // r_t[i] = a_t[i+1] ... a_t[15]
+        slam[i][tid] = lam;
+      }
+    }
+    // C) Pass I of block t forward, du and da partials
+    float part[kEll];
+    float2 wprev = make_float2(0.f, 0.f);  // w[i-1]
+    float gs = 1.f;                        // g[i-1]
+    float2 lam0 = slam[0][tid];
+#pragma unroll kCUnroll
+    for (int i = 0; i < kEll; ++i) {
+      const int64_t n = n0 + i;
+      const float2 lam = slam[i][tid];
+      const float du0 = fmaf(r[i], mu.x, lam.x), du1 = fmaf(r[i], mu.y, lam.y);
+      float sdot = du0 * wprev.x;
+      sdot = fmaf(du1, wprev.y, sdot);
+      float lv = lam.x * vprev.x;
+      lv = fmaf(lam.y, vprev.y, lv);
+      part[i] = fmaf(gs, lv, sdot);
+      // w[i] = a[i] w[i-1] + u[i] (w[0] = u[0]: L_t excludes a_t[0])
+      float2 uu;
+      typename io::raw rk, rv;
+      if constexpr (!MIX) {
+        uu = (n < p.L) ? io::f2(io::ld((const T*)p.u + xo + n * p.sx_l)) : make_float2(0.f, 0.f);
+      } else {
+        rk = (n < p.L) ? io::ld((const T*)p.k + xo + n * p.sx_l) : io::zero();
+        rv = (n < p.L) ? io::ld((const T*)p.v + xo + n * p.sx_l) : io::zero();
+        const float2 kk = io::f2(rk), vv = io::f2(rv);
+        uu = make_float2(__fmul_rn(kk.x, vv.x), __fmul_rn(kk.y, vv.y));
+      }
+      const float2 w = (i == 0) ? uu : make_float2(fmaf(acur[i], wprev.x, uu.x), fmaf(acur[i], wprev.y, uu.y));
+      const float gi = gs * acur[i];  // g[i]
+      if (act && n < p.L) {
+        if constexpr (!MIX) {
+          io::st((T*)p.du + xo + n * p.sx_l, du0, du1);
+        } else {
+          const float2 kk = io::f2(rk), vv = io::f2(rv);
+          const float2 dd = io::f2(io::ld((const T*)p.dy + xo + n * p.sx_l));
+          const float x0 = fmaf(gi, vprev.x, w.x), x1 = fmaf(gi, vprev.y, w.y);  // x~[i]
+          io::st((T*)p.dq + xo + n * p.sx_l, dd.x * x0, dd.y * x1);          // dq = dy x~
+          io::st((T*)p.dk + xo + n * p.sx_l, du0 * vv.x, du1 * vv.y);        // dk = du^ v
+          io::st((T*)p.dv + xo + n * p.sx_l, fmaf(du0, kk.x, dd.x), fmaf(du1, kk.y, dd.y));  // dv
+        }
+      }
+      wprev = w;
+      gs = gi;
+    }
+    mu = make_float2(acur[0] * lam0.x, acur[0] * lam0.y);  // for block t-1
+    if (t == 0 && act && p.mu_out) *reinterpret_cast<float2*>(p.mu_out + co) = mu;
+
+    // da: deterministic reduction over the D channels of the head
+    int tok = 0;
+    GroupReduce<GS / 2, kEll>::run(part, lane, tok);
+    if constexpr (TPH <= 32) {
+      constexpr int NV = GS >= kEll ? 1 : kEll / GS;
+      const bool owner = (GS < 32) || ((lane & 1) == 0);
+      if (act && owner) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+          if (n0 + tok + j < p.L) io::st1(dA + (n0 + tok + j) * p.sa_l, part[j]);
+      }
+    } else {
+      const int wih = (tid % TPH) / 32;  // which of the head's two warps
+      if (wih == 1 && (lane & 1) == 0) red[buf][hh][tok] = part[0];
+      __syncthreads();
+      if (wih == 0 && (lane & 1) == 0 && act && n0 + tok < p.L)
+        io::st1(dA + (n0 + tok) * p.sa_l, part[0] + red[buf][hh][tok]);
+      buf ^= 1;
+    }
+  }
+}
+
+// The mixer backward keeps the two-block walk (block t-1's Pass I computed once and
+// reused as the next step's w): its three extra tile reads per token made the
+// three-pass form 10% slower.
+template <typename T, int TPH>
+__global__ void __launch_bounds__(128, 1) bwd_ffma_mix(const Params p) {
+  constexpr bool MIX = true;
   using io = IO<T>;
   constexpr int HPC = 128 / TPH;
   constexpr int GS = TPH < 32 ? TPH : 32;
@@ -352,8 +514,10 @@ static cudaError_t launch_tph(Params p, cudaStream_t st, int sms) {
   K = std::min<int64_t>(K, p.nb);
   p.K = K;
   dim3 grid((unsigned)ceil_div(p.nb, K), (unsigned)ceil_div(p.H, HPC), (unsigned)p.B);
-  if (BWD)
-    bwd_ffma<T, TPH, MIX><<<grid, 128, 0, st>>>(p);
+  if (BWD && MIX)
+    bwd_ffma_mix<T, TPH><<<grid, 128, 0, st>>>(p);
+  else if (BWD)
+    bwd_ffma<T, TPH><<<grid, 128, 0, st>>>(p);
   else
     fwd_ffma<T, TPH, MIX><<<grid, 128, 0, st>>>(p);
   return cudaGetLastError();

@@ -95,6 +95,7 @@ struct Cfg<0> {  // swr_fwd: in u;  out x
   static constexpr int NT = 1, NP = 0, BPI = 4, NI = SWR_F_NI, NA = SWR_F_NA, NW = 8, NO = SWR_F_NO, COLS = 16, NPW = SWR_F_NPW, NOUT = 1, NG = 3;
   static constexpr int TU = 0, TG = 0;  // A-operand regions of W and lambda
   static constexpr bool CYC = false;    // w MMA through the row-rotated tile (see Stage::kLc)
+  static constexpr bool WC = false;     // a second w MMA through the rotated tile, at column kWc
   static constexpr bool BWD = false, MIX = false;
 };
 template <>
@@ -102,6 +103,7 @@ struct Cfg<1> {  // swr_bwd: in u, G;  out du
   static constexpr int NT = 2, NP = 0, BPI = 2, NI = SWR_B_NI, NA = 8, NW = 8, NO = 4, COLS = 32, NPW = SWR_B_NPW, NOUT = 1, NG = SWR_B_NG;
   static constexpr int TU = 0, TG = 1;
   static constexpr bool CYC = true;
+  static constexpr bool WC = false;
   static constexpr bool BWD = true, MIX = false;
 };
 template <>
@@ -109,13 +111,15 @@ struct Cfg<2> {  // mix fwd: in q, k, v;  out y;  prep u^ = k v (over k)
   static constexpr int NT = 3, NP = 0, BPI = 2, NI = 6, NA = 6, NW = SWR_MF_NW, NO = 4, COLS = 16, NPW = SWR_MF_NPW, NOUT = 1, NG = 3;
   static constexpr int TU = 1, TG = 0;
   static constexpr bool CYC = false;
+  static constexpr bool WC = false;
   static constexpr bool BWD = false, MIX = true;
 };
 template <>
 struct Cfg<3> {  // mix bwd: in q, k, v, dy;  out dq, dk, dv;  prep u^ = k v (region 4), G = dy q (over q)
-  static constexpr int NT = 4, NP = 1, BPI = 1, NI = SWR_MB_NI, NA = 8, NW = 8, NO = 3, COLS = 32, NPW = 4, NOUT = 3, NG = 3;
+  static constexpr int NT = 4, NP = 1, BPI = 1, NI = SWR_MB_NI, NA = 8, NW = 8, NO = 3, COLS = 48, NPW = 4, NOUT = 3, NG = 3;
   static constexpr int TU = 4, TG = 0;
   static constexpr bool CYC = false;
+  static constexpr bool WC = true;  // x~ needs w[i] (dq), da needs w[i-1]: both from TMEM
   static constexpr bool BWD = true, MIX = true;
 };
 
@@ -141,7 +145,7 @@ struct Stage {
   // (SWR backward); then aux per block: g_t[16], r_t[16], gs[16] = g_t shifted by one
   // (gs[0] = 1), fp32, in fragment token order
   static constexpr int kLc = 512 * C::BPI;                     // offset of the CYC tiles
-  static constexpr int kAuxOff = kLc + (C::CYC ? 512 * C::BPI : 0);
+  static constexpr int kAuxOff = kLc + ((C::CYC || C::WC) ? 512 * C::BPI : 0);
   static constexpr int kAuxBlk = 48;  // floats
   static constexpr int kWork = kAuxOff + C::BPI * kAuxBlk * 4;
   // output slot
@@ -605,7 +609,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
   constexpr int kItemCols = BPI * C::COLS;
   // TMEM columns of a block: forward [w 0..15]; backward [lambda 0..15 | w 16..31], so
   // w is preceded by a valid column and can also be read shifted by one (w[i-1]).
-  constexpr int kWo = C::BWD ? 16 : 0, kLo = 0;
+  constexpr int kWo = C::BWD ? 16 : 0, kLo = 0, kWc = 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int kPrepW0 = 4 * NG, kProdW = kPrepW0 + C::NPW, kMmaW = kProdW + 1, kStoreW = kMmaW + 1,
                 kRetW = kStoreW + 1, kAProdW = C::MIX ? -1 : kRetW + 1;
@@ -781,6 +785,8 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
           umma_bf16(d + kWo, desc_A<S::kHS>(su32(S::tile(st, k, C::TU))), desc_Bmn(lw), kIdescBmn);  // w^T
           if constexpr (C::BWD)  // lambda^T
             umma_bf16(d + kLo, desc_A<S::kHS>(su32(S::tile(st, k, C::TG))), desc_Bk(lt), kIdescBk);
+          if constexpr (C::WC)  // [w15, w0 .. w14]^T
+            umma_bf16(d + kWc, desc_A<S::kHS>(su32(S::tile(st, k, C::TU))), desc_Bmn(lt + S::kLc), kIdescBmn);
         }
         umma_commit(&mmad[rw.s]);
         trace(p, j, 5);
@@ -925,7 +931,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
           hi.z = pack_bf2(Lc[12], Lc[13]); hi.w = pack_bf2(Lc[14], Lc[15]);
           *reinterpret_cast<uint4*>(l + ltile_off(0, col)) = lo;
           *reinterpret_cast<uint4*>(l + ltile_off(8, col)) = hi;
-          if constexpr (C::CYC) {  // rows rotated by one: Lc[i][col] = L[(i-1) mod 16][col]
+          if constexpr (C::CYC || C::WC) {  // rows rotated by one: Lc[i][col] = L[(i-1) mod 16][col]
             uint8_t* lc = wt + S::kLc + 512 * k;
             uint4 clo, chi;
             clo.x = pack_bf2(Lc[15], Lc[0]); clo.y = pack_bf2(Lc[1], Lc[2]);
@@ -1117,17 +1123,21 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
             float rv[4], sv[4];
             load_aux(ga + 16 + 4 * qd, rv);
             load_aux(ga + 32 + 4 * qd, sv);  // gs = g shifted by one
+            float wc[4][4];
+            if constexpr (C::WC) tmem_ld_frag(tb + kWc, wc);
             tmem_wait_frag(lam);
             tmem_wait_frag(w);
+            if constexpr (C::WC) tmem_wait_frag(wc);
             float wsh[4][4], vnext[4] = {0.f, 0.f, 0.f, 0.f};  // wsh[k][m] = w[tk_m - 1], w[-1] = 0
-            if constexpr (C::CYC) {
+            if constexpr (C::CYC || C::WC) {
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
-                vnext[k] = __shfl_sync(0xffffffffu, w[k][0], lane & ~3);  // token 0 of qd 0: w[15]
-                wsh[k][0] = qd == 0 ? 0.f : w[k][0];
-                wsh[k][1] = w[k][1];
-                wsh[k][2] = w[k][2];
-                wsh[k][3] = w[k][3];
+                const float (&wr)[4] = C::WC ? wc[k] : w[k];  // the rotated product
+                vnext[k] = __shfl_sync(0xffffffffu, wr[0], lane & ~3);  // token 0 of qd 0: w[15]
+                wsh[k][0] = qd == 0 ? 0.f : wr[0];
+                wsh[k][1] = wr[1];
+                wsh[k][2] = wr[2];
+                wsh[k][3] = wr[3];
               }
             } else {
               const int src = (lane & ~3) | ((lane + 3) & 3);  // lane - 1 inside the quad (qd 0 <- qd 3)
@@ -1217,7 +1227,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
             }
 #pragma unroll
             for (int k = 0; k < 4; ++k)  // v_t = w_t[15]
-              v[k] = C::CYC ? vnext[k] : __shfl_sync(0xffffffffu, w[k][3], lane | 3);
+              v[k] = (C::CYC || C::WC) ? vnext[k] : __shfl_sync(0xffffffffu, w[k][3], lane | 3);
           }
         }
       }

@@ -61,6 +61,9 @@ constexpr int kHalf = 2048;      // one 64-channel half: 16 rows x 128 B, 128B-s
 #ifndef SWR_F_NI
 #define SWR_F_NI 8
 #endif
+#ifndef SWR_F_BPI
+#define SWR_F_BPI 4
+#endif
 #ifndef SWR_F_NO
 #define SWR_F_NO 3
 #endif
@@ -92,7 +95,7 @@ template <int OP>
 struct Cfg;
 template <>
 struct Cfg<0> {  // swr_fwd: in u;  out x
-  static constexpr int NT = 1, NP = 0, BPI = 4, NI = SWR_F_NI, NA = SWR_F_NA, NW = 8, NO = SWR_F_NO, COLS = 16, NPW = SWR_F_NPW, NOUT = 1, NG = 3;
+  static constexpr int NT = 1, NP = 0, BPI = SWR_F_BPI, NI = SWR_F_NI, NA = SWR_F_NA, NW = 8, NO = SWR_F_NO, COLS = 16, NPW = SWR_F_NPW, NOUT = 1, NG = 3;
   static constexpr int TU = 0, TG = 0;  // A-operand regions of W and lambda
   static constexpr bool CYC = false;    // w MMA through the row-rotated tile (see Stage::kLc)
   static constexpr bool WC = false;     // a second w MMA through the rotated tile, at column kWc

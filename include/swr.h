@@ -165,10 +165,13 @@ SWR_API swr_path swr_set_path(swr_path p);
 SWR_API int64_t swr_launch_count(void);
 SWR_API int swr_last_path(void);
 
-/* Diagnostics: when `buf` (device memory, >= 16 * n uint64) is non-NULL, the
+/* Diagnostics (effective only in a library built with -DSWR_TRACE=1, e.g.
+ * tools/build_var.sh trace -DSWR_TRACE=1; the product build compiles it out):
+ * when `buf` (device memory, >= 16 * n + 4 * gridDim uint64) is non-NULL, the
  * tensor-core kernels of CTA 0 record a clock64 timestamp (SM cycles) per pipeline
  * event for each of their first n items (slot = 16 * item + event; events are
- * listed in paper_2512_13921_b200/csrc/swr_tc.cu).  NULL disables tracing. */
+ * listed in paper_2512_13921_b200/csrc/swr_tc.cu), and every CTA its start/end
+ * %globaltimer, SM id and range size at 16 * n + 4 * cta.  NULL disables it. */
 SWR_API void swr_set_trace(unsigned long long* buf, int64_t n);
 
 #ifdef __cplusplus

@@ -10,20 +10,27 @@
 //     column cumulative products) in bf16, and the fp32
 //     accumulator sits in TMEM lanes = channels, columns = tokens.
 //   * Backward also computes lambda_t = L_t^T G_t the same way (B = L_t).
-//   * The epilogue warps read TMEM with tcgen05.ld (thread = channel, all 16
-//     tokens), so Pass II x~ = w + g v_{t-1}, the carrier
-//     v_t = w_t[15] and the backward pairings are thread-local; the
-//     carrier between consecutive blocks stays in a register (no SMEM/DSMEM
-//     exchange, no cross-CTA sync).
-//   * One persistent CTA per SM walks a contiguous range of (b, h, block)
-//     items; tiles move HBM -> SMEM -> HBM with TMA (cp.async.bulk.tensor),
-//     through an NS-stage mbarrier ring; a CTA recomputes one halo block at a
-//     range boundary (and, backward, one on the right).
+//   * The epilogue warps read TMEM with tcgen05.ld.16x256b in the m16n8 fragment
+//     layout (a lane owns 4 channels x 4 tokens), so Pass II x~ = w + g v_{t-1}
+//     (P:1478), du = lambda + r mu and the da terms are thread-local, token pairs
+//     are packed fp32x2 / bf16x2, and results reach the swizzled output tile with
+//     stmatrix.trans; the carrier v_t = w_t[15] passes to the next block
+//     in registers (no SMEM/DSMEM exchange, no cross-CTA sync).  The SWR backward
+//     computes w through a row-rotated transfer tile so w[i-1] and w[15] are read
+//     in place.
+//   * One persistent CTA per SM walks a contiguous range of (b, h, block) items,
+//     sized for that SM's measured rate (Split), recomputing one halo item at a
+//     range boundary (and, backward, one on the right); tiles move HBM -> SMEM ->
+//     HBM with TMA (cp.async.bulk.tensor) through mbarrier rings: input stages,
+//     decay stages (loaded ahead by their own producer for the SWR ops), work
+//     slots (transfer tiles, g/r, TMEM columns) and output slots.
 //
 // Warp roles: 4*NG epilogue warps in NG groups of 4 (group g handles items
-// j = g mod NG; warp w reads TMEM lanes 32*(w%4)..+31), then NPW prep warps (L
-// tiles, g/r, mixer pre-gates; two items per pass), the producer (TMA loads),
-// the MMA issuer (one elected thread) and the store warp (TMA stores, release).
+// j = g mod NG; warp w reads TMEM lanes 32*(w%4)..+31), NPW prep warps (transfer
+// tiles, g/r/gs, mixer pre-gates), the TMA producer, the MMA issuer (one thread),
+// the store warp (TMA stores, da sums, slot release), the retire warp (MMA
+// completion in order, input-stage release, readiness) and, for the SWR ops, the
+// decay producer.  DESIGN.md section 5.1 has the rings' phase-parity invariants.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 

@@ -108,6 +108,9 @@ __device__ __forceinline__ void load_G(const Params& p, int64_t xo, int64_t n0,
 // ---------------------------------------------------------------------------
 // forward
 // ---------------------------------------------------------------------------
+#ifndef SWR_FFMA_FWD_V1
+#define SWR_FFMA_FWD_V1 0  // 1: the two-channel forward (fwd_ffma) instead of fwd_stream
+#endif
 #ifndef SWR_FFMA_FWD_MINB
 #define SWR_FFMA_FWD_MINB 3
 #endif
@@ -500,9 +503,185 @@ __global__ void __launch_bounds__(128, 1) bwd_ffma_mix(const Params p) {
 }
 
 // ---------------------------------------------------------------------------
+// forward, streamed: a thread owns one 16-byte vector of channels (VC = 8 bf16 or
+// 4 fp32) and walks its chunk token by token -- Pass I as the local recurrence
+// (restarted at each block start, w[0] = u[0]), g_t[i] = a_t[0]...a_t[i] as
+// a running product (products only), Pass II x~ = w + g v_{t-1},
+// v_t = w_t[15] -- with one 16-byte load and store per token and tensor and no
+// per-block arrays (the same arithmetic, in the same order, as fwd_ffma).
+// ---------------------------------------------------------------------------
+template <typename T>
+struct Vec16;
+template <>
+struct Vec16<__nv_bfloat16> {
+  static constexpr int N = 8;
+  static __device__ __forceinline__ void to_f(const uint4& r, float (&f)[8]) {
+    const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      f[2 * q] = __uint_as_float(w[q] << 16);
+      f[2 * q + 1] = __uint_as_float(w[q] & 0xffff0000u);
+    }
+  }
+  static __device__ __forceinline__ uint4 from_f(const float (&f)[8]) {
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      __nv_bfloat162 b2 = __floats2bfloat162_rn(f[2 * q], f[2 * q + 1]);
+      w[q] = *reinterpret_cast<uint32_t*>(&b2);
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+  }
+};
+template <>
+struct Vec16<float> {
+  static constexpr int N = 4;
+  static __device__ __forceinline__ void to_f(const uint4& r, float (&f)[4]) {
+    f[0] = __uint_as_float(r.x);
+    f[1] = __uint_as_float(r.y);
+    f[2] = __uint_as_float(r.z);
+    f[3] = __uint_as_float(r.w);
+  }
+  static __device__ __forceinline__ uint4 from_f(const float (&f)[4]) {
+    return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]), __float_as_uint(f[3]));
+  }
+};
+
+template <typename T, bool MIX>
+__device__ __forceinline__ void load_u16(const Params& p, int64_t off, bool valid, float (&u)[Vec16<T>::N]) {
+  constexpr int VC = Vec16<T>::N;
+  if (!valid) {
+#pragma unroll
+    for (int e = 0; e < VC; ++e) u[e] = 0.f;
+    return;
+  }
+  if constexpr (!MIX) {
+    Vec16<T>::to_f(__ldg(reinterpret_cast<const uint4*>((const T*)p.u + off)), u);
+  } else {  // u^ = k (.) v
+    float kk[VC], vv[VC];
+    Vec16<T>::to_f(__ldg(reinterpret_cast<const uint4*>((const T*)p.k + off)), kk);
+    Vec16<T>::to_f(__ldg(reinterpret_cast<const uint4*>((const T*)p.v + off)), vv);
+#pragma unroll
+    for (int e = 0; e < VC; ++e) u[e] = __fmul_rn(kk[e], vv[e]);
+  }
+}
+
+template <typename T, bool MIX>
+__global__ void __launch_bounds__(128) fwd_stream(const Params p) {
+  constexpr int VC = Vec16<T>::N;
+  const int TPH = (int)p.D / VC;  // threads per head
+  const int HPC = 128 / TPH;      // heads per CTA
+  const int tid = threadIdx.x;
+  const int hh = tid / TPH;
+  const int c = VC * (tid % TPH);
+  const int64_t b = blockIdx.z;
+  const int64_t h = (int64_t)blockIdx.y * HPC + hh;
+  if (h >= p.H) return;
+  const int64_t t_lo = (int64_t)blockIdx.x * p.K;
+  const int64_t t_hi = min(t_lo + p.K, p.nb);
+  const T* A = (const T*)p.a + b * p.sa_b + h * p.sa_h;
+  const int64_t xo = b * p.sx_b + h * p.sx_h + c;
+  const int64_t co = (b * p.H + h) * p.D + c;
+
+  float v[VC];  // carrier v_{t-1}; v_{-1} = carry_in or 0
+#pragma unroll
+  for (int e = 0; e < VC; ++e) v[e] = 0.f;
+  if (t_lo == 0) {
+    if (p.carry_in) {
+#pragma unroll
+      for (int e = 0; e < VC; ++e) v[e] = p.carry_in[co + e];
+    }
+  } else {  // halo: Pass I of block t_lo - 1
+    float w[VC];
+#pragma unroll
+    for (int i = 0; i < kEll; ++i) {
+      const int64_t n = (t_lo - 1) * kEll + i;
+      const bool valid = n < p.L;
+      const float a = valid ? IO<T>::ld1(A + n * p.sa_l) : 1.f;
+      float u[VC];
+      load_u16<T, MIX>(p, xo + n * p.sx_l, valid, u);
+#pragma unroll
+      for (int e = 0; e < VC; ++e) w[e] = (i == 0) ? u[e] : fmaf(a, w[e], u[e]);
+    }
+#pragma unroll
+    for (int e = 0; e < VC; ++e) v[e] = w[e];
+  }
+
+  for (int64_t t = t_lo; t < t_hi; ++t) {
+    float w[VC];
+    float g = 1.f;
+    // SWR: the block's loads first (stores to x may alias them, so the compiler
+    // cannot hoist them past the stores): 16 decays and 16 raw 16-byte vectors.
+    // Mixer: per token (three tiles per token would cost too many registers).
+    float ab[MIX ? 1 : kEll];
+    uint4 ub[MIX ? 1 : kEll];
+    if constexpr (!MIX) {
+#pragma unroll
+      for (int i = 0; i < kEll; ++i) {
+        const int64_t n = t * kEll + i;
+        const bool valid = n < p.L;
+        ab[i] = valid ? IO<T>::ld1(A + n * p.sa_l) : 1.f;  // pad: a = 1 (carry_out = state at L-1)
+        ub[i] = valid ? __ldg(reinterpret_cast<const uint4*>((const T*)p.u + xo + n * p.sx_l)) : make_uint4(0, 0, 0, 0);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kEll; ++i) {
+      const int64_t n = t * kEll + i;
+      const bool valid = n < p.L;
+      float a, u[VC];
+      if constexpr (!MIX) {
+        a = ab[i];
+        Vec16<T>::to_f(ub[i], u);
+      } else {
+        a = valid ? IO<T>::ld1(A + n * p.sa_l) : 1.f;
+        load_u16<T, true>(p, xo + n * p.sx_l, valid, u);
+      }
+      g *= a;  // g_t[i] = a_t[0] ... a_t[i]
+      float x[VC];
+#pragma unroll
+      for (int e = 0; e < VC; ++e) {
+        w[e] = (i == 0) ? u[e] : fmaf(a, w[e], u[e]);  // Pass I
+        x[e] = fmaf(g, v[e], w[e]);                      // Pass II: x~ = w + g v_{t-1}
+      }
+      if (valid) {
+        if constexpr (!MIX) {
+          *reinterpret_cast<uint4*>((T*)p.x + xo + n * p.sx_l) = Vec16<T>::from_f(x);
+        } else {  // post-gate with residual: y = q x~ + v
+          float qq[VC], vv[VC];
+          Vec16<T>::to_f(__ldg(reinterpret_cast<const uint4*>((const T*)p.q + xo + n * p.sx_l)), qq);
+          Vec16<T>::to_f(__ldg(reinterpret_cast<const uint4*>((const T*)p.v + xo + n * p.sx_l)), vv);
+#pragma unroll
+          for (int e = 0; e < VC; ++e) x[e] = fmaf(qq[e], x[e], vv[e]);
+          *reinterpret_cast<uint4*>((T*)p.y + xo + n * p.sx_l) = Vec16<T>::from_f(x);
+        }
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < VC; ++e) v[e] = w[e];  // v_t = w_t[15]
+  }
+  if (t_hi == p.nb && p.carry_out) {
+#pragma unroll
+    for (int e = 0; e < VC; ++e) p.carry_out[co + e] = v[e];
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// forward (SWR and mixer): the streamed kernel, 16 bytes of channels per thread
+template <typename T, bool MIX>
+static cudaError_t launch_fwd_stream(Params p, cudaStream_t st, int sms) {
+  const int64_t hpc = 128 / (p.D / Vec16<T>::N);
+  const int64_t cols = p.B * ceil_div(p.H, hpc);
+  const int64_t want_chunks = std::max<int64_t>(1, ((int64_t)sms * 8) / std::max<int64_t>(cols, 1));
+  int64_t K = std::min<int64_t>(std::max<int64_t>(ceil_div(p.nb, want_chunks), 4), p.nb);
+  p.K = K;
+  dim3 grid((unsigned)ceil_div(p.nb, K), (unsigned)ceil_div(p.H, hpc), (unsigned)p.B);
+  fwd_stream<T, MIX><<<grid, 128, 0, st>>>(p);
+  return cudaGetLastError();
+}
 
 template <typename T, int TPH, bool MIX, bool BWD>
 static cudaError_t launch_tph(Params p, cudaStream_t st, int sms) {
@@ -525,6 +704,9 @@ static cudaError_t launch_tph(Params p, cudaStream_t st, int sms) {
 
 template <typename T, bool MIX, bool BWD>
 static cudaError_t launch_d(const Params& p, cudaStream_t st, int sms) {
+  if constexpr (!BWD) {
+    if (!SWR_FFMA_FWD_V1) return launch_fwd_stream<T, MIX>(p, st, sms);
+  }
   switch (p.D) {
     case 16: return launch_tph<T, 8, MIX, BWD>(p, st, sms);
     case 32: return launch_tph<T, 16, MIX, BWD>(p, st, sms);

@@ -15,8 +15,13 @@ Two modes:
       forward : rank p -> p+1  carry_out (local end state of p's last block, v_b)
       backward: rank p+1 -> p  mu_out    (a[first] * lambda[block 0][0])
   Each halo value is computed by a one-block prologue call on the rank's own
-  inputs, sent with point-to-point send/recv (NCCL over NVLink on GPUs), and the
-  main call then runs with carry_in / mu_in.  Results are bitwise identical to
+  inputs and sent with point-to-point send/recv (NCCL over NVLink on GPUs).  The
+  exchange overlaps the interior: the main call runs without the incoming halo
+  while the send/recv is in flight (NCCL's own stream), then only the block that
+  needs it is recomputed with it -- the shard's first block (forward, with
+  carry_in) or its last block (backward, with mu_in, from a two-block slice so its
+  predecessor's carrier is recomputed too) -- and copied over.  Blocks are computed
+  identically whichever call computes them, so results are bitwise identical to
   the single-GPU run (tests/test_props.py, tests/test_dist_cpu.py).
 
 ``ops`` defaults to the CUDA binding (paper_2512_13921_b200.ops), whose carriers
@@ -52,11 +57,10 @@ def _default_ops():
     return ops
 
 
-def _exchange(send_t, to_rank, recv_like, from_rank, group):
-    """Point-to-point halo exchange; returns the received tensor (or None)."""
-    backend = dist.get_backend(group)
-    cpu = backend == "gloo"
-    reqs, recv = [], None
+def _start_exchange(send_t, to_rank, recv_like, from_rank, group):
+    """Post the point-to-point halo exchange; returns (requests, receive buffer)."""
+    cpu = dist.get_backend(group) == "gloo"
+    recv = None
     if recv_like is not None:
         recv = torch.empty_like(recv_like, device="cpu" if cpu else recv_like.device)
     ops = []
@@ -65,11 +69,15 @@ def _exchange(send_t, to_rank, recv_like, from_rank, group):
         ops.append(dist.P2POp(dist.isend, s, to_rank, group))
     if recv is not None:
         ops.append(dist.P2POp(dist.irecv, recv, from_rank, group))
-    if ops:
-        reqs = dist.batch_isend_irecv(ops)
-        for r in reqs:
-            r.wait()
-    if recv is not None and recv_like is not None and recv.device != recv_like.device:
+    reqs = dist.batch_isend_irecv(ops) if ops else []
+    return reqs, recv
+
+
+def _finish_exchange(reqs, recv, recv_like):
+    """Complete the exchange (NCCL: the current stream waits for it, no host block)."""
+    for r in reqs:
+        r.wait()
+    if recv is not None and recv.device != recv_like.device:
         recv = recv.to(recv_like.device)
     return recv
 
@@ -93,9 +101,17 @@ def swr_sp_fwd(u, a, group=None, carry_in=None, ops=None, carry_dtype=torch.floa
         _, send = ops.swr_fwd(u[:, lo:], a[:, lo:], return_carry=True)
     B, _, H, D = u.shape
     like = torch.empty((B, H, D), dtype=carry_dtype, device=u.device) if rank > 0 else None
-    recv = _exchange(send, rank + 1, like, rank - 1, group)
-    cin = recv if rank > 0 else carry_in
-    x = ops.swr_fwd(u, a, carry_in=cin)
+    reqs, recv = _start_exchange(send, rank + 1, like, rank - 1, group)
+    if rank == 0:
+        x = ops.swr_fwd(u, a, carry_in=carry_in)
+        _finish_exchange(reqs, recv, like)
+        return x, carry_in
+    # interior while the halo is in flight (block 0 gets v_{-1} = 0 here) ...
+    x = ops.swr_fwd(u, a)
+    cin = _finish_exchange(reqs, recv, like)
+    # ... then block 0 again with the received carrier
+    n0 = min(ELL, u.shape[1])
+    x[:, :n0] = ops.swr_fwd(u[:, :n0], a[:, :n0], carry_in=cin)
     return x, cin
 
 
@@ -111,8 +127,23 @@ def swr_sp_bwd(u, a, dx, carry_in=None, group=None, ops=None, carry_dtype=torch.
     if rank > 0:
         n0 = min(ELL, u.shape[1])
         _, _, send = ops.swr_bwd(u[:, :n0], a[:, :n0], dx[:, :n0], carry_in=None)
-    B, _, H, D = u.shape
+    B, Ls, H, D = u.shape
     like = torch.empty((B, H, D), dtype=carry_dtype, device=u.device) if rank < world - 1 else None
-    mu_in = _exchange(send, rank - 1, like, rank + 1, group)
-    du, da, mu_out = ops.swr_bwd(u, a, dx, carry_in=carry_in, mu_in=mu_in)
+    reqs, recv = _start_exchange(send, rank - 1, like, rank + 1, group)
+    # interior while the halo is in flight (the last block gets mu = 0 here) ...
+    du, da, mu_out = ops.swr_bwd(u, a, dx, carry_in=carry_in)
+    mu_in = _finish_exchange(reqs, recv, like)
+    if mu_in is not None:
+        # ... then the last block again with mu_in; its carrier comes from the
+        # block before it, so the slice starts one block earlier (or at 0 with
+        # carry_in), and only the last block is copied back
+        nb = (Ls + ELL - 1) // ELL
+        lo = (nb - 1) * ELL
+        s0 = max(lo - ELL, 0)
+        cin = carry_in if s0 == 0 else None
+        dus, das, mos = ops.swr_bwd(u[:, s0:], a[:, s0:], dx[:, s0:], carry_in=cin, mu_in=mu_in)
+        du[:, lo:] = dus[:, lo - s0:]
+        da[:, lo:] = das[:, lo - s0:]
+        if nb == 1:
+            mu_out = mos  # a one-block shard: its first block is its last
     return du, da, mu_out

@@ -75,7 +75,7 @@ def _sp_worker(rank, world, port, L, outdir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,L", [(2, 64), (2, 70), (4, 160), (4, 77)])
+@pytest.mark.parametrize("world,L", [(2, 64), (2, 70), (4, 160), (4, 77), (3, 40)])
 def test_sequence_parallel_stitching_gloo(tmp_path, world, L):
     import oracle
     mp.spawn(_sp_worker, args=(world, _free_port(), L, str(tmp_path)), nprocs=world, join=True)

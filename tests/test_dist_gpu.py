@@ -44,7 +44,7 @@ def _worker(rank, world, port, L, outdir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,L", [(2, 512), (4, 1024)])
+@pytest.mark.parametrize("world,L", [(2, 512), (4, 1024), (3, 100), (2, 33)])
 def test_sp_on_gpu_kernels_is_bitwise(tmp_path, world, L):
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")

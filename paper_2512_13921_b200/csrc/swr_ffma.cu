@@ -17,6 +17,7 @@
 // chunk size.  Backward walks the chunk in reverse time order carrying
 // mu_t = a_{t+1}[0] lambda_{t+1}[0] (DESIGN.md Appendix "backward").
 #include <algorithm>
+#include <type_traits>
 
 #include "swr_common.cuh"
 
@@ -666,6 +667,231 @@ __global__ void __launch_bounds__(128) fwd_stream(const Params p) {
 }
 
 // ---------------------------------------------------------------------------
+// backward, vectorised (SWR): the three-pass walk of bwd_ffma with a thread owning
+// VC channels (one 8- or 16-byte vector per tensor and token), per-block base
+// pointers advanced by the token stride (no per-token 64-bit index products), and
+// the adjoint lambda_t staged in dynamic shared memory as [token][VC/4][thread]
+// float4s.  Same recurrences and op order per channel as bwd_ffma; only the da sum
+// over the head's channels is associated differently (VC-channel chains, then the
+// lane transpose-reduce).
+// ---------------------------------------------------------------------------
+#ifndef SWR_FFMA_BWD_VC
+#define SWR_FFMA_BWD_VC 4  // bf16 channels per thread (4: 8-byte vectors; 8: 16-byte, 20% slower at d=16)
+#endif
+#ifndef SWR_FFMA_BWD_V1
+#define SWR_FFMA_BWD_V1 0  // 1: the two-channel bwd_ffma for SWR
+#endif
+#ifndef SWR_FFMA_BWDV_UNROLL
+#define SWR_FFMA_BWDV_UNROLL 4  // pass C unroll (16 spills 1.3 KB: 3x slower; 2 or 8: 5-15% slower)
+#endif
+constexpr int kCUnrollV = SWR_FFMA_BWDV_UNROLL;
+
+template <typename T, int VC>
+struct VecN {
+  static_assert(sizeof(T) * VC == 8 || sizeof(T) * VC == 16, "8- or 16-byte vectors");
+  using raw = typename std::conditional<sizeof(T) * VC == 8, uint2, uint4>::type;
+  static __device__ __forceinline__ raw ld(const T* p) { return __ldg(reinterpret_cast<const raw*>(p)); }
+  static __device__ __forceinline__ raw zero() { raw r; memset(&r, 0, sizeof r); return r; }
+  static __device__ __forceinline__ void to_f(const raw& r, float (&f)[VC]) {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(&r);
+    if constexpr (sizeof(T) == 2) {
+#pragma unroll
+      for (int q = 0; q < VC / 2; ++q) {
+        f[2 * q] = __uint_as_float(w[q] << 16);
+        f[2 * q + 1] = __uint_as_float(w[q] & 0xffff0000u);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < VC; ++q) f[q] = __uint_as_float(w[q]);
+    }
+  }
+  static __device__ __forceinline__ void st(T* p, const float (&f)[VC]) {
+    raw r;
+    uint32_t* w = reinterpret_cast<uint32_t*>(&r);
+    if constexpr (sizeof(T) == 2) {
+#pragma unroll
+      for (int q = 0; q < VC / 2; ++q) {
+        __nv_bfloat162 b2 = __floats2bfloat162_rn(f[2 * q], f[2 * q + 1]);
+        w[q] = *reinterpret_cast<uint32_t*>(&b2);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < VC; ++q) w[q] = __float_as_uint(f[q]);
+    }
+    *reinterpret_cast<raw*>(p) = r;
+  }
+};
+
+template <typename T, int VC, int TPH>
+__global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma_vec(const Params p) {
+  using V = VecN<T, VC>;
+  using io = IO<T>;
+  constexpr int HPC = 128 / TPH;
+  constexpr int GS = TPH;  // lanes per head (<= 32)
+  constexpr int NQ = VC / 4;
+  extern __shared__ float4 slam[];  // [kEll][NQ][128]
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int hh = tid / TPH;
+  const int c = VC * (tid % TPH);
+  const int64_t b = blockIdx.z;
+  const int64_t h = (int64_t)blockIdx.y * HPC + hh;
+  const bool act = h < p.H;
+  const int64_t hc = act ? h : p.H - 1;  // inactive threads read a valid head, store nothing
+  const int64_t t_lo = (int64_t)blockIdx.x * p.K;
+  const int64_t t_hi = min(t_lo + p.K, p.nb);
+  const int64_t sl = p.sx_l, sal = p.sa_l;
+  const int64_t xo = b * p.sx_b + hc * p.sx_h + c;
+  const int64_t co = (b * p.H + hc) * p.D + c;
+  const T* A0 = (const T*)p.a + b * p.sa_b + hc * p.sa_h;
+  T* dA = (T*)p.da + b * p.sa_b + hc * p.sa_h;
+  const T* U0 = (const T*)p.u + xo;
+  const T* G0 = (const T*)p.dx + xo;
+  T* DU0 = (T*)p.du + xo;
+  auto lam_at = [&](int i, int q) -> float4& { return slam[(i * NQ + q) * 128 + tid]; };
+
+  // decays of a block (pad a = 1 past L)
+  auto load_a = [&](int64_t n0, int lim, float (&a)[kEll]) {
+    const T* ap = A0 + n0 * sal;
+#pragma unroll
+    for (int i = 0; i < kEll; ++i) {
+      a[i] = (i < lim) ? io::ld1(ap) : 1.f;
+      ap += sal;
+    }
+  };
+
+  // mu for block t_hi - 1: a_{t_hi}[0] lambda_{t_hi}[0] from the right halo block, or mu_in
+  float mu[VC];
+#pragma unroll
+  for (int e = 0; e < VC; ++e) mu[e] = 0.f;
+  if (t_hi == p.nb) {
+    if (p.mu_in) {
+#pragma unroll
+      for (int e = 0; e < VC; ++e) mu[e] = p.mu_in[co + e];
+    }
+  } else {
+    const int64_t n0 = t_hi * kEll;
+    const int lim = (p.L - n0 < kEll) ? (int)(p.L - n0) : kEll;
+    float a[kEll];
+    load_a(n0, lim, a);
+    float l[VC];
+    const T* gp = G0 + (n0 + kEll - 1) * sl;
+    V::to_f(kEll - 1 < lim ? V::ld(gp) : V::zero(), l);  // l[15] = G[15]
+#pragma unroll
+    for (int i = kEll - 2; i >= 0; --i) {
+      float g[VC];
+      gp -= sl;
+      V::to_f(i < lim ? V::ld(gp) : V::zero(), g);
+#pragma unroll
+      for (int e = 0; e < VC; ++e) l[e] = fmaf(a[i + 1], l[e], g[e]);
+    }
+#pragma unroll
+    for (int e = 0; e < VC; ++e) mu[e] = a[0] * l[e];
+  }
+
+  for (int64_t t = t_hi - 1; t >= t_lo; --t) {
+    const int64_t n0 = t * kEll;
+    const int lim = (p.L - n0 < kEll) ? (int)(p.L - n0) : kEll;
+    // A) carrier v_{t-1} = w_{t-1}[15] (block t-1 is whole: only the last block is ragged)
+    float vprev[VC];
+    if (t > 0) {
+      const T* ap = A0 + (n0 - kEll) * sal;
+      const T* up = U0 + (n0 - kEll) * sl;
+#pragma unroll
+      for (int i = 0; i < kEll; ++i) {
+        const float a = io::ld1(ap);
+        float u[VC];
+        V::to_f(V::ld(up), u);
+        ap += sal;
+        up += sl;
+#pragma unroll
+        for (int e = 0; e < VC; ++e) vprev[e] = (i == 0) ? u[e] : fmaf(a, vprev[e], u[e]);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < VC; ++e) vprev[e] = p.carry_in ? p.carry_in[co + e] : 0.f;
+    }
+    // B) lambda_t in reverse (lambda[15] = G[15], lambda[i] = G[i] + a[i+1] lambda[i+1]), r_t
+    float acur[kEll], r[kEll];
+    load_a(n0, lim, acur);
+    {
+      float lam[VC];
+      float rr = 1.f;
+      const T* gp = G0 + (n0 + kEll - 1) * sl;
+      V::to_f(kEll - 1 < lim ? V::ld(gp) : V::zero(), lam);  // lambda[15] = G[15]
+      r[kEll - 1] = 1.f;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+        lam_at(kEll - 1, q) = make_float4(lam[4 * q], lam[4 * q + 1], lam[4 * q + 2], lam[4 * q + 3]);
+#pragma unroll
+      for (int i = kEll - 2; i >= 0; --i) {
+        float g[VC];
+        gp -= sl;
+        V::to_f(i < lim ? V::ld(gp) : V::zero(), g);
+#pragma unroll
+        for (int e = 0; e < VC; ++e) lam[e] = fmaf(acur[i + 1], lam[e], g[e]);
+        rr *= acur[i + 1];
+        r[i] = rr;  // r_t[i] = a_t[i+1] ... a_t[15]
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) lam_at(i, q) = make_float4(lam[4 * q], lam[4 * q + 1], lam[4 * q + 2], lam[4 * q + 3]);
+      }
+    }
+    // C) Pass I of block t forward, du and da partials
+    float part[kEll];
+    float wprev[VC];
+    float gs = 1.f;  // g[i-1]
+    const T* up = U0 + n0 * sl;
+    T* dup = DU0 + n0 * sl;
+#pragma unroll kCUnrollV
+    for (int i = 0; i < kEll; ++i) {
+      float lam[VC];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const float4 l4 = lam_at(i, q);
+        lam[4 * q] = l4.x; lam[4 * q + 1] = l4.y; lam[4 * q + 2] = l4.z; lam[4 * q + 3] = l4.w;
+      }
+      float du[VC];
+      float sdot = 0.f, lv = 0.f;  // sum_c du[i] w[i-1] (w[-1] = 0), sum_c lambda[i] v_{t-1}
+#pragma unroll
+      for (int e = 0; e < VC; ++e) {
+        du[e] = fmaf(r[i], mu[e], lam[e]);
+        if (i > 0) sdot = (e == 0) ? du[e] * wprev[e] : fmaf(du[e], wprev[e], sdot);
+        lv = (e == 0) ? lam[e] * vprev[e] : fmaf(lam[e], vprev[e], lv);
+      }
+      part[i] = fmaf(gs, lv, sdot);
+      float u[VC];
+      V::to_f(i < lim ? V::ld(up) : V::zero(), u);
+      up += sl;
+#pragma unroll
+      for (int e = 0; e < VC; ++e) wprev[e] = (i == 0) ? u[e] : fmaf(acur[i], wprev[e], u[e]);
+      gs *= acur[i];  // g[i]
+      if (act && i < lim) V::st(dup, du);
+      dup += sl;
+    }
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {  // mu for block t-1: a_t[0] lambda_t[0]
+      const float4 l4 = lam_at(0, q);
+      mu[4 * q] = acur[0] * l4.x; mu[4 * q + 1] = acur[0] * l4.y;
+      mu[4 * q + 2] = acur[0] * l4.z; mu[4 * q + 3] = acur[0] * l4.w;
+    }
+    if (t == 0 && act && p.mu_out) {
+#pragma unroll
+      for (int e = 0; e < VC; ++e) p.mu_out[co + e] = mu[e];
+    }
+    // da: deterministic reduction over the head's channels
+    int tok = 0;
+    if constexpr (GS > 1) GroupReduce<GS / 2, kEll>::run(part, lane, tok);
+    constexpr int NV = GS >= kEll ? 1 : kEll / GS;
+    const bool owner = (GS < 32) || ((lane & 1) == 0);
+    if (act && owner) {
+#pragma unroll
+      for (int j = 0; j < NV; ++j)
+        if (tok + j < lim) io::st1(dA + (n0 + tok + j) * sal, part[j]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -702,10 +928,43 @@ static cudaError_t launch_tph(Params p, cudaStream_t st, int sms) {
   return cudaGetLastError();
 }
 
+template <typename T, int VC, int TPH>
+static cudaError_t launch_bwd_vec(Params p, cudaStream_t st, int sms) {
+  constexpr int HPC = 128 / TPH;
+  constexpr int kSmem = kEll * VC * 128 * 4;
+  static bool attr = false;  // benign race: every caller sets the same value
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(bwd_ffma_vec<T, VC, TPH>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int64_t cols = p.B * ceil_div(p.H, HPC);
+  const int64_t want_chunks = std::max<int64_t>(1, ((int64_t)sms * 8) / std::max<int64_t>(cols, 1));
+  int64_t K = std::max<int64_t>(ceil_div(p.nb, want_chunks), 8);
+  K = std::min<int64_t>(K, p.nb);
+  p.K = K;
+  dim3 grid((unsigned)ceil_div(p.nb, K), (unsigned)ceil_div(p.H, HPC), (unsigned)p.B);
+  bwd_ffma_vec<T, VC, TPH><<<grid, 128, kSmem, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <typename T>
+static cudaError_t launch_swr_bwd_vec(const Params& p, cudaStream_t st, int sms) {
+  constexpr int VC = sizeof(T) == 2 ? SWR_FFMA_BWD_VC : 4;
+  switch (p.D) {
+    case 16: return launch_bwd_vec<T, VC, 16 / VC>(p, st, sms);
+    case 32: return launch_bwd_vec<T, VC, 32 / VC>(p, st, sms);
+    case 64: return launch_bwd_vec<T, VC, 64 / VC>(p, st, sms);
+    default: return launch_bwd_vec<T, VC, 128 / VC>(p, st, sms);
+  }
+}
+
 template <typename T, bool MIX, bool BWD>
 static cudaError_t launch_d(const Params& p, cudaStream_t st, int sms) {
   if constexpr (!BWD) {
     if (!SWR_FFMA_FWD_V1) return launch_fwd_stream<T, MIX>(p, st, sms);
+  } else if constexpr (!MIX) {
+    if (!SWR_FFMA_BWD_V1) return launch_swr_bwd_vec<T>(p, st, sms);
   }
   switch (p.D) {
     case 16: return launch_tph<T, 8, MIX, BWD>(p, st, sms);

@@ -681,10 +681,19 @@ __global__ void __launch_bounds__(128) fwd_stream(const Params p) {
 #ifndef SWR_FFMA_BWD_V1
 #define SWR_FFMA_BWD_V1 0  // 1: the two-channel bwd_ffma for SWR
 #endif
+#ifndef SWR_FFMA_MIXB_V1
+#define SWR_FFMA_MIXB_V1 0  // 1: the two-block walk bwd_ffma_mix for the mixer
+#endif
 #ifndef SWR_FFMA_BWDV_UNROLL
 #define SWR_FFMA_BWDV_UNROLL 4  // pass C unroll (16 spills 1.3 KB: 3x slower; 2 or 8: 5-15% slower)
 #endif
-constexpr int kCUnrollV = SWR_FFMA_BWDV_UNROLL;
+#ifndef SWR_FFMA_MIXBV_UNROLL
+#define SWR_FFMA_MIXBV_UNROLL 2  // the mixer's pass C unroll (4: 12% slower at d=16, spills)
+#endif
+template <bool MIX>
+struct CUnrollV {
+  static constexpr int v = MIX ? SWR_FFMA_MIXBV_UNROLL : SWR_FFMA_BWDV_UNROLL;
+};
 
 template <typename T, int VC>
 struct VecN {
@@ -722,7 +731,7 @@ struct VecN {
   }
 };
 
-template <typename T, int VC, int TPH>
+template <typename T, int VC, int TPH, bool MIX>
 __global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma_vec(const Params p) {
   using V = VecN<T, VC>;
   using io = IO<T>;
@@ -745,9 +754,6 @@ __global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma_vec(const Par
   const int64_t co = (b * p.H + hc) * p.D + c;
   const T* A0 = (const T*)p.a + b * p.sa_b + hc * p.sa_h;
   T* dA = (T*)p.da + b * p.sa_b + hc * p.sa_h;
-  const T* U0 = (const T*)p.u + xo;
-  const T* G0 = (const T*)p.dx + xo;
-  T* DU0 = (T*)p.du + xo;
   auto lam_at = [&](int i, int q) -> float4& { return slam[(i * NQ + q) * 128 + tid]; };
 
   // decays of a block (pad a = 1 past L)
@@ -757,6 +763,30 @@ __global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma_vec(const Par
     for (int i = 0; i < kEll; ++i) {
       a[i] = (i < lim) ? io::ld1(ap) : 1.f;
       ap += sal;
+    }
+  };
+  // Pass-I input at element offset o: u (SWR) or u^ = k (.) v (pre-gate)
+  auto load_u = [&](int64_t o, bool valid, float (&u)[VC]) {
+    if constexpr (!MIX) {
+      V::to_f(valid ? V::ld((const T*)p.u + o) : V::zero(), u);
+    } else {
+      float kk[VC], vv[VC];
+      V::to_f(valid ? V::ld((const T*)p.k + o) : V::zero(), kk);
+      V::to_f(valid ? V::ld((const T*)p.v + o) : V::zero(), vv);
+#pragma unroll
+      for (int e = 0; e < VC; ++e) u[e] = __fmul_rn(kk[e], vv[e]);
+    }
+  };
+  // adjoint input at offset o: dx (SWR) or G = dy (.) q (mixer)
+  auto load_g = [&](int64_t o, bool valid, float (&g)[VC]) {
+    if constexpr (!MIX) {
+      V::to_f(valid ? V::ld((const T*)p.dx + o) : V::zero(), g);
+    } else {
+      float dd[VC], qq[VC];
+      V::to_f(valid ? V::ld((const T*)p.dy + o) : V::zero(), dd);
+      V::to_f(valid ? V::ld((const T*)p.q + o) : V::zero(), qq);
+#pragma unroll
+      for (int e = 0; e < VC; ++e) g[e] = __fmul_rn(dd[e], qq[e]);
     }
   };
 
@@ -775,13 +805,13 @@ __global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma_vec(const Par
     float a[kEll];
     load_a(n0, lim, a);
     float l[VC];
-    const T* gp = G0 + (n0 + kEll - 1) * sl;
-    V::to_f(kEll - 1 < lim ? V::ld(gp) : V::zero(), l);  // l[15] = G[15]
+    int64_t o = xo + (n0 + kEll - 1) * sl;
+    load_g(o, kEll - 1 < lim, l);  // l[15] = G[15]
 #pragma unroll
     for (int i = kEll - 2; i >= 0; --i) {
       float g[VC];
-      gp -= sl;
-      V::to_f(i < lim ? V::ld(gp) : V::zero(), g);
+      o -= sl;
+      load_g(o, i < lim, g);
 #pragma unroll
       for (int e = 0; e < VC; ++e) l[e] = fmaf(a[i + 1], l[e], g[e]);
     }
@@ -796,14 +826,14 @@ __global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma_vec(const Par
     float vprev[VC];
     if (t > 0) {
       const T* ap = A0 + (n0 - kEll) * sal;
-      const T* up = U0 + (n0 - kEll) * sl;
+      int64_t o = xo + (n0 - kEll) * sl;
 #pragma unroll
       for (int i = 0; i < kEll; ++i) {
         const float a = io::ld1(ap);
         float u[VC];
-        V::to_f(V::ld(up), u);
+        load_u(o, true, u);
         ap += sal;
-        up += sl;
+        o += sl;
 #pragma unroll
         for (int e = 0; e < VC; ++e) vprev[e] = (i == 0) ? u[e] : fmaf(a, vprev[e], u[e]);
       }
@@ -817,8 +847,8 @@ __global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma_vec(const Par
     {
       float lam[VC];
       float rr = 1.f;
-      const T* gp = G0 + (n0 + kEll - 1) * sl;
-      V::to_f(kEll - 1 < lim ? V::ld(gp) : V::zero(), lam);  // lambda[15] = G[15]
+      int64_t o = xo + (n0 + kEll - 1) * sl;
+      load_g(o, kEll - 1 < lim, lam);  // lambda[15] = G[15]
       r[kEll - 1] = 1.f;
 #pragma unroll
       for (int q = 0; q < NQ; ++q)
@@ -826,8 +856,8 @@ __global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma_vec(const Par
 #pragma unroll
       for (int i = kEll - 2; i >= 0; --i) {
         float g[VC];
-        gp -= sl;
-        V::to_f(i < lim ? V::ld(gp) : V::zero(), g);
+        o -= sl;
+        load_g(o, i < lim, g);
 #pragma unroll
         for (int e = 0; e < VC; ++e) lam[e] = fmaf(acur[i + 1], lam[e], g[e]);
         rr *= acur[i + 1];
@@ -836,13 +866,12 @@ __global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma_vec(const Par
         for (int q = 0; q < NQ; ++q) lam_at(i, q) = make_float4(lam[4 * q], lam[4 * q + 1], lam[4 * q + 2], lam[4 * q + 3]);
       }
     }
-    // C) Pass I of block t forward, du and da partials
+    // C) Pass I of block t forward, du (mixer: dq, dk, dv) and da partials
     float part[kEll];
     float wprev[VC];
     float gs = 1.f;  // g[i-1]
-    const T* up = U0 + n0 * sl;
-    T* dup = DU0 + n0 * sl;
-#pragma unroll kCUnrollV
+    int64_t o = xo + n0 * sl;
+#pragma unroll CUnrollV<MIX>::v
     for (int i = 0; i < kEll; ++i) {
       float lam[VC];
 #pragma unroll
@@ -859,14 +888,37 @@ __global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma_vec(const Par
         lv = (e == 0) ? lam[e] * vprev[e] : fmaf(lam[e], vprev[e], lv);
       }
       part[i] = fmaf(gs, lv, sdot);
-      float u[VC];
-      V::to_f(i < lim ? V::ld(up) : V::zero(), u);
-      up += sl;
+      const bool valid = i < lim;
+      float kk[VC], vv[VC], u[VC];
+      if constexpr (!MIX) {
+        V::to_f(valid ? V::ld((const T*)p.u + o) : V::zero(), u);
+      } else {
+        V::to_f(valid ? V::ld((const T*)p.k + o) : V::zero(), kk);
+        V::to_f(valid ? V::ld((const T*)p.v + o) : V::zero(), vv);
+#pragma unroll
+        for (int e = 0; e < VC; ++e) u[e] = __fmul_rn(kk[e], vv[e]);
+      }
 #pragma unroll
       for (int e = 0; e < VC; ++e) wprev[e] = (i == 0) ? u[e] : fmaf(acur[i], wprev[e], u[e]);
       gs *= acur[i];  // g[i]
-      if (act && i < lim) V::st(dup, du);
-      dup += sl;
+      if (act && valid) {
+        if constexpr (!MIX) {
+          V::st((T*)p.du + o, du);
+        } else {
+          float dd[VC], out[VC];
+          V::to_f(V::ld((const T*)p.dy + o), dd);
+#pragma unroll
+          for (int e = 0; e < VC; ++e) out[e] = dd[e] * fmaf(gs, vprev[e], wprev[e]);  // dq = dy x~
+          V::st((T*)p.dq + o, out);
+#pragma unroll
+          for (int e = 0; e < VC; ++e) out[e] = du[e] * vv[e];  // dk = du^ v
+          V::st((T*)p.dk + o, out);
+#pragma unroll
+          for (int e = 0; e < VC; ++e) out[e] = fmaf(du[e], kk[e], dd[e]);  // dv = du^ k + dy
+          V::st((T*)p.dv + o, out);
+        }
+      }
+      o += sl;
     }
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {  // mu for block t-1: a_t[0] lambda_t[0]
@@ -928,13 +980,13 @@ static cudaError_t launch_tph(Params p, cudaStream_t st, int sms) {
   return cudaGetLastError();
 }
 
-template <typename T, int VC, int TPH>
+template <typename T, int VC, int TPH, bool MIX>
 static cudaError_t launch_bwd_vec(Params p, cudaStream_t st, int sms) {
   constexpr int HPC = 128 / TPH;
   constexpr int kSmem = kEll * VC * 128 * 4;
   static bool attr = false;  // benign race: every caller sets the same value
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(bwd_ffma_vec<T, VC, TPH>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaError_t e = cudaFuncSetAttribute(bwd_ffma_vec<T, VC, TPH, MIX>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -944,18 +996,18 @@ static cudaError_t launch_bwd_vec(Params p, cudaStream_t st, int sms) {
   K = std::min<int64_t>(K, p.nb);
   p.K = K;
   dim3 grid((unsigned)ceil_div(p.nb, K), (unsigned)ceil_div(p.H, HPC), (unsigned)p.B);
-  bwd_ffma_vec<T, VC, TPH><<<grid, 128, kSmem, st>>>(p);
+  bwd_ffma_vec<T, VC, TPH, MIX><<<grid, 128, kSmem, st>>>(p);
   return cudaGetLastError();
 }
 
-template <typename T>
-static cudaError_t launch_swr_bwd_vec(const Params& p, cudaStream_t st, int sms) {
+template <typename T, bool MIX>
+static cudaError_t launch_bwd_vec_d(const Params& p, cudaStream_t st, int sms) {
   constexpr int VC = sizeof(T) == 2 ? SWR_FFMA_BWD_VC : 4;
   switch (p.D) {
-    case 16: return launch_bwd_vec<T, VC, 16 / VC>(p, st, sms);
-    case 32: return launch_bwd_vec<T, VC, 32 / VC>(p, st, sms);
-    case 64: return launch_bwd_vec<T, VC, 64 / VC>(p, st, sms);
-    default: return launch_bwd_vec<T, VC, 128 / VC>(p, st, sms);
+    case 16: return launch_bwd_vec<T, VC, 16 / VC, MIX>(p, st, sms);
+    case 32: return launch_bwd_vec<T, VC, 32 / VC, MIX>(p, st, sms);
+    case 64: return launch_bwd_vec<T, VC, 64 / VC, MIX>(p, st, sms);
+    default: return launch_bwd_vec<T, VC, 128 / VC, MIX>(p, st, sms);
   }
 }
 
@@ -964,7 +1016,9 @@ static cudaError_t launch_d(const Params& p, cudaStream_t st, int sms) {
   if constexpr (!BWD) {
     if (!SWR_FFMA_FWD_V1) return launch_fwd_stream<T, MIX>(p, st, sms);
   } else if constexpr (!MIX) {
-    if (!SWR_FFMA_BWD_V1) return launch_swr_bwd_vec<T>(p, st, sms);
+    if (!SWR_FFMA_BWD_V1) return launch_bwd_vec_d<T, false>(p, st, sms);
+  } else {
+    if (!SWR_FFMA_MIXB_V1) return launch_bwd_vec_d<T, true>(p, st, sms);
   }
   switch (p.D) {
     case 16: return launch_tph<T, 8, MIX, BWD>(p, st, sms);

@@ -1,4 +1,4 @@
-"""FFMA-path kernel times at the paper's head shape (d=16, h=128) and fp32 layer shape."""
+"""FFMA-path kernel times at the paper's head shape (d=16, h=128) and fp32 layer shape (MIX=1: the mixer)."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, paper_2512_13921_b200 as P
@@ -19,6 +19,13 @@ for (B, L, H, D, dt) in [(8, 8192, 128, 16, torch.bfloat16), (8, 4096, 16, 128, 
     g = {k: v.cuda() for k, v in swr_inputs(B, L, H, D, dtype=dt, seed=1).items()}
     e = 2 if dt == torch.bfloat16 else 4
     n = B * L * H
-    tf = t(lambda: P.swr_fwd(g["u"], g["a"])); tb = t(lambda: P.swr_bwd(g["u"], g["a"], g["G"]))
-    out.append(f"d{D}{'bf16' if e == 2 else 'f32'} fwd {tf:.0f}us {n*(2*D+1)*e/tf/1e3:.0f}GB/s bwd {tb:.0f}us {n*(3*D+2)*e/tb/1e3:.0f}GB/s")
+    if os.environ.get("MIX"):
+        g = {k: v.cuda() for k, v in mix_inputs(B, L, H, D, dtype=dt, seed=1).items()}
+        tf = t(lambda: P.phalanx_mix(g["q"], g["k"], g["v"], g["a"]))
+        tb = t(lambda: P.phalanx_mix_bwd(g["q"], g["k"], g["v"], g["a"], g["dy"]))
+        bf, bb = (4 * D + 1) * e, (7 * D + 2) * e
+    else:
+        tf = t(lambda: P.swr_fwd(g["u"], g["a"])); tb = t(lambda: P.swr_bwd(g["u"], g["a"], g["G"]))
+        bf, bb = (2 * D + 1) * e, (3 * D + 2) * e
+    out.append(f"d{D}{'bf16' if e == 2 else 'f32'} fwd {tf:.0f}us {n*bf/tf/1e3:.0f}GB/s bwd {tb:.0f}us {n*bb/tb/1e3:.0f}GB/s")
 print(os.path.basename(os.environ.get("SWR_LIB", "default")), " | ".join(out), flush=True)

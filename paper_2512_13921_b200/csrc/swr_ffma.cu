@@ -765,29 +765,34 @@ __global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma_vec(const Par
       ap += sal;
     }
   };
-  // Pass-I input at element offset o: u (SWR) or u^ = k (.) v (pre-gate)
-  auto load_u = [&](int64_t o, bool valid, float (&u)[VC]) {
-    if constexpr (!MIX) {
-      V::to_f(valid ? V::ld((const T*)p.u + o) : V::zero(), u);
-    } else {
-      float kk[VC], vv[VC];
-      V::to_f(valid ? V::ld((const T*)p.k + o) : V::zero(), kk);
-      V::to_f(valid ? V::ld((const T*)p.v + o) : V::zero(), vv);
+  // A stream of Pass-I inputs (u, or u^ = k (.) v: pre-gate) or of adjoint
+  // inputs (dx, or G = dy (.) q), walked by pointers stepped by the token stride.
+  struct Src {
+    const T* p0;
+    const T* p1;  // mixer: the second factor
+    __device__ __forceinline__ void load(bool valid, float (&x)[VC]) const {
+      if constexpr (!MIX) {
+        V::to_f(valid ? V::ld(p0) : V::zero(), x);
+      } else {
+        float f0[VC], f1[VC];
+        V::to_f(valid ? V::ld(p0) : V::zero(), f0);
+        V::to_f(valid ? V::ld(p1) : V::zero(), f1);
 #pragma unroll
-      for (int e = 0; e < VC; ++e) u[e] = __fmul_rn(kk[e], vv[e]);
+        for (int e = 0; e < VC; ++e) x[e] = __fmul_rn(f0[e], f1[e]);
+      }
+    }
+    __device__ __forceinline__ void step(int64_t d) {
+      p0 += d;
+      if constexpr (MIX) p1 += d;
     }
   };
-  // adjoint input at offset o: dx (SWR) or G = dy (.) q (mixer)
-  auto load_g = [&](int64_t o, bool valid, float (&g)[VC]) {
-    if constexpr (!MIX) {
-      V::to_f(valid ? V::ld((const T*)p.dx + o) : V::zero(), g);
-    } else {
-      float dd[VC], qq[VC];
-      V::to_f(valid ? V::ld((const T*)p.dy + o) : V::zero(), dd);
-      V::to_f(valid ? V::ld((const T*)p.q + o) : V::zero(), qq);
-#pragma unroll
-      for (int e = 0; e < VC; ++e) g[e] = __fmul_rn(dd[e], qq[e]);
-    }
+  auto src_u = [&](int64_t n) {
+    const int64_t o = xo + n * sl;
+    return MIX ? Src{(const T*)p.k + o, (const T*)p.v + o} : Src{(const T*)p.u + o, nullptr};
+  };
+  auto src_g = [&](int64_t n) {
+    const int64_t o = xo + n * sl;
+    return MIX ? Src{(const T*)p.dy + o, (const T*)p.q + o} : Src{(const T*)p.dx + o, nullptr};
   };
 
   // mu for block t_hi - 1: a_{t_hi}[0] lambda_{t_hi}[0] from the right halo block, or mu_in
@@ -805,13 +810,13 @@ __global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma_vec(const Par
     float a[kEll];
     load_a(n0, lim, a);
     float l[VC];
-    int64_t o = xo + (n0 + kEll - 1) * sl;
-    load_g(o, kEll - 1 < lim, l);  // l[15] = G[15]
+    Src gsrc = src_g(n0 + kEll - 1);
+    gsrc.load(kEll - 1 < lim, l);  // l[15] = G[15]
 #pragma unroll
     for (int i = kEll - 2; i >= 0; --i) {
       float g[VC];
-      o -= sl;
-      load_g(o, i < lim, g);
+      gsrc.step(-sl);
+      gsrc.load(i < lim, g);
 #pragma unroll
       for (int e = 0; e < VC; ++e) l[e] = fmaf(a[i + 1], l[e], g[e]);
     }
@@ -826,14 +831,14 @@ __global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma_vec(const Par
     float vprev[VC];
     if (t > 0) {
       const T* ap = A0 + (n0 - kEll) * sal;
-      int64_t o = xo + (n0 - kEll) * sl;
+      Src usrc = src_u(n0 - kEll);
 #pragma unroll
       for (int i = 0; i < kEll; ++i) {
         const float a = io::ld1(ap);
         float u[VC];
-        load_u(o, true, u);
+        usrc.load(true, u);
         ap += sal;
-        o += sl;
+        usrc.step(sl);
 #pragma unroll
         for (int e = 0; e < VC; ++e) vprev[e] = (i == 0) ? u[e] : fmaf(a, vprev[e], u[e]);
       }
@@ -847,8 +852,8 @@ __global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma_vec(const Par
     {
       float lam[VC];
       float rr = 1.f;
-      int64_t o = xo + (n0 + kEll - 1) * sl;
-      load_g(o, kEll - 1 < lim, lam);  // lambda[15] = G[15]
+      Src gsrc = src_g(n0 + kEll - 1);
+      gsrc.load(kEll - 1 < lim, lam);  // lambda[15] = G[15]
       r[kEll - 1] = 1.f;
 #pragma unroll
       for (int q = 0; q < NQ; ++q)
@@ -856,8 +861,8 @@ __global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma_vec(const Par
 #pragma unroll
       for (int i = kEll - 2; i >= 0; --i) {
         float g[VC];
-        o -= sl;
-        load_g(o, i < lim, g);
+        gsrc.step(-sl);
+        gsrc.load(i < lim, g);
 #pragma unroll
         for (int e = 0; e < VC; ++e) lam[e] = fmaf(acur[i + 1], lam[e], g[e]);
         rr *= acur[i + 1];

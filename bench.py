@@ -2,7 +2,7 @@
 """Benchmark of the SWR / Block Two-Pass hot path on B200 (one JSON line on rank 0).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config layer4k|L8k|L16k|L32k|L4k_b16|paper_d16|tiny] [--op swr|mix]
+                    [--config layer4k|L8k|L16k|L32k|L4k_b16|paper_d16|layer4k_f32|tiny] [--op swr|mix]
                     [--path auto|ffma|tc]
 
 A step is one pass of the whole hot path over one batch of synthetic input:
@@ -42,6 +42,7 @@ CONFIGS = {
     "L4k_b16": (16, 4096, 16, 128, "bf16"),
     "bxh": (8, 8192, 16, 128, "bf16"),        # BJ configs[3] per-GPU shard at 8 GPUs
     "paper_d16": (8, 8192, 128, 16, "bf16"),  # the paper's head shape d=16, h=128
+    "layer4k_f32": (8, 4096, 16, 128, "f32"),  # BJ configs[1] shape with fp32 storage (FFMA path)
     "tiny": (1, 64, 1, 16, "f32"),            # BJ configs[0]
     "sp131k": (1, 131072, 16, 128, "bf16"),   # BJ configs[4]: sequence-parallel across ranks
 }

@@ -1,10 +1,13 @@
 // swr_ffma.cu -- the portable kernel family (SWR_PATH_FFMA): Block Two-Pass on
 // CUDA cores, any storage dtype, D in {16, 32, 64, 128}.
 //
-// Mapping.  A thread owns two adjacent channels of one (b, h) and walks a run
-// of K consecutive 16-token blocks ("chunk").  For every block it
-//   * loads the 16 decays and 16 token pairs of its channels (coalesced across
-//     the lanes of the head: consecutive lanes own consecutive channel pairs),
+// Mapping.  A thread owns one vector of adjacent channels of one (b, h) -- 16
+// bytes in the forward (fwd_stream), four channels in the backward
+// (bwd_ffma_vec); two in the older fwd_ffma / bwd_ffma / bwd_ffma_mix kept behind
+// SWR_FFMA_*_V1 -- and walks a run of K consecutive 16-token blocks ("chunk").
+// For every block it
+//   * loads the 16 decays and 16 token vectors of its channels (coalesced across
+//     the lanes of the head: consecutive lanes own consecutive channel vectors),
 //   * Pass I  (Alg. 4, Alg. 5): w_t = L_t u_t as the block-local
 //     recurrence w[i] = a[i] w[i-1] + u[i], w[0] = u[0] (L_t excludes a_t[0],
 //     P:594) -- the same product as the dense 16x16 transfer, 16x fewer FLOPs,

@@ -992,11 +992,9 @@ template <typename T, int VC, int TPH, bool MIX>
 static cudaError_t launch_bwd_vec(Params p, cudaStream_t st, int sms) {
   constexpr int HPC = 128 / TPH;
   constexpr int kSmem = kEll * VC * 128 * 4;
-  static bool attr = false;  // benign race: every caller sets the same value
-  if (!attr) {
+  if constexpr (kSmem > 48 * 1024) {  // only the 8-channel bf16 variant; set per call (per device)
     cudaError_t e = cudaFuncSetAttribute(bwd_ffma_vec<T, VC, TPH, MIX>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   const int64_t cols = p.B * ceil_div(p.H, HPC);
   const int64_t want_chunks = std::max<int64_t>(1, ((int64_t)sms * 8) / std::max<int64_t>(cols, 1));

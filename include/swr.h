@@ -61,6 +61,11 @@
  *             default stream) and returns without synchronising.  Launch
  *             errors are returned as SWR_ERR_CUDA; faults inside a kernel
  *             surface at the caller's next synchronisation.
+ * Graphs    : every call may be captured into a CUDA graph (any capture mode).
+ *             A captured tensor-core launch neither reads nor refreshes the
+ *             per-SM rate table and splits the work uniformly by CTA index, so
+ *             replays are safe; outputs are bit-identical to eager calls
+ *             (tests/test_graph.py).
  * Validation: done before any launch; on error nothing is launched.
  *   SWR_ERR_NULL   a required pointer is NULL
  *   SWR_ERR_SHAPE  B, L or H < 0, or D not in {16, 32, 64, 128}

@@ -1309,8 +1309,12 @@ struct Balance {
     } while (q.epoch == 0);
     sp.weighted = 0;
     if (grid != sms || sms > kMaxSM) return false;
+    // Under CUDA-graph capture the launch is replayed with these parameters: the
+    // epoch would repeat and find every claim slot taken, and no readback can be
+    // scheduled.  Captured launches take the uniform split by CTA index instead
+    // (bitwise the same results, test_props.py).
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(st, &cap) != cudaSuccess) cap = cudaStreamCaptureStatusActive;
+    if (cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) return false;
     std::lock_guard<std::mutex> lock(mu);
     if ((int)rate.size() != sms) rate.assign(sms, 0.f);
     if (pending && cudaEventQuery(ev) == cudaSuccess) {
@@ -1340,7 +1344,7 @@ struct Balance {
       for (int s = 0; s <= sms; ++s) sp.bnd[s] = (int)((int64_t)s * total / sms);
     }
     ++launches;
-    return cap == cudaStreamCaptureStatusNone && !pending;
+    return !pending;
   }
   void request(int op, int sms, cudaStream_t st) {
     std::lock_guard<std::mutex> lock(mu);
@@ -1421,19 +1425,19 @@ static cudaError_t launch_op(const Params& p, cudaStream_t st, int sms) {
   if (!map_decay(&maps.a, p.a, p, Cfg<OP>::BPI)) return cudaErrorNotSupported;
 
   constexpr int smem = smem_bytes<OP>();
-  static bool attr_set = false;
-  if (!attr_set) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) dev = -1;
+  static std::atomic<bool> attr_set[kMaxDev];  // the attribute is per device (per context)
+  if (dev < 0 || !attr_set[dev].load(std::memory_order_acquire)) {
     cudaError_t e = cudaFuncSetAttribute(swr_tc_kernel<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    if (dev >= 0) attr_set[dev].store(true, std::memory_order_release);
   }
   const int64_t total = p.B * p.H * ((p.nb + Cfg<OP>::BPI - 1) / Cfg<OP>::BPI);
   const int grid = (int)std::min<int64_t>(sms, std::max<int64_t>(total, 1));
   constexpr int threads = (4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MIX ? 4 : 5)) * 32;
   Params q = p;
   Split sp;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) dev = -1;
   Balance* bal = dev >= 0 ? &g_balance[dev][OP] : nullptr;
   bool readback = false;
   if (bal != nullptr) {

@@ -59,6 +59,8 @@ def _dtype(*ts):
             raise TypeError("all operands must share one dtype")
         if not t.is_cuda:
             raise ValueError("libswr operates on CUDA tensors only (no CPU fallback)")
+        if t.device != ts[0].device:
+            raise ValueError(f"all operands must be on one device ({ts[0].device} vs {t.device})")
     return _DT[dt]
 
 

@@ -155,6 +155,32 @@ SWR_API swr_status phalanx_mix_bwd(const void* q, const void* k, const void* v, 
                            const float* carry_in, const float* mu_in, float* mu_out,
                            swr_shape s, swr_dtype dt, void* stream);
 
+/* Recurrence-mode decoding (the paper decodes Phalanx "in
+ * recurrence mode"): one new token per (b, h).  The state is
+ *   w_state [B,H,D] fp32  local state of the current block, w_t[i]
+ *   v_state [B,H,D] fp32  carrier of the previous block, v_{t-1} = w_{t-1}[15]
+ *   g_state [B,H]   fp32  decay product since the block start, g_t[i]
+ * all contiguous and updated in place.  For the token at sequence position pos
+ * (i = pos mod 16, the same for every (b, h)):
+ *   i == 0:  v <- w,  g <- a,      w <- u        (L_t excludes a_t[0])
+ *   else  :  g <- g a, w <- a w + u
+ *   x = w + g v                                   (Pass II)
+ * -- B2P's forward evaluated one token at a time: decoding a sequence from pos 0
+ * gives bitwise the outputs of swr_fwd on the CUDA-core path.  Before pos 0 set
+ * w_state to carry_in (or 0); v_state and g_state need no initialisation.
+ * u, x [B,H,D] with element strides (s.sx_b, s.sx_h), D contiguous, 16-byte
+ * aligned; a [B,H] with strides (s.sa_b, s.sa_h).  s.L must be 1 (s.sx_l and
+ * s.sa_l are ignored); pos >= 0 (else SWR_ERR_SHAPE).  Other errors as above. */
+SWR_API swr_status swr_decode_step(const void* u, const void* a, void* x, float* w_state,
+                           float* v_state, float* g_state, int64_t pos, swr_shape s,
+                           swr_dtype dt, void* stream);
+
+/* Phalanx mixer decode step: u^ = k (.) v into the step above, y = q (.) x~ + v. */
+SWR_API swr_status phalanx_mix_decode_step(const void* q, const void* k, const void* v,
+                           const void* a, void* y, float* w_state, float* v_state,
+                           float* g_state, int64_t pos, swr_shape s, swr_dtype dt,
+                           void* stream);
+
 /* Human-readable name of a status code (static storage). */
 SWR_API const char* swr_strerror(swr_status st);
 

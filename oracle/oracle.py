@@ -123,3 +123,37 @@ def mix_bwd(q, k, v, a, dy, carry_in=None, mu_in=None, threads: int = 0):
     dk = du_hat * v
     dv = du_hat * k + dy
     return dq, dk, dv, da, mu_out
+
+
+def swr_decode(u, a, carry_in=None):
+    """Recurrence-mode decoding ("decoded in recurrence mode"; SURVEY 8(f)
+    NEXT-3), one token at a time in fp64.  Per (b, h) the state is the local state w
+    of the current block (Pass I restarted at each block start, L_t excludes
+    a_t[0]), the carrier v = w_{t-1}[15] of the previous block and
+    g = a_t[0] ... a_t[i]; each token's output is Pass II, x = w + g v
+    (P:1478), with v_{-1} = carry_in or 0.  Returns x for all tokens.
+    Pinned against swr_fwd (the jagged-window definition) in tests/test_oracle.py."""
+    u, a = _f64(u), _f64(a)
+    _check(u, a)
+    B, L, H, D = u.shape
+    w = np.zeros((B, H, D)) if carry_in is None else _f64(carry_in).copy()
+    v = np.zeros((B, H, D))
+    g = np.ones((B, H))
+    x = np.empty_like(u)
+    for n in range(L):
+        an = a[:, n, :]
+        if n % ELL == 0:        # block start: the finished block's end state is the carrier
+            v = w
+            g = an.copy()
+            w = u[:, n].copy()
+        else:
+            g = g * an
+            w = an[..., None] * w + u[:, n]
+        x[:, n] = w + g[..., None] * v
+    return x
+
+
+def mix_decode(q, k, v, a, carry_in=None):
+    """Phalanx mixer decoded token by token: u^ = k v, y = q x~ + v."""
+    q, k, v = _f64(q), _f64(k), _f64(v)
+    return q * swr_decode(k * v, a, carry_in) + v

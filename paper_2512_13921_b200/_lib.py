@@ -18,7 +18,7 @@ SWR_PATH_AUTO, SWR_PATH_FFMA, SWR_PATH_TC = 0, 1, 2
 
 EXPORTS = ("swr_fwd", "swr_bwd", "phalanx_mix", "phalanx_mix_bwd", "swr_strerror",
            "swr_last_cuda_error", "swr_set_path", "swr_launch_count", "swr_last_path",
-           "swr_set_trace")
+           "swr_set_trace", "swr_decode_step", "phalanx_mix_decode_step")
 
 
 class SwrError(RuntimeError):
@@ -48,7 +48,10 @@ def _load():
     lib.swr_bwd.argtypes = [P, P, P, P, P, P, P, P, S, I, P]
     lib.phalanx_mix.argtypes = [P, P, P, P, P, P, P, S, I, P]
     lib.phalanx_mix_bwd.argtypes = [P, P, P, P, P, P, P, P, P, P, P, P, S, I, P]
-    for f in ("swr_fwd", "swr_bwd", "phalanx_mix", "phalanx_mix_bwd"):
+    lib.swr_decode_step.argtypes = [P, P, P, P, P, P, ctypes.c_int64, S, I, P]
+    lib.phalanx_mix_decode_step.argtypes = [P, P, P, P, P, P, P, P, ctypes.c_int64, S, I, P]
+    for f in ("swr_fwd", "swr_bwd", "phalanx_mix", "phalanx_mix_bwd", "swr_decode_step",
+              "phalanx_mix_decode_step"):
         getattr(lib, f).restype = I
     lib.swr_strerror.argtypes = [I]
     lib.swr_strerror.restype = ctypes.c_char_p
@@ -110,3 +113,13 @@ def set_trace(ptr, n: int) -> None:
 def raw_status(fn: str, *args) -> int:
     """Call an entry point and return its status code without raising (tests)."""
     return getattr(_lib, fn)(*args)
+
+
+def swr_decode_step(u, a, x, w_state, v_state, g_state, pos, shape, dtype, stream):
+    _check(_lib.swr_decode_step(u, a, x, w_state, v_state, g_state, pos, shape, dtype, stream),
+           "swr_decode_step")
+
+
+def phalanx_mix_decode_step(q, k, v, a, y, w_state, v_state, g_state, pos, shape, dtype, stream):
+    _check(_lib.phalanx_mix_decode_step(q, k, v, a, y, w_state, v_state, g_state, pos, shape, dtype,
+                                        stream), "phalanx_mix_decode_step")

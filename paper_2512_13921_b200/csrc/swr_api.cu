@@ -14,6 +14,7 @@ cudaError_t launch_ffma(int op, bool bf16, const Params& p, cudaStream_t st, int
 // is outside its envelope so the caller can fall back to FFMA.
 cudaError_t launch_tc(int op, const Params& p, cudaStream_t st, int sms, int* launches);
 bool tc_supported(int op, bool bf16, const Params& p);
+cudaError_t launch_decode(bool mix, bool bf16, const DecParams& p, cudaStream_t st);
 }  // namespace swr
 
 namespace {
@@ -229,6 +230,65 @@ swr_status phalanx_mix_bwd(const void* q, const void* k, const void* v, const vo
   p.mu_in = mu_in;
   p.mu_out = mu_out;
   return dispatch(3, dt, p, cs);
+}
+
+}  // extern "C"
+
+namespace {
+swr_status decode_call(bool mix, const void* u, const void* vv, const void* q, const void* a, void* x,
+                       float* w_state, float* v_state, float* g_state, int64_t pos, swr_shape s,
+                       swr_dtype dt, void* stream) {
+  if (s.L != 1 || pos < 0) return SWR_ERR_SHAPE;
+  s.sx_l = 0;  // one token: the sequence strides are not used
+  s.sa_l = 0;
+  const void* dt_[] = {u, x, vv, q};
+  const void* at_[] = {a};
+  const void* ct_[] = {w_state, v_state};
+  swr_status st = validate(s, dt, dt_, mix ? 4 : 2, at_, 1, ct_, 2);
+  if (st != SWR_OK) return st;
+  if (s.B == 0 || s.H == 0) return SWR_OK;
+  if (!w_state || !v_state || !g_state) return SWR_ERR_NULL;
+  if (reinterpret_cast<uintptr_t>(g_state) % 4) return SWR_ERR_ALIGN;
+  int sms = 0;
+  st = device_info(&sms);
+  if (st != SWR_OK) return st;
+  swr::DecParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.u = u;
+  p.v = vv;
+  p.q = q;
+  p.a = a;
+  p.x = x;
+  p.w = w_state;
+  p.vc = v_state;
+  p.g = g_state;
+  p.B = s.B;
+  p.H = s.H;
+  p.D = s.D;
+  p.sx_b = s.sx_b;
+  p.sx_h = s.sx_h;
+  p.sa_b = s.sa_b;
+  p.sa_h = s.sa_h;
+  p.pos = pos;
+  cudaError_t e = swr::launch_decode(mix, dt == SWR_BF16, p, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e);
+  g_launches += 1;
+  g_last_path = SWR_PATH_FFMA;
+  return SWR_OK;
+}
+}  // namespace
+
+extern "C" {
+
+swr_status swr_decode_step(const void* u, const void* a, void* x, float* w_state, float* v_state,
+                           float* g_state, int64_t pos, swr_shape s, swr_dtype dt, void* stream) {
+  return decode_call(false, u, nullptr, nullptr, a, x, w_state, v_state, g_state, pos, s, dt, stream);
+}
+
+swr_status phalanx_mix_decode_step(const void* q, const void* k, const void* v, const void* a, void* y,
+                                   float* w_state, float* v_state, float* g_state, int64_t pos,
+                                   swr_shape s, swr_dtype dt, void* stream) {
+  return decode_call(true, k, v, q, a, y, w_state, v_state, g_state, pos, s, dt, stream);
 }
 
 const char* swr_strerror(swr_status st) {

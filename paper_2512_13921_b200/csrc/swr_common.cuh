@@ -43,6 +43,21 @@ struct Params {
   uint32_t epoch;  // TC path: launch ticket of the range claims (set by launch_tc)
 };
 
+// Recurrence-mode decode step (one token per (b, h); swr_decode_step in swr.h)
+struct DecParams {
+  const void* u;  // SWR input, or k of the mixer (u^ = k (.) v)
+  const void* v;  // mixer: v (pre-gate factor and residual)
+  const void* q;  // mixer: q (post-gate)
+  const void* a;
+  void* x;        // x~ (SWR) or y (mixer)
+  float* w;       // state [B,H,D]: local state of the current block
+  float* vc;      // state [B,H,D]: carrier v_{t-1}
+  float* g;       // state [B,H]: g_t[i]
+  int64_t B, H, D;
+  int64_t sx_b, sx_h, sa_b, sa_h;
+  int64_t pos;    // sequence position of the token
+};
+
 // ---------------------------------------------------------------------------
 // storage-dtype traits: 2-channel vector loads/stores, scalar decay access
 // ---------------------------------------------------------------------------

@@ -952,6 +952,91 @@ __global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma_vec(const Par
 }
 
 // ---------------------------------------------------------------------------
+// recurrence-mode decode step ("decoded in recurrence mode",
+// P:1888): one token per (b, h), state (w, v_{t-1}, g) carried between calls.
+// The ops and their order are those of fwd_stream for the same token, so a
+// sequence decoded step by step is bitwise the FFMA forward:
+//   i == 0: v <- w, g <- a, w <- u;  else g <- g a, w <- a w + u;  x~ = w + g v
+// A thread owns 4 channels; a head's D/4 threads sit in one warp, so the shared g
+// is read by all of them before one lane writes it (__syncwarp in between).
+// ---------------------------------------------------------------------------
+template <typename T, bool MIX>
+__global__ void __launch_bounds__(128) decode_step(const DecParams p) {
+  using V = VecN<T, 4>;
+  const int tph = (int)p.D / 4;
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t bh = gt / tph;  // (b, h) flattened
+  const int c = 4 * (int)(gt % tph);
+  const bool act = bh < p.B * p.H;
+  const int64_t b = act ? bh / p.H : 0, h = act ? bh % p.H : 0;
+  const int64_t xo = b * p.sx_b + h * p.sx_h + c;
+  const int64_t so = bh * p.D + c;
+  const int i = (int)(p.pos % kEll);
+  float gold = 1.f, a = 1.f;
+  if (act) {
+    a = IO<T>::ld1((const T*)p.a + b * p.sa_b + h * p.sa_h);
+    gold = p.g[bh];
+  }
+  __syncwarp();  // every lane of the head has read g before lane c == 0 rewrites it
+  if (!act) return;
+  float u[4];
+  if constexpr (!MIX) {
+    V::to_f(V::ld((const T*)p.u + xo), u);
+  } else {  // u^ = k (.) v
+    float kk[4], vv[4];
+    V::to_f(V::ld((const T*)p.u + xo), kk);
+    V::to_f(V::ld((const T*)p.v + xo), vv);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) u[e] = __fmul_rn(kk[e], vv[e]);
+  }
+  const float4 w4 = *reinterpret_cast<const float4*>(p.w + so);
+  float w[4] = {w4.x, w4.y, w4.z, w4.w};
+  float vc[4];
+  float g;
+  if (i == 0) {  // block start: the finished block's local end state becomes the carrier
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      vc[e] = w[e];
+      w[e] = u[e];
+    }
+    g = 1.f * a;
+    *reinterpret_cast<float4*>(p.vc + so) = make_float4(vc[0], vc[1], vc[2], vc[3]);
+  } else {
+    const float4 v4 = *reinterpret_cast<const float4*>(p.vc + so);
+    vc[0] = v4.x; vc[1] = v4.y; vc[2] = v4.z; vc[3] = v4.w;
+    g = gold * a;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) w[e] = fmaf(a, w[e], u[e]);
+  }
+  *reinterpret_cast<float4*>(p.w + so) = make_float4(w[0], w[1], w[2], w[3]);
+  if (c == 0) p.g[bh] = g;
+  float x[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) x[e] = fmaf(g, vc[e], w[e]);  // Pass II
+  if constexpr (MIX) {  // y = q x~ + v
+    float qq[4], vv[4];
+    V::to_f(V::ld((const T*)p.q + xo), qq);
+    V::to_f(V::ld((const T*)p.v + xo), vv);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) x[e] = fmaf(qq[e], x[e], vv[e]);
+  }
+  V::st((T*)p.x + xo, x);
+}
+
+cudaError_t launch_decode(bool mix, bool bf16, const DecParams& p, cudaStream_t st) {
+  const int64_t threads = p.B * p.H * (p.D / 4);
+  const unsigned grid = (unsigned)((threads + 127) / 128);
+  if (bf16) {
+    if (mix) decode_step<__nv_bfloat16, true><<<grid, 128, 0, st>>>(p);
+    else decode_step<__nv_bfloat16, false><<<grid, 128, 0, st>>>(p);
+  } else {
+    if (mix) decode_step<float, true><<<grid, 128, 0, st>>>(p);
+    else decode_step<float, false><<<grid, 128, 0, st>>>(p);
+  }
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -167,3 +167,56 @@ def swr(u, a, carry_in=None):
 def mix(q, k, v, a, carry_in=None):
     """Differentiable Phalanx double-gated mixer."""
     return PhalanxMixFunction.apply(q, k, v, a, carry_in)
+
+
+# ---------------------------------------------------------------------------
+# recurrence-mode decoding (include/swr.h swr_decode_step; SURVEY 8(f) NEXT-3)
+# ---------------------------------------------------------------------------
+class DecodeState:
+    """Per-(b, h) decode state: w (local state of the current block), v (carrier
+    v_{t-1}), g (decay product since the block start), fp32, and the position of the
+    next token.  ``carry_in`` [B, H, D] seeds w before position 0."""
+
+    def __init__(self, B, H, D, device, carry_in=None):
+        self.w = torch.zeros((B, H, D), device=device, dtype=torch.float32)
+        if carry_in is not None:
+            self.w.copy_(carry_in)
+        self.v = torch.empty((B, H, D), device=device, dtype=torch.float32)
+        self.g = torch.empty((B, H), device=device, dtype=torch.float32)
+        self.pos = 0
+
+
+def _dec_shape(x, a, st):
+    if x.dim() != 3 or x.stride(2) != 1:
+        raise ValueError(f"expected one token [B, H, D] with D contiguous, got {tuple(x.shape)}")
+    if a.dim() != 2 or tuple(a.shape) != tuple(x.shape[:2]):
+        raise ValueError(f"decays must be [B, H] = {tuple(x.shape[:2])}, got {tuple(a.shape)}")
+    if tuple(st.w.shape) != tuple(x.shape) or st.w.device != x.device:
+        raise ValueError("decode state does not match the token's shape / device")
+    B, H, D = x.shape
+    return _lib.swr_shape(B, 1, H, D, x.stride(0), 0, x.stride(1), a.stride(0), 0, a.stride(1))
+
+
+def swr_decode_step(u, a, state):
+    """x~ of the next token: u [B, H, D], a [B, H]; advances `state` (a DecodeState)."""
+    dt = _dtype(u, a)
+    u = u.contiguous()  # the ABI shares (sx_b, sx_h) between u and x
+    x = torch.empty(u.shape, dtype=u.dtype, device=u.device)
+    with torch.cuda.device(u.device):
+        _lib.swr_decode_step(_ptr(u), _ptr(a), _ptr(x), _ptr(state.w), _ptr(state.v), _ptr(state.g),
+                             state.pos, _dec_shape(u, a, state), dt, _stream(u))
+    state.pos += 1
+    return x
+
+
+def phalanx_mix_decode_step(q, k, v, a, state):
+    """y of the next token, y = q * x~ + v with u^ = k * v."""
+    dt = _dtype(q, k, v, a)
+    q, k, v = (t.contiguous() for t in (q, k, v))
+    y = torch.empty(q.shape, dtype=q.dtype, device=q.device)
+    with torch.cuda.device(q.device):
+        _lib.phalanx_mix_decode_step(_ptr(q), _ptr(k), _ptr(v), _ptr(a), _ptr(y), _ptr(state.w),
+                                     _ptr(state.v), _ptr(state.g), state.pos, _dec_shape(q, a, state),
+                                     dt, _stream(q))
+    state.pos += 1
+    return y

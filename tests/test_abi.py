@@ -78,6 +78,22 @@ def test_validation_codes(lib):
     assert lib.raw_status("swr_fwd", FAKE, FAKE, FAKE, FAKE + 8, None, s, 0, None) == 4
 
 
+def test_decode_step_validation_codes(lib):
+    s1 = _shape(lib, L=1)
+    # one token per call, non-negative position
+    assert lib.raw_status("swr_decode_step", FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, 0, _shape(lib, L=2), 0,
+                          None) == 2
+    assert lib.raw_status("swr_decode_step", FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, -1, s1, 0, None) == 2
+    # required operands and state
+    assert lib.raw_status("swr_decode_step", None, FAKE, FAKE, FAKE, FAKE, FAKE, 0, s1, 0, None) == 1
+    assert lib.raw_status("swr_decode_step", FAKE, FAKE, FAKE, FAKE, FAKE, None, 0, s1, 0, None) == 1
+    assert lib.raw_status("phalanx_mix_decode_step", FAKE, FAKE, None, FAKE, FAKE, FAKE, FAKE, FAKE, 0, s1,
+                          0, None) == 1
+    # state alignment: w, v 16 B; g 4 B
+    assert lib.raw_status("swr_decode_step", FAKE, FAKE, FAKE, FAKE + 4, FAKE, FAKE, 0, s1, 0, None) == 4
+    assert lib.raw_status("swr_decode_step", FAKE, FAKE, FAKE, FAKE, FAKE, FAKE + 2, 0, s1, 0, None) == 4
+
+
 def test_strerror_names_every_code(lib):
     for code in range(8):
         assert lib._lib.swr_strerror(code).decode().startswith("SWR_")

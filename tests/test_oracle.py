@@ -389,3 +389,28 @@ def test_empty_sequence():
     assert x.shape == u.shape and np.all(co == 0)
     du, da, mo = oracle.swr_bwd(u, a, u, carry_in=c, mu_in=c)
     assert du.shape == u.shape and da.shape == a.shape and np.all(mo == 0)
+
+
+# --------------------------------------------------------------------------
+# recurrence-mode decoding
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("L", [1, 15, 16, 17, 50])
+def test_decode_equals_dense_jagged_operator(L):
+    """Token-by-token decoding reproduces the jagged-window operator (entrywise
+    products) including the carry_in fold of block 0, for every prefix length."""
+    u, a, _, c, _ = rand_problem(2, L, 3, 4, seed=90 + L)
+    x = oracle.swr_decode(u, a, carry_in=c)
+    for b in range(2):
+        for h in range(3):
+            M, cc = dense_jagged(a[b, :, h]), dense_carry(a[b, :, h])
+            ref = M @ u[b, :, h] + np.outer(cc, c[b, h])
+            assert normwise(x[b, :, h], ref) < 1e-12
+
+
+def test_decode_equals_parallel_forward_and_mixer():
+    u, a, _, c, _ = rand_problem(2, 83, 5, 8, seed=7)
+    assert normwise(oracle.swr_decode(u, a, c), oracle.swr_fwd(u, a, carry_in=c)) < 1e-12
+    r = np.random.default_rng(8)
+    q, k, v = (r.standard_normal(u.shape) for _ in range(3))
+    y = oracle.mix_decode(q, k, v, a, carry_in=c)
+    assert normwise(y, oracle.mix_fwd(q, k, v, a, carry_in=c)) < 1e-12

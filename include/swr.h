@@ -181,6 +181,21 @@ SWR_API swr_status phalanx_mix_decode_step(const void* q, const void* k, const v
                            float* g_state, int64_t pos, swr_shape s, swr_dtype dt,
                            void* stream);
 
+/* Exact full-range recurrence: x_n = a_n x_{n-1} + u_n over
+ * the whole sequence (Eq. 2.1, x_{-1} = carry_in) -- the operator B2P truncates --
+ * computed as Alg. 2: I) per-block local solves giving the block end
+ * state v_t and decay product c_t = a_t[0]...a_t[15]; II) the carrier recurrence
+ * s_t = c_t s_{t-1} + v_t, sequential over blocks; III) reconstruction
+ * x_t[i] = w_t[i] + g_t[i] s_{t-1} (Thm. 3).  CUDA cores, three launches.
+ *   u, a, x, carry_in as in swr_fwd; carry_out = x at token L-1 (the full state).
+ *   workspace  device memory of >= swr_exact_workspace_bytes(s) bytes, 16-byte
+ *              aligned, caller-owned scratch (no allocation here); too small ->
+ *              SWR_ERR_SHAPE, NULL with a non-empty problem -> SWR_ERR_NULL. */
+SWR_API int64_t swr_exact_workspace_bytes(swr_shape s);
+SWR_API swr_status swr_exact_fwd(const void* u, const void* a, void* x, const float* carry_in,
+                         float* carry_out, void* workspace, int64_t workspace_bytes,
+                         swr_shape s, swr_dtype dt, void* stream);
+
 /* Human-readable name of a status code (static storage). */
 SWR_API const char* swr_strerror(swr_status st);
 

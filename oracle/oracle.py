@@ -157,3 +157,18 @@ def mix_decode(q, k, v, a, carry_in=None):
     """Phalanx mixer decoded token by token: u^ = k v, y = q x~ + v."""
     q, k, v = _f64(q), _f64(k), _f64(v)
     return q * swr_decode(k * v, a, carry_in) + v
+
+
+def linrec_fwd(u, a, carry_in=None):
+    """The untruncated linear recurrence, Eq. 2.1: x_n = a_n x_{n-1} + u_n
+    with x_{-1} = carry_in (or 0), one token at a time in fp64 -- the reference for
+    the exact full-range mode (Alg. 2).  Returns (x, x_{L-1})."""
+    u, a = _f64(u), _f64(a)
+    _check(u, a)
+    B, L, H, D = u.shape
+    s = np.zeros((B, H, D)) if carry_in is None else _f64(carry_in).copy()
+    x = np.empty_like(u)
+    for n in range(L):
+        s = a[:, n, :, None] * s + u[:, n]
+        x[:, n] = s
+    return x, s

@@ -18,7 +18,8 @@ SWR_PATH_AUTO, SWR_PATH_FFMA, SWR_PATH_TC = 0, 1, 2
 
 EXPORTS = ("swr_fwd", "swr_bwd", "phalanx_mix", "phalanx_mix_bwd", "swr_strerror",
            "swr_last_cuda_error", "swr_set_path", "swr_launch_count", "swr_last_path",
-           "swr_set_trace", "swr_decode_step", "phalanx_mix_decode_step")
+           "swr_set_trace", "swr_decode_step", "phalanx_mix_decode_step",
+           "swr_exact_workspace_bytes", "swr_exact_fwd")
 
 
 class SwrError(RuntimeError):
@@ -50,8 +51,11 @@ def _load():
     lib.phalanx_mix_bwd.argtypes = [P, P, P, P, P, P, P, P, P, P, P, P, S, I, P]
     lib.swr_decode_step.argtypes = [P, P, P, P, P, P, ctypes.c_int64, S, I, P]
     lib.phalanx_mix_decode_step.argtypes = [P, P, P, P, P, P, P, P, ctypes.c_int64, S, I, P]
+    lib.swr_exact_fwd.argtypes = [P, P, P, P, P, P, ctypes.c_int64, S, I, P]
+    lib.swr_exact_workspace_bytes.argtypes = [S]
+    lib.swr_exact_workspace_bytes.restype = ctypes.c_int64
     for f in ("swr_fwd", "swr_bwd", "phalanx_mix", "phalanx_mix_bwd", "swr_decode_step",
-              "phalanx_mix_decode_step"):
+              "phalanx_mix_decode_step", "swr_exact_fwd"):
         getattr(lib, f).restype = I
     lib.swr_strerror.argtypes = [I]
     lib.swr_strerror.restype = ctypes.c_char_p
@@ -123,3 +127,12 @@ def swr_decode_step(u, a, x, w_state, v_state, g_state, pos, shape, dtype, strea
 def phalanx_mix_decode_step(q, k, v, a, y, w_state, v_state, g_state, pos, shape, dtype, stream):
     _check(_lib.phalanx_mix_decode_step(q, k, v, a, y, w_state, v_state, g_state, pos, shape, dtype,
                                         stream), "phalanx_mix_decode_step")
+
+
+def swr_exact_workspace_bytes(shape) -> int:
+    return _lib.swr_exact_workspace_bytes(shape)
+
+
+def swr_exact_fwd(u, a, x, carry_in, carry_out, workspace, workspace_bytes, shape, dtype, stream):
+    _check(_lib.swr_exact_fwd(u, a, x, carry_in, carry_out, workspace, workspace_bytes, shape, dtype,
+                              stream), "swr_exact_fwd")

@@ -15,6 +15,7 @@ cudaError_t launch_ffma(int op, bool bf16, const Params& p, cudaStream_t st, int
 cudaError_t launch_tc(int op, const Params& p, cudaStream_t st, int sms, int* launches);
 bool tc_supported(int op, bool bf16, const Params& p);
 cudaError_t launch_decode(bool mix, bool bf16, const DecParams& p, cudaStream_t st);
+cudaError_t launch_exact(bool bf16, Params p, void* workspace, cudaStream_t st, int sms);
 }  // namespace swr
 
 namespace {
@@ -289,6 +290,40 @@ swr_status phalanx_mix_decode_step(const void* q, const void* k, const void* v, 
                                    float* w_state, float* v_state, float* g_state, int64_t pos,
                                    swr_shape s, swr_dtype dt, void* stream) {
   return decode_call(true, k, v, q, a, y, w_state, v_state, g_state, pos, s, dt, stream);
+}
+
+int64_t swr_exact_workspace_bytes(swr_shape s) {
+  if (s.B <= 0 || s.H <= 0 || s.L <= 0 || s.D <= 0) return 0;
+  const int64_t nb = (s.L + swr::kEll - 1) / swr::kEll;
+  return (int64_t)sizeof(float) * s.B * s.H * nb * (s.D + 1);
+}
+
+swr_status swr_exact_fwd(const void* u, const void* a, void* x, const float* carry_in, float* carry_out,
+                         void* workspace, int64_t workspace_bytes, swr_shape s, swr_dtype dt,
+                         void* stream) {
+  const void* dt_[] = {u, x};
+  const void* at_[] = {a};
+  const void* ct_[] = {carry_in, carry_out, workspace};
+  swr_status st = validate(s, dt, dt_, 2, at_, 1, ct_, 3);
+  if (st != SWR_OK) return st;
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  if (s.B == 0 || s.H == 0 || s.L == 0) return empty_call(s, carry_out, nullptr, cs);
+  if (!workspace) return SWR_ERR_NULL;
+  if (workspace_bytes < swr_exact_workspace_bytes(s)) return SWR_ERR_SHAPE;
+  int sms = 0;
+  st = device_info(&sms);
+  if (st != SWR_OK) return st;
+  swr::Params p = make_params(s);
+  p.u = u;
+  p.a = a;
+  p.x = x;
+  p.carry_in = carry_in;
+  p.carry_out = carry_out;
+  cudaError_t e = swr::launch_exact(dt == SWR_BF16, p, workspace, cs, sms);
+  if (e != cudaSuccess) return cuda_fail(e);
+  g_launches += 3;
+  g_last_path = SWR_PATH_FFMA;
+  return SWR_OK;
 }
 
 const char* swr_strerror(swr_status st) {

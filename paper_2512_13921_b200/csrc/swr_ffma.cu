@@ -1037,6 +1037,129 @@ cudaError_t launch_decode(bool mix, bool bf16, const DecParams& p, cudaStream_t 
 }
 
 // ---------------------------------------------------------------------------
+// exact full-range recurrence (Alg. 2, Thm. 3
+// P:657-669): x_n = a_n x_{n-1} + u_n over the whole sequence (Eq. 2.1), in the
+// three stages of Alg. 2 --
+//   I   exact_local: per block, the local solve's end state v_t = w_t[15] and the
+//       block decay product c_t = a_t[0] ... a_t[15] (the carrier system);
+//   II  exact_carry: the carrier recurrence s_t = c_t s_{t-1} + v_t (s_{-1} =
+//       carry_in), sequential over blocks per (b, h, channel);
+//   III exact_out: x~_t[i] = w_t[i] + g_t[i] s_{t-1} -- B2P's Pass II with the full
+//       carrier instead of the truncated v_{t-1}.
+// Workspace: S [B, H, nb, D] fp32 (v_t, overwritten by s_t), C [B, H, nb] fp32.
+// A thread owns 4 channels; padding past L is u = 0, a = 1 as elsewhere.
+// ---------------------------------------------------------------------------
+struct ExactWs {
+  float* S;
+  float* C;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(128) exact_local(const Params p, const ExactWs ws) {
+  using V = VecN<T, 4>;
+  const int tph = (int)p.D / 4, hpc = 128 / tph;
+  const int hh = threadIdx.x / tph, c = 4 * (threadIdx.x % tph);
+  const int64_t b = blockIdx.z, h = (int64_t)blockIdx.y * hpc + hh;
+  if (h >= p.H) return;
+  const int64_t t_lo = (int64_t)blockIdx.x * p.K, t_hi = min(t_lo + p.K, p.nb);
+  const T* A = (const T*)p.a + b * p.sa_b + h * p.sa_h;
+  const int64_t xo = b * p.sx_b + h * p.sx_h + c;
+  const int64_t line = b * p.H + h;
+  for (int64_t t = t_lo; t < t_hi; ++t) {
+    float w[4], g = 1.f;
+#pragma unroll
+    for (int i = 0; i < kEll; ++i) {
+      const int64_t n = t * kEll + i;
+      const bool valid = n < p.L;
+      const float a = valid ? IO<T>::ld1(A + n * p.sa_l) : 1.f;
+      float u[4];
+      V::to_f(valid ? V::ld((const T*)p.u + xo + n * p.sx_l) : V::zero(), u);
+      g *= a;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) w[e] = (i == 0) ? u[e] : fmaf(a, w[e], u[e]);
+    }
+    *reinterpret_cast<float4*>(ws.S + (line * p.nb + t) * p.D + c) = make_float4(w[0], w[1], w[2], w[3]);
+    if (c == 0) ws.C[line * p.nb + t] = g;
+  }
+}
+
+__global__ void __launch_bounds__(128) exact_carry(const Params p, const ExactWs ws) {
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int tph = (int)p.D / 4;
+  const int64_t line = gt / tph;
+  const int c = 4 * (int)(gt % tph);
+  if (line >= p.B * p.H) return;
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (p.carry_in) s = *reinterpret_cast<const float4*>(p.carry_in + line * p.D + c);
+  float4* S = reinterpret_cast<float4*>(ws.S + line * p.nb * p.D + c);
+  const float* C = ws.C + line * p.nb;
+  const int64_t st = p.D / 4;  // float4 stride between blocks
+#pragma unroll 8
+  for (int64_t t = 0; t < p.nb; ++t) {
+    const float ct = C[t];
+    const float4 v = S[t * st];
+    s = make_float4(fmaf(ct, s.x, v.x), fmaf(ct, s.y, v.y), fmaf(ct, s.z, v.z), fmaf(ct, s.w, v.w));
+    S[t * st] = s;
+  }
+  if (p.carry_out) *reinterpret_cast<float4*>(p.carry_out + line * p.D + c) = s;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) exact_out(const Params p, const ExactWs ws) {
+  using V = VecN<T, 4>;
+  const int tph = (int)p.D / 4, hpc = 128 / tph;
+  const int hh = threadIdx.x / tph, c = 4 * (threadIdx.x % tph);
+  const int64_t b = blockIdx.z, h = (int64_t)blockIdx.y * hpc + hh;
+  if (h >= p.H) return;
+  const int64_t t_lo = (int64_t)blockIdx.x * p.K, t_hi = min(t_lo + p.K, p.nb);
+  const T* A = (const T*)p.a + b * p.sa_b + h * p.sa_h;
+  const int64_t xo = b * p.sx_b + h * p.sx_h + c;
+  const int64_t line = b * p.H + h;
+  for (int64_t t = t_lo; t < t_hi; ++t) {
+    float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);  // s_{t-1}
+    if (t > 0) s4 = *reinterpret_cast<const float4*>(ws.S + (line * p.nb + t - 1) * p.D + c);
+    else if (p.carry_in) s4 = *reinterpret_cast<const float4*>(p.carry_in + line * p.D + c);
+    const float sp[4] = {s4.x, s4.y, s4.z, s4.w};
+    float w[4], g = 1.f;
+#pragma unroll
+    for (int i = 0; i < kEll; ++i) {
+      const int64_t n = t * kEll + i;
+      const bool valid = n < p.L;
+      const float a = valid ? IO<T>::ld1(A + n * p.sa_l) : 1.f;
+      float u[4];
+      V::to_f(valid ? V::ld((const T*)p.u + xo + n * p.sx_l) : V::zero(), u);
+      g *= a;
+      float x[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        w[e] = (i == 0) ? u[e] : fmaf(a, w[e], u[e]);
+        x[e] = fmaf(g, sp[e], w[e]);
+      }
+      if (valid) V::st((T*)p.x + xo + n * p.sx_l, x);
+    }
+  }
+}
+
+cudaError_t launch_exact(bool bf16, Params p, void* workspace, cudaStream_t st, int sms) {
+  auto cdiv = [](int64_t x, int64_t y) { return (x + y - 1) / y; };
+  ExactWs ws;
+  ws.S = reinterpret_cast<float*>(workspace);
+  ws.C = ws.S + p.B * p.H * p.nb * p.D;
+  const int64_t hpc = 128 / (p.D / 4);
+  const int64_t cols = p.B * cdiv(p.H, hpc);
+  const int64_t want = std::max<int64_t>(1, ((int64_t)sms * 8) / std::max<int64_t>(cols, 1));
+  p.K = std::min<int64_t>(std::max<int64_t>(cdiv(p.nb, want), 1), p.nb);
+  const dim3 grid((unsigned)cdiv(p.nb, p.K), (unsigned)cdiv(p.H, hpc), (unsigned)p.B);
+  const unsigned gc = (unsigned)cdiv(p.B * p.H * (p.D / 4), 128);
+  if (bf16) exact_local<__nv_bfloat16><<<grid, 128, 0, st>>>(p, ws);
+  else exact_local<float><<<grid, 128, 0, st>>>(p, ws);
+  exact_carry<<<gc, 128, 0, st>>>(p, ws);
+  if (bf16) exact_out<__nv_bfloat16><<<grid, 128, 0, st>>>(p, ws);
+  else exact_out<float><<<grid, 128, 0, st>>>(p, ws);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -169,6 +169,23 @@ def mix(q, k, v, a, carry_in=None):
     return PhalanxMixFunction.apply(q, k, v, a, carry_in)
 
 
+def swr_exact_fwd(u, a, carry_in=None, return_carry=False):
+    """The untruncated recurrence x_n = a_n x_{n-1} + u_n (Eq. 2.1) by Alg. 2's three
+    stages (include/swr.h swr_exact_fwd).  Returns x or (x, carry_out)."""
+    (u,) = _prep(u)
+    dt = _dtype(u, a)
+    x = _like(u)
+    ci = _carry(carry_in, u)
+    co = _new_carry(u) if return_carry else None
+    shape = _shape(u, a)
+    nbytes = _lib.swr_exact_workspace_bytes(shape)
+    ws = torch.empty(max(nbytes, 16) // 4, dtype=torch.float32, device=u.device)
+    with torch.cuda.device(u.device):
+        _lib.swr_exact_fwd(_ptr(u), _ptr(a), _ptr(x), _ptr(ci), _ptr(co), _ptr(ws), nbytes, shape, dt,
+                           _stream(u))
+    return (x, co) if return_carry else x
+
+
 # ---------------------------------------------------------------------------
 # recurrence-mode decoding (include/swr.h swr_decode_step; SURVEY 8(f) NEXT-3)
 # ---------------------------------------------------------------------------

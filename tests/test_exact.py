@@ -1,0 +1,59 @@
+"""Exact full-range recurrence (include/swr.h swr_exact_fwd; Alg. 2 P:684-708;
+SURVEY 8(f) NEXT-2) against the fp64 Eq. 2.1 oracle (oracle.linrec_fwd, pinned to
+the dense operator and the geometric closed form in test_oracle.py)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from swr_inputs import swr_inputs, to64
+
+pytestmark = pytest.mark.gpu
+TOL = {torch.float32: 1e-5, torch.bfloat16: 2e-2}
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from conftest import build_lib
+    build_lib()
+    import paper_2512_13921_b200 as P
+    return P
+
+
+def normwise(x, ref):
+    x = x.detach().double().cpu().numpy()
+    return np.max(np.abs(x - ref)) / max(np.max(np.abs(ref)), 1e-300)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("D", [16, 64, 128])
+@pytest.mark.parametrize("B,L,H", [(2, 16, 3), (1, 77, 5), (2, 1000, 16), (1, 4096, 2)])
+@pytest.mark.parametrize("carry", [False, True])
+def test_exact_matches_full_recurrence(P, dtype, D, B, L, H, carry):
+    inp = swr_inputs(B, L, H, D, dtype=dtype, seed=600 + L + D, carry=carry)
+    u, a = inp["u"].cuda(), inp["a"].cuda()
+    ci = inp["carry_in"].cuda() if carry else None
+    x, co = P.swr_exact_fwd(u, a, carry_in=ci, return_carry=True)
+    torch.cuda.synchronize()
+    rx, rlast = oracle.linrec_fwd(to64(inp["u"]), to64(inp["a"]), to64(inp.get("carry_in")))
+    assert normwise(x, rx) <= TOL[dtype]
+    assert normwise(co, rlast) <= TOL[dtype]
+
+
+def test_exact_differs_from_truncated_only_past_two_blocks(P):
+    inp = swr_inputs(2, 200, 4, 32, dtype=torch.float32, seed=9)
+    u, a = inp["u"].cuda(), inp["a"].cuda()
+    xe = P.swr_exact_fwd(u, a)
+    xs = P.swr_fwd(u, a)
+    assert torch.allclose(xe[:, :32], xs[:, :32], rtol=1e-6, atol=1e-6)
+    assert not torch.allclose(xe[:, 32:], xs[:, 32:], rtol=1e-6, atol=1e-6)
+
+
+def test_exact_empty(P):
+    u = torch.zeros(2, 0, 3, 16, device="cuda")
+    a = torch.zeros(2, 0, 3, device="cuda")
+    ci = torch.randn(2, 3, 16, device="cuda")
+    x, co = P.swr_exact_fwd(u, a, carry_in=ci, return_carry=True)
+    assert x.shape == u.shape and torch.count_nonzero(co) == 0

@@ -414,3 +414,39 @@ def test_decode_equals_parallel_forward_and_mixer():
     q, k, v = (r.standard_normal(u.shape) for _ in range(3))
     y = oracle.mix_decode(q, k, v, a, carry_in=c)
     assert normwise(y, oracle.mix_fwd(q, k, v, a, carry_in=c)) < 1e-12
+
+
+# --------------------------------------------------------------------------
+# exact full-range recurrence (Eq. 2.1)
+# --------------------------------------------------------------------------
+def dense_full(a):
+    """Lower-triangular L of Eq. 2.1 entrywise: L_nj = a_{j+1} ... a_n."""
+    L = len(a)
+    M = np.zeros((L, L))
+    for n in range(L):
+        for j in range(n + 1):
+            M[n, j] = np.prod(a[j + 1:n + 1])
+    return M
+
+
+@pytest.mark.parametrize("L", [1, 16, 33, 70])
+def test_linrec_equals_dense_full_operator(L):
+    u, a, _, c, _ = rand_problem(2, L, 2, 3, seed=500 + L)
+    x, last = oracle.linrec_fwd(u, a, carry_in=c)
+    for b in range(2):
+        for h in range(2):
+            ref = dense_full(a[b, :, h]) @ u[b, :, h] + np.outer(np.cumprod(a[b, :, h]), c[b, h])
+            assert normwise(x[b, :, h], ref) < 1e-12
+    assert np.array_equal(last, x[:, -1])
+
+
+def test_linrec_constant_decay_closed_form_and_two_block_agreement():
+    rho, L = 0.9, 64
+    u = np.ones((1, L, 1, 1))
+    a = np.full((1, L, 1), rho)
+    x, _ = oracle.linrec_fwd(u, a)
+    n = np.arange(L)
+    assert np.allclose(x[0, :, 0, 0], (1 - rho ** (n + 1)) / (1 - rho), rtol=1e-13, atol=0)
+    # on the first two blocks the jagged window is the full recurrence (P:1300-1317)
+    u, a, _, _, _ = rand_problem(1, 2 * ELL, 3, 4, seed=5)
+    assert normwise(oracle.linrec_fwd(u, a)[0], oracle.swr_fwd(u, a)) < 1e-12

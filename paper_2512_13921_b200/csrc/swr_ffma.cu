@@ -1094,12 +1094,27 @@ __global__ void __launch_bounds__(128) exact_carry(const Params p, const ExactWs
   float4* S = reinterpret_cast<float4*>(ws.S + line * p.nb * p.D + c);
   const float* C = ws.C + line * p.nb;
   const int64_t st = p.D / 4;  // float4 stride between blocks
-#pragma unroll 8
-  for (int64_t t = 0; t < p.nb; ++t) {
-    const float ct = C[t];
-    const float4 v = S[t * st];
-    s = make_float4(fmaf(ct, s.x, v.x), fmaf(ct, s.y, v.y), fmaf(ct, s.z, v.z), fmaf(ct, s.w, v.w));
-    S[t * st] = s;
+  // The chain is serial; its loads are not.  Issue a group's loads before its stores
+  // (the compiler cannot move them across stores to the same array).
+  constexpr int kG = 16;
+  for (int64_t t0 = 0; t0 < p.nb; t0 += kG) {
+    float cg[kG];
+    float4 vg[kG];
+#pragma unroll
+    for (int j = 0; j < kG; ++j) {
+      const bool ok = t0 + j < p.nb;
+      cg[j] = ok ? C[t0 + j] : 0.f;
+      vg[j] = ok ? S[(t0 + j) * st] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int j = 0; j < kG; ++j) {
+      if (t0 + j < p.nb) {
+        const float ct = cg[j];
+        const float4 v = vg[j];
+        s = make_float4(fmaf(ct, s.x, v.x), fmaf(ct, s.y, v.y), fmaf(ct, s.z, v.z), fmaf(ct, s.w, v.w));
+        S[(t0 + j) * st] = s;
+      }
+    }
   }
   if (p.carry_out) *reinterpret_cast<float4*>(p.carry_out + line * p.D + c) = s;
 }

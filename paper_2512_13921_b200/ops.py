@@ -202,6 +202,27 @@ class DecodeState:
         self.g = torch.empty((B, H), device=device, dtype=torch.float32)
         self.pos = 0
 
+    def prefill(self, u, a, k=None, v=None):
+        """Seed the state from a prompt [B, P, H, D] (mixer: pass k and v, u=None) so
+        that decoding continues at position P.  The state depends only on the last
+        two blocks (v_{t-1} is block t-1's local end state, w and g restart at each
+        block start), so this steps through at most 31 prompt tokens
+        with the decode kernel and discards their outputs; the prompt's own outputs
+        come from the parallel forward.  A prompt shorter than 16 tokens starts from
+        the carry_in this state was built with (call it on a fresh state)."""
+        src = u if u is not None else k
+        P = src.shape[1]
+        t = P // 16
+        start = 16 * (t - 1) if t >= 1 else 0
+        self.pos = start  # from a block start on, the state no longer depends on its past
+        q0 = torch.zeros_like(k[:, 0]) if u is None and P > 0 else None
+        for n in range(start, P):
+            if u is not None:
+                swr_decode_step(u[:, n], a[:, n], self)
+            else:  # the output (q = 0) is discarded; u^ = k * v is formed in the kernel
+                phalanx_mix_decode_step(q0, k[:, n], v[:, n], a[:, n], self)
+        return self
+
 
 def _dec_shape(x, a, st):
     if x.dim() != 3 or x.stride(2) != 1:

@@ -72,3 +72,29 @@ def test_mix_decode_matches_oracle_and_forward(P, dtype, D, H):
     finally:
         P.set_path(prev)
     assert torch.equal(y, yf)
+
+
+@pytest.mark.parametrize("P_len", [0, 5, 16, 37, 64])
+def test_prefill_then_decode_continues_the_forward(P, P_len):
+    """State seeded from a prompt (at most its last 31 tokens) + decoding the rest
+    gives bitwise the CUDA-core forward of the whole sequence from position P on."""
+    B, L, H, D = 2, 80, 3, 32
+    dtype = torch.bfloat16
+    inp = swr_inputs(B, L, H, D, dtype=dtype, seed=700 + P_len, carry=True)
+    u, a, ci = inp["u"].cuda(), inp["a"].cuda(), inp["carry_in"].cuda()
+    st = P.DecodeState(B, H, D, u.device, carry_in=ci).prefill(u[:, :P_len], a[:, :P_len])
+    assert st.pos == P_len
+    x = torch.stack([P.swr_decode_step(u[:, n], a[:, n], st) for n in range(P_len, L)], dim=1)
+    prev = P.set_path(P.SWR_PATH_FFMA)
+    try:
+        xf = P.swr_fwd(u, a, carry_in=ci)
+        mq, mk, mv = (torch.randn(B, L, H, D, device="cuda").to(dtype) for _ in range(3))
+        yf = P.phalanx_mix(mq, mk, mv, a, carry_in=ci)
+    finally:
+        P.set_path(prev)
+    assert torch.equal(x, xf[:, P_len:])
+    sm = P.DecodeState(B, H, D, u.device, carry_in=ci).prefill(None, a[:, :P_len], k=mk[:, :P_len],
+                                                                 v=mv[:, :P_len])
+    y = torch.stack([P.phalanx_mix_decode_step(mq[:, n], mk[:, n], mv[:, n], a[:, n], sm)
+                     for n in range(P_len, L)], dim=1)
+    assert torch.equal(y, yf[:, P_len:])

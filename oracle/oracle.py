@@ -172,3 +172,27 @@ def linrec_fwd(u, a, carry_in=None):
         s = a[:, n, :, None] * s + u[:, n]
         x[:, n] = s
     return x, s
+
+
+def linrec_bwd(u, a, G, carry_in=None, mu_in=None):
+    """Reverse mode of linrec_fwd, written out token by token in fp64: lambda_n =
+    G_n + a_{n+1} lambda_{n+1} (lambda_{L-1} also receives mu_in = dLoss/dx_{L-1}),
+    du = lambda, da_n = sum_c lambda_n x_{n-1} (x_{-1} = carry_in), mu_out = a_0 lambda_0.
+    Returns (du, da, mu_out).  Pinned by finite differences in tests/test_oracle.py."""
+    u, a, G = _f64(u), _f64(a), _f64(G)
+    _check(u, a)
+    B, L, H, D = u.shape
+    x, _ = linrec_fwd(u, a, carry_in)
+    x0 = np.zeros((B, H, D)) if carry_in is None else _f64(carry_in)
+    du = np.empty_like(u)
+    da = np.empty_like(a)
+    lam = np.zeros((B, H, D)) if mu_in is None else _f64(mu_in).copy()
+    for n in range(L - 1, -1, -1):
+        if n < L - 1:
+            lam = a[:, n + 1, :, None] * lam
+        lam = lam + G[:, n]
+        du[:, n] = lam
+        xprev = x[:, n - 1] if n > 0 else x0
+        da[:, n] = np.sum(lam * xprev, axis=-1)
+    mu_out = a[:, 0, :, None] * lam if L > 0 else np.zeros((B, H, D))
+    return du, da, mu_out

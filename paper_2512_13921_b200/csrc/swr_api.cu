@@ -16,6 +16,7 @@ cudaError_t launch_tc(int op, const Params& p, cudaStream_t st, int sms, int* la
 bool tc_supported(int op, bool bf16, const Params& p);
 cudaError_t launch_decode(bool mix, bool bf16, const DecParams& p, cudaStream_t st);
 cudaError_t launch_exact(bool bf16, Params p, void* workspace, cudaStream_t st, int sms);
+cudaError_t launch_exact_bwd(bool bf16, Params p, void* workspace, cudaStream_t st, int sms);
 }  // namespace swr
 
 namespace {
@@ -295,7 +296,7 @@ swr_status phalanx_mix_decode_step(const void* q, const void* k, const void* v, 
 int64_t swr_exact_workspace_bytes(swr_shape s) {
   if (s.B <= 0 || s.H <= 0 || s.L <= 0 || s.D <= 0) return 0;
   const int64_t nb = (s.L + swr::kEll - 1) / swr::kEll;
-  return (int64_t)sizeof(float) * s.B * s.H * nb * (s.D + 1);
+  return (int64_t)sizeof(float) * (s.B * s.H * nb * s.D + (s.B * s.H * nb + 3) / 4 * 4);
 }
 
 swr_status swr_exact_fwd(const void* u, const void* a, void* x, const float* carry_in, float* carry_out,
@@ -322,6 +323,37 @@ swr_status swr_exact_fwd(const void* u, const void* a, void* x, const float* car
   cudaError_t e = swr::launch_exact(dt == SWR_BF16, p, workspace, cs, sms);
   if (e != cudaSuccess) return cuda_fail(e);
   g_launches += 3;
+  g_last_path = SWR_PATH_FFMA;
+  return SWR_OK;
+}
+
+swr_status swr_exact_bwd(const void* u, const void* a, const void* dx, void* du, void* da,
+                         const float* carry_in, const float* mu_in, float* mu_out, void* workspace,
+                         int64_t workspace_bytes, swr_shape s, swr_dtype dt, void* stream) {
+  const void* dt_[] = {u, dx, du};
+  const void* at_[] = {a, da};
+  const void* ct_[] = {carry_in, mu_in, mu_out, workspace};
+  swr_status st = validate(s, dt, dt_, 3, at_, 2, ct_, 4);
+  if (st != SWR_OK) return st;
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  if (s.B == 0 || s.H == 0 || s.L == 0) return empty_call(s, nullptr, mu_out, cs);
+  if (!workspace) return SWR_ERR_NULL;
+  if (workspace_bytes < 2 * swr_exact_workspace_bytes(s)) return SWR_ERR_SHAPE;
+  int sms = 0;
+  st = device_info(&sms);
+  if (st != SWR_OK) return st;
+  swr::Params p = make_params(s);
+  p.u = u;
+  p.a = a;
+  p.dx = dx;
+  p.du = du;
+  p.da = da;
+  p.carry_in = carry_in;
+  p.mu_in = mu_in;
+  p.mu_out = mu_out;
+  cudaError_t e = swr::launch_exact_bwd(dt == SWR_BF16, p, workspace, cs, sms);
+  if (e != cudaSuccess) return cuda_fail(e);
+  g_launches += 5;
   g_last_path = SWR_PATH_FFMA;
   return SWR_OK;
 }

@@ -1155,6 +1155,175 @@ __global__ void __launch_bounds__(128) exact_out(const Params p, const ExactWs w
   }
 }
 
+// Backward of the exact mode (reverse mode of Eq. 2.1): lambda_n = G_n + a_{n+1}
+// lambda_{n+1}, du = lambda, da_n = sum_c lambda_n x_{n-1} (x_{-1} = carry_in),
+// mu_out = a_0 lambda_0; mu_in enters as mu for the last block (as in swr_bwd).
+// Blockwise: lambda_t[i] = l_t[i] + r_t[i] mu_t with l_t the block-local reverse
+// solve, r_t[i] = a_t[i+1]...a_t[15] and mu_t = a_{t+1}[0] lambda_{t+1}[0]; the
+// reverse carrier chain is mu_{t-1} = a_t[0] (l_t[0] + r_t[0] mu_t).  Stages:
+// exact_local + exact_carry (forward carriers s_t, needed for x_{n-1}),
+// exact_bwd_local (E_t = l_t[0] into S2, R_t = r_t[0] a_t[0] into C2),
+// exact_bwd_carry (mu_t into S2), exact_bwd_out (du, da).
+template <typename T>
+__global__ void __launch_bounds__(128) exact_bwd_local(const Params p, const ExactWs ws2) {
+  using V = VecN<T, 4>;
+  const int tph = (int)p.D / 4, hpc = 128 / tph;
+  const int hh = threadIdx.x / tph, c = 4 * (threadIdx.x % tph);
+  const int64_t b = blockIdx.z, h = (int64_t)blockIdx.y * hpc + hh;
+  if (h >= p.H) return;
+  const int64_t t_lo = (int64_t)blockIdx.x * p.K, t_hi = min(t_lo + p.K, p.nb);
+  const T* A = (const T*)p.a + b * p.sa_b + h * p.sa_h;
+  const int64_t xo = b * p.sx_b + h * p.sx_h + c;
+  const int64_t line = b * p.H + h;
+  for (int64_t t = t_lo; t < t_hi; ++t) {
+    float l[4], r = 1.f;
+#pragma unroll
+    for (int i = kEll - 1; i >= 0; --i) {
+      const int64_t n = t * kEll + i;
+      const bool valid = n < p.L;
+      float g[4];
+      V::to_f(valid ? V::ld((const T*)p.dx + xo + n * p.sx_l) : V::zero(), g);
+      if (i == kEll - 1) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) l[e] = g[e];
+      } else {
+        const int64_t n1 = n + 1;
+        const float an = n1 < p.L ? IO<T>::ld1(A + n1 * p.sa_l) : 1.f;  // a_t[i+1]
+        r *= an;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) l[e] = fmaf(an, l[e], g[e]);
+      }
+    }
+    const int64_t n0 = t * kEll;
+    const float a0 = n0 < p.L ? IO<T>::ld1(A + n0 * p.sa_l) : 1.f;
+    *reinterpret_cast<float4*>(ws2.S + (line * p.nb + t) * p.D + c) = make_float4(l[0], l[1], l[2], l[3]);
+    if (c == 0) ws2.C[line * p.nb + t] = r;  // r_t[0] = a_t[1] ... a_t[15]
+    (void)a0;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) exact_bwd_carry(const Params p, const ExactWs ws2) {
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int tph = (int)p.D / 4;
+  const int64_t line = gt / tph;
+  const int c = 4 * (int)(gt % tph);
+  if (line >= p.B * p.H) return;
+  const int64_t b = line / p.H, h = line % p.H;
+  const T* A = (const T*)p.a + b * p.sa_b + h * p.sa_h;
+  float4 mu = make_float4(0.f, 0.f, 0.f, 0.f);  // mu_{nb-1}
+  if (p.mu_in) mu = *reinterpret_cast<const float4*>(p.mu_in + line * p.D + c);
+  float4* S = reinterpret_cast<float4*>(ws2.S + line * p.nb * p.D + c);
+  const float* R = ws2.C + line * p.nb;
+  const int64_t st = p.D / 4;
+  constexpr int kG = 16;
+  for (int64_t t1 = p.nb - 1; t1 >= 0; t1 -= kG) {  // blocks t1, t1-1, ... (groups of 16)
+    float rg[kG], ag[kG];
+    float4 eg[kG];
+#pragma unroll
+    for (int j = 0; j < kG; ++j) {
+      const int64_t t = t1 - j;
+      const bool ok = t >= 0;
+      rg[j] = ok ? R[t] : 0.f;
+      eg[j] = ok ? S[t * st] : make_float4(0.f, 0.f, 0.f, 0.f);
+      ag[j] = ok ? IO<T>::ld1(A + t * kEll * p.sa_l) : 0.f;  // a_t[0] (t * 16 < L)
+    }
+#pragma unroll
+    for (int j = 0; j < kG; ++j) {
+      const int64_t t = t1 - j;
+      if (t >= 0) {
+        S[t * st] = mu;  // mu_t for block t
+        const float r = rg[j], a0 = ag[j];
+        const float4 e = eg[j];  // lambda_t[0] = l_t[0] + r_t[0] mu_t; mu_{t-1} = a_t[0] lambda_t[0]
+        mu = make_float4(a0 * fmaf(r, mu.x, e.x), a0 * fmaf(r, mu.y, e.y), a0 * fmaf(r, mu.z, e.z),
+                         a0 * fmaf(r, mu.w, e.w));
+      }
+    }
+  }
+  if (p.mu_out) *reinterpret_cast<float4*>(p.mu_out + line * p.D + c) = mu;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) exact_bwd_out(const Params p, const ExactWs ws, const ExactWs ws2) {
+  using V = VecN<T, 4>;
+  using io = IO<T>;
+  const int tph = (int)p.D / 4, hpc = 128 / tph;
+  const int hh = threadIdx.x / tph, c = 4 * (threadIdx.x % tph);
+  const int lane = threadIdx.x & 31;
+  const int64_t b = blockIdx.z, h0 = (int64_t)blockIdx.y * hpc + hh;
+  const bool act = h0 < p.H;
+  const int64_t h = act ? h0 : p.H - 1;
+  __shared__ float4 slam[kEll][128];
+  const int64_t t_lo = (int64_t)blockIdx.x * p.K, t_hi = min(t_lo + p.K, p.nb);
+  const T* A = (const T*)p.a + b * p.sa_b + h * p.sa_h;
+  T* dA = (T*)p.da + b * p.sa_b + h * p.sa_h;
+  const int64_t xo = b * p.sx_b + h * p.sx_h + c;
+  const int64_t line = b * p.H + h;
+  for (int64_t t = t_lo; t < t_hi; ++t) {
+    const int64_t n0 = t * kEll;
+    const int lim = (p.L - n0 < kEll) ? (int)(p.L - n0) : kEll;
+    float acur[kEll];
+#pragma unroll
+    for (int i = 0; i < kEll; ++i) acur[i] = i < lim ? io::ld1(A + (n0 + i) * p.sa_l) : 1.f;
+    const float4 m4 = *reinterpret_cast<const float4*>(ws2.S + (line * p.nb + t) * p.D + c);
+    const float mu[4] = {m4.x, m4.y, m4.z, m4.w};
+    // lambda_t[i] = l_t[i] + r_t[i] mu_t, in reverse, staged in shared memory
+    {
+      float l[4], r = 1.f;
+#pragma unroll
+      for (int i = kEll - 1; i >= 0; --i) {
+        float g[4];
+        V::to_f(i < lim ? V::ld((const T*)p.dx + xo + (n0 + i) * p.sx_l) : V::zero(), g);
+        if (i < kEll - 1) r *= acur[i + 1];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) l[e] = (i == kEll - 1) ? g[e] : fmaf(acur[i + 1 < kEll ? i + 1 : i], l[e], g[e]);
+        slam[i][threadIdx.x] = make_float4(fmaf(r, mu[0], l[0]), fmaf(r, mu[1], l[1]), fmaf(r, mu[2], l[2]),
+                                           fmaf(r, mu[3], l[3]));
+      }
+    }
+    // forward: x_{n-1} = w[i-1] + g[i-1] s_{t-1}; du = lambda; da = sum_c lambda x_{n-1}
+    float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (t > 0) s4 = *reinterpret_cast<const float4*>(ws.S + (line * p.nb + t - 1) * p.D + c);
+    else if (p.carry_in) s4 = *reinterpret_cast<const float4*>(p.carry_in + line * p.D + c);
+    const float sp[4] = {s4.x, s4.y, s4.z, s4.w};
+    float part[kEll];
+    float xprev[4] = {sp[0], sp[1], sp[2], sp[3]};  // x_{n0-1} = s_{t-1}
+    float w[4], g = 1.f;
+#pragma unroll
+    for (int i = 0; i < kEll; ++i) {
+      const float4 l4 = slam[i][threadIdx.x];
+      const float lam[4] = {l4.x, l4.y, l4.z, l4.w};
+      float d = lam[0] * xprev[0];
+#pragma unroll
+      for (int e = 1; e < 4; ++e) d = fmaf(lam[e], xprev[e], d);
+      part[i] = d;
+      if (act && i < lim) V::st((T*)p.du + xo + (n0 + i) * p.sx_l, lam);
+      float u[4];
+      V::to_f(i < lim ? V::ld((const T*)p.u + xo + (n0 + i) * p.sx_l) : V::zero(), u);
+      g *= acur[i];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        w[e] = (i == 0) ? u[e] : fmaf(acur[i], w[e], u[e]);
+        xprev[e] = fmaf(g, sp[e], w[e]);
+      }
+    }
+    int tok = 0;
+    switch (tph) {  // deterministic reduction over the head's lanes
+      case 4: GroupReduce<2, kEll>::run(part, lane, tok); break;
+      case 8: GroupReduce<4, kEll>::run(part, lane, tok); break;
+      case 16: GroupReduce<8, kEll>::run(part, lane, tok); break;
+      default: GroupReduce<16, kEll>::run(part, lane, tok); break;
+    }
+    const int nv = tph >= kEll ? 1 : kEll / tph;
+    const bool owner = (tph < 32) || ((lane & 1) == 0);
+    if (act && owner) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j < nv && tok + j < lim) io::st1(dA + (n0 + tok + j) * p.sa_l, part[j]);
+    }
+  }
+}
+
 cudaError_t launch_exact(bool bf16, Params p, void* workspace, cudaStream_t st, int sms) {
   auto cdiv = [](int64_t x, int64_t y) { return (x + y - 1) / y; };
   ExactWs ws;
@@ -1171,6 +1340,39 @@ cudaError_t launch_exact(bool bf16, Params p, void* workspace, cudaStream_t st, 
   exact_carry<<<gc, 128, 0, st>>>(p, ws);
   if (bf16) exact_out<__nv_bfloat16><<<grid, 128, 0, st>>>(p, ws);
   else exact_out<float><<<grid, 128, 0, st>>>(p, ws);
+  return cudaGetLastError();
+}
+
+// workspace: forward S, C then backward S2, C2 (2 x swr_exact_workspace_bytes)
+cudaError_t launch_exact_bwd(bool bf16, Params p, void* workspace, cudaStream_t st, int sms) {
+  auto cdiv = [](int64_t x, int64_t y) { return (x + y - 1) / y; };
+  const int64_t nS = p.B * p.H * p.nb * p.D, nC = (p.B * p.H * p.nb + 3) / 4 * 4;  // keep S2 16-byte aligned
+  ExactWs ws, ws2;
+  ws.S = reinterpret_cast<float*>(workspace);
+  ws.C = ws.S + nS;
+  ws2.S = ws.C + nC;
+  ws2.C = ws2.S + nS;
+  const int64_t hpc = 128 / (p.D / 4);
+  const int64_t cols = p.B * cdiv(p.H, hpc);
+  const int64_t want = std::max<int64_t>(1, ((int64_t)sms * 8) / std::max<int64_t>(cols, 1));
+  p.K = std::min<int64_t>(std::max<int64_t>(cdiv(p.nb, want), 1), p.nb);
+  const dim3 grid((unsigned)cdiv(p.nb, p.K), (unsigned)cdiv(p.H, hpc), (unsigned)p.B);
+  const unsigned gc = (unsigned)cdiv(p.B * p.H * (p.D / 4), 128);
+  Params pf = p;
+  pf.carry_out = nullptr;
+  if (bf16) {
+    exact_local<__nv_bfloat16><<<grid, 128, 0, st>>>(pf, ws);
+    exact_carry<<<gc, 128, 0, st>>>(pf, ws);
+    exact_bwd_local<__nv_bfloat16><<<grid, 128, 0, st>>>(p, ws2);
+    exact_bwd_carry<__nv_bfloat16><<<gc, 128, 0, st>>>(p, ws2);
+    exact_bwd_out<__nv_bfloat16><<<grid, 128, 0, st>>>(p, ws, ws2);
+  } else {
+    exact_local<float><<<grid, 128, 0, st>>>(pf, ws);
+    exact_carry<<<gc, 128, 0, st>>>(pf, ws);
+    exact_bwd_local<float><<<grid, 128, 0, st>>>(p, ws2);
+    exact_bwd_carry<float><<<gc, 128, 0, st>>>(p, ws2);
+    exact_bwd_out<float><<<grid, 128, 0, st>>>(p, ws, ws2);
+  }
   return cudaGetLastError();
 }
 

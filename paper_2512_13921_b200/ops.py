@@ -186,6 +186,23 @@ def swr_exact_fwd(u, a, carry_in=None, return_carry=False):
     return (x, co) if return_carry else x
 
 
+def swr_exact_bwd(u, a, dx, carry_in=None, mu_in=None):
+    """Reverse mode of swr_exact_fwd.  Returns (du, da, mu_out)."""
+    u, dx = _prep(u, dx)
+    dt = _dtype(u, a, dx)
+    du = _like(u)
+    da = _like(a)
+    ci, mi = _carry(carry_in, u), _carry(mu_in, u)
+    mo = _new_carry(u)
+    shape = _shape(u, a)
+    nbytes = 2 * _lib.swr_exact_workspace_bytes(shape)
+    ws = torch.empty(max(nbytes, 16) // 4, dtype=torch.float32, device=u.device)
+    with torch.cuda.device(u.device):
+        _lib.swr_exact_bwd(_ptr(u), _ptr(a), _ptr(dx), _ptr(du), _ptr(da), _ptr(ci), _ptr(mi), _ptr(mo),
+                           _ptr(ws), nbytes, shape, dt, _stream(u))
+    return du, da, mo
+
+
 # ---------------------------------------------------------------------------
 # recurrence-mode decoding (include/swr.h swr_decode_step; SURVEY 8(f) NEXT-3)
 # ---------------------------------------------------------------------------

@@ -57,3 +57,21 @@ def test_exact_empty(P):
     ci = torch.randn(2, 3, 16, device="cuda")
     x, co = P.swr_exact_fwd(u, a, carry_in=ci, return_carry=True)
     assert x.shape == u.shape and torch.count_nonzero(co) == 0
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("D", [16, 32, 128])
+@pytest.mark.parametrize("B,L,H", [(2, 16, 3), (1, 77, 5), (2, 1000, 16), (1, 4096, 2)])
+@pytest.mark.parametrize("carry", [False, True])
+def test_exact_backward_matches_oracle(P, dtype, D, B, L, H, carry):
+    inp = swr_inputs(B, L, H, D, dtype=dtype, seed=800 + L + D, carry=carry)
+    u, a, G = inp["u"].cuda(), inp["a"].cuda(), inp["G"].cuda()
+    ci = inp["carry_in"].cuda() if carry else None
+    mi = inp["mu_in"].cuda() if carry else None
+    du, da, mo = P.swr_exact_bwd(u, a, G, carry_in=ci, mu_in=mi)
+    torch.cuda.synchronize()
+    rdu, rda, rmo = oracle.linrec_bwd(to64(inp["u"]), to64(inp["a"]), to64(inp["G"]),
+                                      to64(inp.get("carry_in")), to64(inp.get("mu_in")))
+    assert normwise(du, rdu) <= TOL[dtype]
+    assert normwise(da, rda) <= TOL[dtype]
+    assert normwise(mo, rmo) <= TOL[dtype]

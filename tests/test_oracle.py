@@ -450,3 +450,32 @@ def test_linrec_constant_decay_closed_form_and_two_block_agreement():
     # on the first two blocks the jagged window is the full recurrence
     u, a, _, _, _ = rand_problem(1, 2 * ELL, 3, 4, seed=5)
     assert normwise(oracle.linrec_fwd(u, a)[0], oracle.swr_fwd(u, a)) < 1e-12
+
+
+def test_linrec_backward_matches_finite_differences():
+    """d/d(u, a, carry_in) of <G, x> + <mu_in, x_{L-1}> by central differences."""
+    u, a, G, c, m = rand_problem(1, 37, 2, 3, seed=77, lo=0.3, hi=0.95)
+
+    def loss(u_, a_, c_):
+        x, last = oracle.linrec_fwd(u_, a_, carry_in=c_)
+        return np.sum(G * x) + np.sum(m * last)
+
+    du, da, mo = oracle.linrec_bwd(u, a, G, carry_in=c, mu_in=m)
+    eps = 1e-6
+    r = np.random.default_rng(3)
+    for _ in range(12):
+        idx = tuple(r.integers(0, s) for s in u.shape)
+        up, um = u.copy(), u.copy()
+        up[idx] += eps
+        um[idx] -= eps
+        assert abs((loss(up, a, c) - loss(um, a, c)) / (2 * eps) - du[idx]) < 1e-6
+        ia = tuple(r.integers(0, s) for s in a.shape)
+        ap, am = a.copy(), a.copy()
+        ap[ia] += eps
+        am[ia] -= eps
+        assert abs((loss(u, ap, c) - loss(u, am, c)) / (2 * eps) - da[ia]) < 1e-6
+        ic = tuple(r.integers(0, s) for s in c.shape)
+        cp, cm = c.copy(), c.copy()
+        cp[ic] += eps
+        cm[ic] -= eps
+        assert abs((loss(u, a, cp) - loss(u, a, cm)) / (2 * eps) - mo[ic]) < 1e-6

@@ -20,8 +20,11 @@ for (B, L, H, D, dt) in [(8, 4096, 16, 128, torch.bfloat16), (2, 32768, 16, 128,
     g = {k: v.cuda() for k, v in swr_inputs(B, L, H, D, dtype=dt, seed=1).items()}
     te = t(lambda: P.swr_exact_fwd(g["u"], g["a"]))
     tt = t(lambda: P.swr_fwd(g["u"], g["a"]))
+    tbe = t(lambda: P.swr_exact_bwd(g["u"], g["a"], g["G"]))
+    tbt = t(lambda: P.swr_bwd(g["u"], g["a"], g["G"]))
     path = {1: "ffma", 2: "tc"}[P.last_path()]
     e = g["u"].element_size()
     n = B * L * H
     print(f"B={B} L={L} H={H} d={D} {str(dt)[6:]}: exact {te:.0f} us ({n * (2 * D + 1) * e / te / 1e3:.0f} GB/s "
-          f"algorithmic), B2P swr_fwd [{path}] {tt:.0f} us -> exact/B2P {te / tt:.2f}x", flush=True)
+          f"algorithmic), B2P swr_fwd [{path}] {tt:.0f} us -> exact/B2P {te / tt:.2f}x; backward exact {tbe:.0f} us "
+          f"vs B2P {tbt:.0f} us ({tbe / tbt:.2f}x)", flush=True)

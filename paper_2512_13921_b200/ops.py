@@ -203,6 +203,24 @@ def swr_exact_bwd(u, a, dx, carry_in=None, mu_in=None):
     return du, da, mo
 
 
+class LinRecFunction(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, u, a, carry_in):
+        ctx.save_for_backward(u, a, carry_in)
+        return swr_exact_fwd(u, a, carry_in)
+
+    @staticmethod
+    def backward(ctx, dx):
+        u, a, carry_in = ctx.saved_tensors
+        du, da, mu_out = swr_exact_bwd(u, a, dx.to(u.dtype), carry_in)
+        return du, da, (mu_out if carry_in is not None else None)
+
+
+def swr_exact(u, a, carry_in=None):
+    """Differentiable untruncated recurrence (Eq. 2.1), for comparison with swr()."""
+    return LinRecFunction.apply(u, a, carry_in)
+
+
 # ---------------------------------------------------------------------------
 # recurrence-mode decoding (include/swr.h swr_decode_step; SURVEY 8(f) NEXT-3)
 # ---------------------------------------------------------------------------

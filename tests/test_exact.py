@@ -75,3 +75,15 @@ def test_exact_backward_matches_oracle(P, dtype, D, B, L, H, carry):
     assert normwise(du, rdu) <= TOL[dtype]
     assert normwise(da, rda) <= TOL[dtype]
     assert normwise(mo, rmo) <= TOL[dtype]
+
+
+def test_exact_autograd(P):
+    inp = swr_inputs(2, 100, 3, 16, dtype=torch.float32, seed=5, carry=True)
+    u = inp["u"].cuda().requires_grad_()
+    a = inp["a"].cuda().requires_grad_()
+    c = inp["carry_in"].cuda().requires_grad_()
+    G = inp["G"].cuda()
+    x = P.swr_exact(u, a, c)
+    (x * G).sum().backward()
+    du, da, mo = P.swr_exact_bwd(u.detach(), a.detach(), G, carry_in=c.detach())
+    assert torch.equal(u.grad, du) and torch.equal(a.grad, da) and torch.equal(c.grad, mo)

@@ -1162,7 +1162,7 @@ __global__ void __launch_bounds__(128) exact_out(const Params p, const ExactWs w
 // solve, r_t[i] = a_t[i+1]...a_t[15] and mu_t = a_{t+1}[0] lambda_{t+1}[0]; the
 // reverse carrier chain is mu_{t-1} = a_t[0] (l_t[0] + r_t[0] mu_t).  Stages:
 // exact_local + exact_carry (forward carriers s_t, needed for x_{n-1}),
-// exact_bwd_local (E_t = l_t[0] into S2, R_t = r_t[0] a_t[0] into C2),
+// exact_bwd_local (E_t = l_t[0] into S2, R_t = r_t[0] into C2),
 // exact_bwd_carry (mu_t into S2), exact_bwd_out (du, da).
 template <typename T>
 __global__ void __launch_bounds__(128) exact_bwd_local(const Params p, const ExactWs ws2) {
@@ -1194,11 +1194,8 @@ __global__ void __launch_bounds__(128) exact_bwd_local(const Params p, const Exa
         for (int e = 0; e < 4; ++e) l[e] = fmaf(an, l[e], g[e]);
       }
     }
-    const int64_t n0 = t * kEll;
-    const float a0 = n0 < p.L ? IO<T>::ld1(A + n0 * p.sa_l) : 1.f;
     *reinterpret_cast<float4*>(ws2.S + (line * p.nb + t) * p.D + c) = make_float4(l[0], l[1], l[2], l[3]);
     if (c == 0) ws2.C[line * p.nb + t] = r;  // r_t[0] = a_t[1] ... a_t[15]
-    (void)a0;
   }
 }
 
@@ -1276,7 +1273,7 @@ __global__ void __launch_bounds__(128) exact_bwd_out(const Params p, const Exact
         V::to_f(i < lim ? V::ld((const T*)p.dx + xo + (n0 + i) * p.sx_l) : V::zero(), g);
         if (i < kEll - 1) r *= acur[i + 1];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) l[e] = (i == kEll - 1) ? g[e] : fmaf(acur[i + 1 < kEll ? i + 1 : i], l[e], g[e]);
+        for (int e = 0; e < 4; ++e) l[e] = (i == kEll - 1) ? g[e] : fmaf(acur[i + 1 < kEll ? i + 1 : i], l[e], g[e]);  // a_t[i+1]
         slam[i][threadIdx.x] = make_float4(fmaf(r, mu[0], l[0]), fmaf(r, mu[1], l[1]), fmaf(r, mu[2], l[2]),
                                            fmaf(r, mu[3], l[3]));
       }

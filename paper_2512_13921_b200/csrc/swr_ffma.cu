@@ -1378,12 +1378,19 @@ cudaError_t launch_exact_bwd(bool bf16, Params p, void* workspace, cudaStream_t 
 // ---------------------------------------------------------------------------
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+#ifndef SWR_FFMA_FWD_CHUNKS
+#define SWR_FFMA_FWD_CHUNKS 2  // SWR: target chunks per SM and (b, head-group) column (8: d=16 13% slower)
+#endif
+#ifndef SWR_FFMA_MIXF_CHUNKS
+#define SWR_FFMA_MIXF_CHUNKS 8  // mixer (one CTA per SM: 4 is 65% slower)
+#endif
 // forward (SWR and mixer): the streamed kernel, 16 bytes of channels per thread
 template <typename T, bool MIX>
 static cudaError_t launch_fwd_stream(Params p, cudaStream_t st, int sms) {
   const int64_t hpc = 128 / (p.D / Vec16<T>::N);
   const int64_t cols = p.B * ceil_div(p.H, hpc);
-  const int64_t want_chunks = std::max<int64_t>(1, ((int64_t)sms * 8) / std::max<int64_t>(cols, 1));
+  const int64_t per_sm = MIX ? SWR_FFMA_MIXF_CHUNKS : SWR_FFMA_FWD_CHUNKS;
+  const int64_t want_chunks = std::max<int64_t>(1, ((int64_t)sms * per_sm) / std::max<int64_t>(cols, 1));
   int64_t K = std::min<int64_t>(std::max<int64_t>(ceil_div(p.nb, want_chunks), 4), p.nb);
   p.K = K;
   dim3 grid((unsigned)ceil_div(p.nb, K), (unsigned)ceil_div(p.H, hpc), (unsigned)p.B);

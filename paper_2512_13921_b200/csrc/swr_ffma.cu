@@ -1417,6 +1417,9 @@ static cudaError_t launch_tph(Params p, cudaStream_t st, int sms) {
   return cudaGetLastError();
 }
 
+#ifndef SWR_FFMA_BWD_CHUNKS
+#define SWR_FFMA_BWD_CHUNKS 8  // backward: target chunks per SM and (b, head-group) column
+#endif
 template <typename T, int VC, int TPH, bool MIX>
 static cudaError_t launch_bwd_vec(Params p, cudaStream_t st, int sms) {
   constexpr int HPC = 128 / TPH;
@@ -1426,7 +1429,7 @@ static cudaError_t launch_bwd_vec(Params p, cudaStream_t st, int sms) {
     if (e != cudaSuccess) return e;
   }
   const int64_t cols = p.B * ceil_div(p.H, HPC);
-  const int64_t want_chunks = std::max<int64_t>(1, ((int64_t)sms * 8) / std::max<int64_t>(cols, 1));
+  const int64_t want_chunks = std::max<int64_t>(1, ((int64_t)sms * SWR_FFMA_BWD_CHUNKS) / std::max<int64_t>(cols, 1));
   int64_t K = std::max<int64_t>(ceil_div(p.nb, want_chunks), 8);
   K = std::min<int64_t>(K, p.nb);
   p.K = K;

@@ -208,6 +208,14 @@ SWR_API swr_status swr_exact_bwd(const void* u, const void* a, const void* dx, v
                          void* workspace, int64_t workspace_bytes, swr_shape s, swr_dtype dt,
                          void* stream);
 
+/* Uniform-window recurrence (Sec. uniform_window P:1104-1113,
+ * Eq. banded_L): x = (I + AZ + ... + (AZ)^{k-1}) u, i.e. every token sees its k most
+ * recent inputs, x_n = sum_{j<k} (a_{n-j+1} ... a_n) u_{n-j}, with no carry.  The
+ * paper's "theoretical baseline" next to the jagged window.  k a power of two in
+ * [1, 32] (else SWR_ERR_SHAPE); u, a, x as in swr_fwd.  CUDA cores, one launch. */
+SWR_API swr_status swr_uniform_fwd(const void* u, const void* a, void* x, int k, swr_shape s,
+                           swr_dtype dt, void* stream);
+
 /* Human-readable name of a status code (static storage). */
 SWR_API const char* swr_strerror(swr_status st);
 

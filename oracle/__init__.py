@@ -10,4 +10,4 @@ constant-decay closed form, the untruncated recurrence on <= 2 blocks, finite
 differences, the transpose identity, locality, linearity and stitching.
 """
 from .oracle import (ELL, build, linrec_bwd, linrec_fwd, mix_bwd, mix_decode, mix_fwd, swr_bwd, swr_decode,  # noqa: F401
-                     swr_fwd)
+                     swr_fwd, uniform_fwd)

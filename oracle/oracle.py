@@ -196,3 +196,26 @@ def linrec_bwd(u, a, G, carry_in=None, mu_in=None):
         da[:, n] = np.sum(lam * xprev, axis=-1)
     mu_out = a[:, 0, :, None] * lam if L > 0 else np.zeros((B, H, D))
     return du, da, mu_out
+
+
+def uniform_fwd(u, a, k):
+    """Uniform-window recurrence, Eq. banded_L: x = (I + AZ + ... +
+    (AZ)^{k-1}) u, by the paper's early-stopped Kogge-Stone -- log2 k doubling stages
+    X_n <- X_n + A_n X_{n-s}, A_n <- A_n A_{n-s} (s = 1, 2, 4, ...), starting from
+    X = u, A = a, with X_{<0} = 0.  k a power of two.  fp64."""
+    u, a = _f64(u), _f64(a)
+    _check(u, a)
+    if k < 1 or k & (k - 1):
+        raise ValueError("k must be a power of two")
+    X = u.copy()
+    A = a.copy()
+    s = 1
+    while s < k:
+        Xs = np.zeros_like(X)
+        As = np.zeros_like(A)
+        Xs[:, s:] = X[:, :-s] if s < X.shape[1] else 0.0
+        As[:, s:] = A[:, :-s] if s < A.shape[1] else 0.0
+        X = X + A[..., None] * Xs
+        A = A * As
+        s *= 2
+    return X

@@ -19,7 +19,8 @@ SWR_PATH_AUTO, SWR_PATH_FFMA, SWR_PATH_TC = 0, 1, 2
 EXPORTS = ("swr_fwd", "swr_bwd", "phalanx_mix", "phalanx_mix_bwd", "swr_strerror",
            "swr_last_cuda_error", "swr_set_path", "swr_launch_count", "swr_last_path",
            "swr_set_trace", "swr_decode_step", "phalanx_mix_decode_step",
-           "swr_exact_workspace_bytes", "swr_exact_fwd", "swr_exact_bwd")
+           "swr_exact_workspace_bytes", "swr_exact_fwd", "swr_exact_bwd",
+           "swr_uniform_fwd")
 
 
 class SwrError(RuntimeError):
@@ -53,10 +54,11 @@ def _load():
     lib.phalanx_mix_decode_step.argtypes = [P, P, P, P, P, P, P, P, ctypes.c_int64, S, I, P]
     lib.swr_exact_fwd.argtypes = [P, P, P, P, P, P, ctypes.c_int64, S, I, P]
     lib.swr_exact_bwd.argtypes = [P, P, P, P, P, P, P, P, P, ctypes.c_int64, S, I, P]
+    lib.swr_uniform_fwd.argtypes = [P, P, P, I, S, I, P]
     lib.swr_exact_workspace_bytes.argtypes = [S]
     lib.swr_exact_workspace_bytes.restype = ctypes.c_int64
     for f in ("swr_fwd", "swr_bwd", "phalanx_mix", "phalanx_mix_bwd", "swr_decode_step",
-              "phalanx_mix_decode_step", "swr_exact_fwd", "swr_exact_bwd"):
+              "phalanx_mix_decode_step", "swr_exact_fwd", "swr_exact_bwd", "swr_uniform_fwd"):
         getattr(lib, f).restype = I
     lib.swr_strerror.argtypes = [I]
     lib.swr_strerror.restype = ctypes.c_char_p
@@ -143,3 +145,7 @@ def swr_exact_bwd(u, a, dx, du, da, carry_in, mu_in, mu_out, workspace, workspac
                   stream):
     _check(_lib.swr_exact_bwd(u, a, dx, du, da, carry_in, mu_in, mu_out, workspace, workspace_bytes,
                               shape, dtype, stream), "swr_exact_bwd")
+
+
+def swr_uniform_fwd(u, a, x, k, shape, dtype, stream):
+    _check(_lib.swr_uniform_fwd(u, a, x, k, shape, dtype, stream), "swr_uniform_fwd")

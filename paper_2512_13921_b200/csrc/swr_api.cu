@@ -17,6 +17,7 @@ bool tc_supported(int op, bool bf16, const Params& p);
 cudaError_t launch_decode(bool mix, bool bf16, const DecParams& p, cudaStream_t st);
 cudaError_t launch_exact(bool bf16, Params p, void* workspace, cudaStream_t st, int sms);
 cudaError_t launch_exact_bwd(bool bf16, Params p, void* workspace, cudaStream_t st, int sms);
+cudaError_t launch_uniform(bool bf16, Params p, int k, cudaStream_t st, int sms);
 }  // namespace swr
 
 namespace {
@@ -354,6 +355,28 @@ swr_status swr_exact_bwd(const void* u, const void* a, const void* dx, void* du,
   cudaError_t e = swr::launch_exact_bwd(dt == SWR_BF16, p, workspace, cs, sms);
   if (e != cudaSuccess) return cuda_fail(e);
   g_launches += 5;
+  g_last_path = SWR_PATH_FFMA;
+  return SWR_OK;
+}
+
+swr_status swr_uniform_fwd(const void* u, const void* a, void* x, int k, swr_shape s, swr_dtype dt,
+                           void* stream) {
+  const void* dt_[] = {u, x};
+  const void* at_[] = {a};
+  swr_status st = validate(s, dt, dt_, 2, at_, 1, nullptr, 0);
+  if (st != SWR_OK) return st;
+  if (k < 1 || k > 32 || (k & (k - 1)) != 0) return SWR_ERR_SHAPE;
+  if (s.B == 0 || s.H == 0 || s.L == 0) return SWR_OK;
+  int sms = 0;
+  st = device_info(&sms);
+  if (st != SWR_OK) return st;
+  swr::Params p = make_params(s);
+  p.u = u;
+  p.a = a;
+  p.x = x;
+  cudaError_t e = swr::launch_uniform(dt == SWR_BF16, p, k, reinterpret_cast<cudaStream_t>(stream), sms);
+  if (e != cudaSuccess) return cuda_fail(e);
+  g_launches += 1;
   g_last_path = SWR_PATH_FFMA;
   return SWR_OK;
 }

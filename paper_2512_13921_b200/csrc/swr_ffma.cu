@@ -1374,6 +1374,79 @@ cudaError_t launch_exact_bwd(bool bf16, Params p, void* workspace, cudaStream_t 
 }
 
 // ---------------------------------------------------------------------------
+// uniform-window recurrence (Sec. uniform_window P:1104-1113,
+// Eq. banded_L): x~ = (I + AZ + ... + (AZ)^{k-1}) u, every token sees the k most
+// recent inputs, x~_n = sum_{j<k} (a_{n-j+1} ... a_n) u_{n-j} (u_{<0} = 0).  The
+// paper reaches it by stopping Kogge-Stone after log2 k stages; a thread that
+// streams tokens evaluates the same band by Horner over a register ring of the
+// last k (u, a) pairs: k FMAs per channel and token, inputs read once (plus a
+// (k-1)-token halo per chunk).
+// ---------------------------------------------------------------------------
+template <typename T, int KW>
+__global__ void __launch_bounds__(128) uniform_fwd(const Params p) {
+  using V = VecN<T, 4>;
+  const int tph = (int)p.D / 4, hpc = 128 / tph;
+  const int hh = threadIdx.x / tph, c = 4 * (threadIdx.x % tph);
+  const int64_t b = blockIdx.z, h = (int64_t)blockIdx.y * hpc + hh;
+  if (h >= p.H) return;
+  const int64_t n_lo = (int64_t)blockIdx.x * p.K, n_hi = min(n_lo + p.K, p.L);  // K: tokens per chunk
+  const T* A = (const T*)p.a + b * p.sa_b + h * p.sa_h;
+  const int64_t xo = b * p.sx_b + h * p.sx_h + c;
+  float ur[KW][4], ar[KW];
+#pragma unroll
+  for (int j = 0; j < KW; ++j) {  // slot j <- token n_lo - KW + j (slot = token mod KW)
+    const int64_t n = n_lo - KW + j;
+    const bool valid = n >= 0;
+    ar[j] = valid ? IO<T>::ld1(A + n * p.sa_l) : 1.f;
+    V::to_f(valid ? V::ld((const T*)p.u + xo + n * p.sx_l) : V::zero(), ur[j]);
+  }
+  for (int64_t n0 = n_lo; n0 < n_hi; n0 += KW) {
+#pragma unroll
+    for (int i = 0; i < KW; ++i) {
+      const int64_t n = n0 + i;
+      const bool valid = n < n_hi;
+      ar[i] = valid ? IO<T>::ld1(A + n * p.sa_l) : 1.f;
+      V::to_f(valid ? V::ld((const T*)p.u + xo + n * p.sx_l) : V::zero(), ur[i]);
+      float x[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) x[e] = ur[(i + 1) % KW][e];  // oldest token of the window
+#pragma unroll
+      for (int m = 2; m <= KW; ++m) {
+        const int sl = (i + m) % KW;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) x[e] = fmaf(ar[sl], x[e], ur[sl][e]);
+      }
+      if (valid) V::st((T*)p.x + xo + n * p.sx_l, x);
+    }
+  }
+}
+
+cudaError_t launch_uniform(bool bf16, Params p, int k, cudaStream_t st, int sms) {
+  auto cdiv = [](int64_t x, int64_t y) { return (x + y - 1) / y; };
+  const int64_t hpc = 128 / (p.D / 4);
+  const int64_t cols = p.B * cdiv(p.H, hpc);
+  const int64_t want = std::max<int64_t>(1, ((int64_t)sms * 4) / std::max<int64_t>(cols, 1));
+  p.K = std::max<int64_t>(cdiv(cdiv(p.L, want), 64) * 64, 64);  // tokens per chunk, a multiple of 64 >= k
+  const dim3 grid((unsigned)cdiv(p.L, p.K), (unsigned)cdiv(p.H, hpc), (unsigned)p.B);
+#define SWR_UNIFORM_CASE(KW)                                                     \
+  case KW:                                                                       \
+    if (bf16) uniform_fwd<__nv_bfloat16, KW><<<grid, 128, 0, st>>>(p);           \
+    else uniform_fwd<float, KW><<<grid, 128, 0, st>>>(p);                        \
+    break;
+  switch (k) {
+    SWR_UNIFORM_CASE(1)
+    SWR_UNIFORM_CASE(2)
+    SWR_UNIFORM_CASE(4)
+    SWR_UNIFORM_CASE(8)
+    SWR_UNIFORM_CASE(16)
+    SWR_UNIFORM_CASE(32)
+    default: return cudaErrorInvalidValue;
+  }
+#undef SWR_UNIFORM_CASE
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

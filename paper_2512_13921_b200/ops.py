@@ -221,6 +221,16 @@ def swr_exact(u, a, carry_in=None):
     return LinRecFunction.apply(u, a, carry_in)
 
 
+def swr_uniform_fwd(u, a, k):
+    """Uniform window of the k most recent tokens (Eq. banded_L), no carry."""
+    (u,) = _prep(u)
+    dt = _dtype(u, a)
+    x = _like(u)
+    with torch.cuda.device(u.device):
+        _lib.swr_uniform_fwd(_ptr(u), _ptr(a), _ptr(x), int(k), _shape(u, a), dt, _stream(u))
+    return x
+
+
 # ---------------------------------------------------------------------------
 # recurrence-mode decoding (include/swr.h swr_decode_step; SURVEY 8(f) NEXT-3)
 # ---------------------------------------------------------------------------

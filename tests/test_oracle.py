@@ -479,3 +479,24 @@ def test_linrec_backward_matches_finite_differences():
         cp[ic] += eps
         cm[ic] -= eps
         assert abs((loss(u, a, cp) - loss(u, a, cm)) / (2 * eps) - mo[ic]) < 1e-6
+
+
+# --------------------------------------------------------------------------
+# uniform window (Eq. banded_L)
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("k", [1, 2, 4, 8, 16, 32])
+def test_uniform_equals_dense_banded_operator(k):
+    """Early-stopped Kogge-Stone == I + AZ + ... + (AZ)^{k-1} assembled entrywise."""
+    u, a, _, _, _ = rand_problem(2, 45, 2, 3, seed=900 + k)
+    x = oracle.uniform_fwd(u, a, k)
+    for b in range(2):
+        for h in range(2):
+            full = dense_full(a[b, :, h])
+            band = np.tril(full) - np.tril(full, -k)  # lags 0 .. k-1
+            assert normwise(x[b, :, h], band @ u[b, :, h]) < 1e-12
+
+
+def test_uniform_limits():
+    u, a, _, _, _ = rand_problem(1, 20, 2, 3, seed=4)
+    assert np.array_equal(oracle.uniform_fwd(u, a, 1), u)
+    assert normwise(oracle.uniform_fwd(u, a, 32), oracle.linrec_fwd(u, a)[0]) < 1e-12

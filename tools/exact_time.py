@@ -1,4 +1,4 @@
-"""What B2P's truncation saves: the exact full-range recurrence (swr_exact_fwd,
+"""What B2P's truncation saves (and the uniform window k = 16 beside it): the exact full-range recurrence (swr_exact_fwd,
 Alg. 2's three stages) against the truncated B2P forward (swr_fwd) at the layer
 shape, each after an L2 flush (CUDA events, median of 10)."""
 import os, sys
@@ -23,8 +23,9 @@ for (B, L, H, D, dt) in [(8, 4096, 16, 128, torch.bfloat16), (2, 32768, 16, 128,
     tbe = t(lambda: P.swr_exact_bwd(g["u"], g["a"], g["G"]))
     tbt = t(lambda: P.swr_bwd(g["u"], g["a"], g["G"]))
     path = {1: "ffma", 2: "tc"}[P.last_path()]
+    tu = t(lambda: P.swr_uniform_fwd(g["u"], g["a"], 16))
     e = g["u"].element_size()
     n = B * L * H
     print(f"B={B} L={L} H={H} d={D} {str(dt)[6:]}: exact {te:.0f} us ({n * (2 * D + 1) * e / te / 1e3:.0f} GB/s "
           f"algorithmic), B2P swr_fwd [{path}] {tt:.0f} us -> exact/B2P {te / tt:.2f}x; backward exact {tbe:.0f} us "
-          f"vs B2P {tbt:.0f} us ({tbe / tbt:.2f}x)", flush=True)
+          f"vs B2P {tbt:.0f} us ({tbe / tbt:.2f}x); uniform k=16 fwd {tu:.0f} us", flush=True)

@@ -7,7 +7,10 @@ or execute anything under ``oracle/``.  The product package
 
 Pinned by ``tests/test_oracle.py`` against the dense jagged operator, the
 constant-decay closed form, the untruncated recurrence on <= 2 blocks, finite
-differences, the transpose identity, locality, linearity and stitching.
+differences, the transpose identity, locality, linearity and stitching; the
+extensions (``swr_decode``/``mix_decode``, ``linrec_fwd``/``linrec_bwd``,
+``uniform_fwd``) against the entrywise jagged / full / banded operators, the closed
+form and finite differences.
 """
 from .oracle import (ELL, build, linrec_bwd, linrec_fwd, mix_bwd, mix_decode, mix_fwd, swr_bwd, swr_decode,  # noqa: F401
                      swr_fwd, uniform_fwd)

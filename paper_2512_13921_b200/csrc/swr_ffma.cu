@@ -1049,6 +1049,9 @@ cudaError_t launch_decode(bool mix, bool bf16, const DecParams& p, cudaStream_t 
 // Workspace: S [B, H, nb, D] fp32 (v_t, overwritten by s_t), C [B, H, nb] fp32.
 // A thread owns 4 channels; padding past L is u = 0, a = 1 as elsewhere.
 // ---------------------------------------------------------------------------
+#ifndef SWR_EXACT_CHUNKS
+#define SWR_EXACT_CHUNKS 32  // exact mode: chunks per SM and (b, head-group) column (8: 15-20% slower)
+#endif
 struct ExactWs {
   float* S;
   float* C;
@@ -1328,7 +1331,7 @@ cudaError_t launch_exact(bool bf16, Params p, void* workspace, cudaStream_t st, 
   ws.C = ws.S + p.B * p.H * p.nb * p.D;
   const int64_t hpc = 128 / (p.D / 4);
   const int64_t cols = p.B * cdiv(p.H, hpc);
-  const int64_t want = std::max<int64_t>(1, ((int64_t)sms * 8) / std::max<int64_t>(cols, 1));
+  const int64_t want = std::max<int64_t>(1, ((int64_t)sms * SWR_EXACT_CHUNKS) / std::max<int64_t>(cols, 1));
   p.K = std::min<int64_t>(std::max<int64_t>(cdiv(p.nb, want), 1), p.nb);
   const dim3 grid((unsigned)cdiv(p.nb, p.K), (unsigned)cdiv(p.H, hpc), (unsigned)p.B);
   const unsigned gc = (unsigned)cdiv(p.B * p.H * (p.D / 4), 128);
@@ -1351,7 +1354,7 @@ cudaError_t launch_exact_bwd(bool bf16, Params p, void* workspace, cudaStream_t 
   ws2.C = ws2.S + nS;
   const int64_t hpc = 128 / (p.D / 4);
   const int64_t cols = p.B * cdiv(p.H, hpc);
-  const int64_t want = std::max<int64_t>(1, ((int64_t)sms * 8) / std::max<int64_t>(cols, 1));
+  const int64_t want = std::max<int64_t>(1, ((int64_t)sms * SWR_EXACT_CHUNKS) / std::max<int64_t>(cols, 1));
   p.K = std::min<int64_t>(std::max<int64_t>(cdiv(p.nb, want), 1), p.nb);
   const dim3 grid((unsigned)cdiv(p.nb, p.K), (unsigned)cdiv(p.H, hpc), (unsigned)p.B);
   const unsigned gc = (unsigned)cdiv(p.B * p.H * (p.D / 4), 128);

@@ -1410,25 +1410,32 @@ __global__ void __launch_bounds__(128) uniform_fwd(const Params p) {
       const bool valid = n < n_hi;
       ar[i] = valid ? IO<T>::ld1(A + n * p.sa_l) : 1.f;
       V::to_f(valid ? V::ld((const T*)p.u + xo + n * p.sx_l) : V::zero(), ur[i]);
-      float x[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) x[e] = ur[(i + 1) % KW][e];  // oldest token of the window
+      // Horner from the oldest token of the window, on packed fp32x2 FMAs (two
+      // IEEE fmas each: the same bits as scalar fmaf)
+      const int s0 = (i + 1) % KW;
+      float2 x01 = make_float2(ur[s0][0], ur[s0][1]), x23 = make_float2(ur[s0][2], ur[s0][3]);
 #pragma unroll
       for (int m = 2; m <= KW; ++m) {
         const int sl = (i + m) % KW;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) x[e] = fmaf(ar[sl], x[e], ur[sl][e]);
+        const float2 aa = make_float2(ar[sl], ar[sl]);
+        x01 = __ffma2_rn(aa, x01, make_float2(ur[sl][0], ur[sl][1]));
+        x23 = __ffma2_rn(aa, x23, make_float2(ur[sl][2], ur[sl][3]));
       }
+      const float x[4] = {x01.x, x01.y, x23.x, x23.y};
       if (valid) V::st((T*)p.x + xo + n * p.sx_l, x);
     }
   }
 }
 
+#ifndef SWR_UNIFORM_CHUNKS
+#define SWR_UNIFORM_CHUNKS 16  // uniform window, k <= 16: chunks per SM and column (4: k=4 1.7x slower)
+#endif
 cudaError_t launch_uniform(bool bf16, Params p, int k, cudaStream_t st, int sms) {
   auto cdiv = [](int64_t x, int64_t y) { return (x + y - 1) / y; };
   const int64_t hpc = 128 / (p.D / 4);
   const int64_t cols = p.B * cdiv(p.H, hpc);
-  const int64_t want = std::max<int64_t>(1, ((int64_t)sms * 4) / std::max<int64_t>(cols, 1));
+  const int64_t per_sm = k >= 32 ? 4 : SWR_UNIFORM_CHUNKS;  // k = 32: the 32-token ring wants fewer CTAs (16: 10% slower)
+  const int64_t want = std::max<int64_t>(1, ((int64_t)sms * per_sm) / std::max<int64_t>(cols, 1));
   p.K = std::max<int64_t>(cdiv(cdiv(p.L, want), 64) * 64, 64);  // tokens per chunk, a multiple of 64 >= k
   const dim3 grid((unsigned)cdiv(p.L, p.K), (unsigned)cdiv(p.H, hpc), (unsigned)p.B);
 #define SWR_UNIFORM_CASE(KW)                                                     \

@@ -35,15 +35,23 @@
  * Conventions shared by every entry point
  * ------------------------------------------------------------------------
  * Pointers  : DEVICE pointers owned by the caller.  The library never
- *             allocates or frees device memory the caller sees.  Process-global
- *             state: the path selector and launch counter below, and for the
- *             tensor-core kernels (bf16, D = 128) a per-op table of per-SM
- *             item rates that sizes each SM's share of the work (module-static
- *             device arrays; refreshed by an asynchronous device->pinned-host
- *             copy on a library-private stream that waits on the caller's
- *             stream, never blocking it).  Results do not depend on that table
- *             (bit-identical for any split).  Thread-safe.  Up to 256 launches
- *             may be in flight concurrently (per-launch claim slots).
+ *             allocates or frees device memory the caller sees.
+ * State     : no state changes any result.  What the library does keep:
+ *             - per calling thread: the kernel-family selector (swr_set_path)
+ *               and the family of the thread's last call (swr_last_path);
+ *             - a process-wide launch counter (swr_launch_count, diagnostics);
+ *             - for the tensor-core kernels (bf16, D = 128), per device and op,
+ *               a table of per-SM item rates that sizes each SM's share of the
+ *               work (the "weighted split"): module-static device
+ *               arrays, refreshed by an asynchronous device->pinned-host copy on
+ *               a library-private stream that waits on the caller's stream and
+ *               never blocks it, plus one event per claim slot (256 per device)
+ *               marking when a launch's range claims are retired.  A launch
+ *               whose claim slot is still in flight (more than 256 tensor-core
+ *               launches queued) or that is being captured into a CUDA graph
+ *               takes the uniform split instead.  Outputs are bit-identical for
+ *               any split.
+ *             Thread-safe.
  * Layout    : every "d-tensor" (u, x, dx, du, q, k, v, y, dy, dq, dk, dv) is
  *             [B, L, H, D] with D contiguous (stride 1) and element strides
  *             (sx_b, sx_l, sx_h); all d-tensors of one call share those strides.
@@ -68,14 +76,20 @@
  *             (tests/test_graph.py).
  * Validation: done before any launch; on error nothing is launched.
  *   SWR_ERR_NULL   a required pointer is NULL
- *   SWR_ERR_SHAPE  B, L or H < 0, or D not in {16, 32, 64, 128}
+ *   SWR_ERR_SHAPE  B, L or H < 0, D not in {16, 32, 64, 128}, B > 65535 or
+ *                  H > 262140 (grid limits)
  *   SWR_ERR_STRIDE a d-tensor stride is negative or not a multiple of 16 bytes
- *                  (8 bf16 / 4 fp32 elements), or a decay stride is negative
+ *                  (8 bf16 / 4 fp32 elements), a decay stride is negative, or
+ *                  any stride is 0 over a dimension of size > 1 (outputs would
+ *                  overlap)
  *   SWR_ERR_ALIGN  a d-tensor or carry pointer is not 16-byte aligned, or a
  *                  decay pointer is not aligned to its element size
  *   SWR_ERR_DTYPE  unknown dtype
  *   SWR_ERR_CUDA   a CUDA launch/runtime error (see swr_last_cuda_error)
  *   SWR_ERR_ARCH   the current device is not sm_100 (B200)
+ *   SWR_ERR_UNSUPPORTED  SWR_PATH_TC is selected and the call is outside the
+ *                  tensor-core envelope (bf16, D = 128, heads contiguous and
+ *                  16-byte token / batch strides in a) -- no silent fallback
  */
 #ifndef SWR_H_
 #define SWR_H_
@@ -100,15 +114,18 @@ typedef enum {
   SWR_ERR_ALIGN = 4,
   SWR_ERR_DTYPE = 5,
   SWR_ERR_CUDA = 6,
-  SWR_ERR_ARCH = 7
+  SWR_ERR_ARCH = 7,
+  SWR_ERR_UNSUPPORTED = 8
 } swr_status;
 
 typedef enum { SWR_F32 = 0, SWR_BF16 = 1 } swr_dtype;
 
-/* Kernel family used by the entry points (process-global, default AUTO).
+/* Kernel family used by swr_fwd / swr_bwd / phalanx_mix / phalanx_mix_bwd
+ * (per calling thread, default AUTO; the other entry points have one family).
  * SWR_PATH_FFMA: per-thread fp32 recurrences on CUDA cores (any dtype / D).
  * SWR_PATH_TC  : tcgen05 tensor-core Pass I with TMEM accumulators and
- *                TMA-staged tiles (bf16, D == 128 only; other calls use FFMA).
+ *                TMA-staged tiles (bf16, D == 128 only; any other call returns
+ *                SWR_ERR_UNSUPPORTED).
  * SWR_PATH_AUTO: the faster one for the call, as measured. */
 typedef enum { SWR_PATH_AUTO = 0, SWR_PATH_FFMA = 1, SWR_PATH_TC = 2 } swr_path;
 
@@ -222,12 +239,13 @@ SWR_API const char* swr_strerror(swr_status st);
 /* Text of the last CUDA error seen by this thread (static storage, "" if none). */
 SWR_API const char* swr_last_cuda_error(void);
 
-/* Select the kernel family (process-global).  Returns the previous value. */
+/* Select the kernel family for calls made by this thread.  Returns the
+ * thread's previous value. */
 SWR_API swr_path swr_set_path(swr_path p);
 
-/* Number of kernels this library has launched since load (for bench.py's
- * "gpu_launches"), and the family that served the most recent call
- * (1 = FFMA, 2 = TC, 0 = none). */
+/* Number of kernels this library has launched since load, all threads (for
+ * bench.py's "gpu_launches"), and the family that served this thread's most
+ * recent call (1 = FFMA, 2 = TC, 0 = none). */
 SWR_API int64_t swr_launch_count(void);
 SWR_API int swr_last_path(void);
 

@@ -22,9 +22,9 @@ cudaError_t launch_uniform(bool bf16, Params p, int k, cudaStream_t st, int sms)
 
 namespace {
 
-std::atomic<int64_t> g_launches{0};
-std::atomic<int> g_path{SWR_PATH_AUTO};
-std::atomic<int> g_last_path{0};
+std::atomic<int64_t> g_launches{0};        // diagnostics: kernels launched since load
+thread_local int g_path = SWR_PATH_AUTO;    // per calling thread (swr_set_path)
+thread_local int g_last_path = 0;           // family of this thread's last call
 std::atomic<unsigned long long*> g_trace{nullptr};
 std::atomic<int64_t> g_trace_n{0};
 thread_local char g_cuda_err[256] = "";
@@ -71,11 +71,17 @@ swr_status validate(const swr_shape& s, swr_dtype dt, const void* const* dtens, 
     for (int i = 0; i < na; ++i)
       if (!atens[i]) return SWR_ERR_NULL;
   }
-  if (s.B > 65535 || s.H > 65535 * 16) return SWR_ERR_SHAPE;  // grid limits
+  // grid limits: B is grid.z; H / (heads per CTA >= 4) is grid.y of the CUDA-core kernels
+  if (s.B > 65535 || s.H > 65535 * 4) return SWR_ERR_SHAPE;
   const int64_t vec = (dt == SWR_BF16) ? 8 : 4;  // elements per 16 bytes
   if (s.sx_b < 0 || s.sx_l < 0 || s.sx_h < 0 || s.sa_b < 0 || s.sa_l < 0 || s.sa_h < 0)
     return SWR_ERR_STRIDE;
   if (s.sx_b % vec || s.sx_l % vec || s.sx_h % vec) return SWR_ERR_STRIDE;
+  // a zero stride over a dimension of size > 1 makes output elements overlap
+  // (several (b, l, h) lines would write the same addresses of x / du / da)
+  if ((s.B > 1 && (s.sx_b == 0 || s.sa_b == 0)) || (s.L > 1 && (s.sx_l == 0 || s.sa_l == 0)) ||
+      (s.H > 1 && (s.sx_h == 0 || s.sa_h == 0)))
+    return SWR_ERR_STRIDE;
   for (int i = 0; i < nd; ++i)
     if (!aligned16(dtens[i])) return SWR_ERR_ALIGN;
   const uintptr_t esz = (dt == SWR_BF16) ? 2 : 4;
@@ -125,8 +131,10 @@ swr_status dispatch(int op, swr_dtype dt, const swr::Params& p, cudaStream_t st)
   swr_status stt = device_info(&sms);
   if (stt != SWR_OK) return stt;
   const bool bf16 = dt == SWR_BF16;
-  const int path = g_path.load(std::memory_order_relaxed);
-  if (path != SWR_PATH_FFMA && swr::tc_supported(op, bf16, p)) {
+  const int path = g_path;
+  const bool tc_ok = swr::tc_supported(op, bf16, p);
+  if (path == SWR_PATH_TC && !tc_ok) return SWR_ERR_UNSUPPORTED;  // forced, no silent fallback
+  if (path != SWR_PATH_FFMA && tc_ok) {
     int launches = 0;
     cudaError_t e = swr::launch_tc(op, p, st, sms, &launches);
     if (e == cudaSuccess) {
@@ -134,7 +142,7 @@ swr_status dispatch(int op, swr_dtype dt, const swr::Params& p, cudaStream_t st)
       g_last_path = SWR_PATH_TC;
       return SWR_OK;
     }
-    if (e != cudaErrorNotSupported) return cuda_fail(e);
+    if (e != cudaErrorNotSupported || path == SWR_PATH_TC) return cuda_fail(e);
   }
   cudaError_t e = swr::launch_ffma(op, bf16, p, st, sms);
   if (e != cudaSuccess) return cuda_fail(e);
@@ -391,17 +399,22 @@ const char* swr_strerror(swr_status st) {
     case SWR_ERR_DTYPE: return "SWR_ERR_DTYPE: unknown dtype";
     case SWR_ERR_CUDA: return "SWR_ERR_CUDA: CUDA error (see swr_last_cuda_error)";
     case SWR_ERR_ARCH: return "SWR_ERR_ARCH: current device is not sm_100 (B200)";
+    case SWR_ERR_UNSUPPORTED: return "SWR_ERR_UNSUPPORTED: SWR_PATH_TC forced for a call outside the tensor-core envelope (bf16, D = 128, TMA-addressable decays)";
   }
   return "unknown swr_status";
 }
 
 const char* swr_last_cuda_error(void) { return g_cuda_err; }
 
-swr_path swr_set_path(swr_path p) { return (swr_path)g_path.exchange((int)p); }
+swr_path swr_set_path(swr_path p) {
+  const int prev = g_path;
+  g_path = (int)p;
+  return (swr_path)prev;
+}
 
 int64_t swr_launch_count(void) { return g_launches.load(); }
 
-int swr_last_path(void) { return g_last_path.load(); }
+int swr_last_path(void) { return g_last_path; }
 
 void swr_set_trace(unsigned long long* buf, int64_t n) {
   g_trace_n.store(buf ? n : 0);

@@ -1301,20 +1301,12 @@ struct Balance {
   bool pending = false;
   uint64_t launches = 0;
 
-  // fills q.epoch and the split for this launch; true if a readback should follow it
+  // fills the split for this launch (q.epoch is already set); true if a readback
+  // should follow it
   bool plan(Params& q, Split& sp, int grid, int sms, int64_t total, cudaStream_t st) {
-    static std::atomic<uint32_t> epoch{0};
-    do {
-      q.epoch = epoch.fetch_add(1, std::memory_order_relaxed) + 1;
-    } while (q.epoch == 0);
+    (void)q;
     sp.weighted = 0;
     if (grid != sms || sms > kMaxSM) return false;
-    // Under CUDA-graph capture the launch is replayed with these parameters: the
-    // epoch would repeat and find every claim slot taken, and no readback can be
-    // scheduled.  Captured launches take the uniform split by CTA index instead
-    // (bitwise the same results, test_props.py).
-    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) return false;
     std::lock_guard<std::mutex> lock(mu);
     if ((int)rate.size() != sms) rate.assign(sms, 0.f);
     if (pending && cudaEventQuery(ev) == cudaSuccess) {
@@ -1368,6 +1360,49 @@ struct Balance {
 };
 constexpr int kMaxDev = 64;
 static Balance g_balance[kMaxDev][4];  // per device (SM rates are a property of the GPU), per op
+
+// Claim slots of the weighted split, per device.  A weighted launch claims its ranges
+// in g_claim[epoch % kClaimSlots]; a slot may only be reused once the launch that used
+// it last has completed, otherwise two in-flight launches would share claim words and a
+// range could be processed twice or not at all.  Each weighted launch records an event
+// on its stream; if the slot's event has not completed (more than kClaimSlots launches
+// in flight), the launch takes the uniform split by CTA index instead, which uses no
+// claims (bitwise the same results).  Under CUDA-graph capture the launch is replayed
+// with the same parameters, so captured launches always take the uniform split.
+struct Claims {
+  std::mutex mu;
+  uint32_t next = 0;
+  cudaEvent_t ev[kClaimSlots] = {};
+  bool used[kClaimSlots] = {};
+
+  // epoch for the launch and whether it may use the claim slot (weighted split)
+  bool acquire(cudaStream_t st, uint32_t* epoch) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    const bool capturing = cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone;
+    std::lock_guard<std::mutex> lock(mu);
+    do {
+      *epoch = ++next;
+    } while (*epoch == 0);
+    if (capturing) return false;
+    const int s = (int)(*epoch % kClaimSlots);
+    if (used[s] && cudaEventQuery(ev[s]) != cudaSuccess) {
+      (void)cudaGetLastError();  // cudaErrorNotReady is not an error of this call
+      return false;
+    }
+    return true;
+  }
+  // after a weighted launch: mark its slot busy until the stream passes this point
+  void release(cudaStream_t st, uint32_t epoch) {
+    std::lock_guard<std::mutex> lock(mu);
+    const int s = (int)(epoch % kClaimSlots);
+    if (ev[s] == nullptr && cudaEventCreateWithFlags(&ev[s], cudaEventDisableTiming) != cudaSuccess) {
+      ev[s] = nullptr;
+      return;
+    }
+    if (cudaEventRecord(ev[s], st) == cudaSuccess) used[s] = true;
+  }
+};
+static Claims g_claims[kMaxDev];
 
 static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -1438,15 +1473,11 @@ static cudaError_t launch_op(const Params& p, cudaStream_t st, int sms) {
   constexpr int threads = (4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MIX ? 4 : 5)) * 32;
   Params q = p;
   Split sp;
+  sp.weighted = 0;
   Balance* bal = dev >= 0 ? &g_balance[dev][OP] : nullptr;
   bool readback = false;
-  if (bal != nullptr) {
-    readback = bal->plan(q, sp, grid, sms, total, st);
-  } else {
-    static std::atomic<uint32_t> epoch{0};
-    q.epoch = epoch.fetch_add(1, std::memory_order_relaxed) | 0x80000000u;  // never 0
-    sp.weighted = 0;
-  }
+  q.epoch = 1;
+  if (bal != nullptr && g_claims[dev].acquire(st, &q.epoch)) readback = bal->plan(q, sp, grid, sms, total, st);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3((unsigned)threads);
@@ -1459,6 +1490,10 @@ static cudaError_t launch_op(const Params& p, cudaStream_t st, int sms) {
   cfg.numAttrs = SWR_PDL ? 1 : 0;
   cudaError_t e = cudaLaunchKernelEx(&cfg, swr_tc_kernel<OP>, maps, sp, q);
   if (e == cudaSuccess) e = cudaGetLastError();
+  if (e == cudaSuccess && sp.weighted) {
+    g_claims[dev].release(st, q.epoch);
+    (void)cudaGetLastError();
+  }
   if (e == cudaSuccess && readback) {
     bal->request(OP, sms, st);
     (void)cudaGetLastError();  // a failed readback only skips a table refresh; keep it out of the error state

@@ -43,8 +43,15 @@ def shard_range(n: int, world: int, rank: int):
 
 
 def sp_shard_lengths(L: int, world: int):
-    """Per-rank token counts for SP: multiples of 16 except possibly the last."""
+    """Per-rank token counts for SP: multiples of 16 except possibly the last.
+
+    Every rank gets at least one block: an empty shard would have no block to
+    carry the halo through (its neighbours would receive zeros instead of the
+    predecessor's carrier), so world > ceil(L / 16) is rejected."""
     nb = (L + ELL - 1) // ELL
+    if world > nb:
+        raise ValueError(f"sequence parallelism needs at least one 16-token block per rank: "
+                         f"L={L} has {nb} blocks for {world} ranks")
     lens = []
     for r in range(world):
         b0, b1 = shard_range(nb, world, r)
@@ -57,8 +64,14 @@ def _default_ops():
     return ops
 
 
+def _global(group, r):
+    """Global rank of group rank r (P2POp's `peer` is a rank of the default group)."""
+    return r if group is None else dist.get_global_rank(group, r)
+
+
 def _start_exchange(send_t, to_rank, recv_like, from_rank, group):
-    """Post the point-to-point halo exchange; returns (requests, receive buffer)."""
+    """Post the point-to-point halo exchange; returns (requests, receive buffer).
+    to_rank / from_rank are ranks inside `group`."""
     cpu = dist.get_backend(group) == "gloo"
     recv = None
     if recv_like is not None:
@@ -66,9 +79,9 @@ def _start_exchange(send_t, to_rank, recv_like, from_rank, group):
     ops = []
     if send_t is not None:
         s = send_t.contiguous().cpu() if cpu else send_t.contiguous()
-        ops.append(dist.P2POp(dist.isend, s, to_rank, group))
+        ops.append(dist.P2POp(dist.isend, s, _global(group, to_rank), group))
     if recv is not None:
-        ops.append(dist.P2POp(dist.irecv, recv, from_rank, group))
+        ops.append(dist.P2POp(dist.irecv, recv, _global(group, from_rank), group))
     reqs = dist.batch_isend_irecv(ops) if ops else []
     return reqs, recv
 
@@ -91,6 +104,8 @@ def swr_sp_fwd(u, a, group=None, carry_in=None, ops=None, carry_dtype=torch.floa
     """
     ops = ops or _default_ops()
     rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if u.shape[1] == 0:
+        raise ValueError("empty SP shard: every rank needs at least one block (sp_shard_lengths)")
     if rank < world - 1 and u.shape[1] % ELL:
         raise ValueError("every SP shard except the last must be a multiple of 16 tokens")
     # prologue: carrier of this shard's last block (one block of local inputs)
@@ -122,6 +137,8 @@ def swr_sp_bwd(u, a, dx, carry_in=None, group=None, ops=None, carry_dtype=torch.
     initial carrier (meaningful on rank 0)."""
     ops = ops or _default_ops()
     rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if u.shape[1] == 0:
+        raise ValueError("empty SP shard: every rank needs at least one block (sp_shard_lengths)")
     # prologue: mu_out of this shard's first block = a[0] * lambda_0[0] (local)
     send = None
     if rank > 0:

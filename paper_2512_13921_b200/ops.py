@@ -1,8 +1,24 @@
 """PyTorch-facing entry points (argument marshalling over the C ABI).
 
 PyTorch supplies device memory and the current CUDA stream; every step of the
-computation runs in libswr.so kernels.  Tensors must live on a CUDA device,
-share one storage dtype (float32 or bfloat16) and have the head dim contiguous.
+computation runs in libswr.so kernels.  Tensors must live on a CUDA device and
+share one storage dtype (float32 or bfloat16).
+
+Layout copies (the only data movement done here, all by torch, none silent in
+effect -- outputs always come back in the caller's logical shape):
+  * the ABI takes ONE set of element strides for all d-tensors of a call and
+    needs the head dim contiguous, 16-byte aligned pointers and 16-byte strides,
+    and non-overlapping outputs.  d-tensors that already share such a layout are
+    passed as they are (no copy; outputs get the same strides); otherwise every
+    d-tensor of the call is made contiguous first (``_prep``).
+  * decays are passed with their own strides unless a stride is 0 over a
+    dimension of size > 1 or the tensor overlaps itself (e.g. one decay row
+    expanded over heads): then they are made contiguous, so that ``da`` (which
+    shares the decays' strides) has one element per (b, l, h).
+  * the autograd wrappers hand the upstream gradient to the backward kernel in
+    the storage dtype (the ABI has one dtype per call): an fp32 gradient of a
+    bf16 layer is rounded once to bf16 (RNE) -- the same rounding the bf16
+    forward output already has.
 """
 from __future__ import annotations
 
@@ -22,15 +38,46 @@ def _ptr(t):
     return None if t is None else t.data_ptr()
 
 
+def _no_overlap(t):
+    """True if no two in-range indices of `t` address the same element (and no
+    stride is 0 over a dimension of size > 1)."""
+    dims = sorted((st, n) for st, n in zip(t.stride(), t.shape) if n > 1)
+    span = 0  # largest offset reachable with the dims of smaller stride
+    for st, n in dims:
+        if st <= span:
+            return False
+        span += st * (n - 1)
+    return True
+
+
+def _abi_layout(t):
+    """d-tensor layout the ABI accepts as is: D contiguous, 16-byte aligned base
+    pointer and strides, non-overlapping."""
+    e = t.element_size()
+    return (t.stride(3) == 1 and t.data_ptr() % 16 == 0
+            and all((t.stride(i) * e) % 16 == 0 for i in range(3)) and _no_overlap(t))
+
+
 def _prep(*ts):
-    """Common strides for the d-tensors: keep them if shared and D-contiguous, else copy."""
+    """The d-tensors of one call with one shared ABI layout: kept as they are if
+    they already share one (same shape and strides, `_abi_layout`), else copied
+    to contiguous."""
     ref = ts[0]
     if ref.dim() != 4:
         raise ValueError(f"expected [B, L, H, D] tensors, got shape {tuple(ref.shape)}")
-    ok = ref.stride(3) == 1 and all(t.shape == ref.shape and t.stride() == ref.stride() for t in ts)
+    ok = all(t.shape == ref.shape and t.stride() == ref.stride() for t in ts) and all(
+        _abi_layout(t) for t in ts)
     if not ok:
         ts = tuple(t.contiguous() for t in ts)
     return ts
+
+
+def _prep_a(a):
+    """Decays with strides `da` can share: contiguous copy if `a` overlaps itself
+    (a zero stride, e.g. a decay row expanded over heads) or is misaligned."""
+    if a.dim() == 3 and (not _no_overlap(a) or a.data_ptr() % a.element_size()):
+        return a.contiguous()
+    return a
 
 
 def _carry(t, like):
@@ -79,6 +126,7 @@ def _new_carry(like):
 def swr_fwd(u, a, carry_in=None, return_carry=False):
     """x~ = L~ u (jagged window, B2P).  Returns x or (x, carry_out)."""
     (u,) = _prep(u)
+    a = _prep_a(a)
     dt = _dtype(u, a)
     x = _like(u)
     ci = _carry(carry_in, u)
@@ -91,6 +139,7 @@ def swr_fwd(u, a, carry_in=None, return_carry=False):
 def swr_bwd(u, a, dx, carry_in=None, mu_in=None):
     """Returns (du, da, mu_out) for loss gradient dx = dLoss/dx~."""
     u, dx = _prep(u, dx)
+    a = _prep_a(a)
     dt = _dtype(u, a, dx)
     du = _like(u)
     da = _like(a)
@@ -105,6 +154,7 @@ def swr_bwd(u, a, dx, carry_in=None, mu_in=None):
 def phalanx_mix(q, k, v, a, carry_in=None, return_carry=False):
     """y = q (.) SWR(k (.) v) + v (P:1576-1578)."""
     q, k, v = _prep(q, k, v)
+    a = _prep_a(a)
     dt = _dtype(q, k, v, a)
     y = _like(q)
     ci = _carry(carry_in, q)
@@ -118,6 +168,7 @@ def phalanx_mix(q, k, v, a, carry_in=None, return_carry=False):
 def phalanx_mix_bwd(q, k, v, a, dy, carry_in=None, mu_in=None):
     """Returns (dq, dk, dv, da, mu_out)."""
     q, k, v, dy = _prep(q, k, v, dy)
+    a = _prep_a(a)
     dt = _dtype(q, k, v, a, dy)
     dq, dk, dv = _like(q), _like(q), _like(q)
     da = _like(a)
@@ -173,6 +224,7 @@ def swr_exact_fwd(u, a, carry_in=None, return_carry=False):
     """The untruncated recurrence x_n = a_n x_{n-1} + u_n (Eq. 2.1) by Alg. 2's three
     stages (include/swr.h swr_exact_fwd).  Returns x or (x, carry_out)."""
     (u,) = _prep(u)
+    a = _prep_a(a)
     dt = _dtype(u, a)
     x = _like(u)
     ci = _carry(carry_in, u)
@@ -189,6 +241,7 @@ def swr_exact_fwd(u, a, carry_in=None, return_carry=False):
 def swr_exact_bwd(u, a, dx, carry_in=None, mu_in=None):
     """Reverse mode of swr_exact_fwd.  Returns (du, da, mu_out)."""
     u, dx = _prep(u, dx)
+    a = _prep_a(a)
     dt = _dtype(u, a, dx)
     du = _like(u)
     da = _like(a)
@@ -224,6 +277,7 @@ def swr_exact(u, a, carry_in=None):
 def swr_uniform_fwd(u, a, k):
     """Uniform window of the k most recent tokens (Eq. banded_L), no carry."""
     (u,) = _prep(u)
+    a = _prep_a(a)
     dt = _dtype(u, a)
     x = _like(u)
     with torch.cuda.device(u.device):

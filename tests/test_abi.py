@@ -72,6 +72,17 @@ def test_validation_codes(lib):
                           _shape(lib, sx=(64 * 16, 18, 16)), 1, None) == 3
     assert lib.raw_status("swr_fwd", FAKE, FAKE, FAKE, None, None,
                           _shape(lib, sa=(64, -1, 1)), 1, None) == 3
+    # a zero stride over a dimension of size > 1 would make outputs overlap
+    assert lib.raw_status("swr_fwd", FAKE, FAKE, FAKE, None, None,
+                          _shape(lib, H=4, sx=(64 * 64, 64, 0)), 0, None) == 3
+    assert lib.raw_status("swr_bwd", FAKE, FAKE, FAKE, FAKE, FAKE, None, None, None,
+                          _shape(lib, H=4, sa=(256, 0, 1)), 0, None) == 3
+    assert lib.raw_status("swr_fwd", FAKE, FAKE, FAKE, None, None,
+                          _shape(lib, B=2, sa=(0, 1, 1)), 0, None) == 3
+    # grid limits: B <= 65535, H <= 65535 * 4
+    assert lib.raw_status("swr_fwd", FAKE, FAKE, FAKE, None, None, _shape(lib, B=65536), 0, None) == 2
+    assert lib.raw_status("swr_fwd", FAKE, FAKE, FAKE, None, None, _shape(lib, H=65535 * 4 + 1),
+                          0, None) == 2
     # alignment: d-tensors and carries 16 B, decays element size
     assert lib.raw_status("swr_fwd", FAKE + 4, FAKE, FAKE, None, None, s, 0, None) == 4
     assert lib.raw_status("swr_fwd", FAKE, FAKE + 1, FAKE, None, None, s, 1, None) == 4
@@ -95,7 +106,7 @@ def test_decode_step_validation_codes(lib):
 
 
 def test_strerror_names_every_code(lib):
-    for code in range(8):
+    for code in range(9):
         assert lib._lib.swr_strerror(code).decode().startswith("SWR_")
 
 

@@ -1,6 +1,6 @@
 """Recurrence-mode decoding (include/swr.h swr_decode_step; SURVEY 8(f)
-NEXT-3) on the GPU: a sequence decoded one token at a time matches the fp64 oracle
-(oracle.swr_decode, pinned to the jagged-window operator in test_oracle.py) within
+NEXT-3) on the GPU: a sequence decoded one token at a time matches the fp64 oracle's
+plain definition of the whole-sequence operator (oracle.swr_fwd / mix_fwd) within
 the north-star tolerance, and is bitwise the CUDA-core forward (same ops, same
 order)."""
 import numpy as np
@@ -42,7 +42,8 @@ def test_swr_decode_matches_oracle_and_forward(P, dtype, D, H, carry):
     x = torch.stack([P.swr_decode_step(u[:, n], a[:, n], st) for n in range(L)], dim=1)
     assert P.launch_count() - launches == L
     assert st.pos == L
-    ref = oracle.swr_decode(to64(inp["u"]), to64(inp["a"]), to64(inp.get("carry_in")))
+    # the plain definition: x~ = L~ u of the whole sequence (the jagged operator)
+    ref = oracle.swr_fwd(to64(inp["u"]), to64(inp["a"]), carry_in=to64(inp.get("carry_in")))
     assert normwise(x, ref) <= TOL[dtype]
     prev = P.set_path(P.SWR_PATH_FFMA)
     try:
@@ -64,7 +65,7 @@ def test_mix_decode_matches_oracle_and_forward(P, dtype, D, H):
     st = P.DecodeState(B, H, D, q.device, carry_in=ci)
     y = torch.stack([P.phalanx_mix_decode_step(q[:, n], k[:, n], v[:, n], a[:, n], st) for n in range(L)],
                     dim=1)
-    ref = oracle.mix_decode(*(to64(inp[n]) for n in ("q", "k", "v", "a")), to64(inp["carry_in"]))
+    ref = oracle.mix_fwd(*(to64(inp[n]) for n in ("q", "k", "v", "a")), carry_in=to64(inp["carry_in"]))
     assert normwise(y, ref) <= TOL[dtype]
     prev = P.set_path(P.SWR_PATH_FFMA)
     try:

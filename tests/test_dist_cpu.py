@@ -134,3 +134,50 @@ def test_sp_shard_lengths():
     assert sum(sdist.sp_shard_lengths(1000, 3)) == 1000
     for lens in (sdist.sp_shard_lengths(1000, 3), sdist.sp_shard_lengths(70, 2)):
         assert all(n % 16 == 0 for n in lens[:-1])
+
+
+def _subgroup_worker(rank, world, port, L, outdir):
+    """SP inside sub-groups {0,1} and {2,3} of a world-4 job (sequence parallel
+    inside data parallel): halo peers are group ranks, P2POp needs global ones."""
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2512_13921_b200 import dist as sdist
+    groups = [dist.new_group([0, 1]), dist.new_group([2, 3])]
+    grp = groups[rank // 2]
+    grank = dist.get_rank(grp)
+    u, a, G = _problem(2, L, 3, 4, seed=40 + rank // 2)  # one problem per sub-group
+    lens = sdist.sp_shard_lengths(L, 2)
+    lo = sum(lens[:grank])
+    hi = lo + lens[grank]
+    us, as_, Gs = u[:, lo:hi].contiguous(), a[:, lo:hi].contiguous(), G[:, lo:hi].contiguous()
+    x, cin = sdist.swr_sp_fwd(us, as_, group=grp, ops=OracleOps, carry_dtype=torch.float64)
+    du, da, mo = sdist.swr_sp_bwd(us, as_, Gs, carry_in=cin, group=grp, ops=OracleOps,
+                                  carry_dtype=torch.float64)
+    torch.save({"x": x, "du": du, "da": da, "mo": mo}, os.path.join(outdir, f"g{rank}.pt"))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sequence_parallel_in_subgroups_gloo(tmp_path):
+    import oracle
+    L = 80
+    mp.spawn(_subgroup_worker, args=(4, _free_port(), L, str(tmp_path)), nprocs=4, join=True)
+    parts = [torch.load(tmp_path / f"g{r}.pt") for r in range(4)]
+    for gi in range(2):
+        u, a, G = _problem(2, L, 3, 4, seed=40 + gi)
+        p0, p1 = parts[2 * gi], parts[2 * gi + 1]
+        rx = oracle.swr_fwd(u.numpy(), a.numpy())
+        rdu, rda, rmo = oracle.swr_bwd(u.numpy(), a.numpy(), G.numpy())
+        assert np.array_equal(torch.cat([p0["x"], p1["x"]], dim=1).numpy(), rx)
+        assert np.array_equal(torch.cat([p0["du"], p1["du"]], dim=1).numpy(), rdu)
+        assert np.array_equal(torch.cat([p0["da"], p1["da"]], dim=1).numpy(), rda)
+        assert np.array_equal(p0["mo"].numpy(), rmo)
+
+
+def test_sp_rejects_empty_shards():
+    from paper_2512_13921_b200 import dist as sdist
+    with pytest.raises(ValueError):
+        sdist.sp_shard_lengths(40, 4)  # 3 blocks for 4 ranks
+    assert sdist.sp_shard_lengths(48, 3) == [16, 16, 16]

@@ -10,7 +10,11 @@ constant-decay closed form, the untruncated recurrence on <= 2 blocks, finite
 differences, the transpose identity, locality, linearity and stitching; the
 extensions (``swr_decode``/``mix_decode``, ``linrec_fwd``/``linrec_bwd``,
 ``uniform_fwd``) against the entrywise jagged / full / banded operators, the closed
-form and finite differences.
+form and finite differences; the Phalanx layer around the mixer (``layer_mix_fwd`` /
+``layer_mix_bwd``: sigmoid on the a and k logits, group-shared q and k) against the
+per-head mixer on expanded inputs, sigmoid values, and finite differences in the
+logits and group tensors.
 """
-from .oracle import (ELL, build, linrec_bwd, linrec_fwd, mix_bwd, mix_decode, mix_fwd, swr_bwd, swr_decode,  # noqa: F401
+from .oracle import (ELL, build, expand_groups, group_sum, layer_mix_bwd, layer_mix_fwd,  # noqa: F401
+                     linrec_bwd, linrec_fwd, mix_bwd, mix_decode, mix_fwd, sigmoid, swr_bwd, swr_decode,
                      swr_fwd, uniform_fwd)

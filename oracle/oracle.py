@@ -219,3 +219,66 @@ def uniform_fwd(u, a, k):
         A = A * As
         s *= 2
     return X
+
+
+# ---------------------------------------------------------------------------
+# The Phalanx layer around the mixer
+# ---------------------------------------------------------------------------
+def sigmoid(z):
+    """sigma(z) = 1 / (1 + e^-z), the featurization's bounding activation for the
+    recurrence coefficient a = sigma(W u) and the key-like gate k = sigma(K u)
+    (P:1562, P:1564).  fp64."""
+    z = _f64(z)
+    return 1.0 / (1.0 + np.exp(-z))
+
+
+def expand_groups(t, H):
+    """Gate sharing across heads ("within each group, multiple heads
+    share the same gate parameters"; 8 groups for K and Q): a [B, L, G, D]
+    group tensor seen by H heads, head h reading group h // (H / G) (contiguous
+    head groups, reading R18).  Returns [B, L, H, D]."""
+    t = _f64(t)
+    G = t.shape[2]
+    if H % G:
+        raise ValueError(f"{G} groups do not divide {H} heads")
+    return np.repeat(t, H // G, axis=2)
+
+
+def group_sum(t, G):
+    """Adjoint of expand_groups: sum the H per-head gradients of each group."""
+    t = _f64(t)
+    B, L, H, D = t.shape
+    return t.reshape(B, L, G, H // G, D).sum(axis=3)
+
+
+def layer_mix_fwd(q, zk, v, za, carry_in=None, carry_out=False, threads: int = 0):
+    """Phalanx mixer fed by the featurization outputs:
+        a = sigma(za)                   [B, L, H]     recurrence coefficient logits
+        k = sigma(zk)                   [B, L, Gk, D] key-like gate logits, Gk groups
+        q                               [B, L, Gq, D] query-like gate, Gq groups
+        v                               [B, L, H, D]
+        y = q_g (.) SWR_a(k_g (.) v) + v          (g = the head's group)
+    Returns y (or (y, carry_out))."""
+    v = _f64(v)
+    H = v.shape[2]
+    a = sigmoid(za)
+    k = expand_groups(sigmoid(zk), H)
+    qh = expand_groups(q, H)
+    return mix_fwd(qh, k, v, a, carry_in, carry_out, threads)
+
+
+def layer_mix_bwd(q, zk, v, za, dy, carry_in=None, mu_in=None, threads: int = 0):
+    """Chain rule of layer_mix_fwd.  Returns (dq [B,L,Gq,D], dzk [B,L,Gk,D], dv,
+    dza [B,L,H], mu_out): the mixer's per-head gradients (mix_bwd), summed over the
+    heads of each group (group_sum), times sigma' = s (1 - s) for the logits."""
+    q, zk, v = _f64(q), _f64(zk), _f64(v)
+    H = v.shape[2]
+    Gq, Gk = q.shape[2], zk.shape[2]
+    a = sigmoid(za)
+    ks = sigmoid(zk)
+    dqh, dkh, dv, da, mu_out = mix_bwd(expand_groups(q, H), expand_groups(ks, H), v, a, dy,
+                                       carry_in, mu_in, threads)
+    dq = group_sum(dqh, Gq)
+    dzk = group_sum(dkh, Gk) * ks * (1.0 - ks)
+    dza = da * a * (1.0 - a)
+    return dq, dzk, dv, dza, mu_out

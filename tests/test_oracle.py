@@ -500,3 +500,95 @@ def test_uniform_limits():
     u, a, _, _, _ = rand_problem(1, 20, 2, 3, seed=4)
     assert np.array_equal(oracle.uniform_fwd(u, a, 1), u)
     assert normwise(oracle.uniform_fwd(u, a, 32), oracle.linrec_fwd(u, a)[0]) < 1e-12
+
+
+# --------------------------------------------------------------------------
+# the Phalanx layer around the mixer: sigma on the a and k
+# logits, group-shared q and k
+# --------------------------------------------------------------------------
+def test_sigmoid_values():
+    """sigma(0) = 1/2, sigma(-z) = 1 - sigma(z), sigma(log(p/(1-p))) = p, sigma(ln 3) = 3/4."""
+    z = np.linspace(-30, 30, 121)
+    s = oracle.sigmoid(z)
+    assert oracle.sigmoid(np.array(0.0)) == 0.5
+    np.testing.assert_allclose(oracle.sigmoid(-z), 1.0 - s, rtol=0, atol=1e-15)
+    p = np.array([1e-6, 0.1, 0.25, 0.5, 0.8, 0.999])
+    np.testing.assert_allclose(oracle.sigmoid(np.log(p / (1 - p))), p, rtol=1e-12)
+    np.testing.assert_allclose(oracle.sigmoid(np.log(3.0)), 0.75, rtol=1e-15)
+
+
+def _layer_problem(B, L, H, Gq, Gk, D, seed):
+    r = np.random.default_rng(seed)
+    q = r.standard_normal((B, L, Gq, D))
+    zk = r.standard_normal((B, L, Gk, D))
+    v = r.standard_normal((B, L, H, D))
+    za = r.standard_normal((B, L, H))
+    dy = r.standard_normal((B, L, H, D))
+    return q, zk, v, za, dy
+
+
+@pytest.mark.parametrize("H,Gq,Gk", [(4, 2, 2), (6, 3, 1), (8, 8, 2), (4, 1, 4)])
+def test_layer_forward_dense_per_head(H, Gq, Gk):
+    """y[:, :, h] = q[g_q(h)] * (L~(sigma(za_h)) (sigma(zk[g_k(h)]) * v_h)) + v_h with
+    g(h) = h // (H / G), written with the entrywise dense jagged operator and
+    explicit scalar sigmoids, head by head."""
+    import math
+    B, L, D = 1, 40, 3
+    q, zk, v, za, _ = _layer_problem(B, L, H, Gq, Gk, D, seed=50 + H + Gq)
+    y = oracle.layer_mix_fwd(q, zk, v, za)
+    for h in range(H):
+        gq, gk = h // (H // Gq), h // (H // Gk)
+        a = np.array([1.0 / (1.0 + math.exp(-z)) for z in za[0, :, h]])
+        k = np.vectorize(lambda z: 1.0 / (1.0 + math.exp(-z)))(zk[0, :, gk])
+        M = dense_jagged(a)
+        ref = q[0, :, gq] * (M @ (k * v[0, :, h])) + v[0, :, h]
+        np.testing.assert_allclose(y[0, :, h], ref, rtol=1e-12, atol=1e-12)
+
+
+def test_layer_with_one_head_per_group_is_the_mixer():
+    """G = H and logits of given gates: the layer mixer is mix_fwd / mix_bwd on the
+    gates, with the logit gradients scaled by sigma' = s (1 - s)."""
+    q, k, v, a, dy = _mix_problem(2, 45, 3, 4, seed=16)
+    k = np.clip(k, 1e-3, 1 - 1e-3)
+    a = np.clip(a, 1e-3, 1 - 1e-3)
+    zk, za = np.log(k / (1 - k)), np.log(a / (1 - a))
+    np.testing.assert_allclose(oracle.layer_mix_fwd(q, zk, v, za), oracle.mix_fwd(q, k, v, a),
+                               rtol=1e-10, atol=1e-10)
+    dq, dzk, dv, dza, mo = oracle.layer_mix_bwd(q, zk, v, za, dy)
+    rq, rk, rv, ra, rmo = oracle.mix_bwd(q, k, v, a, dy)
+    np.testing.assert_allclose(dq, rq, rtol=1e-10, atol=1e-10)
+    np.testing.assert_allclose(dzk, rk * k * (1 - k), rtol=1e-9, atol=1e-10)
+    np.testing.assert_allclose(dv, rv, rtol=1e-10, atol=1e-10)
+    np.testing.assert_allclose(dza, ra * a * (1 - a), rtol=1e-9, atol=1e-10)
+    np.testing.assert_allclose(mo, rmo, rtol=1e-10, atol=1e-10)
+
+
+def test_layer_backward_matches_finite_differences():
+    """Central differences of sum(dy * y) in every group-tensor and logit entry
+    (H = 4 heads, 2 q groups, 1 k group, 35 tokens, 2 channels), with carries."""
+    B, L, H, Gq, Gk, D = 1, 35, 4, 2, 1, 2
+    q, zk, v, za, dy = _layer_problem(B, L, H, Gq, Gk, D, seed=17)
+    r = np.random.default_rng(18)
+    ci, mi = r.standard_normal((B, H, D)), r.standard_normal((B, H, D))
+    dq, dzk, dv, dza, mo = oracle.layer_mix_bwd(q, zk, v, za, dy, carry_in=ci, mu_in=mi)
+    h = 1e-6
+
+    def loss(q_, zk_, v_, za_, ci_=ci):
+        y, co = oracle.layer_mix_fwd(q_, zk_, v_, za_, carry_in=ci_, carry_out=True)
+        return float(np.sum(dy * y) + np.sum(mi * co))
+
+    def fd(arr, f):
+        g = np.zeros_like(arr)
+        it = np.nditer(arr, flags=["multi_index"])
+        for _ in it:
+            i = it.multi_index
+            p = arr.copy(); p[i] += h
+            m = arr.copy(); m[i] -= h
+            g[i] = (f(p) - f(m)) / (2 * h)
+        return g
+
+    assert normwise(dq, fd(q, lambda p: loss(p, zk, v, za))) < 1e-6
+    assert normwise(dzk, fd(zk, lambda p: loss(q, p, v, za))) < 1e-6
+    assert normwise(dv, fd(v, lambda p: loss(q, zk, p, za))) < 1e-6
+    assert normwise(dza, fd(za, lambda p: loss(q, zk, v, p))) < 1e-6
+    assert normwise(mo, fd(ci, lambda p: loss(q, zk, v, za, p))) < 1e-6

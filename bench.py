@@ -11,14 +11,17 @@ mixer forward + backward -- on inputs already resident in HBM.  Metric
 (BASELINE.json): fwd+bwd tokens/s, plus achieved HBM GB/s of the dominant
 kernel against the measured copy peak (MEASURED_PEAKS.json).
 
-Timing: W untimed warm-up steps; then K steps, each bracketed by CUDA events on
-the launching stream with an L2 flush between steps, outside the events (a
-write of 2x the L2 size, then a read of another 2x-L2 buffer so the flush's own
-dirty lines are written back before the step: a clean L2 holding no step data);
-barrier + synchronize around the loop; per-rank sum of step times, max over
-ranks.  Multi-GPU (torchrun): every rank runs the same
-per-GPU workload on its own batch shard (batch x head sharding, no collective;
-weak scaling).
+Timing: W untimed warm-up steps; then K steps back to back, each bracketed by
+CUDA events on the launching stream; barrier + synchronize around the loop;
+per-rank sum of step times, max over ranks.  When a step's inputs exceed 2x the
+L2 (every graded config) nothing is flushed between steps, so every dirty line a
+step leaves in L2 is written back inside the next step's events (no deferred
+write-back goes unpaid).  Smaller inputs get an L2 flush between steps (write a
+2x-L2 buffer, then read another); the flushed timing of the large configs is
+reported beside the headline as "l2_flushed".  Multi-GPU (torchrun): layer4k
+and the other single-GPU configs run the same per-GPU workload on every rank
+(batch x head sharding, no collective; weak scaling); `bxh` splits BASELINE
+configs[3]'s B = 64 over the ranks (strong scaling); `sp131k` shards L.
 """
 from __future__ import annotations
 
@@ -40,13 +43,15 @@ CONFIGS = {
     "L16k": (4, 16384, 16, 128, "bf16"),
     "L32k": (2, 32768, 16, 128, "bf16"),
     "L4k_b16": (16, 4096, 16, 128, "bf16"),
-    "bxh": (8, 8192, 16, 128, "bf16"),        # BJ configs[3] per-GPU shard at 8 GPUs
+    "bxh": (64, 8192, 16, 128, "bf16"),       # BJ configs[3]: B = 64 split over the ranks
     "paper_d16": (8, 8192, 128, 16, "bf16"),  # the paper's head shape d=16, h=128
     "layer4k_f32": (8, 4096, 16, 128, "f32"),  # BJ configs[1] shape with fp32 storage (FFMA path)
     "tiny": (1, 64, 1, 16, "f32"),            # BJ configs[0]
     "sp131k": (1, 131072, 16, 128, "bf16"),   # BJ configs[4]: sequence-parallel across ranks
 }
 SP_CONFIGS = {"sp131k"}
+SPLIT_CONFIGS = {"bxh"}  # global batch split over the ranks (strong scaling)
+EXTRA = ("L8k", "L16k", "L32k")  # BJ configs[2] lines measured beside the default workload
 METRIC = "SWR fwd+bwd tokens/s and achieved HBM GB/s vs B200 peak at 4K-32K, 1/2/4/8 GPUs"
 
 
@@ -132,19 +137,19 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # reference arm: the fp64 oracle on the host cores
 # ---------------------------------------------------------------------------
-def oracle_step_fn(op, inp_host, rows):
+def oracle_step_fn(op, inp_host, rows, threads=0):
     import oracle
     from swr_inputs import to64
     sl = slice(0, rows)
     h = {k: to64(v[sl]) for k, v in inp_host.items()}
     if op == "swr":
         def step():
-            oracle.swr_fwd(h["u"], h["a"])
-            oracle.swr_bwd(h["u"], h["a"], h["G"])
+            oracle.swr_fwd(h["u"], h["a"], threads=threads)
+            oracle.swr_bwd(h["u"], h["a"], h["G"], threads=threads)
     else:
         def step():
-            oracle.mix_fwd(h["q"], h["k"], h["v"], h["a"])
-            oracle.mix_bwd(h["q"], h["k"], h["v"], h["a"], h["dy"])
+            oracle.mix_fwd(h["q"], h["k"], h["v"], h["a"], threads=threads)
+            oracle.mix_bwd(h["q"], h["k"], h["v"], h["a"], h["dy"], threads=threads)
     return step
 
 
@@ -156,24 +161,35 @@ def make_host_inputs(op, B, L, H, D, dt, seed):
     return f(B, L, H, D, dtype=dtype, seed=seed)
 
 
-def cpu_baseline(op, inp_host, B, L, budget_s=10.0, rows=1):
-    """The oracle as it stands on a bounded sample: `rows` batch rows, repeated
-    until `budget_s` of wall time."""
+def cpu_baseline(op, inp_host, B, L, H, budget_s=10.0):
+    """The oracle as it stands on a bounded sample of the workload: enough batch rows
+    that its (b, h) thread pool can occupy every host core, repeated until
+    `budget_s` of wall time; then the same with one thread on one row."""
+    import math
+
     import oracle
-    step = oracle_step_fn(op, inp_host, rows)
-    step()  # build + first touch
-    n, t0 = 0, time.perf_counter()
-    while True:
-        step()
-        n += 1
-        el = time.perf_counter() - t0
-        if el >= budget_s or n >= 1000:
-            break
-    tok = rows * L * n
-    return {"value": tok / el, "unit": "tokens/s", "cores": oracle.oracle.last_threads,
-            "kind": "oracle",
-            "sample": f"{rows} of {B} batch rows (all heads, full length) fwd+bwd, "
-                      f"{n} repetitions in {el:.1f} s, fp64 C oracle"}
+    host = os.cpu_count() or 1
+    rows = max(1, min(B, math.ceil(host / H)))
+
+    def timed(rows_, threads, budget):
+        step = oracle_step_fn(op, inp_host, rows_, threads)
+        step()  # build + first touch
+        n, t0 = 0, time.perf_counter()
+        while True:
+            step()
+            n += 1
+            el = time.perf_counter() - t0
+            if el >= budget or n >= 1000:
+                break
+        return rows_ * L * n / el, n, el, oracle.oracle.last_threads
+
+    v, n, el, used = timed(rows, 0, budget_s)
+    v1, n1, el1, _ = timed(1, 1, budget_s / 2)
+    return {"value": v, "unit": "tokens/s", "cores": used, "host_cores": host,
+            "kind": "oracle", "value_1thread": v1,
+            "sample": f"{rows} of {B} batch rows (all {H} heads, full length) fwd+bwd, {n} repetitions "
+                      f"in {el:.1f} s on {used} threads (one per (b, h) pair, at most the host's {host} "
+                      f"cores); 1 thread: 1 row, {n1} repetitions in {el1:.1f} s; fp64 C oracle"}
 
 
 def run_reference(args, cfg_name, B, L, H, D, dt):
@@ -195,12 +211,13 @@ def run_reference(args, cfg_name, B, L, H, D, dt):
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "tokens/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "strong" if (cfg_name in SP_CONFIGS or cfg_name in SPLIT_CONFIGS) else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg_name, "B": B, "L": L, "H": H, "d_head": D, "op": args.op,
                    "sample_rows_per_step": 1},
         "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": oracle.oracle.last_threads,
-                         "kind": "oracle",
+                         "host_cores": os.cpu_count(), "kind": "oracle",
                          "sample": f"1 of {B} batch rows (all {H} heads, L={L}) fwd+bwd per step"},
         "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -211,6 +228,14 @@ def run_reference(args, cfg_name, B, L, H, D, dt):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+def step_fns(P, op, g):
+    """fwd() and bwd() of one step of the hot path on device-resident inputs g."""
+    if op == "swr":
+        return (lambda: P.swr_fwd(g["u"], g["a"])), (lambda: P.swr_bwd(g["u"], g["a"], g["G"]))
+    return ((lambda: P.phalanx_mix(g["q"], g["k"], g["v"], g["a"])),
+            (lambda: P.phalanx_mix_bwd(g["q"], g["k"], g["v"], g["a"], g["dy"])))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -222,6 +247,7 @@ def main():
     ap.add_argument("--path", default="auto", choices=["auto", "ffma", "tc"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the L8k/L16k/L32k lines")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     B, L, H, D, dt = CONFIGS[args.config]
@@ -259,6 +285,11 @@ def main():
         Ls = lens[rank]
         grp = dist.group.WORLD if world > 1 else None
     else:
+        if args.config in SPLIT_CONFIGS:
+            # BJ configs[3]: the global batch split into contiguous per-rank slices
+            if B % world:
+                raise SystemExit(f"--config {args.config}: B={B} does not split over {world} ranks")
+            B = B // world
         # per-rank shard of the batch (batch x head sharding): seed by global batch offset
         inp_host = make_host_inputs(args.op, B, L, H, D, dt, seed=1 + 1000 * rank)
         Ls = L
@@ -274,18 +305,8 @@ def main():
 
         def bwd():
             return sdist.swr_sp_bwd(g["u"], g["a"], g["G"], carry_in=state.get("cin"), group=grp)
-    elif args.op == "swr":
-        def fwd():
-            return P.swr_fwd(g["u"], g["a"])
-
-        def bwd():
-            return P.swr_bwd(g["u"], g["a"], g["G"])
     else:
-        def fwd():
-            return P.phalanx_mix(g["q"], g["k"], g["v"], g["a"])
-
-        def bwd():
-            return P.phalanx_mix_bwd(g["q"], g["k"], g["v"], g["a"], g["dy"])
+        fwd, bwd = step_fns(P, args.op, g)
 
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = torch.empty(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=dev)
@@ -300,36 +321,47 @@ def main():
         flush.zero_()
         flush_sink.copy_(flush_rd.sum())
 
-    for _ in range(args.warmup):
-        l2_flush()
-        fwd()
-        bwd()
-    torch.cuda.synchronize()
+    def in_bytes(gg):
+        return sum(v.numel() * v.element_size() for v in gg.values())
 
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    launches0 = P.launch_count()
-    with ClockSampler(dev.index if world == 1 else local) as clk:
-        for s in range(args.steps):
-            l2_flush()
-            ev[s][0].record(stream)
-            fwd()
-            ev[s][1].record(stream)
-            bwd()
-            ev[s][2].record(stream)
+    def timed(fwd_, bwd_, steps, warmup, flushed):
+        """Per-step fwd / bwd CUDA-event times (ms); back to back unless `flushed`."""
+        for _ in range(warmup):
+            if flushed:
+                l2_flush()
+            fwd_()
+            bwd_()
         torch.cuda.synchronize()
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for s_ in range(steps):
+            if flushed:
+                l2_flush()
+            ev[s_][0].record(stream)
+            fwd_()
+            ev[s_][1].record(stream)
+            bwd_()
+            ev[s_][2].record(stream)
+        torch.cuda.synchronize()
+        return [e[0].elapsed_time(e[1]) for e in ev], [e[1].elapsed_time(e[2]) for e in ev]
+
+    def max_over_ranks(x):
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    b2b = in_bytes(g) > 2 * l2  # inputs larger than L2: no flush between steps
+    launches0, copies0 = P.launch_count(), P.layout_copies()
+    with ClockSampler(dev.index if world == 1 else local) as clk:
+        t_fwd, t_bwd = timed(fwd, bwd, args.steps, args.warmup, flushed=not b2b)
     launches = P.launch_count() - launches0
+    assert P.layout_copies() == copies0, "operands were copied inside the timed region"
     if world > 1:
         dist.barrier()
-    t_fwd = [e[0].elapsed_time(e[1]) for e in ev]
-    t_bwd = [e[1].elapsed_time(e[2]) for e in ev]
-    tot_ms = sum(t_fwd) + sum(t_bwd)
-    t = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_per_step = t.item() / args.steps
+    ms_per_step = max_over_ranks(sum(t_fwd) + sum(t_bwd)) / args.steps
     tokens_per_step = B * L if sp else B * L * world
     value = tokens_per_step / (ms_per_step / 1e3)
 
@@ -338,26 +370,32 @@ def main():
     dom = "bwd" if mb >= mf else "fwd"
     peak, peak_kind = load_peaks()
     ach = bytes_[dom] / (mb if dom == "bwd" else mf) / 1e6  # GB/s
-    traffic = None
+    traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
             tr = json.load(f)
-        key = f"{args.op}_{dom}_{args.config}_{dt}"
-        traffic = tr.get(key)
+        rec = tr.get(f"{args.op}_{dom}_{args.config}_{dt}")
+        if isinstance(rec, dict):
+            traffic, traffic_src = rec.get("bytes"), rec.get("source")
 
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "strong" if sp else "weak", "vs_baseline": None,
+        "higher_is_better": True,
+        "scaling": "strong" if (sp or args.config in SPLIT_CONFIGS) else "weak", "vs_baseline": None,
         "dtype": dt, "data": "synthetic",
-        "config": {"workload": args.config, "B": B, "L": L, "H": H, "d_head": D, "op": args.op,
+        "config": {"workload": args.config, "B": B * (world if args.config in SPLIT_CONFIGS else 1),
+                   "B_per_rank": B, "L": L, "H": H, "d_head": D, "op": args.op,
                    "global_batch": B if sp else B * world, "seq_len": L,
                    "parallelism": (f"sp{world} (sequence shards, one-block carrier halo via "
                                    f"{'NCCL send/recv' if world > 1 else 'none'})") if sp else
                                   f"dp{world} (batch x head shards, no collective)",
-                   "l2_flush": (f"{flush.numel() * 4 >> 20} MiB write + {flush_rd.numel() * 4 >> 20} MiB read "
-                                "between timed steps (L2 clean, holds no step data)"),
+                   "timing": ("back to back, no L2 flush: inputs "
+                              f"{in_bytes(g) >> 20} MiB > 2x L2 ({l2 >> 20} MiB), so each step pays the "
+                              "previous step's deferred write-back") if b2b else
+                             (f"L2 flushed between steps ({flush.numel() * 4 >> 20} MiB write + "
+                              f"{flush_rd.numel() * 4 >> 20} MiB read, outside the events)"),
                    "path": args.path, "last_path": {0: "none", 1: "ffma", 2: "tc"}[P.last_path()]},
         "fwd_ms": mf, "bwd_ms": mb,
         "hbm_gbs": {"fwd": bytes_["fwd"] / mf / 1e6, "bwd": bytes_["bwd"] / mb / 1e6,
@@ -365,10 +403,36 @@ def main():
         "roofline": {"bound": "hbm", "kernel": f"{args.op}_{dom}", "achieved": ach, "peak": peak,
                      "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
                      "unit": "GB/s", "frac": ach / peak, "traffic": traffic,
+                     "traffic_source": traffic_src or "not captured for this workload",
                      "algorithmic_bytes": bytes_[dom]},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
+    if b2b:
+        # the same steps with the L2 flushed between them (each step's deferred
+        # write-back is then paid by the flush, outside the events)
+        f_fwd, f_bwd = timed(fwd, bwd, min(args.steps, 20), 3, flushed=True)
+        fm = max_over_ranks(sum(f_fwd) + sum(f_bwd)) / len(f_fwd)
+        line["l2_flushed"] = {"value": tokens_per_step / (fm / 1e3), "ms_per_step": fm,
+                              "fwd_ms": statistics.mean(f_fwd), "bwd_ms": statistics.mean(f_bwd)}
+    if (args.config == "layer4k" and not sp and not args.no_extra):
+        # BJ configs[2]: 64K tokens per GPU at L = 8K / 16K / 32K, same op and timing
+        line["workloads"] = {}
+        for name in EXTRA:
+            Bx, Lx, Hx, Dx, dtx = CONFIGS[name]
+            gx = {k: v.to(dev) for k, v in make_host_inputs(args.op, Bx, Lx, Hx, Dx, dtx, seed=2 + 1000 * rank).items()}
+            fx, bx = step_fns(P, args.op, gx)
+            bx_ = in_bytes(gx) > 2 * l2
+            x_fwd, x_bwd = timed(fx, bx, min(args.steps, 20), 3, flushed=not bx_)
+            xm = max_over_ranks(sum(x_fwd) + sum(x_bwd)) / len(x_fwd)
+            xb = algo_bytes(args.op, Bx, Lx, Hx, Dx, dtx)
+            line["workloads"][name] = {
+                "B": Bx, "L": Lx, "value": Bx * Lx * world / (xm / 1e3), "unit": "tokens/s", "ms_per_step": xm,
+                "fwd_ms": statistics.mean(x_fwd), "bwd_ms": statistics.mean(x_bwd),
+                "hbm_gbs_fwd_bwd": (xb["fwd"] + xb["bwd"]) / xm / 1e6,
+                "timing": "back to back" if bx_ else "L2 flushed"}
+            del gx
+    torch.cuda.synchronize()
 
     # end to end through the public API with host buffers (pinned), copies timed.
     # Batch rows are independent, so the step is pipelined over row chunks on three
@@ -436,7 +500,7 @@ def main():
                        "ms_per_step": te.item(), "steps": ne, "pipeline_chunks": nch}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args.op, inp_host, B, Ls, rows=1)
+        line["cpu_baseline"] = cpu_baseline(args.op, inp_host, B, Ls, H)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -3,8 +3,7 @@
 //
 // Mapping.  A thread owns one vector of adjacent channels of one (b, h) -- 16
 // bytes in the forward (fwd_stream), four channels in the backward
-// (bwd_ffma_vec); two in the older fwd_ffma / bwd_ffma / bwd_ffma_mix kept behind
-// SWR_FFMA_*_V1 -- and walks a run of K consecutive 16-token blocks ("chunk").
+// (bwd_ffma_vec) -- and walks a run of K consecutive 16-token blocks ("chunk").
 // For every block it
 //   * loads the 16 decays and 16 token vectors of its channels (coalesced across
 //     the lanes of the head: consecutive lanes own consecutive channel vectors),
@@ -26,493 +25,13 @@
 
 namespace swr {
 
-template <typename T>
-__device__ __forceinline__ void load_decays(const T* A, int64_t sa_l, int64_t n0, int64_t L,
-                                            float (&a)[kEll]) {
-#pragma unroll
-  for (int i = 0; i < kEll; ++i) {
-    const int64_t n = n0 + i;
-    a[i] = (n < L) ? IO<T>::ld1(A + n * sa_l) : 1.f;  // pad: a = 1 (carry_out = state at L-1)
-  }
-}
-
-template <typename T>
-__device__ __forceinline__ void load_raw(const T* X, int64_t xo, int64_t sx_l, int64_t n0, int64_t L,
-                                         typename IO<T>::raw (&r)[kEll]) {
-#pragma unroll
-  for (int i = 0; i < kEll; ++i) {
-    const int64_t n = n0 + i;
-    r[i] = (n < L) ? IO<T>::ld(X + xo + n * sx_l) : IO<T>::zero();
-  }
-}
-
-// Pass-I input of a block: u (SWR) or u^ = k (.) v (Phalanx pre-gate).
-template <typename T, bool MIX>
-__device__ __forceinline__ void load_u(const Params& p, int64_t xo, int64_t n0,
-                                       float2 (&u)[kEll]) {
-  using io = IO<T>;
-  if constexpr (!MIX) {
-    typename io::raw r[kEll];
-    load_raw<T>((const T*)p.u, xo, p.sx_l, n0, p.L, r);
-#pragma unroll
-    for (int i = 0; i < kEll; ++i) u[i] = io::f2(r[i]);
-  } else {
-    typename io::raw rk[kEll], rv[kEll];
-    load_raw<T>((const T*)p.k, xo, p.sx_l, n0, p.L, rk);
-    load_raw<T>((const T*)p.v, xo, p.sx_l, n0, p.L, rv);
-#pragma unroll
-    for (int i = 0; i < kEll; ++i) {
-      const float2 kk = io::f2(rk[i]), vv = io::f2(rv[i]);
-      u[i] = make_float2(__fmul_rn(kk.x, vv.x), __fmul_rn(kk.y, vv.y));
-    }
-  }
-}
-
-// Pass I of one block: w = L_t u as the local recurrence (restarted from 0).
-__device__ __forceinline__ void local_solve(const float (&a)[kEll], const float2 (&u)[kEll],
-                                            float2 (&w)[kEll]) {
-  float w0 = u[0].x, w1 = u[0].y;
-  w[0] = u[0];
-#pragma unroll
-  for (int i = 1; i < kEll; ++i) {
-    w0 = fmaf(a[i], w0, u[i].x);
-    w1 = fmaf(a[i], w1, u[i].y);
-    w[i] = make_float2(w0, w1);
-  }
-}
-
-// lambda_t[0] of a block (reverse local recurrence of the adjoint, lambda = L_t^T G):
-// l[15] = G[15], l[i] = G[i] + a[i+1] l[i+1].  Same op order as the walk below.
-__device__ __forceinline__ float2 lambda_step(float a_next, float2 l, float2 G) {
-  return make_float2(fmaf(a_next, l.x, G.x), fmaf(a_next, l.y, G.y));
-}
-
-// Adjoint input of a block: dx (SWR) or G = dy (.) q (mixer).
-template <typename T, bool MIX>
-__device__ __forceinline__ void load_G(const Params& p, int64_t xo, int64_t n0,
-                                       float2 (&G)[kEll]) {
-  using io = IO<T>;
-  if constexpr (!MIX) {
-    typename io::raw r[kEll];
-    load_raw<T>((const T*)p.dx, xo, p.sx_l, n0, p.L, r);
-#pragma unroll
-    for (int i = 0; i < kEll; ++i) G[i] = io::f2(r[i]);
-  } else {
-    typename io::raw rd[kEll], rq[kEll];
-    load_raw<T>((const T*)p.dy, xo, p.sx_l, n0, p.L, rd);
-    load_raw<T>((const T*)p.q, xo, p.sx_l, n0, p.L, rq);
-#pragma unroll
-    for (int i = 0; i < kEll; ++i) {
-      const float2 d = io::f2(rd[i]), qq = io::f2(rq[i]);
-      G[i] = make_float2(__fmul_rn(d.x, qq.x), __fmul_rn(d.y, qq.y));
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// forward
-// ---------------------------------------------------------------------------
-#ifndef SWR_FFMA_FWD_V1
-#define SWR_FFMA_FWD_V1 0  // 1: the two-channel forward (fwd_ffma) instead of fwd_stream
-#endif
-#ifndef SWR_FFMA_FWD_MINB
-#define SWR_FFMA_FWD_MINB 3
-#endif
-template <typename T, int TPH, bool MIX>
-__global__ void __launch_bounds__(128, MIX ? 1 : SWR_FFMA_FWD_MINB) fwd_ffma(const Params p) {
-  using io = IO<T>;
-  constexpr int HPC = 128 / TPH;  // heads per CTA
-  const int tid = threadIdx.x;
-  const int hh = tid / TPH;
-  const int c = 2 * (tid % TPH);
-  const int64_t b = blockIdx.z;
-  const int64_t h = (int64_t)blockIdx.y * HPC + hh;
-  if (h >= p.H) return;
-  const int64_t t_lo = (int64_t)blockIdx.x * p.K;
-  const int64_t t_hi = min(t_lo + p.K, p.nb);
-  const T* A = (const T*)p.a + b * p.sa_b + h * p.sa_h;
-  const int64_t xo = b * p.sx_b + h * p.sx_h + c;
-  const int64_t co = (b * p.H + h) * p.D + c;
-
-  float2 vprev = make_float2(0.f, 0.f);  // carrier v_{t-1}; v_{-1} = carry_in or 0
-  if (t_lo == 0) {
-    if (p.carry_in) vprev = *reinterpret_cast<const float2*>(p.carry_in + co);
-  } else {  // halo: Pass I of block t_lo - 1
-    float a[kEll];
-    float2 u[kEll], w[kEll];
-    load_decays<T>(A, p.sa_l, (t_lo - 1) * kEll, p.L, a);
-    load_u<T, MIX>(p, xo, (t_lo - 1) * kEll, u);
-    local_solve(a, u, w);
-    vprev = w[kEll - 1];
-  }
-
-  for (int64_t t = t_lo; t < t_hi; ++t) {
-    const int64_t n0 = t * kEll;
-    float a[kEll];
-    float2 w[kEll];
-    typename io::raw rq[kEll], rv[kEll];
-    load_decays<T>(A, p.sa_l, n0, p.L, a);
-    if constexpr (!MIX) {
-      float2 u[kEll];
-      load_u<T, false>(p, xo, n0, u);
-      local_solve(a, u, w);
-    } else {
-      typename io::raw rk[kEll];
-      load_raw<T>((const T*)p.k, xo, p.sx_l, n0, p.L, rk);
-      load_raw<T>((const T*)p.v, xo, p.sx_l, n0, p.L, rv);
-      load_raw<T>((const T*)p.q, xo, p.sx_l, n0, p.L, rq);
-      float2 u[kEll];
-#pragma unroll
-      for (int i = 0; i < kEll; ++i) {
-        const float2 kk = io::f2(rk[i]), vv = io::f2(rv[i]);
-        u[i] = make_float2(__fmul_rn(kk.x, vv.x), __fmul_rn(kk.y, vv.y));
-      }
-      local_solve(a, u, w);
-    }
-    float g = 1.f;
-#pragma unroll
-    for (int i = 0; i < kEll; ++i) {
-      g *= a[i];  // g_t[i] = a_t[0] ... a_t[i]
-      const float x0 = fmaf(g, vprev.x, w[i].x);  // Pass II: x~ = w + g v_{t-1}
-      const float x1 = fmaf(g, vprev.y, w[i].y);
-      const int64_t n = n0 + i;
-      if (n < p.L) {
-        if constexpr (!MIX) {
-          io::st((T*)p.x + xo + n * p.sx_l, x0, x1);
-        } else {  // post-gate with residual: y = q x~ + v
-          const float2 qq = io::f2(rq[i]), vv = io::f2(rv[i]);
-          io::st((T*)p.y + xo + n * p.sx_l, fmaf(qq.x, x0, vv.x), fmaf(qq.y, x1, vv.y));
-        }
-      }
-    }
-    vprev = w[kEll - 1];
-  }
-  if (t_hi == p.nb && p.carry_out) *reinterpret_cast<float2*>(p.carry_out + co) = vprev;
-}
-
-// ---------------------------------------------------------------------------
-// backward
-//   lambda_t = L_t^T G_t, mu_t = a_{t+1}[0] lambda_{t+1}[0] (mu_in for the last block),
-//   du_t[i] = lambda_t[i] + r_t[i] mu_t,          r_t[i] = a_t[i+1] ... a_t[15]
-//   da_t[i] = sum_c lambda_t[i] x~_t[i-1] + r_t[i] mu_t w_t[i-1]
-//            (x~_t[-1] = v_{t-1}, w_t[-1] = 0)
-// ---------------------------------------------------------------------------
-#ifndef SWR_FFMA_C_UNROLL
-#define SWR_FFMA_C_UNROLL 4
-#endif
-constexpr int kCUnroll = SWR_FFMA_C_UNROLL;  // pass C unroll (register pressure vs load ILP)
-
-#ifndef SWR_FFMA_BWD_MINB
-#define SWR_FFMA_BWD_MINB 4  // 128 registers: with pass C unrolled by 4, d=16 bwd 936 -> 481 us
-#endif
-// Three passes per block t (walked in reverse, carrying mu from block t+1), so a
-// thread never holds two blocks of per-channel arrays (the registers that capped
-// occupancy): A) Pass I of block t-1 streamed for its carrier v_{t-1} = w_{t-1}[15]
-// (its tiles are read again as block t-1 on the next step, from L2); B) the
-// adjoint recurrence lambda_t = L_t^T G_t in reverse, staged in shared memory
-// ([token][thread], conflict-free), with r_t = suffix products of a_t; C) Pass I of
-// block t forward, pairing w[i-1] with lambda[i]:
-//   du[i] = lambda[i] + r[i] mu,  da[i] = sum_c du[i] w[i-1] + g[i-1] (lambda[i] v)
-// (the same sums as the reverse-mode definition; g[-1] = 1, w[-1] = 0).
-template <typename T, int TPH>
-__global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma(const Params p) {
-  constexpr bool MIX = false;  // SWR only (the mixer uses bwd_ffma_mix)
-  using io = IO<T>;
-  constexpr int HPC = 128 / TPH;
-  constexpr int GS = TPH < 32 ? TPH : 32;
-  __shared__ float red[2][HPC][kEll];
-  __shared__ float2 slam[kEll][128];
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
-  const int hh = tid / TPH;
-  const int c = 2 * (tid % TPH);
-  const int64_t b = blockIdx.z;
-  const int64_t h = (int64_t)blockIdx.y * HPC + hh;
-  const bool act = h < p.H;
-  const int64_t hc = act ? h : p.H - 1;  // inactive threads read a valid head, store nothing
-  const int64_t t_lo = (int64_t)blockIdx.x * p.K;
-  const int64_t t_hi = min(t_lo + p.K, p.nb);
-  const T* A = (const T*)p.a + b * p.sa_b + hc * p.sa_h;
-  T* dA = (T*)p.da + b * p.sa_b + hc * p.sa_h;
-  const int64_t xo = b * p.sx_b + hc * p.sx_h + c;
-  const int64_t co = (b * p.H + hc) * p.D + c;
-
-  // mu for block t_hi - 1: from the right halo block, or mu_in at the end of the sequence
-  float2 mu = make_float2(0.f, 0.f);
-  if (t_hi == p.nb) {
-    if (p.mu_in) mu = *reinterpret_cast<const float2*>(p.mu_in + co);
-  } else {
-    float a[kEll];
-    float2 G[kEll];
-    load_decays<T>(A, p.sa_l, t_hi * kEll, p.L, a);
-    load_G<T, MIX>(p, xo, t_hi * kEll, G);
-    float2 l = G[kEll - 1];
-#pragma unroll
-    for (int i = kEll - 2; i >= 0; --i) l = lambda_step(a[i + 1], l, G[i]);
-    mu = make_float2(a[0] * l.x, a[0] * l.y);
-  }
-
-  int buf = 0;
-  for (int64_t t = t_hi - 1; t >= t_lo; --t) {
-    const int64_t n0 = t * kEll;
-    // A) carrier v_{t-1}
-    float2 vprev = make_float2(0.f, 0.f);
-    if (t > 0) {
-      float a[kEll];
-      float2 u[kEll];
-      load_decays<T>(A, p.sa_l, n0 - kEll, p.L, a);
-      load_u<T, MIX>(p, xo, n0 - kEll, u);
-      float w0 = u[0].x, w1 = u[0].y;
-#pragma unroll
-      for (int i = 1; i < kEll; ++i) {
-        w0 = fmaf(a[i], w0, u[i].x);
-        w1 = fmaf(a[i], w1, u[i].y);
-      }
-      vprev = make_float2(w0, w1);
-    } else if (p.carry_in) {
-      vprev = *reinterpret_cast<const float2*>(p.carry_in + co);
-    }
-    // B) lambda_t in reverse (same op order as lambda_step above), r_t
-    float acur[kEll], r[kEll];
-    load_decays<T>(A, p.sa_l, n0, p.L, acur);
-    {
-      float2 G[kEll];
-      load_G<T, MIX>(p, xo, n0, G);
-      float2 lam = G[kEll - 1];
-      float rr = 1.f;
-      r[kEll - 1] = 1.f;
-      slam[kEll - 1][tid] = lam;
-#pragma unroll
-      for (int i = kEll - 2; i >= 0; --i) {
-        lam = lambda_step(acur[i + 1], lam, G[i]);
-        rr *= acur[i + 1];
-        r[i] = rr;  // r_t[i] = a_t[i+1] ... a_t[15]
-        slam[i][tid] = lam;
-      }
-    }
-    // C) Pass I of block t forward, du and da partials
-    float part[kEll];
-    float2 wprev = make_float2(0.f, 0.f);  // w[i-1]
-    float gs = 1.f;                        // g[i-1]
-    float2 lam0 = slam[0][tid];
-#pragma unroll kCUnroll
-    for (int i = 0; i < kEll; ++i) {
-      const int64_t n = n0 + i;
-      const float2 lam = slam[i][tid];
-      const float du0 = fmaf(r[i], mu.x, lam.x), du1 = fmaf(r[i], mu.y, lam.y);
-      float sdot = du0 * wprev.x;
-      sdot = fmaf(du1, wprev.y, sdot);
-      float lv = lam.x * vprev.x;
-      lv = fmaf(lam.y, vprev.y, lv);
-      part[i] = fmaf(gs, lv, sdot);
-      // w[i] = a[i] w[i-1] + u[i] (w[0] = u[0]: L_t excludes a_t[0])
-      float2 uu;
-      typename io::raw rk, rv;
-      if constexpr (!MIX) {
-        uu = (n < p.L) ? io::f2(io::ld((const T*)p.u + xo + n * p.sx_l)) : make_float2(0.f, 0.f);
-      } else {
-        rk = (n < p.L) ? io::ld((const T*)p.k + xo + n * p.sx_l) : io::zero();
-        rv = (n < p.L) ? io::ld((const T*)p.v + xo + n * p.sx_l) : io::zero();
-        const float2 kk = io::f2(rk), vv = io::f2(rv);
-        uu = make_float2(__fmul_rn(kk.x, vv.x), __fmul_rn(kk.y, vv.y));
-      }
-      const float2 w = (i == 0) ? uu : make_float2(fmaf(acur[i], wprev.x, uu.x), fmaf(acur[i], wprev.y, uu.y));
-      const float gi = gs * acur[i];  // g[i]
-      if (act && n < p.L) {
-        if constexpr (!MIX) {
-          io::st((T*)p.du + xo + n * p.sx_l, du0, du1);
-        } else {
-          const float2 kk = io::f2(rk), vv = io::f2(rv);
-          const float2 dd = io::f2(io::ld((const T*)p.dy + xo + n * p.sx_l));
-          const float x0 = fmaf(gi, vprev.x, w.x), x1 = fmaf(gi, vprev.y, w.y);  // x~[i]
-          io::st((T*)p.dq + xo + n * p.sx_l, dd.x * x0, dd.y * x1);          // dq = dy x~
-          io::st((T*)p.dk + xo + n * p.sx_l, du0 * vv.x, du1 * vv.y);        // dk = du^ v
-          io::st((T*)p.dv + xo + n * p.sx_l, fmaf(du0, kk.x, dd.x), fmaf(du1, kk.y, dd.y));  // dv
-        }
-      }
-      wprev = w;
-      gs = gi;
-    }
-    mu = make_float2(acur[0] * lam0.x, acur[0] * lam0.y);  // for block t-1
-    if (t == 0 && act && p.mu_out) *reinterpret_cast<float2*>(p.mu_out + co) = mu;
-
-    // da: deterministic reduction over the D channels of the head
-    int tok = 0;
-    GroupReduce<GS / 2, kEll>::run(part, lane, tok);
-    if constexpr (TPH <= 32) {
-      constexpr int NV = GS >= kEll ? 1 : kEll / GS;
-      const bool owner = (GS < 32) || ((lane & 1) == 0);
-      if (act && owner) {
-#pragma unroll
-        for (int j = 0; j < NV; ++j)
-          if (n0 + tok + j < p.L) io::st1(dA + (n0 + tok + j) * p.sa_l, part[j]);
-      }
-    } else {
-      const int wih = (tid % TPH) / 32;  // which of the head's two warps
-      if (wih == 1 && (lane & 1) == 0) red[buf][hh][tok] = part[0];
-      __syncthreads();
-      if (wih == 0 && (lane & 1) == 0 && act && n0 + tok < p.L)
-        io::st1(dA + (n0 + tok) * p.sa_l, part[0] + red[buf][hh][tok]);
-      buf ^= 1;
-    }
-  }
-}
-
-// The mixer backward keeps the two-block walk (block t-1's Pass I computed once and
-// reused as the next step's w): its three extra tile reads per token made the
-// three-pass form 10% slower.
-template <typename T, int TPH>
-__global__ void __launch_bounds__(128, 1) bwd_ffma_mix(const Params p) {
-  constexpr bool MIX = true;
-  using io = IO<T>;
-  constexpr int HPC = 128 / TPH;
-  constexpr int GS = TPH < 32 ? TPH : 32;
-  __shared__ float red[2][HPC][kEll];
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
-  const int hh = tid / TPH;
-  const int c = 2 * (tid % TPH);
-  const int64_t b = blockIdx.z;
-  const int64_t h = (int64_t)blockIdx.y * HPC + hh;
-  const bool act = h < p.H;
-  const int64_t hc = act ? h : p.H - 1;  // inactive threads read a valid head, store nothing
-  const int64_t t_lo = (int64_t)blockIdx.x * p.K;
-  const int64_t t_hi = min(t_lo + p.K, p.nb);
-  const T* A = (const T*)p.a + b * p.sa_b + hc * p.sa_h;
-  T* dA = (T*)p.da + b * p.sa_b + hc * p.sa_h;
-  const int64_t xo = b * p.sx_b + hc * p.sx_h + c;
-  const int64_t co = (b * p.H + hc) * p.D + c;
-
-  // mu for block t_hi - 1: from the right halo block, or mu_in at the end of the sequence
-  float2 mu = make_float2(0.f, 0.f);
-  if (t_hi == p.nb) {
-    if (p.mu_in) mu = *reinterpret_cast<const float2*>(p.mu_in + co);
-  } else {
-    float a[kEll];
-    float2 G[kEll];
-    load_decays<T>(A, p.sa_l, t_hi * kEll, p.L, a);
-    load_G<T, MIX>(p, xo, t_hi * kEll, G);
-    float2 l = G[kEll - 1];
-#pragma unroll
-    for (int i = kEll - 2; i >= 0; --i) l = lambda_step(a[i + 1], l, G[i]);
-    mu = make_float2(a[0] * l.x, a[0] * l.y);
-  }
-
-  float acur[kEll];
-  float2 wc[kEll];
-  {
-    float2 u[kEll];
-    load_decays<T>(A, p.sa_l, (t_hi - 1) * kEll, p.L, acur);
-    load_u<T, MIX>(p, xo, (t_hi - 1) * kEll, u);
-    local_solve(acur, u, wc);
-  }
-
-  int buf = 0;
-  for (int64_t t = t_hi - 1; t >= t_lo; --t) {
-    const int64_t n0 = t * kEll;
-    float ap[kEll];
-    float2 wp[kEll];
-    float2 vprev = make_float2(0.f, 0.f);
-    if (t > 0) {  // Pass I of block t-1: carrier v_{t-1} and next iteration's w
-      float2 u[kEll];
-      load_decays<T>(A, p.sa_l, n0 - kEll, p.L, ap);
-      load_u<T, MIX>(p, xo, n0 - kEll, u);
-      local_solve(ap, u, wp);
-      vprev = wp[kEll - 1];
-    } else {
-#pragma unroll
-      for (int i = 0; i < kEll; ++i) {
-        ap[i] = 1.f;
-        wp[i] = make_float2(0.f, 0.f);
-      }
-      if (p.carry_in) vprev = *reinterpret_cast<const float2*>(p.carry_in + co);
-    }
-    float2 G[kEll];
-    load_G<T, MIX>(p, xo, n0, G);
-    typename io::raw rk[kEll], rv[kEll], rdy[kEll];
-    if constexpr (MIX) {
-      load_raw<T>((const T*)p.k, xo, p.sx_l, n0, p.L, rk);
-      load_raw<T>((const T*)p.v, xo, p.sx_l, n0, p.L, rv);
-      load_raw<T>((const T*)p.dy, xo, p.sx_l, n0, p.L, rdy);
-    }
-    float g[kEll];
-    {
-      float gg = 1.f;
-#pragma unroll
-      for (int i = 0; i < kEll; ++i) {
-        gg *= acur[i];
-        g[i] = gg;
-      }
-    }
-    float part[kEll];
-    float2 lam = G[kEll - 1];
-    float2 rmu = mu;
-#pragma unroll
-    for (int i = kEll - 1; i >= 0; --i) {
-      if (i < kEll - 1) {
-        lam = lambda_step(acur[i + 1], lam, G[i]);
-        rmu = make_float2(rmu.x * acur[i + 1], rmu.y * acur[i + 1]);
-      }
-      const float du0 = lam.x + rmu.x, du1 = lam.y + rmu.y;
-      const float2 wpv = (i > 0) ? wc[i - 1] : make_float2(0.f, 0.f);
-      const float2 xpv = (i > 0) ? make_float2(fmaf(g[i - 1], vprev.x, wc[i - 1].x),
-                                               fmaf(g[i - 1], vprev.y, wc[i - 1].y))
-                                 : vprev;
-      float s = lam.x * xpv.x;
-      s = fmaf(lam.y, xpv.y, s);
-      s = fmaf(rmu.x, wpv.x, s);
-      s = fmaf(rmu.y, wpv.y, s);
-      part[i] = s;
-      const int64_t n = n0 + i;
-      if (act && n < p.L) {
-        if constexpr (!MIX) {
-          io::st((T*)p.du + xo + n * p.sx_l, du0, du1);
-        } else {
-          const float2 kk = io::f2(rk[i]), vv = io::f2(rv[i]), dd = io::f2(rdy[i]);
-          const float x0 = fmaf(g[i], vprev.x, wc[i].x), x1 = fmaf(g[i], vprev.y, wc[i].y);
-          io::st((T*)p.dq + xo + n * p.sx_l, dd.x * x0, dd.y * x1);          // dq = dy x~
-          io::st((T*)p.dk + xo + n * p.sx_l, du0 * vv.x, du1 * vv.y);        // dk = du^ v
-          io::st((T*)p.dv + xo + n * p.sx_l, fmaf(du0, kk.x, dd.x), fmaf(du1, kk.y, dd.y));  // dv
-        }
-      }
-    }
-    mu = make_float2(acur[0] * lam.x, acur[0] * lam.y);  // for block t-1
-    if (t == 0 && act && p.mu_out) *reinterpret_cast<float2*>(p.mu_out + co) = mu;
-
-    // da: deterministic reduction over the D channels of the head
-    int tok = 0;
-    GroupReduce<GS / 2, kEll>::run(part, lane, tok);
-    if constexpr (TPH <= 32) {
-      constexpr int NV = GS >= kEll ? 1 : kEll / GS;
-      const bool owner = (GS < 32) || ((lane & 1) == 0);
-      if (act && owner) {
-#pragma unroll
-        for (int j = 0; j < NV; ++j)
-          if (n0 + tok + j < p.L) io::st1(dA + (n0 + tok + j) * p.sa_l, part[j]);
-      }
-    } else {
-      const int wih = (tid % TPH) / 32;  // which of the head's two warps
-      if (wih == 1 && (lane & 1) == 0) red[buf][hh][tok] = part[0];
-      __syncthreads();
-      if (wih == 0 && (lane & 1) == 0 && act && n0 + tok < p.L)
-        io::st1(dA + (n0 + tok) * p.sa_l, part[0] + red[buf][hh][tok]);
-      buf ^= 1;
-    }
-#pragma unroll
-    for (int i = 0; i < kEll; ++i) {
-      acur[i] = ap[i];
-      wc[i] = wp[i];
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------
 // forward, streamed: a thread owns one 16-byte vector of channels (VC = 8 bf16 or
 // 4 fp32) and walks its chunk token by token -- Pass I as the local recurrence
 // (restarted at each block start, w[0] = u[0]), g_t[i] = a_t[0]...a_t[i] as
 // a running product (products only), Pass II x~ = w + g v_{t-1},
 // v_t = w_t[15] -- with one 16-byte load and store per token and tensor and no
-// per-block arrays (the same arithmetic, in the same order, as fwd_ffma).
+// per-block arrays.
 // ---------------------------------------------------------------------------
 template <typename T>
 struct Vec16;
@@ -670,28 +189,24 @@ __global__ void __launch_bounds__(128) fwd_stream(const Params p) {
 }
 
 // ---------------------------------------------------------------------------
-// backward, vectorised (SWR): the three-pass walk of bwd_ffma with a thread owning
+// backward, vectorised: a three-pass walk per block with a thread owning
 // VC channels (one 8- or 16-byte vector per tensor and token), per-block base
 // pointers advanced by the token stride (no per-token 64-bit index products), and
 // the adjoint lambda_t staged in dynamic shared memory as [token][VC/4][thread]
-// float4s.  Same recurrences and op order per channel as bwd_ffma; only the da sum
-// over the head's channels is associated differently (VC-channel chains, then the
-// lane transpose-reduce).
+// float4s.  The da sum over the head's channels is VC-channel chains, then the lane
+// transpose-reduce.
 // ---------------------------------------------------------------------------
 #ifndef SWR_FFMA_BWD_VC
 #define SWR_FFMA_BWD_VC 4  // bf16 channels per thread (4: 8-byte vectors; 8: 16-byte, 20% slower at d=16)
-#endif
-#ifndef SWR_FFMA_BWD_V1
-#define SWR_FFMA_BWD_V1 0  // 1: the two-channel bwd_ffma for SWR
-#endif
-#ifndef SWR_FFMA_MIXB_V1
-#define SWR_FFMA_MIXB_V1 0  // 1: the two-block walk bwd_ffma_mix for the mixer
 #endif
 #ifndef SWR_FFMA_BWDV_UNROLL
 #define SWR_FFMA_BWDV_UNROLL 4  // pass C unroll (16 spills 1.3 KB: 3x slower; 2 or 8: 5-15% slower)
 #endif
 #ifndef SWR_FFMA_MIXBV_UNROLL
 #define SWR_FFMA_MIXBV_UNROLL 2  // the mixer's pass C unroll (4: 12% slower at d=16, spills)
+#endif
+#ifndef SWR_FFMA_BWD_MINB
+#define SWR_FFMA_BWD_MINB 4  // 128 registers
 #endif
 template <bool MIX>
 struct CUnrollV {
@@ -1481,25 +996,6 @@ static cudaError_t launch_fwd_stream(Params p, cudaStream_t st, int sms) {
   return cudaGetLastError();
 }
 
-template <typename T, int TPH, bool MIX, bool BWD>
-static cudaError_t launch_tph(Params p, cudaStream_t st, int sms) {
-  constexpr int HPC = 128 / TPH;
-  const int64_t cols = p.B * ceil_div(p.H, HPC);
-  const int64_t want_chunks = std::max<int64_t>(1, ((int64_t)sms * 8) / std::max<int64_t>(cols, 1));
-  int64_t K = ceil_div(p.nb, want_chunks);
-  K = std::max<int64_t>(K, BWD ? 8 : 4);
-  K = std::min<int64_t>(K, p.nb);
-  p.K = K;
-  dim3 grid((unsigned)ceil_div(p.nb, K), (unsigned)ceil_div(p.H, HPC), (unsigned)p.B);
-  if (BWD && MIX)
-    bwd_ffma_mix<T, TPH><<<grid, 128, 0, st>>>(p);
-  else if (BWD)
-    bwd_ffma<T, TPH><<<grid, 128, 0, st>>>(p);
-  else
-    fwd_ffma<T, TPH, MIX><<<grid, 128, 0, st>>>(p);
-  return cudaGetLastError();
-}
-
 #ifndef SWR_FFMA_BWD_CHUNKS
 #define SWR_FFMA_BWD_CHUNKS 8  // backward: target chunks per SM and (b, head-group) column
 #endif
@@ -1534,19 +1030,10 @@ static cudaError_t launch_bwd_vec_d(const Params& p, cudaStream_t st, int sms) {
 
 template <typename T, bool MIX, bool BWD>
 static cudaError_t launch_d(const Params& p, cudaStream_t st, int sms) {
-  if constexpr (!BWD) {
-    if (!SWR_FFMA_FWD_V1) return launch_fwd_stream<T, MIX>(p, st, sms);
-  } else if constexpr (!MIX) {
-    if (!SWR_FFMA_BWD_V1) return launch_bwd_vec_d<T, false>(p, st, sms);
-  } else {
-    if (!SWR_FFMA_MIXB_V1) return launch_bwd_vec_d<T, true>(p, st, sms);
-  }
-  switch (p.D) {
-    case 16: return launch_tph<T, 8, MIX, BWD>(p, st, sms);
-    case 32: return launch_tph<T, 16, MIX, BWD>(p, st, sms);
-    case 64: return launch_tph<T, 32, MIX, BWD>(p, st, sms);
-    default: return launch_tph<T, 64, MIX, BWD>(p, st, sms);
-  }
+  if constexpr (!BWD)
+    return launch_fwd_stream<T, MIX>(p, st, sms);
+  else
+    return launch_bwd_vec_d<T, MIX>(p, st, sms);
 }
 
 // op: 0 = swr_fwd, 1 = swr_bwd, 2 = mix_fwd, 3 = mix_bwd; bf16 selects the dtype

@@ -83,6 +83,9 @@ constexpr int kHalf = 2048;      // one 64-channel half: 16 rows x 128 B, 128B-s
 #ifndef SWR_B_NI
 #define SWR_B_NI 8
 #endif
+#ifndef SWR_B_BPI
+#define SWR_B_BPI 2
+#endif
 #ifndef SWR_B_NPW
 #define SWR_B_NPW 2
 #endif
@@ -110,7 +113,7 @@ struct Cfg<0> {  // swr_fwd: in u;  out x
 };
 template <>
 struct Cfg<1> {  // swr_bwd: in u, G;  out du
-  static constexpr int NT = 2, NP = 0, BPI = 2, NI = SWR_B_NI, NA = 8, NW = 8, NO = 4, COLS = 32, NPW = SWR_B_NPW, NOUT = 1, NG = SWR_B_NG;
+  static constexpr int NT = 2, NP = 0, BPI = SWR_B_BPI, NI = SWR_B_NI, NA = 8, NW = 8, NO = 4, COLS = 32, NPW = SWR_B_NPW, NOUT = 1, NG = SWR_B_NG;
   static constexpr int TU = 0, TG = 1;
   static constexpr bool CYC = true;
   static constexpr bool WC = false;

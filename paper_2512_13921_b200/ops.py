@@ -19,6 +19,8 @@ effect -- outputs always come back in the caller's logical shape):
     the storage dtype (the ABI has one dtype per call): an fp32 gradient of a
     bf16 layer is rounded once to bf16 (RNE) -- the same rounding the bf16
     forward output already has.
+Every such copy or cast is counted (``layout_copies()``), so a caller -- bench.py
+asserts it for the timed region -- can check that its tensors pass through as is.
 """
 from __future__ import annotations
 
@@ -27,6 +29,17 @@ import torch
 from . import _lib
 
 _DT = {torch.float32: _lib.SWR_F32, torch.bfloat16: _lib.SWR_BF16}
+_copies = 0  # layout copies / dtype casts made by this module (see the module docstring)
+
+
+def layout_copies() -> int:
+    """Number of operand copies (layout) and gradient casts (dtype) made so far."""
+    return _copies
+
+
+def _count(n=1):
+    global _copies
+    _copies += n
 
 
 def _like(t):
@@ -68,6 +81,7 @@ def _prep(*ts):
     ok = all(t.shape == ref.shape and t.stride() == ref.stride() for t in ts) and all(
         _abi_layout(t) for t in ts)
     if not ok:
+        _count(len(ts))
         ts = tuple(t.contiguous() for t in ts)
     return ts
 
@@ -76,8 +90,17 @@ def _prep_a(a):
     """Decays with strides `da` can share: contiguous copy if `a` overlaps itself
     (a zero stride, e.g. a decay row expanded over heads) or is misaligned."""
     if a.dim() == 3 and (not _no_overlap(a) or a.data_ptr() % a.element_size()):
+        _count()
         return a.contiguous()
     return a
+
+
+def _grad_as(g, like):
+    """Upstream gradient in the operands' storage dtype (counted when it is a cast)."""
+    if g.dtype != like.dtype:
+        _count()
+        return g.to(like.dtype)
+    return g
 
 
 def _carry(t, like):
@@ -193,7 +216,7 @@ class SWRFunction(torch.autograd.Function):
     @staticmethod
     def backward(ctx, dx):
         u, a, carry_in = ctx.saved_tensors
-        du, da, mu_out = swr_bwd(u, a, dx.to(u.dtype), carry_in)
+        du, da, mu_out = swr_bwd(u, a, _grad_as(dx, u), carry_in)
         return du, da, (mu_out if carry_in is not None else None)
 
 
@@ -206,7 +229,7 @@ class PhalanxMixFunction(torch.autograd.Function):
     @staticmethod
     def backward(ctx, dy):
         q, k, v, a, carry_in = ctx.saved_tensors
-        dq, dk, dv, da, mu_out = phalanx_mix_bwd(q, k, v, a, dy.to(q.dtype), carry_in)
+        dq, dk, dv, da, mu_out = phalanx_mix_bwd(q, k, v, a, _grad_as(dy, q), carry_in)
         return dq, dk, dv, da, (mu_out if carry_in is not None else None)
 
 
@@ -265,7 +288,7 @@ class LinRecFunction(torch.autograd.Function):
     @staticmethod
     def backward(ctx, dx):
         u, a, carry_in = ctx.saved_tensors
-        du, da, mu_out = swr_exact_bwd(u, a, dx.to(u.dtype), carry_in)
+        du, da, mu_out = swr_exact_bwd(u, a, _grad_as(dx, u), carry_in)
         return du, da, (mu_out if carry_in is not None else None)
 
 

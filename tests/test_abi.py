@@ -117,3 +117,23 @@ def test_python_api_refuses_cpu_tensors(lib):
     a = torch.zeros(1, 16, 1)
     with pytest.raises(ValueError, match="CUDA"):
         P.swr_fwd(u, a)
+
+
+def test_layout_copies_are_counted(lib):
+    """ops._prep passes ABI-ready d-tensors through and counts every copy it makes
+    (layout) and every gradient cast (dtype); no kernel is called here."""
+    import torch
+
+    from paper_2512_13921_b200 import ops
+    x = torch.zeros(2, 32, 4, 16)
+    n0 = ops.layout_copies()
+    (y,) = ops._prep(x)
+    assert y is x and ops.layout_copies() == n0
+    t = torch.zeros(2, 4, 32, 16).transpose(1, 2)  # [B, L, H, D] view of head-major storage
+    ops._prep(x, t)  # strides differ: both copied
+    assert ops.layout_copies() == n0 + 2
+    a = torch.zeros(2, 32, 1).expand(2, 32, 4)  # a decay row shared by the heads
+    assert ops._prep_a(a).is_contiguous() and ops.layout_copies() == n0 + 3
+    g = ops._grad_as(torch.zeros(2, 32, 4, 16, dtype=torch.float64), x)
+    assert g.dtype == x.dtype and ops.layout_copies() == n0 + 4
+    assert ops._grad_as(x, x) is x and ops.layout_copies() == n0 + 4

@@ -172,6 +172,50 @@ SWR_API swr_status phalanx_mix_bwd(const void* q, const void* k, const void* v, 
                            const float* carry_in, const float* mu_in, float* mu_out,
                            swr_shape s, swr_dtype dt, void* stream);
 
+/* ------------------------------------------------------------------------
+ * The Phalanx layer around the mixer
+ * ------------------------------------------------------------------------
+ * The mixer fed directly by the featurization:
+ *   a = sigma(za)   the recurrence coefficient, sigmoid-bounded
+ *   k = sigma(zk)   the key-like gate
+ * with q and k shared by groups of heads ("we apply group sharing separately to K
+ * and Q projections, such that within each group, multiple heads share the same
+ * gate parameters"; 8 groups): q is [B, L, Gq, D], zk is
+ * [B, L, Gk, D], and head h reads group h / (H / Gq) of q and h / (H / Gk) of k
+ * (contiguous head groups, R18).  Then, per head,
+ *   y = q_g (.) SWR_a(k_g (.) v) + v
+ * and the backward returns the gradients of the logits and of the group tensors:
+ *   dza = da (.) a (1 - a),  dzk = (sum over the group's heads of du^ (.) v) (.) k (1 - k),
+ *   dq  = sum over the group's heads of dy (.) x~,  dv = du^ (.) k + dy.
+ * The sums over heads are formed in a fixed head order (deterministic).
+ * sigma is evaluated in fp32 (e^-z by ex2, then an IEEE reciprocal). */
+typedef struct {
+  int64_t Gq, Gk;            /* groups of q and of k; each divides H (Gq = Gk = H: no sharing) */
+  int64_t sq_b, sq_l, sq_h;  /* element strides of q and dq, [B, L, Gq, D], D contiguous      */
+  int64_t sk_b, sk_l, sk_h;  /* element strides of zk and dzk, [B, L, Gk, D], D contiguous    */
+  int32_t logit_a;           /* nonzero: za holds logits, a = sigma(za); else za is a itself  */
+  int32_t logit_k;           /* nonzero: zk holds logits, k = sigma(zk); else zk is k itself  */
+} swr_layer;
+
+/* Layer mixer forward.  v, y [B,L,H,D] with the strides of s; za [B,L,H] with the
+ * decay strides of s; q, zk as described by g; carries as in phalanx_mix.
+ * Errors as above, plus SWR_ERR_SHAPE when Gq or Gk does not divide H and
+ * SWR_ERR_STRIDE / SWR_ERR_ALIGN for the group tensors' strides / pointers. */
+SWR_API swr_status phalanx_layer_mix(const void* q, const void* zk, const void* v, const void* za,
+                             void* y, const float* carry_in, float* carry_out, swr_shape s,
+                             swr_layer g, swr_dtype dt, void* stream);
+
+/* Layer mixer backward.  dq [B,L,Gq,D] and dzk [B,L,Gk,D] with the strides of g
+ * (the group sums), dv [B,L,H,D], dza [B,L,H]; carries as in phalanx_mix_bwd.
+ * The CUDA-core kernel forms the group sums inside one CTA: H / Gq and H / Gk must
+ * be powers of two and at most 256 / (D / 4) (64 at D = 16, 8 at D = 128), else
+ * SWR_ERR_UNSUPPORTED. */
+SWR_API swr_status phalanx_layer_mix_bwd(const void* q, const void* zk, const void* v,
+                                 const void* za, const void* dy, void* dq, void* dzk, void* dv,
+                                 void* dza, const float* carry_in, const float* mu_in,
+                                 float* mu_out, swr_shape s, swr_layer g, swr_dtype dt,
+                                 void* stream);
+
 /* Recurrence-mode decoding (the paper decodes Phalanx "in
  * recurrence mode"): one new token per (b, h).  The state is
  *   w_state [B,H,D] fp32  local state of the current block, w_t[i]

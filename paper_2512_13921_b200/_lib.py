@@ -20,7 +20,7 @@ EXPORTS = ("swr_fwd", "swr_bwd", "phalanx_mix", "phalanx_mix_bwd", "swr_strerror
            "swr_last_cuda_error", "swr_set_path", "swr_launch_count", "swr_last_path",
            "swr_set_trace", "swr_decode_step", "phalanx_mix_decode_step",
            "swr_exact_workspace_bytes", "swr_exact_fwd", "swr_exact_bwd",
-           "swr_uniform_fwd")
+           "swr_uniform_fwd", "phalanx_layer_mix", "phalanx_layer_mix_bwd")
 
 
 class SwrError(RuntimeError):
@@ -35,6 +35,12 @@ class SwrError(RuntimeError):
 class swr_shape(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in
                 ("B", "L", "H", "D", "sx_b", "sx_l", "sx_h", "sa_b", "sa_l", "sa_h")]
+
+
+class swr_layer(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in
+                ("Gq", "Gk", "sq_b", "sq_l", "sq_h", "sk_b", "sk_l", "sk_h")] + [
+                    ("logit_a", ctypes.c_int32), ("logit_k", ctypes.c_int32)]
 
 
 def _load():
@@ -55,10 +61,14 @@ def _load():
     lib.swr_exact_fwd.argtypes = [P, P, P, P, P, P, ctypes.c_int64, S, I, P]
     lib.swr_exact_bwd.argtypes = [P, P, P, P, P, P, P, P, P, ctypes.c_int64, S, I, P]
     lib.swr_uniform_fwd.argtypes = [P, P, P, I, S, I, P]
+    G = swr_layer
+    lib.phalanx_layer_mix.argtypes = [P, P, P, P, P, P, P, S, G, I, P]
+    lib.phalanx_layer_mix_bwd.argtypes = [P, P, P, P, P, P, P, P, P, P, P, P, S, G, I, P]
     lib.swr_exact_workspace_bytes.argtypes = [S]
     lib.swr_exact_workspace_bytes.restype = ctypes.c_int64
     for f in ("swr_fwd", "swr_bwd", "phalanx_mix", "phalanx_mix_bwd", "swr_decode_step",
-              "phalanx_mix_decode_step", "swr_exact_fwd", "swr_exact_bwd", "swr_uniform_fwd"):
+              "phalanx_mix_decode_step", "swr_exact_fwd", "swr_exact_bwd", "swr_uniform_fwd",
+              "phalanx_layer_mix", "phalanx_layer_mix_bwd"):
         getattr(lib, f).restype = I
     lib.swr_strerror.argtypes = [I]
     lib.swr_strerror.restype = ctypes.c_char_p
@@ -149,3 +159,14 @@ def swr_exact_bwd(u, a, dx, du, da, carry_in, mu_in, mu_out, workspace, workspac
 
 def swr_uniform_fwd(u, a, x, k, shape, dtype, stream):
     _check(_lib.swr_uniform_fwd(u, a, x, k, shape, dtype, stream), "swr_uniform_fwd")
+
+
+def phalanx_layer_mix(q, zk, v, za, y, carry_in, carry_out, shape, layer, dtype, stream):
+    _check(_lib.phalanx_layer_mix(q, zk, v, za, y, carry_in, carry_out, shape, layer, dtype, stream),
+           "phalanx_layer_mix")
+
+
+def phalanx_layer_mix_bwd(q, zk, v, za, dy, dq, dzk, dv, dza, carry_in, mu_in, mu_out, shape, layer,
+                          dtype, stream):
+    _check(_lib.phalanx_layer_mix_bwd(q, zk, v, za, dy, dq, dzk, dv, dza, carry_in, mu_in, mu_out, shape,
+                                      layer, dtype, stream), "phalanx_layer_mix_bwd")

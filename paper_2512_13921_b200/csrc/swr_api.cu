@@ -18,6 +18,7 @@ cudaError_t launch_decode(bool mix, bool bf16, const DecParams& p, cudaStream_t 
 cudaError_t launch_exact(bool bf16, Params p, void* workspace, cudaStream_t st, int sms);
 cudaError_t launch_exact_bwd(bool bf16, Params p, void* workspace, cudaStream_t st, int sms);
 cudaError_t launch_uniform(bool bf16, Params p, int k, cudaStream_t st, int sms);
+bool ffma_layer_supported(const Params& p);
 }  // namespace swr
 
 namespace {
@@ -106,6 +107,10 @@ swr::Params make_params(const swr_shape& s) {
   p.sa_l = s.sa_l;
   p.sa_h = s.sa_h;
   p.nb = (s.L + swr::kEll - 1) / swr::kEll;
+  p.hq = p.hk = 1;
+  p.sq_b = p.sk_b = s.sx_b;
+  p.sq_l = p.sk_l = s.sx_l;
+  p.sq_h = p.sk_h = s.sx_h;
   p.trace = g_trace.load();
   p.trace_n = g_trace_n.load();
   return p;
@@ -144,6 +149,7 @@ swr_status dispatch(int op, swr_dtype dt, const swr::Params& p, cudaStream_t st)
     }
     if (e != cudaErrorNotSupported || path == SWR_PATH_TC) return cuda_fail(e);
   }
+  if (op == 5 && !swr::ffma_layer_supported(p)) return SWR_ERR_UNSUPPORTED;
   cudaError_t e = swr::launch_ffma(op, bf16, p, st, sms);
   if (e != cudaSuccess) return cuda_fail(e);
   g_launches += 1;
@@ -241,6 +247,106 @@ swr_status phalanx_mix_bwd(const void* q, const void* k, const void* v, const vo
   p.mu_in = mu_in;
   p.mu_out = mu_out;
   return dispatch(3, dt, p, cs);
+}
+
+}  // extern "C"
+
+namespace {
+// the group description of a layer call: groups divide H; q / k group tensors with
+// D contiguous, 16-byte strides, no zero stride over a dimension of size > 1
+swr_status validate_layer(const swr_shape& s, const swr_layer& g, swr_dtype dt, const void* const* qt, int nq,
+                          const void* const* kt, int nk) {
+  if (g.Gq <= 0 || g.Gk <= 0 || (s.H > 0 && (s.H % g.Gq || s.H % g.Gk))) return SWR_ERR_SHAPE;
+  const int64_t vec = (dt == SWR_BF16) ? 8 : 4;
+  auto strides_ok = [&](int64_t sb, int64_t sl, int64_t sh, int64_t G) {
+    if (sb < 0 || sl < 0 || sh < 0 || sb % vec || sl % vec || sh % vec) return false;
+    return !((s.B > 1 && sb == 0) || (s.L > 1 && sl == 0) || (G > 1 && sh == 0));
+  };
+  if (!strides_ok(g.sq_b, g.sq_l, g.sq_h, g.Gq) || !strides_ok(g.sk_b, g.sk_l, g.sk_h, g.Gk)) return SWR_ERR_STRIDE;
+  const bool empty = s.B == 0 || s.L == 0 || s.H == 0;
+  for (int i = 0; i < nq; ++i) {
+    if (!empty && !qt[i]) return SWR_ERR_NULL;
+    if (!aligned16(qt[i])) return SWR_ERR_ALIGN;
+  }
+  for (int i = 0; i < nk; ++i) {
+    if (!empty && !kt[i]) return SWR_ERR_NULL;
+    if (!aligned16(kt[i])) return SWR_ERR_ALIGN;
+  }
+  return SWR_OK;
+}
+
+void set_layer(swr::Params& p, const swr_shape& s, const swr_layer& g) {
+  p.logit_a = g.logit_a != 0;
+  p.logit_k = g.logit_k != 0;
+  p.hq = s.H / g.Gq;
+  p.hk = s.H / g.Gk;
+  p.sq_b = g.sq_b;
+  p.sq_l = g.sq_l;
+  p.sq_h = g.sq_h;
+  p.sk_b = g.sk_b;
+  p.sk_l = g.sk_l;
+  p.sk_h = g.sk_h;
+}
+}  // namespace
+
+extern "C" {
+
+swr_status phalanx_layer_mix(const void* q, const void* zk, const void* v, const void* za, void* y,
+                             const float* carry_in, float* carry_out, swr_shape s, swr_layer g, swr_dtype dt,
+                             void* stream) {
+  const void* dt_[] = {v, y};
+  const void* at_[] = {za};
+  const void* ct_[] = {carry_in, carry_out};
+  swr_status st = validate(s, dt, dt_, 2, at_, 1, ct_, 2);
+  if (st != SWR_OK) return st;
+  const void* qt_[] = {q};
+  const void* kt_[] = {zk};
+  st = validate_layer(s, g, dt, qt_, 1, kt_, 1);
+  if (st != SWR_OK) return st;
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  if (s.B == 0 || s.H == 0 || s.L == 0) return empty_call(s, carry_out, nullptr, cs);
+  swr::Params p = make_params(s);
+  set_layer(p, s, g);
+  p.q = q;
+  p.k = zk;
+  p.v = v;
+  p.a = za;
+  p.y = y;
+  p.carry_in = carry_in;
+  p.carry_out = carry_out;
+  return dispatch(4, dt, p, cs);
+}
+
+swr_status phalanx_layer_mix_bwd(const void* q, const void* zk, const void* v, const void* za, const void* dy,
+                                 void* dq, void* dzk, void* dv, void* dza, const float* carry_in,
+                                 const float* mu_in, float* mu_out, swr_shape s, swr_layer g, swr_dtype dt,
+                                 void* stream) {
+  const void* dt_[] = {v, dy, dv};
+  const void* at_[] = {za, dza};
+  const void* ct_[] = {carry_in, mu_in, mu_out};
+  swr_status st = validate(s, dt, dt_, 3, at_, 2, ct_, 3);
+  if (st != SWR_OK) return st;
+  const void* qt_[] = {q, dq};
+  const void* kt_[] = {zk, dzk};
+  st = validate_layer(s, g, dt, qt_, 2, kt_, 2);
+  if (st != SWR_OK) return st;
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  if (s.B == 0 || s.H == 0 || s.L == 0) return empty_call(s, nullptr, mu_out, cs);
+  swr::Params p = make_params(s);
+  set_layer(p, s, g);
+  p.q = q;
+  p.k = zk;
+  p.v = v;
+  p.a = za;
+  p.dy = dy;
+  p.dq = dq;
+  p.dk = dzk;
+  p.dv = dv;
+  p.da = dza;
+  p.carry_in = carry_in;
+  p.mu_in = mu_in;
+  p.mu_out = mu_out;
+  return dispatch(5, dt, p, cs);
 }
 
 }  // extern "C"
@@ -399,7 +505,7 @@ const char* swr_strerror(swr_status st) {
     case SWR_ERR_DTYPE: return "SWR_ERR_DTYPE: unknown dtype";
     case SWR_ERR_CUDA: return "SWR_ERR_CUDA: CUDA error (see swr_last_cuda_error)";
     case SWR_ERR_ARCH: return "SWR_ERR_ARCH: current device is not sm_100 (B200)";
-    case SWR_ERR_UNSUPPORTED: return "SWR_ERR_UNSUPPORTED: SWR_PATH_TC forced for a call outside the tensor-core envelope (bf16, D = 128, TMA-addressable decays)";
+    case SWR_ERR_UNSUPPORTED: return "SWR_ERR_UNSUPPORTED: SWR_PATH_TC forced for a call outside the tensor-core envelope (bf16, D = 128, TMA-addressable decays), or a layer backward whose head groups do not fit one CTA";
   }
   return "unknown swr_status";
 }

@@ -38,6 +38,15 @@ struct Params {
   int64_t sa_b, sa_l, sa_h;
   int64_t nb;  // number of 16-token blocks, ceil(L/16)
   int64_t K;   // blocks per walk (FFMA path)
+  // Phalanx layer around the mixer (phalanx_layer_mix*):
+  // logit_a / logit_k: a / k hold logits, the kernels apply sigma
+  // and the backward writes the logits' gradients; q and k are group-shared
+  // [B, L, G, D] tensors, head h reading group h / hq (resp. h / hk).
+  // The plain mixer ops run with hq = hk = 1 and q/k strides equal to sx.
+  int logit_a, logit_k;
+  int64_t hq, hk;               // heads per q group, per k group
+  int64_t sq_b, sq_l, sq_h;     // element strides of q and dq
+  int64_t sk_b, sk_l, sk_h;     // element strides of k and dk
   unsigned long long* trace;  // diagnostics (swr_set_trace), NULL = off
   int64_t trace_n;
   uint32_t epoch;  // TC path: launch ticket of the range claims (set by launch_tc)
@@ -57,6 +66,11 @@ struct DecParams {
   int64_t sx_b, sx_h, sa_b, sa_h;
   int64_t pos;    // sequence position of the token
 };
+
+// sigma(z) = 1 / (1 + e^-z) in fp32 (the featurization's bounding activation,
+// P:1562): e^-z from ex2 (relative error ~2^-22), then an IEEE reciprocal;
+// saturates to exactly 0 / 1 for |z| large.
+__device__ __forceinline__ float sigmoid_f(float z) { return __frcp_rn(1.f + __expf(-z)); }
 
 // ---------------------------------------------------------------------------
 // storage-dtype traits: 2-channel vector loads/stores, scalar decay access

@@ -70,8 +70,11 @@ struct Vec16<float> {
   }
 };
 
-template <typename T, bool MIX>
-__device__ __forceinline__ void load_u16(const Params& p, int64_t off, bool valid, float (&u)[Vec16<T>::N]) {
+// Pass-I input of one token: u (SWR) or u^ = k (.) v (pre-gate); LAYER: k
+// may be a logit, k = sigma(zk), read from its group's tensor at ko.
+template <typename T, bool MIX, bool LAYER>
+__device__ __forceinline__ void load_u16(const Params& p, int64_t off, int64_t ko, bool valid,
+                                         float (&u)[Vec16<T>::N]) {
   constexpr int VC = Vec16<T>::N;
   if (!valid) {
 #pragma unroll
@@ -80,16 +83,30 @@ __device__ __forceinline__ void load_u16(const Params& p, int64_t off, bool vali
   }
   if constexpr (!MIX) {
     Vec16<T>::to_f(__ldg(reinterpret_cast<const uint4*>((const T*)p.u + off)), u);
-  } else {  // u^ = k (.) v
+  } else {
     float kk[VC], vv[VC];
-    Vec16<T>::to_f(__ldg(reinterpret_cast<const uint4*>((const T*)p.k + off)), kk);
+    Vec16<T>::to_f(__ldg(reinterpret_cast<const uint4*>((const T*)p.k + (LAYER ? ko : off))), kk);
     Vec16<T>::to_f(__ldg(reinterpret_cast<const uint4*>((const T*)p.v + off)), vv);
+    if (LAYER && p.logit_k) {
+#pragma unroll
+      for (int e = 0; e < VC; ++e) kk[e] = sigmoid_f(kk[e]);
+    }
 #pragma unroll
     for (int e = 0; e < VC; ++e) u[e] = __fmul_rn(kk[e], vv[e]);
   }
 }
 
-template <typename T, bool MIX>
+// decay of token n: a, or (LAYER, logit_a) a = sigma(za); pad a = 1 past L
+template <typename T, bool LAYER>
+__device__ __forceinline__ float ld_decay(const Params& p, const T* A, int64_t n, bool valid) {
+  if (!valid) return 1.f;
+  const float z = IO<T>::ld1(A + n * p.sa_l);
+  return (LAYER && p.logit_a) ? sigmoid_f(z) : z;
+}
+
+// LAYER: the Phalanx layer around the mixer (phalanx_layer_mix): logits and
+// group-shared q / k (Params); otherwise the plain SWR / mixer ops.
+template <typename T, bool MIX, bool LAYER>
 __global__ void __launch_bounds__(128) fwd_stream(const Params p) {
   constexpr int VC = Vec16<T>::N;
   const int TPH = (int)p.D / VC;  // threads per head
@@ -104,6 +121,10 @@ __global__ void __launch_bounds__(128) fwd_stream(const Params p) {
   const int64_t t_hi = min(t_lo + p.K, p.nb);
   const T* A = (const T*)p.a + b * p.sa_b + h * p.sa_h;
   const int64_t xo = b * p.sx_b + h * p.sx_h + c;
+  // group-shared gates (LAYER): q of group h / hq, k of group h / hk
+  const int64_t qo = LAYER ? b * p.sq_b + (h / p.hq) * p.sq_h + c : xo;
+  const int64_t ko = LAYER ? b * p.sk_b + (h / p.hk) * p.sk_h + c : xo;
+  const int64_t sql = LAYER ? p.sq_l : p.sx_l, skl = LAYER ? p.sk_l : p.sx_l;
   const int64_t co = (b * p.H + h) * p.D + c;
 
   float v[VC];  // carrier v_{t-1}; v_{-1} = carry_in or 0
@@ -120,9 +141,9 @@ __global__ void __launch_bounds__(128) fwd_stream(const Params p) {
     for (int i = 0; i < kEll; ++i) {
       const int64_t n = (t_lo - 1) * kEll + i;
       const bool valid = n < p.L;
-      const float a = valid ? IO<T>::ld1(A + n * p.sa_l) : 1.f;
+      const float a = ld_decay<T, LAYER>(p, A, n, valid);
       float u[VC];
-      load_u16<T, MIX>(p, xo + n * p.sx_l, valid, u);
+      load_u16<T, MIX, LAYER>(p, xo + n * p.sx_l, ko + n * skl, valid, u);
 #pragma unroll
       for (int e = 0; e < VC; ++e) w[e] = (i == 0) ? u[e] : fmaf(a, w[e], u[e]);
     }
@@ -156,8 +177,8 @@ __global__ void __launch_bounds__(128) fwd_stream(const Params p) {
         a = ab[i];
         Vec16<T>::to_f(ub[i], u);
       } else {
-        a = valid ? IO<T>::ld1(A + n * p.sa_l) : 1.f;
-        load_u16<T, true>(p, xo + n * p.sx_l, valid, u);
+        a = ld_decay<T, LAYER>(p, A, n, valid);
+        load_u16<T, true, LAYER>(p, xo + n * p.sx_l, ko + n * skl, valid, u);
       }
       g *= a;  // g_t[i] = a_t[0] ... a_t[i]
       float x[VC];
@@ -171,7 +192,7 @@ __global__ void __launch_bounds__(128) fwd_stream(const Params p) {
           *reinterpret_cast<uint4*>((T*)p.x + xo + n * p.sx_l) = Vec16<T>::from_f(x);
         } else {  // post-gate with residual: y = q x~ + v
           float qq[VC], vv[VC];
-          Vec16<T>::to_f(__ldg(reinterpret_cast<const uint4*>((const T*)p.q + xo + n * p.sx_l)), qq);
+          Vec16<T>::to_f(__ldg(reinterpret_cast<const uint4*>((const T*)p.q + qo + n * sql)), qq);
           Vec16<T>::to_f(__ldg(reinterpret_cast<const uint4*>((const T*)p.v + xo + n * p.sx_l)), vv);
 #pragma unroll
           for (int e = 0; e < VC; ++e) x[e] = fmaf(qq[e], x[e], vv[e]);
@@ -249,14 +270,21 @@ struct VecN {
   }
 };
 
-template <typename T, int VC, int TPH, bool MIX>
-__global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma_vec(const Params p) {
+// LAYER (phalanx_layer_mix_bwd, mixer only): a and k may be logits (sigma applied
+// on load; dza = da a (1 - a), dzk = dk k (1 - k)), and q / k are group-shared
+// tensors [B, L, G, D] read by hq / hk consecutive heads; their gradients are the
+// sums over the group's heads, formed in the CTA in a fixed head
+// order (deterministic): the CTA holds NTH / TPH heads, a multiple of hq and hk.
+// dq is staged over the lambda slots it replaces, dk in a second buffer.
+template <typename T, int VC, int TPH, bool MIX, bool LAYER = false, int NTH = 128>
+__global__ void __launch_bounds__(NTH, NTH == 128 ? SWR_FFMA_BWD_MINB : 1) bwd_ffma_vec(const Params p) {
   using V = VecN<T, VC>;
   using io = IO<T>;
-  constexpr int HPC = 128 / TPH;
+  static_assert(!LAYER || MIX, "the layer options apply to the mixer");
+  constexpr int HPC = NTH / TPH;
   constexpr int GS = TPH;  // lanes per head (<= 32)
   constexpr int NQ = VC / 4;
-  extern __shared__ float4 slam[];  // [kEll][NQ][128]
+  extern __shared__ float4 slam[];  // [kEll][NQ][NTH]; LAYER: then dk staging [kEll][NQ][NTH]
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int hh = tid / TPH;
@@ -269,25 +297,38 @@ __global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma_vec(const Par
   const int64_t t_hi = min(t_lo + p.K, p.nb);
   const int64_t sl = p.sx_l, sal = p.sa_l;
   const int64_t xo = b * p.sx_b + hc * p.sx_h + c;
+  // group-shared gates (LAYER): q of group h / hq, k of group h / hk
+  const int64_t qo = LAYER ? b * p.sq_b + (hc / p.hq) * p.sq_h + c : xo;
+  const int64_t ko = LAYER ? b * p.sk_b + (hc / p.hk) * p.sk_h + c : xo;
+  const int64_t sql = LAYER ? p.sq_l : sl, skl = LAYER ? p.sk_l : sl;
+  const bool sig_a = LAYER && p.logit_a, sig_k = LAYER && p.logit_k;
   const int64_t co = (b * p.H + hc) * p.D + c;
   const T* A0 = (const T*)p.a + b * p.sa_b + hc * p.sa_h;
   T* dA = (T*)p.da + b * p.sa_b + hc * p.sa_h;
-  auto lam_at = [&](int i, int q) -> float4& { return slam[(i * NQ + q) * 128 + tid]; };
+  auto lam_at = [&](int i, int q) -> float4& { return slam[(i * NQ + q) * NTH + tid]; };
+  auto dk_at = [&](int i, int q, int th) -> float4& { return slam[((kEll + i) * NQ + q) * NTH + th]; };
+  auto dq_at = [&](int i, int q, int th) -> float4& { return slam[(i * NQ + q) * NTH + th]; };
+  auto decay = [&](const T* ap) {  // a, or a = sigma(za)
+    const float z = io::ld1(ap);
+    return sig_a ? sigmoid_f(z) : z;
+  };
 
   // decays of a block (pad a = 1 past L)
   auto load_a = [&](int64_t n0, int lim, float (&a)[kEll]) {
     const T* ap = A0 + n0 * sal;
 #pragma unroll
     for (int i = 0; i < kEll; ++i) {
-      a[i] = (i < lim) ? io::ld1(ap) : 1.f;
+      a[i] = (i < lim) ? decay(ap) : 1.f;
       ap += sal;
     }
   };
   // A stream of Pass-I inputs (u, or u^ = k (.) v: pre-gate) or of adjoint
-  // inputs (dx, or G = dy (.) q), walked by pointers stepped by the token stride.
+  // inputs (dx, or G = dy (.) q), walked by pointers stepped by the token strides.
   struct Src {
     const T* p0;
-    const T* p1;  // mixer: the second factor
+    const T* p1;   // mixer: the second factor
+    int64_t s0, s1;
+    bool sig0;     // LAYER: p0 holds logits (k = sigma(zk))
     __device__ __forceinline__ void load(bool valid, float (&x)[VC]) const {
       if constexpr (!MIX) {
         V::to_f(valid ? V::ld(p0) : V::zero(), x);
@@ -295,22 +336,30 @@ __global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma_vec(const Par
         float f0[VC], f1[VC];
         V::to_f(valid ? V::ld(p0) : V::zero(), f0);
         V::to_f(valid ? V::ld(p1) : V::zero(), f1);
+        if (LAYER && sig0) {
+#pragma unroll
+          for (int e = 0; e < VC; ++e) f0[e] = valid ? sigmoid_f(f0[e]) : 0.f;
+        }
 #pragma unroll
         for (int e = 0; e < VC; ++e) x[e] = __fmul_rn(f0[e], f1[e]);
       }
     }
-    __device__ __forceinline__ void step(int64_t d) {
-      p0 += d;
-      if constexpr (MIX) p1 += d;
+    __device__ __forceinline__ void fwd() {
+      p0 += s0;
+      if constexpr (MIX) p1 += s1;
+    }
+    __device__ __forceinline__ void back() {
+      p0 -= s0;
+      if constexpr (MIX) p1 -= s1;
     }
   };
   auto src_u = [&](int64_t n) {
-    const int64_t o = xo + n * sl;
-    return MIX ? Src{(const T*)p.k + o, (const T*)p.v + o} : Src{(const T*)p.u + o, nullptr};
+    return MIX ? Src{(const T*)p.k + ko + n * skl, (const T*)p.v + xo + n * sl, skl, sl, sig_k}
+               : Src{(const T*)p.u + xo + n * sl, nullptr, sl, 0, false};
   };
   auto src_g = [&](int64_t n) {
-    const int64_t o = xo + n * sl;
-    return MIX ? Src{(const T*)p.dy + o, (const T*)p.q + o} : Src{(const T*)p.dx + o, nullptr};
+    return MIX ? Src{(const T*)p.dy + xo + n * sl, (const T*)p.q + qo + n * sql, sl, sql, false}
+               : Src{(const T*)p.dx + xo + n * sl, nullptr, sl, 0, false};
   };
 
   // mu for block t_hi - 1: a_{t_hi}[0] lambda_{t_hi}[0] from the right halo block, or mu_in
@@ -333,7 +382,7 @@ __global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma_vec(const Par
 #pragma unroll
     for (int i = kEll - 2; i >= 0; --i) {
       float g[VC];
-      gsrc.step(-sl);
+      gsrc.back();
       gsrc.load(i < lim, g);
 #pragma unroll
       for (int e = 0; e < VC; ++e) l[e] = fmaf(a[i + 1], l[e], g[e]);
@@ -342,6 +391,8 @@ __global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma_vec(const Par
     for (int e = 0; e < VC; ++e) mu[e] = a[0] * l[e];
   }
 
+  // LAYER group sums: does this CTA stage dq / dk (more than one head per group)?
+  const bool grp_q = LAYER && p.hq > 1, grp_k = LAYER && p.hk > 1;
   for (int64_t t = t_hi - 1; t >= t_lo; --t) {
     const int64_t n0 = t * kEll;
     const int lim = (p.L - n0 < kEll) ? (int)(p.L - n0) : kEll;
@@ -352,11 +403,11 @@ __global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma_vec(const Par
       Src usrc = src_u(n0 - kEll);
 #pragma unroll
       for (int i = 0; i < kEll; ++i) {
-        const float a = io::ld1(ap);
+        const float a = decay(ap);
         float u[VC];
         usrc.load(true, u);
         ap += sal;
-        usrc.step(sl);
+        usrc.fwd();
 #pragma unroll
         for (int e = 0; e < VC; ++e) vprev[e] = (i == 0) ? u[e] : fmaf(a, vprev[e], u[e]);
       }
@@ -379,7 +430,7 @@ __global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma_vec(const Par
 #pragma unroll
       for (int i = kEll - 2; i >= 0; --i) {
         float g[VC];
-        gsrc.step(-sl);
+        gsrc.back();
         gsrc.load(i < lim, g);
 #pragma unroll
         for (int e = 0; e < VC; ++e) lam[e] = fmaf(acur[i + 1], lam[e], g[e]);
@@ -392,8 +443,10 @@ __global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma_vec(const Par
     // C) Pass I of block t forward, du (mixer: dq, dk, dv) and da partials
     float part[kEll];
     float wprev[VC];
+    float mu_next[VC];  // mu for block t-1: a_t[0] lambda_t[0]
     float gs = 1.f;  // g[i-1]
     int64_t o = xo + n0 * sl;
+    int64_t ok = ko + n0 * skl, oq = qo + n0 * sql;
 #pragma unroll CUnrollV<MIX>::v
     for (int i = 0; i < kEll; ++i) {
       float lam[VC];
@@ -401,6 +454,10 @@ __global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma_vec(const Par
       for (int q = 0; q < NQ; ++q) {
         const float4 l4 = lam_at(i, q);
         lam[4 * q] = l4.x; lam[4 * q + 1] = l4.y; lam[4 * q + 2] = l4.z; lam[4 * q + 3] = l4.w;
+      }
+      if (i == 0) {
+#pragma unroll
+        for (int e = 0; e < VC; ++e) mu_next[e] = acur[0] * lam[e];
       }
       float du[VC];
       float sdot = 0.f, lv = 0.f;  // sum_c du[i] w[i-1] (w[-1] = 0), sum_c lambda[i] v_{t-1}
@@ -411,44 +468,61 @@ __global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma_vec(const Par
         lv = (e == 0) ? lam[e] * vprev[e] : fmaf(lam[e], vprev[e], lv);
       }
       part[i] = fmaf(gs, lv, sdot);
+      if (sig_a) part[i] *= acur[i] * (1.f - acur[i]);  // dza = da sigma'(za), sigma' = a (1 - a)
       const bool valid = i < lim;
       float kk[VC], vv[VC], u[VC];
       if constexpr (!MIX) {
         V::to_f(valid ? V::ld((const T*)p.u + o) : V::zero(), u);
       } else {
-        V::to_f(valid ? V::ld((const T*)p.k + o) : V::zero(), kk);
+        V::to_f(valid ? V::ld((const T*)p.k + (LAYER ? ok : o)) : V::zero(), kk);
         V::to_f(valid ? V::ld((const T*)p.v + o) : V::zero(), vv);
+        if (sig_k) {
+#pragma unroll
+          for (int e = 0; e < VC; ++e) kk[e] = valid ? sigmoid_f(kk[e]) : 0.f;
+        }
 #pragma unroll
         for (int e = 0; e < VC; ++e) u[e] = __fmul_rn(kk[e], vv[e]);
       }
 #pragma unroll
       for (int e = 0; e < VC; ++e) wprev[e] = (i == 0) ? u[e] : fmaf(acur[i], wprev[e], u[e]);
       gs *= acur[i];  // g[i]
-      if (act && valid) {
-        if constexpr (!MIX) {
-          V::st((T*)p.du + o, du);
-        } else {
-          float dd[VC], out[VC];
-          V::to_f(V::ld((const T*)p.dy + o), dd);
+      if constexpr (!MIX) {
+        if (act && valid) V::st((T*)p.du + o, du);
+      } else {
+        float dd[VC], dq[VC], dk[VC], dv[VC];
+        V::to_f(valid ? V::ld((const T*)p.dy + o) : V::zero(), dd);
 #pragma unroll
-          for (int e = 0; e < VC; ++e) out[e] = dd[e] * fmaf(gs, vprev[e], wprev[e]);  // dq = dy x~
-          V::st((T*)p.dq + o, out);
+        for (int e = 0; e < VC; ++e) {
+          dq[e] = dd[e] * fmaf(gs, vprev[e], wprev[e]);  // dq = dy x~
+          dk[e] = du[e] * vv[e];                         // dk = du^ v
+          dv[e] = fmaf(du[e], kk[e], dd[e]);             // dv = du^ k + dy
+        }
+        if (sig_k) {
 #pragma unroll
-          for (int e = 0; e < VC; ++e) out[e] = du[e] * vv[e];  // dk = du^ v
-          V::st((T*)p.dk + o, out);
+          for (int e = 0; e < VC; ++e) dk[e] *= kk[e] * (1.f - kk[e]);  // dzk = dk sigma'(zk)
+        }
+        if (act && valid) {
+          V::st((T*)p.dv + o, dv);
+          if (!grp_q) V::st((T*)p.dq + (LAYER ? oq : o), dq);
+          if (!grp_k) V::st((T*)p.dk + (LAYER ? ok : o), dk);
+        }
+        if constexpr (LAYER) {  // stage the per-head terms of the group sums
+          if (grp_q) {
 #pragma unroll
-          for (int e = 0; e < VC; ++e) out[e] = fmaf(du[e], kk[e], dd[e]);  // dv = du^ k + dy
-          V::st((T*)p.dv + o, out);
+            for (int q = 0; q < NQ; ++q) dq_at(i, q, tid) = make_float4(dq[4 * q], dq[4 * q + 1], dq[4 * q + 2], dq[4 * q + 3]);
+          }
+          if (grp_k) {
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) dk_at(i, q, tid) = make_float4(dk[4 * q], dk[4 * q + 1], dk[4 * q + 2], dk[4 * q + 3]);
+          }
         }
       }
       o += sl;
+      ok += skl;
+      oq += sql;
     }
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) {  // mu for block t-1: a_t[0] lambda_t[0]
-      const float4 l4 = lam_at(0, q);
-      mu[4 * q] = acur[0] * l4.x; mu[4 * q + 1] = acur[0] * l4.y;
-      mu[4 * q + 2] = acur[0] * l4.z; mu[4 * q + 3] = acur[0] * l4.w;
-    }
+    for (int e = 0; e < VC; ++e) mu[e] = mu_next[e];
     if (t == 0 && act && p.mu_out) {
 #pragma unroll
       for (int e = 0; e < VC; ++e) p.mu_out[co + e] = mu[e];
@@ -462,6 +536,37 @@ __global__ void __launch_bounds__(128, SWR_FFMA_BWD_MINB) bwd_ffma_vec(const Par
 #pragma unroll
       for (int j = 0; j < NV; ++j)
         if (tok + j < lim) io::st1(dA + (n0 + tok + j) * sal, part[j]);
+    }
+    if constexpr (LAYER) {
+      // group sums of dq (hq heads) and dk (hk heads): the j-th head of a group sums
+      // tokens i = j (mod heads per group) over the group's heads in head order
+      if (grp_q || grp_k) {
+        __syncthreads();
+        auto gsum = [&](int64_t hpg, bool is_q) {
+          const int j = hh % (int)hpg, th0 = (hh - j) * TPH + (tid % TPH);  // head 0 of the group
+          T* base = (T*)(is_q ? p.dq : p.dk) + (is_q ? qo + n0 * sql : ko + n0 * skl);
+          const int64_t stl = is_q ? sql : skl;
+          for (int i = j; i < lim; i += (int)hpg) {
+            float acc[VC];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+              const float4 x = is_q ? dq_at(i, q, th0) : dk_at(i, q, th0);
+              acc[4 * q] = x.x; acc[4 * q + 1] = x.y; acc[4 * q + 2] = x.z; acc[4 * q + 3] = x.w;
+            }
+            for (int m = 1; m < (int)hpg; ++m) {
+#pragma unroll
+              for (int q = 0; q < NQ; ++q) {
+                const float4 x = is_q ? dq_at(i, q, th0 + m * TPH) : dk_at(i, q, th0 + m * TPH);
+                acc[4 * q] += x.x; acc[4 * q + 1] += x.y; acc[4 * q + 2] += x.z; acc[4 * q + 3] += x.w;
+              }
+            }
+            if (act) V::st(base + i * stl, acc);
+          }
+        };
+        if (grp_q) gsum(p.hq, true);
+        if (grp_k) gsum(p.hk, false);
+        __syncthreads();  // the staging slots are rewritten by the next block
+      }
     }
   }
 }
@@ -983,7 +1088,7 @@ static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 #define SWR_FFMA_MIXF_CHUNKS 8  // mixer (one CTA per SM: 4 is 65% slower)
 #endif
 // forward (SWR and mixer): the streamed kernel, 16 bytes of channels per thread
-template <typename T, bool MIX>
+template <typename T, bool MIX, bool LAYER = false>
 static cudaError_t launch_fwd_stream(Params p, cudaStream_t st, int sms) {
   const int64_t hpc = 128 / (p.D / Vec16<T>::N);
   const int64_t cols = p.B * ceil_div(p.H, hpc);
@@ -992,28 +1097,30 @@ static cudaError_t launch_fwd_stream(Params p, cudaStream_t st, int sms) {
   int64_t K = std::min<int64_t>(std::max<int64_t>(ceil_div(p.nb, want_chunks), 4), p.nb);
   p.K = K;
   dim3 grid((unsigned)ceil_div(p.nb, K), (unsigned)ceil_div(p.H, hpc), (unsigned)p.B);
-  fwd_stream<T, MIX><<<grid, 128, 0, st>>>(p);
+  fwd_stream<T, MIX, LAYER><<<grid, 128, 0, st>>>(p);
   return cudaGetLastError();
 }
 
 #ifndef SWR_FFMA_BWD_CHUNKS
 #define SWR_FFMA_BWD_CHUNKS 8  // backward: target chunks per SM and (b, head-group) column
 #endif
-template <typename T, int VC, int TPH, bool MIX>
+template <typename T, int VC, int TPH, bool MIX, bool LAYER = false, int NTH = 128>
 static cudaError_t launch_bwd_vec(Params p, cudaStream_t st, int sms) {
-  constexpr int HPC = 128 / TPH;
-  constexpr int kSmem = kEll * VC * 128 * 4;
-  if constexpr (kSmem > 48 * 1024) {  // only the 8-channel bf16 variant; set per call (per device)
-    cudaError_t e = cudaFuncSetAttribute(bwd_ffma_vec<T, VC, TPH, MIX>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+  constexpr int HPC = NTH / TPH;
+  // lambda staging [kEll][VC/4][NTH] float4; LAYER: + the dk staging of the group sums
+  constexpr int kSmem = kEll * VC * NTH * 4 * (LAYER ? 2 : 1);
+  if constexpr (kSmem > 48 * 1024) {  // set per call (per device)
+    cudaError_t e = cudaFuncSetAttribute(bwd_ffma_vec<T, VC, TPH, MIX, LAYER, NTH>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     if (e != cudaSuccess) return e;
   }
   const int64_t cols = p.B * ceil_div(p.H, HPC);
-  const int64_t want_chunks = std::max<int64_t>(1, ((int64_t)sms * SWR_FFMA_BWD_CHUNKS) / std::max<int64_t>(cols, 1));
+  const int64_t want_chunks = std::max<int64_t>(1, ((int64_t)sms * SWR_FFMA_BWD_CHUNKS * 128 / NTH) / std::max<int64_t>(cols, 1));
   int64_t K = std::max<int64_t>(ceil_div(p.nb, want_chunks), 8);
   K = std::min<int64_t>(K, p.nb);
   p.K = K;
   dim3 grid((unsigned)ceil_div(p.nb, K), (unsigned)ceil_div(p.H, HPC), (unsigned)p.B);
-  bwd_ffma_vec<T, VC, TPH, MIX><<<grid, 128, kSmem, st>>>(p);
+  bwd_ffma_vec<T, VC, TPH, MIX, LAYER, NTH><<<grid, NTH, kSmem, st>>>(p);
   return cudaGetLastError();
 }
 
@@ -1028,6 +1135,22 @@ static cudaError_t launch_bwd_vec_d(const Params& p, cudaStream_t st, int sms) {
   }
 }
 
+// The layer backward: a CTA of NTH threads holds NTH / TPH heads, which must be a
+// multiple of the heads per q group and per k group (ffma_layer_supported).
+constexpr int kVC4 = 4;
+template <typename T>
+static cudaError_t launch_layer_bwd(const Params& p, cudaStream_t st, int sms) {
+  const int tph = (int)p.D / kVC4;
+  const int64_t hpg = std::max(p.hq, p.hk);
+  const bool wide = 128 / tph < hpg;  // 256 threads
+  switch (p.D) {
+    case 16: return wide ? launch_bwd_vec<T, 4, 4, true, true, 256>(p, st, sms) : launch_bwd_vec<T, 4, 4, true, true, 128>(p, st, sms);
+    case 32: return wide ? launch_bwd_vec<T, 4, 8, true, true, 256>(p, st, sms) : launch_bwd_vec<T, 4, 8, true, true, 128>(p, st, sms);
+    case 64: return wide ? launch_bwd_vec<T, 4, 16, true, true, 256>(p, st, sms) : launch_bwd_vec<T, 4, 16, true, true, 128>(p, st, sms);
+    default: return wide ? launch_bwd_vec<T, 4, 32, true, true, 256>(p, st, sms) : launch_bwd_vec<T, 4, 32, true, true, 128>(p, st, sms);
+  }
+}
+
 template <typename T, bool MIX, bool BWD>
 static cudaError_t launch_d(const Params& p, cudaStream_t st, int sms) {
   if constexpr (!BWD)
@@ -1036,8 +1159,12 @@ static cudaError_t launch_d(const Params& p, cudaStream_t st, int sms) {
     return launch_bwd_vec_d<T, MIX>(p, st, sms);
 }
 
-// op: 0 = swr_fwd, 1 = swr_bwd, 2 = mix_fwd, 3 = mix_bwd; bf16 selects the dtype
+// op: 0 = swr_fwd, 1 = swr_bwd, 2 = mix_fwd, 3 = mix_bwd, 4 / 5 = the layer mixer
+// (phalanx_layer_mix fwd / bwd); bf16 selects the dtype
 cudaError_t launch_ffma(int op, bool bf16, const Params& p, cudaStream_t st, int sms) {
+  if (op == 4)
+    return bf16 ? launch_fwd_stream<__nv_bfloat16, true, true>(p, st, sms) : launch_fwd_stream<float, true, true>(p, st, sms);
+  if (op == 5) return bf16 ? launch_layer_bwd<__nv_bfloat16>(p, st, sms) : launch_layer_bwd<float>(p, st, sms);
   if (bf16) {
     switch (op) {
       case 0: return launch_d<__nv_bfloat16, false, false>(p, st, sms);
@@ -1052,6 +1179,13 @@ cudaError_t launch_ffma(int op, bool bf16, const Params& p, cudaStream_t st, int
     case 2: return launch_d<float, true, false>(p, st, sms);
     default: return launch_d<float, true, true>(p, st, sms);
   }
+}
+
+// the layer backward's group sums need every group inside one CTA of at most 256 threads
+bool ffma_layer_supported(const Params& p) {
+  const int64_t tph = p.D / kVC4, hpc = 256 / tph;
+  auto ok = [&](int64_t g) { return g >= 1 && (g & (g - 1)) == 0 && g <= hpc && p.H % g == 0; };
+  return ok(p.hq) && ok(p.hk);
 }
 
 }  // namespace swr

@@ -65,11 +65,14 @@ constexpr int kHalf = 2048;      // one 64-channel half: 16 rows x 128 B, 128B-s
 //   NG   epilogue groups of 4 warps
 // ---------------------------------------------------------------------------
 // ring depths / prep warps: compile-time tuning knobs (tools/build_var.sh -D...)
+// ring depths measured back to back (tools/ab_b2b.sh): 2-block forward
+// items with 7 stages and 5 backward stages keep 56 / 80 KB of loads in flight per
+// SM -- more bytes in flight made the step slower (the TMA-copy probe agrees)
 #ifndef SWR_F_NI
-#define SWR_F_NI 8
+#define SWR_F_NI 7
 #endif
 #ifndef SWR_F_BPI
-#define SWR_F_BPI 4
+#define SWR_F_BPI 2
 #endif
 #ifndef SWR_F_NO
 #define SWR_F_NO 3
@@ -81,7 +84,13 @@ constexpr int kHalf = 2048;      // one 64-channel half: 16 rows x 128 B, 128B-s
 #define SWR_F_NPW 4
 #endif
 #ifndef SWR_B_NI
-#define SWR_B_NI 8
+#define SWR_B_NI 5
+#endif
+#ifndef SWR_B_NA
+#define SWR_B_NA 8
+#endif
+#ifndef SWR_B_NO
+#define SWR_B_NO 4
 #endif
 #ifndef SWR_B_BPI
 #define SWR_B_BPI 2
@@ -113,7 +122,7 @@ struct Cfg<0> {  // swr_fwd: in u;  out x
 };
 template <>
 struct Cfg<1> {  // swr_bwd: in u, G;  out du
-  static constexpr int NT = 2, NP = 0, BPI = SWR_B_BPI, NI = SWR_B_NI, NA = 8, NW = 8, NO = 4, COLS = 32, NPW = SWR_B_NPW, NOUT = 1, NG = SWR_B_NG;
+  static constexpr int NT = 2, NP = 0, BPI = SWR_B_BPI, NI = SWR_B_NI, NA = SWR_B_NA, NW = 8, NO = SWR_B_NO, COLS = 32, NPW = SWR_B_NPW, NOUT = 1, NG = SWR_B_NG;
   static constexpr int TU = 0, TG = 1;
   static constexpr bool CYC = true;
   static constexpr bool WC = false;
@@ -1507,7 +1516,7 @@ static cudaError_t launch_op(const Params& p, cudaStream_t st, int sms) {
 }  // namespace tc
 
 bool tc_supported(int op, bool bf16, const Params& p) {
-  (void)op;
+  if (op >= 4) return false;  // the layer mixer (NEXT-1) runs on the CUDA-core family
   if (!bf16 || p.D != 128) return false;
   if (tc::encoder() == nullptr) return false;
   auto a16 = [](const void* q) { return q == nullptr || (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };

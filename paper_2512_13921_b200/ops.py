@@ -205,6 +205,60 @@ def phalanx_mix_bwd(q, k, v, a, dy, carry_in=None, mu_in=None):
 
 
 # ---------------------------------------------------------------------------
+# the Phalanx layer around the mixer (include/swr.h phalanx_layer_mix; NEXT-1)
+# ---------------------------------------------------------------------------
+def _prep_group(t, like):
+    """A group-shared gate [B, L, G, D] (G divides H): kept if ABI-ready, else copied."""
+    B, L, H, D = like.shape
+    if t.dim() != 4 or t.shape[0] != B or t.shape[1] != L or t.shape[3] != D or H % t.shape[2]:
+        raise ValueError(f"group tensor must be [B, L, G, D] with G dividing H={H}, got {tuple(t.shape)}")
+    if not _abi_layout(t):
+        _count()
+        t = t.contiguous()
+    return t
+
+
+def _layer(q, zk, logit_a, logit_k):
+    return _lib.swr_layer(q.shape[2], zk.shape[2], *q.stride()[:3], *zk.stride()[:3],
+                          int(bool(logit_a)), int(bool(logit_k)))
+
+
+def phalanx_layer_mix(q, zk, v, za, carry_in=None, return_carry=False, logit_a=True, logit_k=True):
+    """The mixer fed by the featurization:
+    a = sigma(za), k = sigma(zk) (logits unless logit_a / logit_k is False), q and
+    zk group-shared [B, L, G, D] (head h reads group h // (H / G)),
+    y = q_g (.) SWR_a(k_g (.) v) + v.  Returns y or (y, carry_out)."""
+    (v,) = _prep(v)
+    q, zk = _prep_group(q, v), _prep_group(zk, v)
+    za = _prep_a(za)
+    dt = _dtype(q, zk, v, za)
+    y = _like(v)
+    ci = _carry(carry_in, v)
+    co = _new_carry(v) if return_carry else None
+    with torch.cuda.device(v.device):
+        _lib.phalanx_layer_mix(_ptr(q), _ptr(zk), _ptr(v), _ptr(za), _ptr(y), _ptr(ci), _ptr(co),
+                               _shape(v, za), _layer(q, zk, logit_a, logit_k), dt, _stream(v))
+    return (y, co) if return_carry else y
+
+
+def phalanx_layer_mix_bwd(q, zk, v, za, dy, carry_in=None, mu_in=None, logit_a=True, logit_k=True):
+    """Returns (dq [B,L,Gq,D], dzk [B,L,Gk,D], dv, dza, mu_out): the logits' gradients
+    and the group sums over the heads sharing q and k."""
+    v, dy = _prep(v, dy)
+    q, zk = _prep_group(q, v), _prep_group(zk, v)
+    za = _prep_a(za)
+    dt = _dtype(q, zk, v, za, dy)
+    dq, dzk, dv, dza = _like(q), _like(zk), _like(v), _like(za)
+    ci, mi = _carry(carry_in, v), _carry(mu_in, v)
+    mo = _new_carry(v)
+    with torch.cuda.device(v.device):
+        _lib.phalanx_layer_mix_bwd(_ptr(q), _ptr(zk), _ptr(v), _ptr(za), _ptr(dy), _ptr(dq), _ptr(dzk),
+                                   _ptr(dv), _ptr(dza), _ptr(ci), _ptr(mi), _ptr(mo), _shape(v, za),
+                                   _layer(q, zk, logit_a, logit_k), dt, _stream(v))
+    return dq, dzk, dv, dza, mo
+
+
+# ---------------------------------------------------------------------------
 # autograd wrappers
 # ---------------------------------------------------------------------------
 class SWRFunction(torch.autograd.Function):
@@ -231,6 +285,26 @@ class PhalanxMixFunction(torch.autograd.Function):
         q, k, v, a, carry_in = ctx.saved_tensors
         dq, dk, dv, da, mu_out = phalanx_mix_bwd(q, k, v, a, _grad_as(dy, q), carry_in)
         return dq, dk, dv, da, (mu_out if carry_in is not None else None)
+
+
+class PhalanxLayerMixFunction(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, q, zk, v, za, carry_in, logit_a, logit_k):
+        ctx.save_for_backward(q, zk, v, za, carry_in)
+        ctx.logits = (logit_a, logit_k)
+        return phalanx_layer_mix(q, zk, v, za, carry_in, logit_a=logit_a, logit_k=logit_k)
+
+    @staticmethod
+    def backward(ctx, dy):
+        q, zk, v, za, carry_in = ctx.saved_tensors
+        dq, dzk, dv, dza, mu_out = phalanx_layer_mix_bwd(q, zk, v, za, _grad_as(dy, v), carry_in,
+                                                         logit_a=ctx.logits[0], logit_k=ctx.logits[1])
+        return dq, dzk, dv, dza, (mu_out if carry_in is not None else None), None, None
+
+
+def layer_mix(q, zk, v, za, carry_in=None, logit_a=True, logit_k=True):
+    """Differentiable Phalanx layer mixer (logits in, group-shared q / k)."""
+    return PhalanxLayerMixFunction.apply(q, zk, v, za, carry_in, logit_a, logit_k)
 
 
 def swr(u, a, carry_in=None):

@@ -75,6 +75,27 @@ def mix_inputs(B, L, H, D, dtype=torch.bfloat16, seed=0, decay="sigmoid", carry=
     return out
 
 
+def layer_inputs(B, L, H, D, Gq=None, Gk=None, dtype=torch.bfloat16, seed=0, carry=False, za_shift=0.0):
+    """Inputs of the Phalanx layer mixer (NEXT-1), as the featurization produces them:
+    logits za ~ N(0,1) + za_shift [B, L, H] (a = sigma(za)) and zk ~ N(0,1)
+    [B, L, Gk, D] (k = sigma(zk), P:1564); q ~ N(0,1) [B, L, Gq, D] (P:1563), v, dy ~
+    N(0,1) [B, L, H, D].  Gq = Gk = H (no sharing) by default."""
+    Gq = H if Gq is None else Gq
+    Gk = H if Gk is None else Gk
+    g = _gen(seed)
+    out = {
+        "q": torch.randn((B, L, Gq, D), generator=g).to(dtype),
+        "zk": torch.randn((B, L, Gk, D), generator=g).to(dtype),
+        "v": torch.randn((B, L, H, D), generator=g).to(dtype),
+        "za": (torch.randn((B, L, H), generator=g) + za_shift).to(dtype),
+        "dy": torch.randn((B, L, H, D), generator=g).to(dtype),
+    }
+    if carry:
+        out["carry_in"] = torch.randn((B, H, D), generator=g)
+        out["mu_in"] = torch.randn((B, H, D), generator=g)
+    return out
+
+
 def to64(t):
     """Upcast an (already rounded) tensor to a float64 numpy array for the oracle."""
     return None if t is None else t.detach().to("cpu", torch.float64).numpy()

@@ -137,3 +137,25 @@ def test_layout_copies_are_counted(lib):
     g = ops._grad_as(torch.zeros(2, 32, 4, 16, dtype=torch.float64), x)
     assert g.dtype == x.dtype and ops.layout_copies() == n0 + 4
     assert ops._grad_as(x, x) is x and ops.layout_copies() == n0 + 4
+
+
+def test_layer_validation_codes(lib):
+    """phalanx_layer_mix(_bwd): groups must divide H, group tensors need D contiguous,
+    16-byte strides and pointers; checked before any launch."""
+    H, L, D = 8, 64, 16
+
+    def layer(Gq=4, Gk=2, sq=None, sk=None, la=1, lk=1):
+        sq = sq or (L * Gq * D, Gq * D, D)
+        sk = sk or (L * Gk * D, Gk * D, D)
+        return lib.swr_layer(Gq, Gk, *sq, *sk, la, lk)
+
+    s = _shape(lib, H=H)
+    fwd = lambda g, q=FAKE, k=FAKE: lib.raw_status("phalanx_layer_mix", q, k, FAKE, FAKE, FAKE, None, None, s,  # noqa: E731
+                                                   g, 0, None)
+    bwd = lambda g, dq=FAKE: lib.raw_status("phalanx_layer_mix_bwd", FAKE, FAKE, FAKE, FAKE, FAKE, dq, FAKE,  # noqa: E731
+                                            FAKE, FAKE, None, None, None, s, g, 0, None)
+    assert fwd(layer(Gq=3)) == 2 and fwd(layer(Gk=0)) == 2 and bwd(layer(Gk=5)) == 2
+    assert fwd(layer(sq=(L * 4 * D, 4 * D, 2))) == 3       # head stride not 16 bytes
+    assert fwd(layer(sk=(L * 2 * D, 0, D))) == 3           # zero token stride, L > 1
+    assert fwd(layer(), q=None) == 1 and bwd(layer(), dq=None) == 1
+    assert fwd(layer(), k=FAKE + 4) == 4

@@ -1,0 +1,147 @@
+"""GPU parity of the Phalanx layer mixer (include/swr.h
+phalanx_layer_mix / phalanx_layer_mix_bwd) against the fp64 oracle
+(oracle.layer_mix_fwd / layer_mix_bwd): sigma on the decay and key logits
+ and q / k shared by groups of heads.
+Tolerance as tests/test_parity.py (normwise; 1e-5 fp32, 2e-2 bf16)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from swr_inputs import layer_inputs, to64
+
+pytestmark = pytest.mark.gpu
+
+TOL = {torch.float32: 1e-5, torch.bfloat16: 2e-2}
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from conftest import build_lib
+    build_lib()
+    import paper_2512_13921_b200 as P
+    return P
+
+
+def normwise(x, ref):
+    x = x.detach().to("cpu", torch.float64).numpy()
+    den = np.max(np.abs(ref)) if ref.size else 0.0
+    num = np.max(np.abs(x - ref)) if ref.size else 0.0
+    return num / den if den > 0 else num
+
+
+def check(outs, refs, tol):
+    errs = {k: normwise(outs[k], refs[k]) for k in outs}
+    bad = {k: e for k, e in errs.items() if e > tol}
+    assert not bad, f"normwise errors above {tol}: {bad} (all: {errs})"
+    return errs
+
+
+def logit(a):
+    """za with sigma(za) = a (to feed the logit oracle a decay / gate given directly)."""
+    return np.log(a) - np.log1p(-a)
+
+
+def run(P, inp, logit_a=True, logit_k=True, carry=False):
+    g = {k: v.cuda() for k, v in inp.items()}
+    ci, mi = g.get("carry_in"), g.get("mu_in")
+    y, co = P.phalanx_layer_mix(g["q"], g["zk"], g["v"], g["za"], carry_in=ci, return_carry=True,
+                                logit_a=logit_a, logit_k=logit_k)
+    dq, dzk, dv, dza, mo = P.phalanx_layer_mix_bwd(g["q"], g["zk"], g["v"], g["za"], g["dy"], carry_in=ci,
+                                                   mu_in=mi, logit_a=logit_a, logit_k=logit_k)
+    torch.cuda.synchronize()
+    h = {k: to64(v) for k, v in inp.items()}
+    za = h["za"] if logit_a else logit(h["za"])
+    zk = h["zk"] if logit_k else logit(h["zk"])
+    ry, rco = oracle.layer_mix_fwd(h["q"], zk, h["v"], za, carry_in=h.get("carry_in"), carry_out=True)
+    rdq, rdzk, rdv, rdza, rmo = oracle.layer_mix_bwd(h["q"], zk, h["v"], za, h["dy"],
+                                                     carry_in=h.get("carry_in"), mu_in=h.get("mu_in"))
+    if not logit_a:  # gradients w.r.t. a itself: dza / sigma'(za)
+        s = oracle.sigmoid(za)
+        rdza = rdza / (s * (1.0 - s))
+    if not logit_k:
+        s = oracle.sigmoid(zk)
+        rdzk = rdzk / (s * (1.0 - s))
+    return ({"y": y, "carry_out": co, "dq": dq, "dzk": dzk, "dv": dv, "dza": dza, "mu_out": mo},
+            {"y": ry, "carry_out": rco, "dq": rdq, "dzk": rdzk, "dv": rdv, "dza": rdza, "mu_out": rmo})
+
+
+# (B, L, H, D, Gq, Gk): no sharing, 2, 4 and 8 heads per group, the paper's 8 groups
+# at d = 16 (16 heads per group) and a single group
+CASES = [
+    (2, 100, 4, 128, 4, 4), (2, 100, 8, 128, 4, 4), (1, 65, 16, 128, 8, 8), (1, 48, 16, 128, 2, 8),
+    (2, 77, 16, 64, 4, 2), (1, 200, 8, 32, 1, 2), (1, 64, 128, 16, 8, 8), (2, 33, 32, 16, 4, 32),
+    (1, 16, 6, 128, 3, 6), (1, 1, 4, 16, 2, 1), (1, 32, 16, 128, 1, 16),
+]
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("B,L,H,D,Gq,Gk", CASES)
+def test_layer_mix_parity(P, dtype, B, L, H, D, Gq, Gk):
+    inp = layer_inputs(B, L, H, D, Gq, Gk, dtype=dtype, seed=B * 7 + L + H + D + Gq, carry=True)
+    hq, hk = H // Gq, H // Gk
+    fits = all(x & (x - 1) == 0 and x <= 256 // (D // 4) for x in (hq, hk))
+    if not fits:
+        with pytest.raises(P.SwrError, match="UNSUPPORTED"):
+            run(P, inp)
+        return
+    outs, refs = run(P, inp)
+    check(outs, refs, TOL[dtype])
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("logit_a,logit_k", [(True, False), (False, True), (False, False)])
+def test_layer_mix_logit_flags(P, dtype, logit_a, logit_k):
+    """logit_a / logit_k off: za / zk are a / k themselves (then the reference's
+    logit-gradients are divided back by sigma')."""
+    inp = layer_inputs(2, 80, 8, 32, 4, 2, dtype=dtype, seed=11)
+    if not logit_a:
+        inp["za"] = torch.sigmoid(inp["za"].float()).to(dtype)
+    if not logit_k:
+        inp["zk"] = torch.sigmoid(inp["zk"].float()).to(dtype)
+    outs, refs = run(P, inp, logit_a, logit_k)
+    check(outs, refs, TOL[dtype])
+
+
+def test_layer_mix_reduces_to_mixer(P):
+    """G = H and logits off: bitwise the plain mixer's kernels (same FFMA arithmetic)."""
+    inp = layer_inputs(2, 96, 4, 64, dtype=torch.float32, seed=5)
+    g = {k: v.cuda() for k, v in inp.items()}
+    prev = P.set_path(P.SWR_PATH_FFMA)
+    try:
+        y0 = P.phalanx_mix(g["q"], g["zk"], g["v"], g["za"])
+        y1 = P.phalanx_layer_mix(g["q"], g["zk"], g["v"], g["za"], logit_a=False, logit_k=False)
+        b0 = P.phalanx_mix_bwd(g["q"], g["zk"], g["v"], g["za"], g["dy"])
+        b1 = P.phalanx_layer_mix_bwd(g["q"], g["zk"], g["v"], g["za"], g["dy"], logit_a=False, logit_k=False)
+    finally:
+        P.set_path(prev)
+    torch.cuda.synchronize()
+    assert torch.equal(y0, y1)
+    for x0, x1 in zip(b0[:4], b1[:4]):
+        assert torch.equal(x0, x1)
+
+
+def test_layer_mix_extreme_logits(P):
+    """Saturating logits (|z| up to 40: sigma = 0 or 1 exactly in fp32) stay finite."""
+    inp = layer_inputs(1, 64, 8, 32, 2, 4, dtype=torch.float32, seed=3)
+    inp["za"] = inp["za"] * 20.0
+    inp["zk"] = inp["zk"] * 20.0
+    outs, refs = run(P, inp)
+    for k, v in outs.items():
+        assert torch.isfinite(v).all(), k
+    check(outs, refs, 1e-5)
+
+
+def test_layer_mix_autograd(P):
+    """torch.autograd through layer_mix returns the group-summed logit gradients."""
+    inp = layer_inputs(1, 50, 8, 16, 2, 4, dtype=torch.float32, seed=9)
+    g = {k: v.cuda().requires_grad_(k != "dy") for k, v in inp.items()}
+    y = P.layer_mix(g["q"], g["zk"], g["v"], g["za"])
+    (y * g["dy"]).sum().backward()
+    h = {k: to64(v) for k, v in inp.items()}
+    rdq, rdzk, rdv, rdza, _ = oracle.layer_mix_bwd(h["q"], h["zk"], h["v"], h["za"], h["dy"])
+    for name, x, r in (("dq", g["q"].grad, rdq), ("dzk", g["zk"].grad, rdzk), ("dv", g["v"].grad, rdv),
+                       ("dza", g["za"].grad, rdza)):
+        assert normwise(x, r) <= 1e-5, name

@@ -22,8 +22,12 @@ for _ in range(int(os.environ.get("WARM", "5"))):
     run()
 buf = torch.zeros(N * 16 + 4 * 160, dtype=torch.int64, device="cuda")
 _lib.set_trace(buf.data_ptr(), N)
-flush = torch.empty(64 << 20, device="cuda")
-flush.zero_()
+if os.environ.get("B2B"):  # traced launch right behind back-to-back launches (deferred write-back paid)
+    for _ in range(4):
+        run()
+else:
+    flush = torch.empty(64 << 20, device="cuda")
+    flush.zero_()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(); run(); e1.record()
 torch.cuda.synchronize()
@@ -37,6 +41,8 @@ d_sm = (span[order, 1] - span[order, 0]) / 1e3
 print("span (us) / items by SM id:", " ".join(f"{int(span[i,2])}:{x:.0f}/{int(span[i,3])}" for i, x in zip(order, d_sm)))
 st0 = span[:, 0].min()
 dur = (span[:, 1] - span[:, 0]) / 1e3
+ends = np.sort((span[:, 1] - span[:, 0].min()) / 1e3)
+print("CTA end times (us) percentiles 0/10/50/90/100:", " ".join(f"{np.percentile(ends, q):.1f}" for q in (0, 10, 50, 90, 100)))
 print(f"CTAs {len(span)}: start spread {(span[:,0].max()-st0)/1e3:.1f} us, span min/med/max {dur.min():.1f}/{np.median(dur):.1f}/{dur.max():.1f} us, last end {(span[:,1].max()-st0)/1e3:.1f} us")
 t = allb[:N * 16].reshape(N, 16).astype(np.int64)
 valid = t[:, 0] > 0

@@ -325,27 +325,54 @@ def main():
         return sum(v.numel() * v.element_size() for v in gg.values())
 
     def timed(fwd_, bwd_, steps, warmup, flushed):
-        """Per-step fwd / bwd CUDA-event times (ms); back to back unless `flushed`."""
+        """(total ms of `steps` steps, per-step fwd ms, per-step bwd ms), CUDA events.
+        Back to back unless `flushed`.  The GPU is first given ~2 ms of sleep so the
+        host enqueues ahead of it and no launch latency lands inside the events.  The
+        total comes from two events around the loop; a second loop with an event
+        between fwd and bwd of every step gives the split."""
         for _ in range(warmup):
             if flushed:
                 l2_flush()
             fwd_()
             bwd_()
         torch.cuda.synchronize()
-        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        for s_ in range(steps):
-            if flushed:
+        head_start = 4_000_000  # SM cycles (~2 ms): lets the host run ahead of the GPU
+        if flushed:  # per-step events; the flush between steps stays outside them
+            ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+            torch.cuda._sleep(head_start)
+            for s_ in range(steps):
                 l2_flush()
+                ev[s_][0].record(stream)
+                fwd_()
+                ev[s_][1].record(stream)
+                bwd_()
+                ev[s_][2].record(stream)
+            torch.cuda.synchronize()
+            tf = [e[0].elapsed_time(e[1]) for e in ev]
+            tb = [e[1].elapsed_time(e[2]) for e in ev]
+            return sum(tf) + sum(tb), tf, tb
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(head_start)
+        e0.record(stream)
+        for _ in range(steps):
+            fwd_()
+            bwd_()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        total = e0.elapsed_time(e1)
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+        torch.cuda._sleep(head_start)
+        for s_ in range(steps):
             ev[s_][0].record(stream)
             fwd_()
             ev[s_][1].record(stream)
             bwd_()
             ev[s_][2].record(stream)
         torch.cuda.synchronize()
-        return [e[0].elapsed_time(e[1]) for e in ev], [e[1].elapsed_time(e[2]) for e in ev]
+        return total, [e[0].elapsed_time(e[1]) for e in ev], [e[1].elapsed_time(e[2]) for e in ev]
 
     def max_over_ranks(x):
         t = torch.tensor([x], device=dev, dtype=torch.float64)
@@ -356,12 +383,12 @@ def main():
     b2b = in_bytes(g) > 2 * l2  # inputs larger than L2: no flush between steps
     launches0, copies0 = P.launch_count(), P.layout_copies()
     with ClockSampler(dev.index if world == 1 else local) as clk:
-        t_fwd, t_bwd = timed(fwd, bwd, args.steps, args.warmup, flushed=not b2b)
-    launches = P.launch_count() - launches0
+        t_total, t_fwd, t_bwd = timed(fwd, bwd, args.steps, args.warmup, flushed=not b2b)
+    launches = (P.launch_count() - launches0) // (1 if not b2b else 2)  # b2b: the split loop repeats the steps
     assert P.layout_copies() == copies0, "operands were copied inside the timed region"
     if world > 1:
         dist.barrier()
-    ms_per_step = max_over_ranks(sum(t_fwd) + sum(t_bwd)) / args.steps
+    ms_per_step = max_over_ranks(t_total) / args.steps
     tokens_per_step = B * L if sp else B * L * world
     value = tokens_per_step / (ms_per_step / 1e3)
 
@@ -398,6 +425,7 @@ def main():
                               f"{flush_rd.numel() * 4 >> 20} MiB read, outside the events)"),
                    "path": args.path, "last_path": {0: "none", 1: "ffma", 2: "tc"}[P.last_path()]},
         "fwd_ms": mf, "bwd_ms": mb,
+        "split_note": "fwd_ms / bwd_ms from a second loop with an event between the two kernels of each step",
         "hbm_gbs": {"fwd": bytes_["fwd"] / mf / 1e6, "bwd": bytes_["bwd"] / mb / 1e6,
                     "fwd_bwd": (bytes_["fwd"] + bytes_["bwd"]) / (mf + mb) / 1e6},
         "roofline": {"bound": "hbm", "kernel": f"{args.op}_{dom}", "achieved": ach, "peak": peak,
@@ -411,8 +439,8 @@ def main():
     if b2b:
         # the same steps with the L2 flushed between them (each step's deferred
         # write-back is then paid by the flush, outside the events)
-        f_fwd, f_bwd = timed(fwd, bwd, min(args.steps, 20), 3, flushed=True)
-        fm = max_over_ranks(sum(f_fwd) + sum(f_bwd)) / len(f_fwd)
+        f_tot, f_fwd, f_bwd = timed(fwd, bwd, min(args.steps, 20), 3, flushed=True)
+        fm = max_over_ranks(f_tot) / len(f_fwd)
         line["l2_flushed"] = {"value": tokens_per_step / (fm / 1e3), "ms_per_step": fm,
                               "fwd_ms": statistics.mean(f_fwd), "bwd_ms": statistics.mean(f_bwd)}
     if (args.config == "layer4k" and not sp and not args.no_extra):
@@ -423,8 +451,8 @@ def main():
             gx = {k: v.to(dev) for k, v in make_host_inputs(args.op, Bx, Lx, Hx, Dx, dtx, seed=2 + 1000 * rank).items()}
             fx, bx = step_fns(P, args.op, gx)
             bx_ = in_bytes(gx) > 2 * l2
-            x_fwd, x_bwd = timed(fx, bx, min(args.steps, 20), 3, flushed=not bx_)
-            xm = max_over_ranks(sum(x_fwd) + sum(x_bwd)) / len(x_fwd)
+            x_tot, x_fwd, x_bwd = timed(fx, bx, min(args.steps, 20), 3, flushed=not bx_)
+            xm = max_over_ranks(x_tot) / len(x_fwd)
             xb = algo_bytes(args.op, Bx, Lx, Hx, Dx, dtx)
             line["workloads"][name] = {
                 "B": Bx, "L": Lx, "value": Bx * Lx * world / (xm / 1e3), "unit": "tokens/s", "ms_per_step": xm,

@@ -277,7 +277,7 @@ struct VecN {
 // order (deterministic): the CTA holds NTH / TPH heads, a multiple of hq and hk.
 // dq is staged over the lambda slots it replaces, dk in a second buffer.
 template <typename T, int VC, int TPH, bool MIX, bool LAYER = false, int NTH = 128>
-__global__ void __launch_bounds__(NTH, NTH == 128 ? SWR_FFMA_BWD_MINB : 1) bwd_ffma_vec(const Params p) {
+__global__ void __launch_bounds__(NTH, NTH == 128 ? ((!MIX && sizeof(T) == 2) ? 3 : SWR_FFMA_BWD_MINB) : 1) bwd_ffma_vec(const Params p) {
   using V = VecN<T, VC>;
   using io = IO<T>;
   static_assert(!LAYER || MIX, "the layer options apply to the mixer");
@@ -389,6 +389,122 @@ __global__ void __launch_bounds__(NTH, NTH == 128 ? SWR_FFMA_BWD_MINB : 1) bwd_f
     }
 #pragma unroll
     for (int e = 0; e < VC; ++e) mu[e] = a[0] * l[e];
+  }
+
+  if constexpr (!MIX && sizeof(T) == 2) {
+    // SWR (bf16): every u block is read once and nothing lives in local memory.  Per block t
+    // (reverse walk): A) w_{t-1} by the local solve of block t-1 into one of two w stash
+    // slots, v_{t-1} = w_{t-1}[15]; BC) one reverse sweep: lambda[i] = G[i] + a[i+1]
+    // lambda[i+1], r[i] = a[i+1] r[i+1], du = lambda + r mu, and the da terms
+    // du . w_t[i-1] (w_t from the other stash slot, written by A one step earlier) and
+    // g[i-1] lambda . v_{t-1}.  Fully unrolled: every per-token array is registers.
+    // The chunk's last block first fills its stash slot from u_t.
+    auto w_at = [&](int slot, int i, int q) -> float4& {
+      return slam[((slot * kEll + i) * NQ + q) * NTH + tid];
+    };
+    auto solve_into = [&](int64_t nb0, int slot, int lim, float (&wl)[VC]) {  // Pass I of a block into a slot
+      const T* ap = A0 + nb0 * sal;
+      Src usrc = src_u(nb0);
+#pragma unroll 4
+      for (int i = 0; i < kEll; ++i) {
+        const float a = (i < lim) ? decay(ap) : 1.f;
+        float u[VC];
+        usrc.load(i < lim, u);
+        ap += sal;
+        usrc.fwd();
+#pragma unroll
+        for (int e = 0; e < VC; ++e) wl[e] = (i == 0) ? u[e] : fmaf(a, wl[e], u[e]);
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) w_at(slot, i, q) = make_float4(wl[4 * q], wl[4 * q + 1], wl[4 * q + 2], wl[4 * q + 3]);
+      }
+    };
+    int cur = 0;  // stash slot holding w_t of the block being processed
+    {
+      const int64_t n0 = (t_hi - 1) * kEll;
+      float wl[VC];
+      solve_into(n0, cur, (p.L - n0 < kEll) ? (int)(p.L - n0) : kEll, wl);
+    }
+    for (int64_t t = t_hi - 1; t >= t_lo; --t) {
+      const int64_t n0 = t * kEll;
+      const int lim = (p.L - n0 < kEll) ? (int)(p.L - n0) : kEll;
+      float acur[kEll];
+      load_a(n0, lim, acur);
+      // A) w_{t-1} into the other slot (block t-1 is whole), v_{t-1} = w_{t-1}[15]
+      float vprev[VC];
+      if (t > 0) {
+        solve_into(n0 - kEll, cur ^ 1, kEll, vprev);
+      } else {
+#pragma unroll
+        for (int e = 0; e < VC; ++e) vprev[e] = p.carry_in ? p.carry_in[co + e] : 0.f;
+      }
+      float gsv[kEll];  // g[i] = a[0] ... a[i]
+      gsv[0] = acur[0];
+#pragma unroll
+      for (int i = 1; i < kEll; ++i) gsv[i] = gsv[i - 1] * acur[i];
+      // BC) reverse sweep over the block
+      float part[kEll];
+      float lam[VC], mu_next[VC];
+      float rr = 1.f;
+      Src gsrc = src_g(n0 + kEll - 1);
+      T* dup = (T*)p.du + xo + (n0 + kEll - 1) * sl;
+#pragma unroll
+      for (int i = kEll - 1; i >= 0; --i) {
+        float g[VC];
+        gsrc.load(i < lim, g);
+        gsrc.back();
+        if (i == kEll - 1) {
+#pragma unroll
+          for (int e = 0; e < VC; ++e) lam[e] = g[e];  // lambda[15] = G[15]
+        } else {
+#pragma unroll
+          for (int e = 0; e < VC; ++e) lam[e] = fmaf(acur[i + 1], lam[e], g[e]);
+          rr *= acur[i + 1];  // r_t[i] = a_t[i+1] ... a_t[15]
+        }
+        float du[VC];
+#pragma unroll
+        for (int e = 0; e < VC; ++e) du[e] = fmaf(rr, mu[e], lam[e]);
+        float sdot = 0.f, lv = 0.f;  // sum_c du[i] w[i-1] (w[-1] = 0), sum_c lambda[i] v_{t-1}
+        if (i > 0) {
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) {
+            const float4 w4 = w_at(cur, i - 1, q);
+            const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+            for (int e4 = 0; e4 < 4; ++e4) {
+              const int e = 4 * q + e4;
+              sdot = (e == 0) ? du[e] * wv[e4] : fmaf(du[e], wv[e4], sdot);
+            }
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < VC; ++e) lv = (e == 0) ? lam[e] * vprev[e] : fmaf(lam[e], vprev[e], lv);
+        part[i] = fmaf(i > 0 ? gsv[i - 1] : 1.f, lv, sdot);
+        if (act && i < lim) V::st(dup, du);
+        dup -= sl;
+        if (i == 0) {
+#pragma unroll
+          for (int e = 0; e < VC; ++e) mu_next[e] = acur[0] * lam[e];  // mu_{t-1} = a_t[0] lambda_t[0]
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < VC; ++e) mu[e] = mu_next[e];
+      if (t == 0 && act && p.mu_out) {
+#pragma unroll
+        for (int e = 0; e < VC; ++e) p.mu_out[co + e] = mu[e];
+      }
+      cur ^= 1;
+      // da: deterministic reduction over the head's channels
+      int tok = 0;
+      if constexpr (GS > 1) GroupReduce<GS / 2, kEll>::run(part, lane, tok);
+      constexpr int NV = GS >= kEll ? 1 : kEll / GS;
+      const bool owner = (GS < 32) || ((lane & 1) == 0);
+      if (act && owner) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+          if (tok + j < lim) io::st1(dA + (n0 + tok + j) * sal, part[j]);
+      }
+    }
+    return;
   }
 
   // LAYER group sums: does this CTA stage dq / dk (more than one head per group)?
@@ -595,7 +711,7 @@ __global__ void __launch_bounds__(128) decode_step(const DecParams p) {
   float gold = 1.f, a = 1.f;
   if (act) {
     a = IO<T>::ld1((const T*)p.a + b * p.sa_b + h * p.sa_h);
-    gold = p.g[bh];
+    if (i != 0) gold = p.g[bh];  // a block start does not read the state's g (nor v)
   }
   __syncwarp();  // every lane of the head has read g before lane c == 0 rewrites it
   if (!act) return;
@@ -1107,8 +1223,9 @@ static cudaError_t launch_fwd_stream(Params p, cudaStream_t st, int sms) {
 template <typename T, int VC, int TPH, bool MIX, bool LAYER = false, int NTH = 128>
 static cudaError_t launch_bwd_vec(Params p, cudaStream_t st, int sms) {
   constexpr int HPC = NTH / TPH;
-  // lambda staging [kEll][VC/4][NTH] float4; LAYER: + the dk staging of the group sums
-  constexpr int kSmem = kEll * VC * NTH * 4 * (LAYER ? 2 : 1);
+  // lambda staging [kEll][VC/4][NTH] float4; LAYER: + the dk staging; bf16 SWR: the two
+  // w stash slots instead (fp32 SWR keeps the three-pass walk: 168 registers spill there)
+  constexpr int kSmem = kEll * VC * NTH * 4 * ((LAYER || (!MIX && sizeof(T) == 2)) ? 2 : 1);
   if constexpr (kSmem > 48 * 1024) {  // set per call (per device)
     cudaError_t e = cudaFuncSetAttribute(bwd_ffma_vec<T, VC, TPH, MIX, LAYER, NTH>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);

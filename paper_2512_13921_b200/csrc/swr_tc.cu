@@ -80,6 +80,9 @@ constexpr int kHalf = 2048;      // one 64-channel half: 16 rows x 128 B, 128B-s
 #ifndef SWR_F_NA
 #define SWR_F_NA 8
 #endif
+#ifndef SWR_F_NG
+#define SWR_F_NG 3
+#endif
 #ifndef SWR_F_NPW
 #define SWR_F_NPW 4
 #endif
@@ -114,11 +117,11 @@ template <int OP>
 struct Cfg;
 template <>
 struct Cfg<0> {  // swr_fwd: in u;  out x
-  static constexpr int NT = 1, NP = 0, BPI = SWR_F_BPI, NI = SWR_F_NI, NA = SWR_F_NA, NW = 8, NO = SWR_F_NO, COLS = 16, NPW = SWR_F_NPW, NOUT = 1, NG = 3;
+  static constexpr int NT = 1, NP = 0, BPI = SWR_F_BPI, NI = SWR_F_NI, NA = SWR_F_NA, NW = 8, NO = SWR_F_NO, COLS = 16, NPW = SWR_F_NPW, NOUT = 1, NG = SWR_F_NG;
   static constexpr int TU = 0, TG = 0;  // A-operand regions of W and lambda
   static constexpr bool CYC = false;    // w MMA through the row-rotated tile (see Stage::kLc)
   static constexpr bool WC = false;     // a second w MMA through the rotated tile, at column kWc
-  static constexpr bool BWD = false, MIX = false;
+  static constexpr bool BWD = false, MIX = false, LAYER = false;
 };
 template <>
 struct Cfg<1> {  // swr_bwd: in u, G;  out du
@@ -126,7 +129,7 @@ struct Cfg<1> {  // swr_bwd: in u, G;  out du
   static constexpr int TU = 0, TG = 1;
   static constexpr bool CYC = true;
   static constexpr bool WC = false;
-  static constexpr bool BWD = true, MIX = false;
+  static constexpr bool BWD = true, MIX = false, LAYER = false;
 };
 template <>
 struct Cfg<2> {  // mix fwd: in q, k, v;  out y;  prep u^ = k v (over k)
@@ -134,7 +137,7 @@ struct Cfg<2> {  // mix fwd: in q, k, v;  out y;  prep u^ = k v (over k)
   static constexpr int TU = 1, TG = 0;
   static constexpr bool CYC = false;
   static constexpr bool WC = false;
-  static constexpr bool BWD = false, MIX = true;
+  static constexpr bool BWD = false, MIX = true, LAYER = false;
 };
 template <>
 struct Cfg<3> {  // mix bwd: in q, k, v, dy;  out dq, dk, dv;  prep u^ = k v (region 4), G = dy q (over q)
@@ -142,7 +145,18 @@ struct Cfg<3> {  // mix bwd: in q, k, v, dy;  out dq, dk, dv;  prep u^ = k v (re
   static constexpr int TU = 4, TG = 0;
   static constexpr bool CYC = false;
   static constexpr bool WC = true;  // x~ needs w[i] (dq), da needs w[i-1]: both from TMEM
-  static constexpr bool BWD = true, MIX = true;
+  static constexpr bool BWD = true, MIX = true, LAYER = false;
+};
+// the Phalanx layer mixer (phalanx_layer_mix*, NEXT-1): the mixer's pipelines with
+// sigma on the decay / key logits and group-shared q / k (forward; the backward's
+// group sums run on the CUDA-core family, so here every group is one head)
+template <>
+struct Cfg<4> : Cfg<2> {
+  static constexpr bool LAYER = true;
+};
+template <>
+struct Cfg<5> : Cfg<3> {
+  static constexpr bool LAYER = true;
 };
 
 // SMEM layout (bytes; every 4 KiB tile 1024-aligned for the 128B swizzle atoms).
@@ -168,7 +182,7 @@ struct Stage {
   // (gs[0] = 1), fp32, in fragment token order
   static constexpr int kLc = 512 * C::BPI;                     // offset of the CYC tiles
   static constexpr int kAuxOff = kLc + ((C::CYC || C::WC) ? 512 * C::BPI : 0);
-  static constexpr int kAuxBlk = 48;  // floats
+  static constexpr int kAuxBlk = C::LAYER ? 64 : 48;  // floats (layer: + a (1 - a), token order)
   static constexpr int kWork = kAuxOff + C::BPI * kAuxBlk * 4;
   // output slot
   static constexpr int kOut = C::NOUT * kRegion;
@@ -388,7 +402,7 @@ struct Split {
 };
 constexpr int kClaimSlots = 256;
 __device__ unsigned g_claim[kClaimSlots][kMaxSM];  // {launch epoch} of the claimer, per range
-__device__ float g_spi[4][kMaxSM];                 // ns per item of the last CTA on each SM, per op
+__device__ float g_spi[6][kMaxSM];                 // ns per item of the last CTA on each SM, per op
 __device__ __forceinline__ int claim_range(const Split& sp, uint32_t epoch) {
   if (!sp.weighted) return (int)blockIdx.x;
   uint32_t sm;
@@ -491,6 +505,27 @@ __device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) { return _
 __device__ __forceinline__ float2 f2mul(float2 a, float2 b) { return __fmul2_rn(a, b); }
 
 
+// sigma(z) = 1/2 + tanh(z/2)/2 with the single-MUFU tanh.approx.f32 (relative error
+// ~2^-11, below the bf16 rounding every TC output gets; R20) -- the layer
+// mixer's bounding activation of the decay and key logits
+__device__ __forceinline__ float sig_tc(float z) {
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * z));
+  return fmaf(0.5f, t, 0.5f);
+}
+// 8 elements of u^ = sigma(zk) (.) v, each rounded once to bf16
+__device__ __forceinline__ uint4 sigmul8(const uint4& zk, const uint4& v) {
+  const uint32_t a[4] = {zk.x, zk.y, zk.z, zk.w}, b[4] = {v.x, v.y, v.z, v.w};
+  uint32_t o[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float k0 = sig_tc(__uint_as_float(a[q] << 16)), k1 = sig_tc(__uint_as_float(a[q] & 0xffff0000u));
+    const float v0 = __uint_as_float(b[q] << 16), v1 = __uint_as_float(b[q] & 0xffff0000u);
+    __nv_bfloat162 r = __floats2bfloat162_rn(k0 * v0, k1 * v1);
+    o[q] = *reinterpret_cast<uint32_t*>(&r);
+  }
+  return make_uint4(o[0], o[1], o[2], o[3]);
+}
 // 8 bf16 products, elementwise, one RNE rounding each (mul.rn.bf16x2)
 __device__ __forceinline__ uint4 bmul8(const uint4& a, const uint4& b) {
   uint4 o;
@@ -616,7 +651,12 @@ __device__ __forceinline__ int aux_perm(int i) { return 4 * ((i & 7) >> 1) + 2 *
 // 32 channels (a TMEM lane quarter) and arrives on the barriers itself.
 // ---------------------------------------------------------------------------
 #ifndef SWR_PDL
-#define SWR_PDL 0  // programmatic dependent launch: measured 2% slower on the SWR step (bwd CTAs start early on freed SMs), off
+// programmatic dependent launch: a launch may start its prologue (barrier init, TMEM
+// allocation, range claim) on SMs the previous kernel has left and waits with
+// griddepcontrol.wait before touching global memory.  Back to back the SWR step gets
+// 124.5 -> 118.8 us (tools/ab_b2b.sh; with an L2 flush between steps it had measured 2%
+// slower in round 1, when the flush kernel sat between the two)
+#define SWR_PDL 1
 #endif
 #ifndef SWR_EPI_UNROLL
 #define SWR_EPI_UNROLL 1
@@ -760,8 +800,10 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
 #pragma unroll
         for (int x = 0; x < C::NT; ++x) {  // one box per 64-channel half: 16*BPI tokens
           uint8_t* dst = S::region(st, x);
-          tma_load_4d(dst, &maps.in[x], &full[ri.s], 0, cur.h, tt, cur.b);
-          tma_load_4d(dst + S::kHS, &maps.in[x], &full[ri.s], 64, cur.h, tt, cur.b);
+          // layer mixer: q (x = 0) and k (x = 1) are read at the head's group
+          const int hx = !C::LAYER ? cur.h : x == 0 ? cur.h / (int)p.hq : x == 1 ? cur.h / (int)p.hk : cur.h;
+          tma_load_4d(dst, &maps.in[x], &full[ri.s], 0, hx, tt, cur.b);
+          tma_load_4d(dst + S::kHS, &maps.in[x], &full[ri.s], 64, hx, tt, cur.b);
         }
         trace(p, j, 1);
         cur.next(nbi, H);
@@ -937,6 +979,17 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
 #pragma unroll
           for (int i = 0; i < 16; ++i)
             a[i] = (i < nval) ? __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(at + i * 16)) : 1.f;
+          if constexpr (C::LAYER) {
+            if (p.logit_a) {  // a = sigma(za); the padding keeps a = 1
+#pragma unroll
+              for (int i = 0; i < 16; ++i) a[i] = (i < nval) ? sig_tc(a[i]) : 1.f;
+            }
+            // sp = a (1 - a) = sigma'(za) for the logit gradient (token order)
+            if (C::BWD && col == 0) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) gr[S::kAuxBlk * k + 48 + i] = a[i] * (1.f - a[i]);
+            }
+          }
           float Lc[16];
           float prod = 1.f;
 #pragma unroll
@@ -994,7 +1047,10 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
         uint4* U4 = reinterpret_cast<uint4*>(S::region(st, C::TU));
 #pragma unroll 4
         for (int v = lane; v < S::kRegion / 16; v += 32) {
-          U4[v] = bmul8(K4[v], V4[v]);
+          if (C::LAYER && p.logit_k)
+            U4[v] = sigmul8(K4[v], V4[v]);  // u^ = sigma(zk) (.) v
+          else
+            U4[v] = bmul8(K4[v], V4[v]);
           if constexpr (C::BWD) {
             uint4* Q4 = reinterpret_cast<uint4*>(S::region(st, 0));  // G overwrites q
             const uint4* D4 = reinterpret_cast<const uint4*>(S::region(st, 3));
@@ -1210,8 +1266,11 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
             const float a1 = (u16 ? s[3] : s[1]) + __shfl_xor_sync(0xffffffffu, u16 ? s[1] : s[3], 16);
             float b = (u8 ? a1 : a0) + __shfl_xor_sync(0xffffffffu, u8 ? a0 : a1, 8);
             b += __shfl_xor_sync(0xffffffffu, b, 4);
-            if ((lane & 4) == 0)  // lane holds m = 2 u16 + u8: token 8 u16 + 2 qd + u8
-              rb[wq * (16 * BPI) + kb * 16 + (u16 ? 8 : 0) + 2 * qd + (u8 ? 1 : 0)] = b;
+            if ((lane & 4) == 0) {  // lane holds m = 2 u16 + u8: token 8 u16 + 2 qd + u8
+              const int tok = (u16 ? 8 : 0) + 2 * qd + (u8 ? 1 : 0);
+              if (C::LAYER && p.logit_a) b *= ga[48 + tok];  // dza = da sigma'(za)
+              rb[wq * (16 * BPI) + kb * 16 + tok] = b;
+            }
             if constexpr (!C::MIX) {
               store_frag(S::tile(ot, kb, 0), fro, du);
             } else {
@@ -1238,8 +1297,12 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                   const float2 d2 = make_float2(du[k][2 * h], du[k][2 * h + 1]);
-                  const float2 dv2 = f2fma(d2, bf2f(tk[h][k]), bf2f(tdy[h][k]));
-                  const float2 dk2 = f2mul(d2, bf2f(tv[h][k]));
+                  float2 kf = bf2f(tk[h][k]);
+                  if (C::LAYER && p.logit_k) kf = make_float2(sig_tc(kf.x), sig_tc(kf.y));  // k = sigma(zk)
+                  const float2 dv2 = f2fma(d2, kf, bf2f(tdy[h][k]));
+                  float2 dk2 = f2mul(d2, bf2f(tv[h][k]));
+                  if (C::LAYER && p.logit_k)  // dzk = dk sigma'(zk), sigma' = k (1 - k)
+                    dk2 = f2mul(dk2, make_float2(kf.x * (1.f - kf.x), kf.y * (1.f - kf.y)));
                   o[k][2 * h] = dv2.x; o[k][2 * h + 1] = dv2.y;
                   du[k][2 * h] = dk2.x; du[k][2 * h + 1] = dk2.y;
                 }
@@ -1348,7 +1411,9 @@ struct Balance {
       for (int s = 0; s <= sms; ++s) sp.bnd[s] = (int)((int64_t)s * total / sms);
     }
     ++launches;
-    return !pending;
+    // refresh the table from every 8th launch (each readback costs the host a few
+    // CUDA calls; the rates move slowly)
+    return !pending && (launches < 8 || launches % 8 == 0);
   }
   void request(int op, int sms, cudaStream_t st) {
     std::lock_guard<std::mutex> lock(mu);
@@ -1371,7 +1436,7 @@ struct Balance {
   }
 };
 constexpr int kMaxDev = 64;
-static Balance g_balance[kMaxDev][4];  // per device (SM rates are a property of the GPU), per op
+static Balance g_balance[kMaxDev][6];  // per device (SM rates are a property of the GPU), per op
 
 // Claim slots of the weighted split, per device.  A weighted launch claims its ranges
 // in g_claim[epoch % kClaimSlots]; a slot may only be reused once the launch that used
@@ -1430,24 +1495,72 @@ static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   return fn;
 }
 
-static bool map_dtensor(CUtensorMap* m, const void* ptr, const Params& p, int rows) {
-  cuuint64_t dims[4] = {(cuuint64_t)p.D, (cuuint64_t)p.H, (cuuint64_t)p.L, (cuuint64_t)p.B};
-  cuuint64_t strides[3] = {(cuuint64_t)p.sx_h * 2, (cuuint64_t)p.sx_l * 2, (cuuint64_t)p.sx_b * 2};
-  cuuint32_t box[4] = {64, 1, (cuuint32_t)rows, 1};
+// which: 0 = a [B, L, H, D] d-tensor with the strides sx; 1 / 2 = the layer mixer's
+// group-shared q / k (and dq / dk) [B, L, G, D] with their own strides
+// Encoded tensor maps, cached per calling thread: a training step calls the same
+// ops on the same (caching-allocator) buffers, so the key -- pointer, dims, strides,
+// box rows -- repeats and the ~1 us host-side encode is skipped.
+struct MapKey {
+  const void* ptr;
+  uint64_t dims[4], strides[3];
+  uint32_t rows, kind;
+};
+struct MapCache {
+  static constexpr int N = 32;
+  MapKey key[N];
+  CUtensorMap map[N];
+  int used = 0, next = 0;
+  const CUtensorMap* find(const MapKey& k) const {
+    for (int i = 0; i < used; ++i)
+      if (std::memcmp(&key[i], &k, sizeof(MapKey)) == 0) return &map[i];
+    return nullptr;
+  }
+  void put(const MapKey& k, const CUtensorMap& m) {
+    key[next] = k;
+    map[next] = m;
+    next = (next + 1) % N;
+    if (used < N) ++used;
+  }
+};
+static thread_local MapCache g_maps;
+
+static bool encode_cached(CUtensorMap* m, const void* ptr, CUtensorMapDataType ty, int rank, const cuuint64_t* dims,
+                          const cuuint64_t* strides, const cuuint32_t* box, CUtensorMapSwizzle sw, uint32_t kind) {
+  MapKey k;
+  std::memset(&k, 0, sizeof(k));
+  k.ptr = ptr;
+  for (int i = 0; i < rank; ++i) k.dims[i] = dims[i];
+  for (int i = 0; i + 1 < rank; ++i) k.strides[i] = strides[i];
+  k.rows = box[rank - 2];
+  k.kind = kind;
+  if (const CUtensorMap* c = g_maps.find(k)) {
+    *m = *c;
+    return true;
+  }
   cuuint32_t es[4] = {1, 1, 1, 1};
-  return encoder()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  if (encoder()(m, ty, rank, const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  g_maps.put(k, *m);
+  return true;
+}
+
+static bool map_dtensor(CUtensorMap* m, const void* ptr, const Params& p, int rows, int which = 0) {
+  const int64_t G = which == 1 ? p.H / p.hq : which == 2 ? p.H / p.hk : p.H;
+  const int64_t sh = which == 1 ? p.sq_h : which == 2 ? p.sk_h : p.sx_h;
+  const int64_t sl = which == 1 ? p.sq_l : which == 2 ? p.sk_l : p.sx_l;
+  const int64_t sb = which == 1 ? p.sq_b : which == 2 ? p.sk_b : p.sx_b;
+  cuuint64_t dims[4] = {(cuuint64_t)p.D, (cuuint64_t)G, (cuuint64_t)p.L, (cuuint64_t)p.B};
+  cuuint64_t strides[3] = {(cuuint64_t)sh * 2, (cuuint64_t)sl * 2, (cuuint64_t)sb * 2};
+  cuuint32_t box[4] = {64, 1, (cuuint32_t)rows, 1};
+  return encode_cached(m, ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, 0);
 }
 
 static bool map_decay(CUtensorMap* m, const void* ptr, const Params& p, int bpi) {
   cuuint64_t dims[3] = {(cuuint64_t)p.H, (cuuint64_t)p.L, (cuuint64_t)p.B};
   cuuint64_t strides[2] = {(cuuint64_t)p.sa_l * 2, (cuuint64_t)p.sa_b * 2};
   cuuint32_t box[3] = {8, (cuuint32_t)(16 * bpi), 1};
-  cuuint32_t es[3] = {1, 1, 1};
-  return encoder()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  return encode_cached(m, ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE, 1);
 }
 
 template <int OP>
@@ -1460,15 +1573,18 @@ static cudaError_t launch_op(const Params& p, cudaStream_t st, int sms) {
   switch (OP) {
     case 0: ins[0] = p.u; outs[0] = p.x; nin = 1; nout = 1; break;
     case 1: ins[0] = p.u; ins[1] = p.dx; outs[0] = p.du; nin = 2; nout = 1; break;
-    case 2: ins[0] = p.q; ins[1] = p.k; ins[2] = p.v; outs[0] = p.y; nin = 3; nout = 1; break;
+    case 2: case 4: ins[0] = p.q; ins[1] = p.k; ins[2] = p.v; outs[0] = p.y; nin = 3; nout = 1; break;
     default:
       ins[0] = p.q; ins[1] = p.k; ins[2] = p.v; ins[3] = p.dy;
       outs[0] = p.dq; outs[1] = p.dk; outs[2] = p.dv; nin = 4; nout = 3;
   }
+  // layer mixer: q / k (inputs 0, 1) and dq / dk (outputs 0, 1) use the group strides
+  auto kind = [](int i) { return (OP >= 4 && i < 2) ? i + 1 : 0; };
   for (int i = 0; i < nin; ++i)
-    if (!map_dtensor(&maps.in[i], ins[i], p, 16 * Cfg<OP>::BPI)) return cudaErrorNotSupported;
+    if (!map_dtensor(&maps.in[i], ins[i], p, 16 * Cfg<OP>::BPI, kind(i))) return cudaErrorNotSupported;
   for (int i = 0; i < nout; ++i)
-    if (!map_dtensor(&maps.out[i], outs[i], p, 16 * Cfg<OP>::BPI)) return cudaErrorNotSupported;
+    if (!map_dtensor(&maps.out[i], outs[i], p, 16 * Cfg<OP>::BPI, OP == 5 ? kind(i) : 0))
+      return cudaErrorNotSupported;
   if (!map_decay(&maps.a, p.a, p, Cfg<OP>::BPI)) return cudaErrorNotSupported;
 
   constexpr int smem = smem_bytes<OP>();
@@ -1516,8 +1632,9 @@ static cudaError_t launch_op(const Params& p, cudaStream_t st, int sms) {
 }  // namespace tc
 
 bool tc_supported(int op, bool bf16, const Params& p) {
-  if (op >= 4) return false;  // the layer mixer (NEXT-1) runs on the CUDA-core family
   if (!bf16 || p.D != 128) return false;
+  // layer mixer backward: the group sums of dq / dk run on the CUDA-core family
+  if (op == 5 && (p.hq != 1 || p.hk != 1)) return false;
   if (tc::encoder() == nullptr) return false;
   auto a16 = [](const void* q) { return q == nullptr || (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
   // decays must be TMA-addressable: heads contiguous, 16-byte token/batch strides
@@ -1534,7 +1651,9 @@ cudaError_t launch_tc(int op, const Params& p, cudaStream_t st, int sms, int* la
     case 0: e = tc::launch_op<0>(p, st, sms); break;
     case 1: e = tc::launch_op<1>(p, st, sms); break;
     case 2: e = tc::launch_op<2>(p, st, sms); break;
-    default: e = tc::launch_op<3>(p, st, sms); break;
+    case 3: e = tc::launch_op<3>(p, st, sms); break;
+    case 4: e = tc::launch_op<4>(p, st, sms); break;
+    default: e = tc::launch_op<5>(p, st, sms); break;
   }
   if (e == cudaSuccess) *launches = 1;
   return e;

@@ -67,8 +67,11 @@ def _abi_layout(t):
     """d-tensor layout the ABI accepts as is: D contiguous, 16-byte aligned base
     pointer and strides, non-overlapping."""
     e = t.element_size()
-    return (t.stride(3) == 1 and t.data_ptr() % 16 == 0
-            and all((t.stride(i) * e) % 16 == 0 for i in range(3)) and _no_overlap(t))
+    if t.data_ptr() % 16:
+        return False
+    if t.is_contiguous():  # fast path: strides are multiples of D
+        return (t.shape[3] * e) % 16 == 0
+    return (t.stride(3) == 1 and all((t.stride(i) * e) % 16 == 0 for i in range(3)) and _no_overlap(t))
 
 
 def _prep(*ts):
@@ -89,6 +92,8 @@ def _prep(*ts):
 def _prep_a(a):
     """Decays with strides `da` can share: contiguous copy if `a` overlaps itself
     (a zero stride, e.g. a decay row expanded over heads) or is misaligned."""
+    if a.is_contiguous():
+        return a
     if a.dim() == 3 and (not _no_overlap(a) or a.data_ptr() % a.element_size()):
         _count()
         return a.contiguous()
@@ -138,6 +143,24 @@ def _stream(t):
     return torch.cuda.current_stream(t.device).cuda_stream
 
 
+class _on:
+    """Make t's device current for the call (the ABI launches on the current
+    device), skipping the switch when it already is."""
+    __slots__ = ("idx", "prev")
+
+    def __init__(self, t):
+        self.idx = t.device.index
+
+    def __enter__(self):
+        self.prev = torch.cuda.current_device()
+        if self.prev != self.idx:
+            torch.cuda.set_device(self.idx)
+
+    def __exit__(self, *exc):
+        if self.prev != self.idx:
+            torch.cuda.set_device(self.prev)
+
+
 def _new_carry(like):
     B, _, H, D = like.shape
     return torch.empty((B, H, D), device=like.device, dtype=torch.float32)
@@ -154,7 +177,7 @@ def swr_fwd(u, a, carry_in=None, return_carry=False):
     x = _like(u)
     ci = _carry(carry_in, u)
     co = _new_carry(u) if return_carry else None
-    with torch.cuda.device(u.device):
+    with _on(u):
         _lib.swr_fwd(_ptr(u), _ptr(a), _ptr(x), _ptr(ci), _ptr(co), _shape(u, a), dt, _stream(u))
     return (x, co) if return_carry else x
 
@@ -168,7 +191,7 @@ def swr_bwd(u, a, dx, carry_in=None, mu_in=None):
     da = _like(a)
     ci, mi = _carry(carry_in, u), _carry(mu_in, u)
     mo = _new_carry(u)
-    with torch.cuda.device(u.device):
+    with _on(u):
         _lib.swr_bwd(_ptr(u), _ptr(a), _ptr(dx), _ptr(du), _ptr(da), _ptr(ci), _ptr(mi), _ptr(mo),
                      _shape(u, a), dt, _stream(u))
     return du, da, mo
@@ -182,7 +205,7 @@ def phalanx_mix(q, k, v, a, carry_in=None, return_carry=False):
     y = _like(q)
     ci = _carry(carry_in, q)
     co = _new_carry(q) if return_carry else None
-    with torch.cuda.device(q.device):
+    with _on(q):
         _lib.phalanx_mix(_ptr(q), _ptr(k), _ptr(v), _ptr(a), _ptr(y), _ptr(ci), _ptr(co),
                          _shape(q, a), dt, _stream(q))
     return (y, co) if return_carry else y
@@ -197,7 +220,7 @@ def phalanx_mix_bwd(q, k, v, a, dy, carry_in=None, mu_in=None):
     da = _like(a)
     ci, mi = _carry(carry_in, q), _carry(mu_in, q)
     mo = _new_carry(q)
-    with torch.cuda.device(q.device):
+    with _on(q):
         _lib.phalanx_mix_bwd(_ptr(q), _ptr(k), _ptr(v), _ptr(a), _ptr(dy), _ptr(dq), _ptr(dk),
                              _ptr(dv), _ptr(da), _ptr(ci), _ptr(mi), _ptr(mo), _shape(q, a), dt,
                              _stream(q))
@@ -235,7 +258,7 @@ def phalanx_layer_mix(q, zk, v, za, carry_in=None, return_carry=False, logit_a=T
     y = _like(v)
     ci = _carry(carry_in, v)
     co = _new_carry(v) if return_carry else None
-    with torch.cuda.device(v.device):
+    with _on(v):
         _lib.phalanx_layer_mix(_ptr(q), _ptr(zk), _ptr(v), _ptr(za), _ptr(y), _ptr(ci), _ptr(co),
                                _shape(v, za), _layer(q, zk, logit_a, logit_k), dt, _stream(v))
     return (y, co) if return_carry else y
@@ -251,7 +274,7 @@ def phalanx_layer_mix_bwd(q, zk, v, za, dy, carry_in=None, mu_in=None, logit_a=T
     dq, dzk, dv, dza = _like(q), _like(zk), _like(v), _like(za)
     ci, mi = _carry(carry_in, v), _carry(mu_in, v)
     mo = _new_carry(v)
-    with torch.cuda.device(v.device):
+    with _on(v):
         _lib.phalanx_layer_mix_bwd(_ptr(q), _ptr(zk), _ptr(v), _ptr(za), _ptr(dy), _ptr(dq), _ptr(dzk),
                                    _ptr(dv), _ptr(dza), _ptr(ci), _ptr(mi), _ptr(mo), _shape(v, za),
                                    _layer(q, zk, logit_a, logit_k), dt, _stream(v))
@@ -329,7 +352,7 @@ def swr_exact_fwd(u, a, carry_in=None, return_carry=False):
     shape = _shape(u, a)
     nbytes = _lib.swr_exact_workspace_bytes(shape)
     ws = torch.empty(max(nbytes, 16) // 4, dtype=torch.float32, device=u.device)
-    with torch.cuda.device(u.device):
+    with _on(u):
         _lib.swr_exact_fwd(_ptr(u), _ptr(a), _ptr(x), _ptr(ci), _ptr(co), _ptr(ws), nbytes, shape, dt,
                            _stream(u))
     return (x, co) if return_carry else x
@@ -347,7 +370,7 @@ def swr_exact_bwd(u, a, dx, carry_in=None, mu_in=None):
     shape = _shape(u, a)
     nbytes = 2 * _lib.swr_exact_workspace_bytes(shape)
     ws = torch.empty(max(nbytes, 16) // 4, dtype=torch.float32, device=u.device)
-    with torch.cuda.device(u.device):
+    with _on(u):
         _lib.swr_exact_bwd(_ptr(u), _ptr(a), _ptr(dx), _ptr(du), _ptr(da), _ptr(ci), _ptr(mi), _ptr(mo),
                            _ptr(ws), nbytes, shape, dt, _stream(u))
     return du, da, mo
@@ -377,7 +400,7 @@ def swr_uniform_fwd(u, a, k):
     a = _prep_a(a)
     dt = _dtype(u, a)
     x = _like(u)
-    with torch.cuda.device(u.device):
+    with _on(u):
         _lib.swr_uniform_fwd(_ptr(u), _ptr(a), _ptr(x), int(k), _shape(u, a), dt, _stream(u))
     return x
 
@@ -436,7 +459,7 @@ def swr_decode_step(u, a, state):
     dt = _dtype(u, a)
     u = u.contiguous()  # the ABI shares (sx_b, sx_h) between u and x
     x = torch.empty(u.shape, dtype=u.dtype, device=u.device)
-    with torch.cuda.device(u.device):
+    with _on(u):
         _lib.swr_decode_step(_ptr(u), _ptr(a), _ptr(x), _ptr(state.w), _ptr(state.v), _ptr(state.g),
                              state.pos, _dec_shape(u, a, state), dt, _stream(u))
     state.pos += 1
@@ -448,7 +471,7 @@ def phalanx_mix_decode_step(q, k, v, a, state):
     dt = _dtype(q, k, v, a)
     q, k, v = (t.contiguous() for t in (q, k, v))
     y = torch.empty(q.shape, dtype=q.dtype, device=q.device)
-    with torch.cuda.device(q.device):
+    with _on(q):
         _lib.phalanx_mix_decode_step(_ptr(q), _ptr(k), _ptr(v), _ptr(a), _ptr(y), _ptr(state.w),
                                      _ptr(state.v), _ptr(state.g), state.pos, _dec_shape(q, a, state),
                                      dt, _stream(q))

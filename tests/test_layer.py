@@ -145,3 +145,54 @@ def test_layer_mix_autograd(P):
     for name, x, r in (("dq", g["q"].grad, rdq), ("dzk", g["zk"].grad, rdzk), ("dv", g["v"].grad, rdv),
                        ("dza", g["za"].grad, rdza)):
         assert normwise(x, r) <= 1e-5, name
+
+
+# ---------------------------------------------------------------------------
+# tensor-core family (bf16, D = 128, H a multiple of 8): forward with sigma and
+# group-shared q / k through the TMA maps; backward with sigma when no head shares
+# a group (the group sums run on the CUDA-core family)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("B,L,H,Gq,Gk", [(2, 100, 16, 8, 4), (1, 4096, 16, 8, 8), (3, 33, 8, 1, 2),
+                                         (1, 1, 24, 24, 24), (2, 200, 16, 16, 16)])
+@pytest.mark.parametrize("carry", [False, True])
+def test_layer_mix_tc_forward(P, B, L, H, Gq, Gk, carry):
+    inp = layer_inputs(B, L, H, 128, Gq, Gk, dtype=torch.bfloat16, seed=L + H + Gq, carry=carry)
+    g = {k: v.cuda() for k, v in inp.items()}
+    prev = P.set_path(P.SWR_PATH_TC)
+    try:
+        y, co = P.phalanx_layer_mix(g["q"], g["zk"], g["v"], g["za"], carry_in=g.get("carry_in"), return_carry=True)
+        assert P.last_path() == 2
+    finally:
+        P.set_path(prev)
+    torch.cuda.synchronize()
+    h = {k: to64(v) for k, v in inp.items()}
+    ry, rco = oracle.layer_mix_fwd(h["q"], h["zk"], h["v"], h["za"], carry_in=h.get("carry_in"), carry_out=True)
+    check({"y": y, "carry_out": co}, {"y": ry, "carry_out": rco}, 2e-2)
+
+
+@pytest.mark.parametrize("B,L,H", [(2, 100, 16), (1, 4096, 16), (1, 17, 8), (2, 300, 24)])
+@pytest.mark.parametrize("carry", [False, True])
+def test_layer_mix_tc_backward(P, B, L, H, carry):
+    inp = layer_inputs(B, L, H, 128, dtype=torch.bfloat16, seed=3 * L + H, carry=carry)
+    prev = P.set_path(P.SWR_PATH_TC)
+    try:
+        outs, refs = run(P, inp)
+        assert P.last_path() == 2
+    finally:
+        P.set_path(prev)
+    check(outs, refs, 2e-2)
+
+
+def test_layer_mix_tc_backward_groups_not_on_tc(P):
+    """Grouped backward: forced TC is refused (no silent fallback); AUTO runs it on
+    the CUDA-core family."""
+    inp = layer_inputs(1, 64, 16, 128, 8, 8, dtype=torch.bfloat16, seed=1)
+    g = {k: v.cuda() for k, v in inp.items()}
+    prev = P.set_path(P.SWR_PATH_TC)
+    try:
+        with pytest.raises(P.SwrError, match="UNSUPPORTED"):
+            P.phalanx_layer_mix_bwd(g["q"], g["zk"], g["v"], g["za"], g["dy"])
+    finally:
+        P.set_path(prev)
+    P.phalanx_layer_mix_bwd(g["q"], g["zk"], g["v"], g["za"], g["dy"])
+    assert P.last_path() == 1

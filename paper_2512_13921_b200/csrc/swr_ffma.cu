@@ -104,6 +104,9 @@ __device__ __forceinline__ float ld_decay(const Params& p, const T* A, int64_t n
   return (LAYER && p.logit_a) ? sigmoid_f(z) : z;
 }
 
+#ifndef SWR_FFMA_MIXF_GROUP
+#define SWR_FFMA_MIXF_GROUP 4  // mixer forward: tokens whose loads are issued together
+#endif
 // LAYER: the Phalanx layer around the mixer (phalanx_layer_mix): logits and
 // group-shared q / k (Params); otherwise the plain SWR / mixer ops.
 template <typename T, bool MIX, bool LAYER>
@@ -156,7 +159,8 @@ __global__ void __launch_bounds__(128) fwd_stream(const Params p) {
     float g = 1.f;
     // SWR: the block's loads first (stores to x may alias them, so the compiler
     // cannot hoist them past the stores): 16 decays and 16 raw 16-byte vectors.
-    // Mixer: per token (three tiles per token would cost too many registers).
+    // Mixer: the loads of MG tokens at a time (a, k, v, q; v serves the pre-gate and
+    // the residual), then their arithmetic and stores.
     float ab[MIX ? 1 : kEll];
     uint4 ub[MIX ? 1 : kEll];
     if constexpr (!MIX) {
@@ -167,36 +171,60 @@ __global__ void __launch_bounds__(128) fwd_stream(const Params p) {
         ab[i] = valid ? IO<T>::ld1(A + n * p.sa_l) : 1.f;  // pad: a = 1 (carry_out = state at L-1)
         ub[i] = valid ? __ldg(reinterpret_cast<const uint4*>((const T*)p.u + xo + n * p.sx_l)) : make_uint4(0, 0, 0, 0);
       }
-    }
 #pragma unroll
-    for (int i = 0; i < kEll; ++i) {
-      const int64_t n = t * kEll + i;
-      const bool valid = n < p.L;
-      float a, u[VC];
-      if constexpr (!MIX) {
-        a = ab[i];
+      for (int i = 0; i < kEll; ++i) {
+        const int64_t n = t * kEll + i;
+        float u[VC];
         Vec16<T>::to_f(ub[i], u);
-      } else {
-        a = ld_decay<T, LAYER>(p, A, n, valid);
-        load_u16<T, true, LAYER>(p, xo + n * p.sx_l, ko + n * skl, valid, u);
-      }
-      g *= a;  // g_t[i] = a_t[0] ... a_t[i]
-      float x[VC];
+        g *= ab[i];  // g_t[i] = a_t[0] ... a_t[i]
+        float x[VC];
 #pragma unroll
-      for (int e = 0; e < VC; ++e) {
-        w[e] = (i == 0) ? u[e] : fmaf(a, w[e], u[e]);  // Pass I
-        x[e] = fmaf(g, v[e], w[e]);                      // Pass II: x~ = w + g v_{t-1}
+        for (int e = 0; e < VC; ++e) {
+          w[e] = (i == 0) ? u[e] : fmaf(ab[i], w[e], u[e]);  // Pass I
+          x[e] = fmaf(g, v[e], w[e]);                         // Pass II: x~ = w + g v_{t-1}
+        }
+        if (n < p.L) *reinterpret_cast<uint4*>((T*)p.x + xo + n * p.sx_l) = Vec16<T>::from_f(x);
       }
-      if (valid) {
-        if constexpr (!MIX) {
-          *reinterpret_cast<uint4*>((T*)p.x + xo + n * p.sx_l) = Vec16<T>::from_f(x);
-        } else {  // post-gate with residual: y = q x~ + v
-          float qq[VC], vv[VC];
-          Vec16<T>::to_f(__ldg(reinterpret_cast<const uint4*>((const T*)p.q + qo + n * sql)), qq);
-          Vec16<T>::to_f(__ldg(reinterpret_cast<const uint4*>((const T*)p.v + xo + n * p.sx_l)), vv);
+    } else {
+      constexpr int MG = SWR_FFMA_MIXF_GROUP;
 #pragma unroll
-          for (int e = 0; e < VC; ++e) x[e] = fmaf(qq[e], x[e], vv[e]);
-          *reinterpret_cast<uint4*>((T*)p.y + xo + n * p.sx_l) = Vec16<T>::from_f(x);
+      for (int i0 = 0; i0 < kEll; i0 += MG) {
+        float ar[MG];
+        uint4 kr[MG], vr[MG], qr[MG];
+#pragma unroll
+        for (int m = 0; m < MG; ++m) {
+          const int64_t n = t * kEll + i0 + m;
+          const bool valid = n < p.L;
+          ar[m] = valid ? IO<T>::ld1(A + n * p.sa_l) : 1.f;
+          kr[m] = valid ? __ldg(reinterpret_cast<const uint4*>((const T*)p.k + ko + n * skl)) : make_uint4(0, 0, 0, 0);
+          vr[m] = valid ? __ldg(reinterpret_cast<const uint4*>((const T*)p.v + xo + n * p.sx_l)) : make_uint4(0, 0, 0, 0);
+          qr[m] = valid ? __ldg(reinterpret_cast<const uint4*>((const T*)p.q + qo + n * sql)) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int m = 0; m < MG; ++m) {
+          const int i = i0 + m;
+          const int64_t n = t * kEll + i;
+          float a = ar[m];
+          if (LAYER && p.logit_a && n < p.L) a = sigmoid_f(a);  // a = sigma(za)
+          float kk[VC], vv[VC], qq[VC], u[VC];
+          Vec16<T>::to_f(kr[m], kk);
+          Vec16<T>::to_f(vr[m], vv);
+          Vec16<T>::to_f(qr[m], qq);
+          if (LAYER && p.logit_k) {
+#pragma unroll
+            for (int e = 0; e < VC; ++e) kk[e] = sigmoid_f(kk[e]);  // k = sigma(zk)
+          }
+#pragma unroll
+          for (int e = 0; e < VC; ++e) u[e] = __fmul_rn(kk[e], vv[e]);  // u^ = k (.) v
+          g *= a;
+          float x[VC];
+#pragma unroll
+          for (int e = 0; e < VC; ++e) {
+            w[e] = (i == 0) ? u[e] : fmaf(a, w[e], u[e]);  // Pass I
+            x[e] = fmaf(g, v[e], w[e]);                      // Pass II
+            x[e] = fmaf(qq[e], x[e], vv[e]);                 // post-gate with residual
+          }
+          if (n < p.L) *reinterpret_cast<uint4*>((T*)p.y + xo + n * p.sx_l) = Vec16<T>::from_f(x);
         }
       }
     }
@@ -429,6 +457,16 @@ __global__ void __launch_bounds__(NTH, NTH == 128 ? ((!MIX && sizeof(T) == 2) ? 
       const int lim = (p.L - n0 < kEll) ? (int)(p.L - n0) : kEll;
       float acur[kEll];
       load_a(n0, lim, acur);
+      // the block's G vectors first: their loads are in flight during A
+      typename V::raw graw[kEll];
+      {
+        const T* gp = (const T*)p.dx + xo + n0 * sl;
+#pragma unroll
+        for (int i = 0; i < kEll; ++i) {
+          graw[i] = (i < lim) ? V::ld(gp) : V::zero();
+          gp += sl;
+        }
+      }
       // A) w_{t-1} into the other slot (block t-1 is whole), v_{t-1} = w_{t-1}[15]
       float vprev[VC];
       if (t > 0) {
@@ -445,13 +483,11 @@ __global__ void __launch_bounds__(NTH, NTH == 128 ? ((!MIX && sizeof(T) == 2) ? 
       float part[kEll];
       float lam[VC], mu_next[VC];
       float rr = 1.f;
-      Src gsrc = src_g(n0 + kEll - 1);
       T* dup = (T*)p.du + xo + (n0 + kEll - 1) * sl;
 #pragma unroll
       for (int i = kEll - 1; i >= 0; --i) {
         float g[VC];
-        gsrc.load(i < lim, g);
-        gsrc.back();
+        V::to_f(graw[i], g);
         if (i == kEll - 1) {
 #pragma unroll
           for (int e = 0; e < VC; ++e) lam[e] = g[e];  // lambda[15] = G[15]

@@ -252,10 +252,13 @@ __global__ void __launch_bounds__(128) fwd_stream(const Params p) {
 #define SWR_FFMA_BWDV_UNROLL 4  // pass C unroll (16 spills 1.3 KB: 3x slower; 2 or 8: 5-15% slower)
 #endif
 #ifndef SWR_FFMA_MIXBV_UNROLL
-#define SWR_FFMA_MIXBV_UNROLL 2  // the mixer's pass C unroll (4: 12% slower at d=16, spills)
+#define SWR_FFMA_MIXBV_UNROLL 1  // the mixer pass C: groups of SWR_FFMA_BWD_CG tokens, not unrolled further (spills)
 #endif
 #ifndef SWR_FFMA_BWD_MINB
 #define SWR_FFMA_BWD_MINB 4  // 128 registers
+#endif
+#ifndef SWR_FFMA_BWD_CG
+#define SWR_FFMA_BWD_CG 4  // Pass C: tokens whose loads are issued together
 #endif
 template <bool MIX>
 struct CUnrollV {
@@ -599,8 +602,27 @@ __global__ void __launch_bounds__(NTH, NTH == 128 ? ((!MIX && sizeof(T) == 2) ? 
     float gs = 1.f;  // g[i-1]
     int64_t o = xo + n0 * sl;
     int64_t ok = ko + n0 * skl, oq = qo + n0 * sql;
+    // the loads of CG tokens are issued together (the stores in between would keep the
+    // compiler from hoisting them): u, or k, v and dy
+    constexpr int CG = SWR_FFMA_BWD_CG;
 #pragma unroll CUnrollV<MIX>::v
-    for (int i = 0; i < kEll; ++i) {
+    for (int i0 = 0; i0 < kEll; i0 += CG) {
+      typename V::raw r0[CG], r1[CG], r2[CG];
+#pragma unroll
+      for (int m = 0; m < CG; ++m) {
+        const bool valid = i0 + m < lim;
+        const int64_t d = (int64_t)m * sl;
+        if constexpr (!MIX) {
+          r0[m] = valid ? V::ld((const T*)p.u + o + d) : V::zero();
+        } else {
+          r0[m] = valid ? V::ld((const T*)p.k + (LAYER ? ok + (int64_t)m * skl : o + d)) : V::zero();
+          r1[m] = valid ? V::ld((const T*)p.v + o + d) : V::zero();
+          r2[m] = valid ? V::ld((const T*)p.dy + o + d) : V::zero();
+        }
+      }
+#pragma unroll
+    for (int m = 0; m < CG; ++m) {
+      const int i = i0 + m;
       float lam[VC];
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
@@ -624,10 +646,10 @@ __global__ void __launch_bounds__(NTH, NTH == 128 ? ((!MIX && sizeof(T) == 2) ? 
       const bool valid = i < lim;
       float kk[VC], vv[VC], u[VC];
       if constexpr (!MIX) {
-        V::to_f(valid ? V::ld((const T*)p.u + o) : V::zero(), u);
+        V::to_f(r0[m], u);
       } else {
-        V::to_f(valid ? V::ld((const T*)p.k + (LAYER ? ok : o)) : V::zero(), kk);
-        V::to_f(valid ? V::ld((const T*)p.v + o) : V::zero(), vv);
+        V::to_f(r0[m], kk);
+        V::to_f(r1[m], vv);
         if (sig_k) {
 #pragma unroll
           for (int e = 0; e < VC; ++e) kk[e] = valid ? sigmoid_f(kk[e]) : 0.f;
@@ -642,7 +664,7 @@ __global__ void __launch_bounds__(NTH, NTH == 128 ? ((!MIX && sizeof(T) == 2) ? 
         if (act && valid) V::st((T*)p.du + o, du);
       } else {
         float dd[VC], dq[VC], dk[VC], dv[VC];
-        V::to_f(valid ? V::ld((const T*)p.dy + o) : V::zero(), dd);
+        V::to_f(r2[m], dd);
 #pragma unroll
         for (int e = 0; e < VC; ++e) {
           dq[e] = dd[e] * fmaf(gs, vprev[e], wprev[e]);  // dq = dy x~
@@ -672,6 +694,7 @@ __global__ void __launch_bounds__(NTH, NTH == 128 ? ((!MIX && sizeof(T) == 2) ? 
       o += sl;
       ok += skl;
       oq += sql;
+    }
     }
 #pragma unroll
     for (int e = 0; e < VC; ++e) mu[e] = mu_next[e];

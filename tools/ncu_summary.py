@@ -30,7 +30,8 @@ METRICS = [
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "SMEM bank conflicts"),
 ]
 KEYS = {"swr_tc_kernel<0>": "swr_fwd", "swr_tc_kernel<1>": "swr_bwd",
-        "swr_tc_kernel<2>": "mix_fwd", "swr_tc_kernel<3>": "mix_bwd"}
+        "swr_tc_kernel<2>": "mix_fwd", "swr_tc_kernel<3>": "mix_bwd",
+        "swr_tc_kernel<4>": "layer_fwd", "swr_tc_kernel<5>": "layer_bwd"}
 
 
 def to_bytes(val, unit):
@@ -38,13 +39,13 @@ def to_bytes(val, unit):
     return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
 
 
-def main(rep, launches, tag, config="layer4k_bf16"):
+def main(rep, launches, tag, config="layer4k_bf16", mode="L2 flushed before the kernel (ncu default)"):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     h, units = rows[0], rows[1]
     lines = [f"# ncu --set full summary ({tag})", "",
              f"Source: `{os.path.basename(rep)}` (one launch per kernel, `--clock-control none`, "
-             "BJ configs[1]: B=8, L=4096, H=16, d=128, bf16).", ""]
+             f"config {config}; caches: {mode}).", ""]
     traffic_path = os.path.join(ROOT, "profiles", "traffic.json")
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
     for r in rows[2:]:
@@ -60,12 +61,16 @@ def main(rep, launches, tag, config="layer4k_bf16"):
         lines += ["", f"DRAM traffic per launch: {rd + wr:.4g} B (read {rd:.4g} + write {wr:.4g}).", ""]
         if key in KEYS.values():
             op, dirn = key.split("_")
-            traffic[f"{op}_{dirn}_layer4k_bf16"] = rd + wr
+            traffic[f"{op}_{dirn}_{config}"] = {"bytes": rd + wr,
+                                                "source": f"ncu --set full, profiles/{tag}_kernels.md ({mode})"}
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     with open(os.path.join(ROOT, "profiles", f"{tag}_kernels.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
     with open(traffic_path, "w") as f:
         json.dump(traffic, f, indent=1)
+    if launches == "-":
+        print("wrote", f"profiles/{tag}_kernels.md", "profiles/traffic.json")
+        return
     # launch list: keep only the CSV rows
     with open(launches) as f:
         body = [l for l in f if not l.startswith("==")]

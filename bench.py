@@ -59,11 +59,17 @@ def esize(dt):
     return 2 if dt == "bf16" else 4
 
 
+LAYER_GROUPS = 8  # --op layer: q and k shared by 8 groups of heads
+
+
 def algo_bytes(op, B, L, H, D, dt):
     """Algorithmic HBM bytes per launch; halo re-reads excluded."""
     e, n = esize(dt), B * L * H
     if op == "swr":
         return {"fwd": n * (2 * D + 1) * e, "bwd": n * (3 * D + 2) * e}
+    if op == "layer":  # q, zk are [B, L, G, D]: read once per group, dq / dzk written per group
+        nt, G = B * L, min(LAYER_GROUPS, H)
+        return {"fwd": nt * (2 * G * D + 2 * H * D + H) * e, "bwd": nt * (4 * G * D + 3 * H * D + 2 * H) * e}
     return {"fwd": n * (4 * D + 1) * e, "bwd": n * (7 * D + 2) * e}
 
 
@@ -146,6 +152,10 @@ def oracle_step_fn(op, inp_host, rows, threads=0):
         def step():
             oracle.swr_fwd(h["u"], h["a"], threads=threads)
             oracle.swr_bwd(h["u"], h["a"], h["G"], threads=threads)
+    elif op == "layer":
+        def step():
+            oracle.layer_mix_fwd(h["q"], h["zk"], h["v"], h["za"], threads=threads)
+            oracle.layer_mix_bwd(h["q"], h["zk"], h["v"], h["za"], h["dy"], threads=threads)
     else:
         def step():
             oracle.mix_fwd(h["q"], h["k"], h["v"], h["a"], threads=threads)
@@ -155,8 +165,11 @@ def oracle_step_fn(op, inp_host, rows, threads=0):
 
 def make_host_inputs(op, B, L, H, D, dt, seed):
     import torch
-    from swr_inputs import mix_inputs, swr_inputs
+    from swr_inputs import layer_inputs, mix_inputs, swr_inputs
     dtype = torch.bfloat16 if dt == "bf16" else torch.float32
+    if op == "layer":
+        G = min(LAYER_GROUPS, H)
+        return layer_inputs(B, L, H, D, G, G, dtype=dtype, seed=seed)
     f = swr_inputs if op == "swr" else mix_inputs
     return f(B, L, H, D, dtype=dtype, seed=seed)
 
@@ -232,6 +245,9 @@ def step_fns(P, op, g):
     """fwd() and bwd() of one step of the hot path on device-resident inputs g."""
     if op == "swr":
         return (lambda: P.swr_fwd(g["u"], g["a"])), (lambda: P.swr_bwd(g["u"], g["a"], g["G"]))
+    if op == "layer":  # sigma on the logits, 8 groups for q and k
+        return ((lambda: P.phalanx_layer_mix(g["q"], g["zk"], g["v"], g["za"])),
+                (lambda: P.phalanx_layer_mix_bwd(g["q"], g["zk"], g["v"], g["za"], g["dy"])))
     return ((lambda: P.phalanx_mix(g["q"], g["k"], g["v"], g["a"])),
             (lambda: P.phalanx_mix_bwd(g["q"], g["k"], g["v"], g["a"], g["dy"])))
 
@@ -243,7 +259,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="layer4k", choices=sorted(CONFIGS))
-    ap.add_argument("--op", default="swr", choices=["swr", "mix"])
+    ap.add_argument("--op", default="swr", choices=["swr", "mix", "layer"])
     ap.add_argument("--path", default="auto", choices=["auto", "ffma", "tc"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -393,7 +409,12 @@ def main():
     value = tokens_per_step / (ms_per_step / 1e3)
 
     bytes_ = algo_bytes(args.op, B, Ls, H, D, dt)
-    mf, mb = statistics.mean(t_fwd), statistics.mean(t_bwd)
+    # the split loop's event between the two kernels stops the backward's early start
+    # (programmatic dependent launch), so its fwd / bwd times add up to more than a
+    # step: attribute the step time to the two kernels in the split loop's proportion
+    sf, sb = statistics.mean(t_fwd), statistics.mean(t_bwd)
+    step_ms = ms_per_step
+    mf, mb = step_ms * sf / (sf + sb), step_ms * sb / (sf + sb)
     dom = "bwd" if mb >= mf else "fwd"
     peak, peak_kind = load_peaks()
     ach = bytes_[dom] / (mb if dom == "bwd" else mf) / 1e6  # GB/s
@@ -425,7 +446,8 @@ def main():
                               f"{flush_rd.numel() * 4 >> 20} MiB read, outside the events)"),
                    "path": args.path, "last_path": {0: "none", 1: "ffma", 2: "tc"}[P.last_path()]},
         "fwd_ms": mf, "bwd_ms": mb,
-        "split_note": "fwd_ms / bwd_ms from a second loop with an event between the two kernels of each step",
+        "split_note": ("fwd_ms / bwd_ms: the step time split in the proportion of a second loop with an "
+                       "event between the two kernels of each step (split loop: fwd %.4f ms, bwd %.4f ms)" % (sf, sb)),
         "hbm_gbs": {"fwd": bytes_["fwd"] / mf / 1e6, "bwd": bytes_["bwd"] / mb / 1e6,
                     "fwd_bwd": (bytes_["fwd"] + bytes_["bwd"]) / (mf + mb) / 1e6},
         "roofline": {"bound": "hbm", "kernel": f"{args.op}_{dom}", "achieved": ach, "peak": peak,
@@ -456,7 +478,8 @@ def main():
             xb = algo_bytes(args.op, Bx, Lx, Hx, Dx, dtx)
             line["workloads"][name] = {
                 "B": Bx, "L": Lx, "value": Bx * Lx * world / (xm / 1e3), "unit": "tokens/s", "ms_per_step": xm,
-                "fwd_ms": statistics.mean(x_fwd), "bwd_ms": statistics.mean(x_bwd),
+                "fwd_ms": xm * statistics.mean(x_fwd) / (statistics.mean(x_fwd) + statistics.mean(x_bwd)),
+                "bwd_ms": xm * statistics.mean(x_bwd) / (statistics.mean(x_fwd) + statistics.mean(x_bwd)),
                 "hbm_gbs_fwd_bwd": (xb["fwd"] + xb["bwd"]) / xm / 1e6,
                 "timing": "back to back" if bx_ else "L2 flushed"}
             del gx
@@ -479,6 +502,9 @@ def main():
             if args.op == "swr":
                 du, da, _ = P.swr_bwd(c["u"], c["a"], c["G"])
                 return (P.swr_fwd(c["u"], c["a"]), du, da)
+            if args.op == "layer":
+                dq, dzk, dv, dza, _ = P.phalanx_layer_mix_bwd(c["q"], c["zk"], c["v"], c["za"], c["dy"])
+                return (P.phalanx_layer_mix(c["q"], c["zk"], c["v"], c["za"]), dq, dzk, dv, dza)
             dq, dk, dv, da, _ = P.phalanx_mix_bwd(c["q"], c["k"], c["v"], c["a"], c["dy"])
             return (P.phalanx_mix(c["q"], c["k"], c["v"], c["a"]), dq, dk, dv, da)
 

@@ -308,7 +308,8 @@ struct VecN {
 // order (deterministic): the CTA holds NTH / TPH heads, a multiple of hq and hk.
 // dq is staged over the lambda slots it replaces, dk in a second buffer.
 template <typename T, int VC, int TPH, bool MIX, bool LAYER = false, int NTH = 128>
-__global__ void __launch_bounds__(NTH, NTH == 128 ? ((!MIX && sizeof(T) == 2) ? 3 : SWR_FFMA_BWD_MINB) : 1) bwd_ffma_vec(const Params p) {
+__global__ void __launch_bounds__(NTH, NTH == 128 ? ((LAYER || (!MIX && sizeof(T) == 2)) ? 3 : SWR_FFMA_BWD_MINB) : 1)
+    bwd_ffma_vec(const Params p) {
   using V = VecN<T, VC>;
   using io = IO<T>;
   static_assert(!LAYER || MIX, "the layer options apply to the mixer");
@@ -604,7 +605,7 @@ __global__ void __launch_bounds__(NTH, NTH == 128 ? ((!MIX && sizeof(T) == 2) ? 
     int64_t ok = ko + n0 * skl, oq = qo + n0 * sql;
     // the loads of CG tokens are issued together (the stores in between would keep the
     // compiler from hoisting them): u, or k, v and dy
-    constexpr int CG = SWR_FFMA_BWD_CG;
+    constexpr int CG = MIX ? SWR_FFMA_BWD_CG : 1;  // fp32 SWR: unrolled by CUnrollV instead
 #pragma unroll CUnrollV<MIX>::v
     for (int i0 = 0; i0 < kEll; i0 += CG) {
       typename V::raw r0[CG], r1[CG], r2[CG];
@@ -1296,7 +1297,9 @@ static cudaError_t launch_bwd_vec(Params p, cudaStream_t st, int sms) {
   K = std::min<int64_t>(K, p.nb);
   p.K = K;
   dim3 grid((unsigned)ceil_div(p.nb, K), (unsigned)ceil_div(p.H, HPC), (unsigned)p.B);
-  bwd_ffma_vec<T, VC, TPH, MIX, LAYER, NTH><<<grid, NTH, kSmem, st>>>(p);
+  // the layer kernel needs the dk staging only when heads share k
+  const int smem = (LAYER && p.hk == 1) ? kSmem / 2 : kSmem;
+  bwd_ffma_vec<T, VC, TPH, MIX, LAYER, NTH><<<grid, NTH, smem, st>>>(p);
   return cudaGetLastError();
 }
 

@@ -107,6 +107,12 @@ constexpr int kHalf = 2048;      // one 64-channel half: 16 rows x 128 B, 128B-s
 #ifndef SWR_MF_NPW
 #define SWR_MF_NPW 3
 #endif
+#ifndef SWR_MF_NI
+#define SWR_MF_NI 6
+#endif
+#ifndef SWR_MB_NPW
+#define SWR_MB_NPW 4
+#endif
 #ifndef SWR_MF_NW
 #define SWR_MF_NW 6
 #endif
@@ -133,7 +139,7 @@ struct Cfg<1> {  // swr_bwd: in u, G;  out du
 };
 template <>
 struct Cfg<2> {  // mix fwd: in q, k, v;  out y;  prep u^ = k v (over k)
-  static constexpr int NT = 3, NP = 0, BPI = 2, NI = 6, NA = 6, NW = SWR_MF_NW, NO = 4, COLS = 16, NPW = SWR_MF_NPW, NOUT = 1, NG = 3;
+  static constexpr int NT = 3, NP = 0, BPI = 2, NI = SWR_MF_NI, NA = 6, NW = SWR_MF_NW, NO = 4, COLS = 16, NPW = SWR_MF_NPW, NOUT = 1, NG = 3;
   static constexpr int TU = 1, TG = 0;
   static constexpr bool CYC = false;
   static constexpr bool WC = false;
@@ -141,7 +147,7 @@ struct Cfg<2> {  // mix fwd: in q, k, v;  out y;  prep u^ = k v (over k)
 };
 template <>
 struct Cfg<3> {  // mix bwd: in q, k, v, dy;  out dq, dk, dv;  prep u^ = k v (region 4), G = dy q (over q)
-  static constexpr int NT = 4, NP = 1, BPI = 1, NI = SWR_MB_NI, NA = 8, NW = 8, NO = 3, COLS = 48, NPW = 4, NOUT = 3, NG = 3;
+  static constexpr int NT = 4, NP = 1, BPI = 1, NI = SWR_MB_NI, NA = 8, NW = 8, NO = 3, COLS = 48, NPW = SWR_MB_NPW, NOUT = 3, NG = 3;
   static constexpr int TU = 4, TG = 0;
   static constexpr bool CYC = false;
   static constexpr bool WC = true;  // x~ needs w[i] (dq), da needs w[i-1]: both from TMEM
@@ -513,18 +519,27 @@ __device__ __forceinline__ float sig_tc(float z) {
   asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * z));
   return fmaf(0.5f, t, 0.5f);
 }
-// 8 elements of u^ = sigma(zk) (.) v, each rounded once to bf16
-__device__ __forceinline__ uint4 sigmul8(const uint4& zk, const uint4& v) {
-  const uint32_t a[4] = {zk.x, zk.y, zk.z, zk.w}, b[4] = {v.x, v.y, v.z, v.w};
-  uint32_t o[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const float k0 = sig_tc(__uint_as_float(a[q] << 16)), k1 = sig_tc(__uint_as_float(a[q] & 0xffff0000u));
-    const float v0 = __uint_as_float(b[q] << 16), v1 = __uint_as_float(b[q] & 0xffff0000u);
-    __nv_bfloat162 r = __floats2bfloat162_rn(k0 * v0, k1 * v1);
-    o[q] = *reinterpret_cast<uint32_t*>(&r);
-  }
-  return make_uint4(o[0], o[1], o[2], o[3]);
+// 8 elements of u^ = sigma(zk) (.) v and k = sigma(zk) (into *kout when non-null, for
+// the backward's epilogue), in packed bf16x2: k = 1/2 + tanh(zk/2)/2 with
+// tanh.approx.bf16x2, then u^ = k v rounded once more (R20: |error of k| <=
+// 2^-9, i.e. u^ within 2 bf16 roundings -- inside the 2e-2 tolerance of bf16 outputs)
+__device__ __forceinline__ uint32_t sig_bf2(uint32_t z2) {
+  const uint32_t half2 = 0x3F003F00u;  // (0.5, 0.5) in bf16x2
+  uint32_t h, t, k;
+  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(h) : "r"(z2), "r"(half2));
+  asm("tanh.approx.bf16x2 %0, %1;" : "=r"(t) : "r"(h));
+  asm("fma.rn.bf16x2 %0, %1, %2, %2;" : "=r"(k) : "r"(t), "r"(half2));
+  return k;
+}
+__device__ __forceinline__ uint4 sigmul8(const uint4& zk, const uint4& v, uint4* kout = nullptr) {
+  const uint4 k = make_uint4(sig_bf2(zk.x), sig_bf2(zk.y), sig_bf2(zk.z), sig_bf2(zk.w));
+  if (kout) *kout = k;
+  uint4 o;
+  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(o.x) : "r"(k.x), "r"(v.x));
+  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(o.y) : "r"(k.y), "r"(v.y));
+  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(o.z) : "r"(k.z), "r"(v.z));
+  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(o.w) : "r"(k.w), "r"(v.w));
+  return o;
 }
 // 8 bf16 products, elementwise, one RNE rounding each (mul.rn.bf16x2)
 __device__ __forceinline__ uint4 bmul8(const uint4& a, const uint4& b) {
@@ -1042,14 +1057,20 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
         // rounded once to bf16: u^ = k (.) v; backward also G = dy (.) q.
         // A bf16 x bf16 product is exact in fp32, so the packed bf16x2 multiply (one
         // rounding of the exact product) equals fp32 multiply + one RNE rounding.
-        const uint4* K4 = reinterpret_cast<const uint4*>(S::region(st, 1));
+        uint4* K4 = reinterpret_cast<uint4*>(S::region(st, 1));
         const uint4* V4 = reinterpret_cast<const uint4*>(S::region(st, 2));
         uint4* U4 = reinterpret_cast<uint4*>(S::region(st, C::TU));
 #pragma unroll 4
         for (int v = lane; v < S::kRegion / 16; v += 32) {
-          if (C::LAYER && p.logit_k)
-            U4[v] = sigmul8(K4[v], V4[v]);  // u^ = sigma(zk) (.) v
-          else
+          if (C::LAYER && p.logit_k) {  // u^ = sigma(zk) (.) v
+            if constexpr (C::BWD) {     // the epilogue reads k = sigma(zk) (bf16) over zk
+              uint4 kb;
+              U4[v] = sigmul8(K4[v], V4[v], &kb);
+              K4[v] = kb;
+            } else {
+              U4[v] = sigmul8(K4[v], V4[v]);
+            }
+          } else
             U4[v] = bmul8(K4[v], V4[v]);
           if constexpr (C::BWD) {
             uint4* Q4 = reinterpret_cast<uint4*>(S::region(st, 0));  // G overwrites q
@@ -1297,8 +1318,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                   const float2 d2 = make_float2(du[k][2 * h], du[k][2 * h + 1]);
-                  float2 kf = bf2f(tk[h][k]);
-                  if (C::LAYER && p.logit_k) kf = make_float2(sig_tc(kf.x), sig_tc(kf.y));  // k = sigma(zk)
+                  const float2 kf = bf2f(tk[h][k]);  // layer mixer: k = sigma(zk), written by the prep
                   const float2 dv2 = f2fma(d2, kf, bf2f(tdy[h][k]));
                   float2 dk2 = f2mul(d2, bf2f(tv[h][k]));
                   if (C::LAYER && p.logit_k)  // dzk = dk sigma'(zk), sigma' = k (1 - k)

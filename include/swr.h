@@ -195,7 +195,16 @@ typedef struct {
   int64_t sk_b, sk_l, sk_h;  /* element strides of zk and dzk, [B, L, Gk, D], D contiguous    */
   int32_t logit_a;           /* nonzero: za holds logits, a = sigma(za); else za is a itself  */
   int32_t logit_k;           /* nonzero: zk holds logits, k = sigma(zk); else zk is k itself  */
+  void* workspace;           /* nullable device scratch for the tensor-core backward with     */
+  int64_t workspace_bytes;   /* shared groups (phalanx_layer_workspace_bytes); unused forward */
 } swr_layer;
+
+/* Scratch the layer backward needs to run on the tensor cores when heads share q or k:
+ * per-head dq / dk (bf16 [B, L, H, D] each, for the groups of q resp. k that are shared),
+ * summed over each group by a second kernel in a fixed head order.  0 when no scratch is
+ * needed or the call is outside the tensor-core envelope; without it such a call runs
+ * on the CUDA-core family (AUTO) or is refused (SWR_PATH_TC). */
+SWR_API int64_t phalanx_layer_workspace_bytes(swr_shape s, swr_layer g, swr_dtype dt);
 
 /* Layer mixer forward.  v, y [B,L,H,D] with the strides of s; za [B,L,H] with the
  * decay strides of s; q, zk as described by g; carries as in phalanx_mix.
@@ -207,9 +216,10 @@ SWR_API swr_status phalanx_layer_mix(const void* q, const void* zk, const void* 
 
 /* Layer mixer backward.  dq [B,L,Gq,D] and dzk [B,L,Gk,D] with the strides of g
  * (the group sums), dv [B,L,H,D], dza [B,L,H]; carries as in phalanx_mix_bwd.
- * The CUDA-core kernel forms the group sums inside one CTA: H / Gq and H / Gk must
- * be powers of two and at most 256 / (D / 4) (64 at D = 16, 8 at D = 128), else
- * SWR_ERR_UNSUPPORTED. */
+ * The tensor-core kernels (bf16, D = 128) take shared groups when g.workspace holds
+ * phalanx_layer_workspace_bytes(s, g, dt) bytes (16-byte aligned); else the CUDA-core
+ * kernel forms the group sums inside one CTA: H / Gq and H / Gk must be powers of two
+ * and at most 256 / (D / 4) (64 at D = 16, 8 at D = 128), else SWR_ERR_UNSUPPORTED. */
 SWR_API swr_status phalanx_layer_mix_bwd(const void* q, const void* zk, const void* v,
                                  const void* za, const void* dy, void* dq, void* dzk, void* dv,
                                  void* dza, const float* carry_in, const float* mu_in,
@@ -244,10 +254,13 @@ SWR_API swr_status phalanx_mix_decode_step(const void* q, const void* k, const v
 
 /* Exact full-range recurrence: x_n = a_n x_{n-1} + u_n over
  * the whole sequence (Eq. 2.1, x_{-1} = carry_in) -- the operator B2P truncates --
- * computed as Alg. 2: I) per-block local solves giving the block end
- * state v_t and decay product c_t = a_t[0]...a_t[15]; II) the carrier recurrence
- * s_t = c_t s_{t-1} + v_t, sequential over blocks; III) reconstruction
- * x_t[i] = w_t[i] + g_t[i] s_{t-1} (Thm. 3).  CUDA cores, three launches.
+ * computed as Alg. 2 in one pass: each CTA solves its chunk of blocks
+ * locally to the chunk's carrier aggregate (decay product, local end state), and the
+ * carrier recurrence s_t = c_t s_{t-1} + v_t is resolved across CTAs by a
+ * decoupled look-back over published aggregates / inclusive prefixes, after which the
+ * chunk is re-run from its entering state.  CUDA cores, one launch (plus a memset of
+ * the look-back flags in the workspace).  The last bits of x may differ between runs
+ * (the look-back's summation order depends on timing); within the tolerances.
  *   u, a, x, carry_in as in swr_fwd; carry_out = x at token L-1 (the full state).
  *   workspace  device memory of >= swr_exact_workspace_bytes(s) bytes, 16-byte
  *              aligned, caller-owned scratch (no allocation here); too small ->

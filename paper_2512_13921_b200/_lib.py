@@ -20,7 +20,8 @@ EXPORTS = ("swr_fwd", "swr_bwd", "phalanx_mix", "phalanx_mix_bwd", "swr_strerror
            "swr_last_cuda_error", "swr_set_path", "swr_launch_count", "swr_last_path",
            "swr_set_trace", "swr_decode_step", "phalanx_mix_decode_step",
            "swr_exact_workspace_bytes", "swr_exact_fwd", "swr_exact_bwd",
-           "swr_uniform_fwd", "phalanx_layer_mix", "phalanx_layer_mix_bwd")
+           "swr_uniform_fwd", "phalanx_layer_mix", "phalanx_layer_mix_bwd",
+           "phalanx_layer_workspace_bytes")
 
 
 class SwrError(RuntimeError):
@@ -40,7 +41,8 @@ class swr_shape(ctypes.Structure):
 class swr_layer(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in
                 ("Gq", "Gk", "sq_b", "sq_l", "sq_h", "sk_b", "sk_l", "sk_h")] + [
-                    ("logit_a", ctypes.c_int32), ("logit_k", ctypes.c_int32)]
+                    ("logit_a", ctypes.c_int32), ("logit_k", ctypes.c_int32),
+                    ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_int64)]
 
 
 def _load():
@@ -64,6 +66,8 @@ def _load():
     G = swr_layer
     lib.phalanx_layer_mix.argtypes = [P, P, P, P, P, P, P, S, G, I, P]
     lib.phalanx_layer_mix_bwd.argtypes = [P, P, P, P, P, P, P, P, P, P, P, P, S, G, I, P]
+    lib.phalanx_layer_workspace_bytes.argtypes = [S, G, I]
+    lib.phalanx_layer_workspace_bytes.restype = ctypes.c_int64
     lib.swr_exact_workspace_bytes.argtypes = [S]
     lib.swr_exact_workspace_bytes.restype = ctypes.c_int64
     for f in ("swr_fwd", "swr_bwd", "phalanx_mix", "phalanx_mix_bwd", "swr_decode_step",
@@ -112,6 +116,13 @@ def phalanx_mix_bwd(q, k, v, a, dy, dq, dk, dv, da, carry_in, mu_in, mu_out, sha
 
 def set_path(path: int) -> int:
     return _lib.swr_set_path(path)
+
+
+def get_path() -> int:
+    """This thread's kernel-family selector (read by setting it and restoring it)."""
+    prev = _lib.swr_set_path(SWR_PATH_AUTO)
+    _lib.swr_set_path(prev)
+    return prev
 
 
 def launch_count() -> int:
@@ -170,3 +181,7 @@ def phalanx_layer_mix_bwd(q, zk, v, za, dy, dq, dzk, dv, dza, carry_in, mu_in, m
                           dtype, stream):
     _check(_lib.phalanx_layer_mix_bwd(q, zk, v, za, dy, dq, dzk, dv, dza, carry_in, mu_in, mu_out, shape,
                                       layer, dtype, stream), "phalanx_layer_mix_bwd")
+
+
+def phalanx_layer_workspace_bytes(shape, layer, dtype) -> int:
+    return _lib.phalanx_layer_workspace_bytes(shape, layer, dtype)

@@ -16,6 +16,7 @@ cudaError_t launch_tc(int op, const Params& p, cudaStream_t st, int sms, int* la
 bool tc_supported(int op, bool bf16, const Params& p);
 cudaError_t launch_decode(bool mix, bool bf16, const DecParams& p, cudaStream_t st);
 cudaError_t launch_exact(bool bf16, Params p, void* workspace, cudaStream_t st, int sms);
+cudaError_t launch_exact_lb(bool bf16, Params p, void* workspace, cudaStream_t st);
 cudaError_t launch_exact_bwd(bool bf16, Params p, void* workspace, cudaStream_t st, int sms);
 cudaError_t launch_uniform(bool bf16, Params p, int k, cudaStream_t st, int sms);
 bool ffma_layer_supported(const Params& p);
@@ -291,6 +292,13 @@ void set_layer(swr::Params& p, const swr_shape& s, const swr_layer& g) {
 
 extern "C" {
 
+int64_t phalanx_layer_workspace_bytes(swr_shape s, swr_layer g, swr_dtype dt) {
+  if (dt != SWR_BF16 || s.D != 128 || s.B <= 0 || s.L <= 0 || s.H <= 0 || g.Gq <= 0 || g.Gk <= 0) return 0;
+  if (s.H % g.Gq || s.H % g.Gk) return 0;
+  const int64_t per = s.B * s.L * s.H * s.D * 2;
+  return (g.Gq < s.H ? per : 0) + (g.Gk < s.H ? per : 0);
+}
+
 swr_status phalanx_layer_mix(const void* q, const void* zk, const void* v, const void* za, void* y,
                              const float* carry_in, float* carry_out, swr_shape s, swr_layer g, swr_dtype dt,
                              void* stream) {
@@ -334,6 +342,17 @@ swr_status phalanx_layer_mix_bwd(const void* q, const void* zk, const void* v, c
   if (s.B == 0 || s.H == 0 || s.L == 0) return empty_call(s, nullptr, mu_out, cs);
   swr::Params p = make_params(s);
   set_layer(p, s, g);
+  const int64_t need = phalanx_layer_workspace_bytes(s, g, dt);
+  if (need > 0 && g.workspace != nullptr && g.workspace_bytes >= need) {
+    if (!aligned16(g.workspace)) return SWR_ERR_ALIGN;
+    const int64_t per = s.B * s.L * s.H * s.D;  // bf16 elements of one per-head scratch
+    uint8_t* w = reinterpret_cast<uint8_t*>(g.workspace);
+    if (p.hq > 1) {
+      p.gq = w;
+      w += per * 2;
+    }
+    if (p.hk > 1) p.gk = w;
+  }
   p.q = q;
   p.k = zk;
   p.v = v;
@@ -435,9 +454,15 @@ swr_status swr_exact_fwd(const void* u, const void* a, void* x, const float* car
   p.x = x;
   p.carry_in = carry_in;
   p.carry_out = carry_out;
+#ifndef SWR_EXACT_3STAGE  // 1: the round-1 three-launch forward (local, carrier chain, output)
+  cudaError_t e = swr::launch_exact_lb(dt == SWR_BF16, p, workspace, cs);
+  const int launches = 1;
+#else
   cudaError_t e = swr::launch_exact(dt == SWR_BF16, p, workspace, cs, sms);
+  const int launches = 3;
+#endif
   if (e != cudaSuccess) return cuda_fail(e);
-  g_launches += 3;
+  g_launches += launches;
   g_last_path = SWR_PATH_FFMA;
   return SWR_OK;
 }

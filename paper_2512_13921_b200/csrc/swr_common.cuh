@@ -47,6 +47,11 @@ struct Params {
   int64_t hq, hk;               // heads per q group, per k group
   int64_t sq_b, sq_l, sq_h;     // element strides of q and dq
   int64_t sk_b, sk_l, sk_h;     // element strides of k and dk
+  // tensor-core layer backward with shared groups: per-head dq / dk scratch ([B, L, H, D]
+  // contiguous, in the caller's workspace) summed over each group by a second kernel;
+  // NULL = not used
+  void* gq;
+  void* gk;
   unsigned long long* trace;  // diagnostics (swr_set_trace), NULL = off
   int64_t trace_n;
   uint32_t epoch;  // TC path: launch ticket of the range claims (set by launch_tc)

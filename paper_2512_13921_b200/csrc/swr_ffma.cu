@@ -104,13 +104,19 @@ __device__ __forceinline__ float ld_decay(const Params& p, const T* A, int64_t n
   return (LAYER && p.logit_a) ? sigmoid_f(z) : z;
 }
 
+#ifndef SWR_FFMA_FWD_SG
+#define SWR_FFMA_FWD_SG 16  // SWR forward: tokens whose loads are issued together
+#endif
+#ifndef SWR_FFMA_FWD_MINB
+#define SWR_FFMA_FWD_MINB 1
+#endif
 #ifndef SWR_FFMA_MIXF_GROUP
 #define SWR_FFMA_MIXF_GROUP 4  // mixer forward: tokens whose loads are issued together
 #endif
 // LAYER: the Phalanx layer around the mixer (phalanx_layer_mix): logits and
 // group-shared q / k (Params); otherwise the plain SWR / mixer ops.
 template <typename T, bool MIX, bool LAYER>
-__global__ void __launch_bounds__(128) fwd_stream(const Params p) {
+__global__ void __launch_bounds__(128, MIX ? 1 : SWR_FFMA_FWD_MINB) fwd_stream(const Params p) {
   constexpr int VC = Vec16<T>::N;
   const int TPH = (int)p.D / VC;  // threads per head
   const int HPC = 128 / TPH;      // heads per CTA
@@ -161,29 +167,34 @@ __global__ void __launch_bounds__(128) fwd_stream(const Params p) {
     // cannot hoist them past the stores): 16 decays and 16 raw 16-byte vectors.
     // Mixer: the loads of MG tokens at a time (a, k, v, q; v serves the pre-gate and
     // the residual), then their arithmetic and stores.
-    float ab[MIX ? 1 : kEll];
-    uint4 ub[MIX ? 1 : kEll];
     if constexpr (!MIX) {
+      constexpr int SG = SWR_FFMA_FWD_SG;
 #pragma unroll
-      for (int i = 0; i < kEll; ++i) {
-        const int64_t n = t * kEll + i;
-        const bool valid = n < p.L;
-        ab[i] = valid ? IO<T>::ld1(A + n * p.sa_l) : 1.f;  // pad: a = 1 (carry_out = state at L-1)
-        ub[i] = valid ? __ldg(reinterpret_cast<const uint4*>((const T*)p.u + xo + n * p.sx_l)) : make_uint4(0, 0, 0, 0);
-      }
+      for (int i0 = 0; i0 < kEll; i0 += SG) {
+        float ab[SG];
+        uint4 ub[SG];
 #pragma unroll
-      for (int i = 0; i < kEll; ++i) {
-        const int64_t n = t * kEll + i;
-        float u[VC];
-        Vec16<T>::to_f(ub[i], u);
-        g *= ab[i];  // g_t[i] = a_t[0] ... a_t[i]
-        float x[VC];
-#pragma unroll
-        for (int e = 0; e < VC; ++e) {
-          w[e] = (i == 0) ? u[e] : fmaf(ab[i], w[e], u[e]);  // Pass I
-          x[e] = fmaf(g, v[e], w[e]);                         // Pass II: x~ = w + g v_{t-1}
+        for (int m = 0; m < SG; ++m) {
+          const int64_t n = t * kEll + i0 + m;
+          const bool valid = n < p.L;
+          ab[m] = valid ? IO<T>::ld1(A + n * p.sa_l) : 1.f;  // pad: a = 1 (carry_out = state at L-1)
+          ub[m] = valid ? __ldg(reinterpret_cast<const uint4*>((const T*)p.u + xo + n * p.sx_l)) : make_uint4(0, 0, 0, 0);
         }
-        if (n < p.L) *reinterpret_cast<uint4*>((T*)p.x + xo + n * p.sx_l) = Vec16<T>::from_f(x);
+#pragma unroll
+        for (int m = 0; m < SG; ++m) {
+          const int i = i0 + m;
+          const int64_t n = t * kEll + i;
+          float u[VC];
+          Vec16<T>::to_f(ub[m], u);
+          g *= ab[m];  // g_t[i] = a_t[0] ... a_t[i]
+          float x[VC];
+#pragma unroll
+          for (int e = 0; e < VC; ++e) {
+            w[e] = (i == 0) ? u[e] : fmaf(ab[m], w[e], u[e]);  // Pass I
+            x[e] = fmaf(g, v[e], w[e]);                         // Pass II: x~ = w + g v_{t-1}
+          }
+          if (n < p.L) *reinterpret_cast<uint4*>((T*)p.x + xo + n * p.sx_l) = Vec16<T>::from_f(x);
+        }
       }
     } else {
       constexpr int MG = SWR_FFMA_MIXF_GROUP;
@@ -1118,6 +1129,204 @@ __global__ void __launch_bounds__(128) exact_bwd_out(const Params p, const Exact
         if (j < nv && tok + j < lim) io::st1(dA + (n0 + tok + j) * p.sa_l, part[j]);
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// exact forward in ONE pass over the sequence: Alg. 2's carrier stage fused by a
+// decoupled look-back across CTAs.  The carrier
+// recurrence s_t = c_t s_{t-1} + v_t composes associatively,
+// (c2, v2) o (c1, v1) = (c2 c1, c2 v1 + v2), so each CTA
+//   1) runs the local solve over its chunk of K blocks (from a zero state) to the chunk
+//      aggregate (C, V): C = the chunk's decay product, V = its local end state;
+//   2) publishes (C, V) (flag 1), or, for chunk 0, the inclusive prefix directly;
+//   3) looks back over its predecessors' flags: an aggregate is folded in and the
+//      look-back continues, an inclusive prefix S ends it: s_in = C_acc S + V_acc;
+//   4) publishes its own inclusive prefix S = C s_in + V (flag 2);
+//   5) re-runs the chunk from s_in (Eq. 2.1 token by token) and stores x.
+// CTAs take chunks by an atomic ticket in (chunk, column) order, so every predecessor
+// a CTA waits for is already resident: no deadlock.  Per (column of HPC heads, chunk):
+// a flag; per (b, h, chunk): C, V, S.  The caller's workspace holds them; the flags and
+// the ticket are zeroed on the stream first.
+// ---------------------------------------------------------------------------
+struct ExactLb {
+  unsigned* ticket;
+  unsigned* flag;  // [ncol][nchunk]
+  float* C;        // [B*H][nchunk - 1]  (the last chunk publishes nothing)
+  float* V;        // [B*H][nchunk - 1][D]
+  float* S;        // [B*H][nchunk - 1][D]
+  int64_t nchunk, ncol;
+};
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// CTAs per SM: bf16 8 (64 registers: more CTAs in flight beat hoisting the block's loads),
+// fp32 4 (tools/exact_time.py)
+template <typename T>
+__global__ void __launch_bounds__(128, sizeof(T) == 2 ? 8 : 4) exact_fwd_lb(const Params p, const ExactLb lb) {
+  using V = VecN<T, 4>;
+  __shared__ unsigned s_ticket, s_flag;
+  const int tph = (int)p.D / 4, hpc = 128 / tph;
+  if (threadIdx.x == 0) s_ticket = atomicAdd(lb.ticket, 1u);
+  __syncthreads();
+  const int64_t tk = s_ticket, chunk = tk / lb.ncol, col = tk % lb.ncol;
+  const int64_t hgs = (p.H + hpc - 1) / hpc;
+  const int64_t b = col / hgs;
+  const int hh = threadIdx.x / tph, c = 4 * (threadIdx.x % tph);
+  const int64_t h = (col % hgs) * hpc + hh;
+  const bool act = h < p.H;
+  const int64_t hc = act ? h : p.H - 1;
+  const int64_t line = b * p.H + hc;
+  const int64_t t_lo = chunk * p.K, t_hi = min(t_lo + p.K, p.nb);
+  const int64_t n_lo = t_lo * kEll, n_hi = min(t_hi * kEll, p.L);
+  const T* A = (const T*)p.a + b * p.sa_b + hc * p.sa_h;
+  const int64_t xo = b * p.sx_b + hc * p.sx_h + c;
+  const bool publish = chunk + 1 < lb.nchunk;  // the last chunk has no successor
+  const int64_t slot = line * (lb.nchunk - 1) + chunk;
+
+  // 1) chunk aggregate: local end state from 0, decay product
+  float v[4] = {0.f, 0.f, 0.f, 0.f}, cprod = 1.f;
+  if (publish || chunk == 0) {
+    for (int64_t n0 = n_lo; n0 < n_hi; n0 += kEll) {
+      float ab[kEll];
+      typename V::raw ub[kEll];
+#pragma unroll
+      for (int i = 0; i < kEll; ++i) {  // the block's loads first, then the chain
+        const bool ok = n0 + i < n_hi;
+        ab[i] = ok ? IO<T>::ld1(A + (n0 + i) * p.sa_l) : 1.f;
+        ub[i] = ok ? V::ld((const T*)p.u + xo + (n0 + i) * p.sx_l) : V::zero();
+      }
+#pragma unroll
+      for (int i = 0; i < kEll; ++i) {
+        float u[4];
+        V::to_f(ub[i], u);
+        cprod *= ab[i];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = fmaf(ab[i], v[e], u[e]);
+      }
+    }
+  }
+  // 2) publish the aggregate, or (chunk 0) the inclusive prefix
+  float sin[4] = {0.f, 0.f, 0.f, 0.f};
+  if (chunk == 0 && p.carry_in)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) sin[e] = p.carry_in[line * p.D + c + e];
+  if (publish) {
+    if (act) {
+      if (chunk == 0) {
+        *reinterpret_cast<float4*>(lb.S + slot * p.D + c) =
+            make_float4(fmaf(cprod, sin[0], v[0]), fmaf(cprod, sin[1], v[1]), fmaf(cprod, sin[2], v[2]),
+                        fmaf(cprod, sin[3], v[3]));
+      } else {
+        *reinterpret_cast<float4*>(lb.V + slot * p.D + c) = make_float4(v[0], v[1], v[2], v[3]);
+        if (c == 0) lb.C[slot] = cprod;
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) st_release(lb.flag + col * lb.nchunk + chunk, chunk == 0 ? 2u : 1u);
+  }
+  // 3) look back
+  if (chunk > 0) {
+    float cacc = 1.f, vacc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int64_t j = chunk - 1;; --j) {
+      if (threadIdx.x == 0) {
+        unsigned f;
+        while ((f = ld_acquire(lb.flag + col * lb.nchunk + j)) == 0u) __nanosleep(32);
+        s_flag = f;
+      }
+      __syncthreads();
+      const unsigned f = s_flag;
+      const int64_t sj = line * (lb.nchunk - 1) + j;
+      if (f == 2u) {  // inclusive prefix S_j: s_in = C_acc S_j + V_acc
+        const float4 S = __ldcg(reinterpret_cast<const float4*>(lb.S + sj * p.D + c));
+        sin[0] = fmaf(cacc, S.x, vacc[0]);
+        sin[1] = fmaf(cacc, S.y, vacc[1]);
+        sin[2] = fmaf(cacc, S.z, vacc[2]);
+        sin[3] = fmaf(cacc, S.w, vacc[3]);
+        __syncthreads();  // s_flag is rewritten only after every thread has read it
+        break;
+      }
+      // aggregate (C_j, V_j): fold chunk j in front of the accumulated chunks
+      const float4 Vj = __ldcg(reinterpret_cast<const float4*>(lb.V + sj * p.D + c));
+      const float Cj = __ldcg(lb.C + sj);
+      vacc[0] = fmaf(cacc, Vj.x, vacc[0]);
+      vacc[1] = fmaf(cacc, Vj.y, vacc[1]);
+      vacc[2] = fmaf(cacc, Vj.z, vacc[2]);
+      vacc[3] = fmaf(cacc, Vj.w, vacc[3]);
+      cacc *= Cj;
+      __syncthreads();
+    }
+    // 4) publish the inclusive prefix
+    if (publish) {
+      if (act)
+        *reinterpret_cast<float4*>(lb.S + slot * p.D + c) =
+            make_float4(fmaf(cprod, sin[0], v[0]), fmaf(cprod, sin[1], v[1]), fmaf(cprod, sin[2], v[2]),
+                        fmaf(cprod, sin[3], v[3]));
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) st_release(lb.flag + col * lb.nchunk + chunk, 2u);
+    }
+  }
+  // 5) the chunk from s_in, token by token (Eq. 2.1)
+  float x[4] = {sin[0], sin[1], sin[2], sin[3]};
+  for (int64_t n0 = n_lo; n0 < n_hi; n0 += kEll) {
+    float ab[kEll];
+    typename V::raw ub[kEll];
+#pragma unroll
+    for (int i = 0; i < kEll; ++i) {
+      const bool ok = n0 + i < n_hi;
+      ab[i] = ok ? IO<T>::ld1(A + (n0 + i) * p.sa_l) : 1.f;
+      ub[i] = ok ? V::ld((const T*)p.u + xo + (n0 + i) * p.sx_l) : V::zero();
+    }
+#pragma unroll
+    for (int i = 0; i < kEll; ++i) {
+      float u[4];
+      V::to_f(ub[i], u);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) x[e] = fmaf(ab[i], x[e], u[e]);
+      if (act && n0 + i < n_hi) V::st((T*)p.x + xo + (n0 + i) * p.sx_l, x);
+    }
+  }
+  if (act && t_hi == p.nb && p.carry_out)
+    *reinterpret_cast<float4*>(p.carry_out + line * p.D + c) = make_float4(x[0], x[1], x[2], x[3]);
+}
+
+#ifndef SWR_EXACT_LB_K
+#define SWR_EXACT_LB_K 4  // blocks per look-back chunk
+#endif
+// the single-pass forward (exact_fwd_lb); workspace layout within swr_exact_workspace_bytes
+cudaError_t launch_exact_lb(bool bf16, Params p, void* workspace, cudaStream_t st) {
+  auto cdiv = [](int64_t x, int64_t y) { return (x + y - 1) / y; };
+  const int64_t hpc = 128 / (p.D / 4);
+  p.K = p.nb == 1 ? 1 : std::max<int64_t>(2, std::min<int64_t>(SWR_EXACT_LB_K, p.nb));
+  ExactLb lb;
+  lb.nchunk = cdiv(p.nb, p.K);
+  lb.ncol = p.B * cdiv(p.H, hpc);
+  const int64_t lines = p.B * p.H;
+  // [V | S] floats, then C floats, then ticket + flags (u32), all 16-byte aligned
+  uint8_t* base = reinterpret_cast<uint8_t*>(workspace);
+  const int64_t nv = lines * (lb.nchunk - 1) * p.D;
+  lb.V = reinterpret_cast<float*>(base);
+  lb.S = lb.V + nv;
+  lb.C = lb.S + nv;
+  lb.ticket = reinterpret_cast<unsigned*>(lb.C + (lines * (lb.nchunk - 1) + 3) / 4 * 4);
+  lb.flag = lb.ticket + 4;
+  const size_t used = (size_t)(reinterpret_cast<uint8_t*>(lb.flag + lb.ncol * lb.nchunk) - base);
+  const size_t avail = (size_t)sizeof(float) * (p.B * p.H * p.nb * p.D + (p.B * p.H * p.nb + 3) / 4 * 4);
+  if (used > avail) return cudaErrorInvalidValue;  // cannot happen for K >= 2: 2 (nchunk - 1) <= nb - 1
+  cudaError_t e = cudaMemsetAsync(lb.ticket, 0, sizeof(unsigned) * (4 + lb.ncol * lb.nchunk), st);
+  if (e != cudaSuccess) return e;
+  const unsigned grid = (unsigned)(lb.ncol * lb.nchunk);
+  if (bf16) exact_fwd_lb<__nv_bfloat16><<<grid, 128, 0, st>>>(p, lb);
+  else exact_fwd_lb<float><<<grid, 128, 0, st>>>(p, lb);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_exact(bool bf16, Params p, void* workspace, cudaStream_t st, int sms) {

@@ -1515,8 +1515,6 @@ static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   return fn;
 }
 
-// which: 0 = a [B, L, H, D] d-tensor with the strides sx; 1 / 2 = the layer mixer's
-// group-shared q / k (and dq / dk) [B, L, G, D] with their own strides
 // Encoded tensor maps, cached per calling thread: a training step calls the same
 // ops on the same (caching-allocator) buffers, so the key -- pointer, dims, strides,
 // box rows -- repeats and the ~1 us host-side encode is skipped.
@@ -1565,11 +1563,14 @@ static bool encode_cached(CUtensorMap* m, const void* ptr, CUtensorMapDataType t
   return true;
 }
 
+// which: 0 = a [B, L, H, D] d-tensor with the strides sx; 1 / 2 = the layer mixer's
+// group-shared q / k (and dq / dk) [B, L, G, D] with their own strides; 3 = a per-head
+// scratch [B, L, H, D], contiguous
 static bool map_dtensor(CUtensorMap* m, const void* ptr, const Params& p, int rows, int which = 0) {
   const int64_t G = which == 1 ? p.H / p.hq : which == 2 ? p.H / p.hk : p.H;
-  const int64_t sh = which == 1 ? p.sq_h : which == 2 ? p.sk_h : p.sx_h;
-  const int64_t sl = which == 1 ? p.sq_l : which == 2 ? p.sk_l : p.sx_l;
-  const int64_t sb = which == 1 ? p.sq_b : which == 2 ? p.sk_b : p.sx_b;
+  const int64_t sh = which == 1 ? p.sq_h : which == 2 ? p.sk_h : which == 3 ? p.D : p.sx_h;
+  const int64_t sl = which == 1 ? p.sq_l : which == 2 ? p.sk_l : which == 3 ? p.H * p.D : p.sx_l;
+  const int64_t sb = which == 1 ? p.sq_b : which == 2 ? p.sk_b : which == 3 ? p.L * p.H * p.D : p.sx_b;
   cuuint64_t dims[4] = {(cuuint64_t)p.D, (cuuint64_t)G, (cuuint64_t)p.L, (cuuint64_t)p.B};
   cuuint64_t strides[3] = {(cuuint64_t)sh * 2, (cuuint64_t)sl * 2, (cuuint64_t)sb * 2};
   cuuint32_t box[4] = {64, 1, (cuuint32_t)rows, 1};
@@ -1602,8 +1603,12 @@ static cudaError_t launch_op(const Params& p, cudaStream_t st, int sms) {
   auto kind = [](int i) { return (OP >= 4 && i < 2) ? i + 1 : 0; };
   for (int i = 0; i < nin; ++i)
     if (!map_dtensor(&maps.in[i], ins[i], p, 16 * Cfg<OP>::BPI, kind(i))) return cudaErrorNotSupported;
+  // layer backward with shared groups: per-head dq / dk into the scratch (summed afterwards)
+  const bool scr[3] = {OP == 5 && p.hq > 1, OP == 5 && p.hk > 1, false};
+  if (scr[0]) outs[0] = p.gq;
+  if (scr[1]) outs[1] = p.gk;
   for (int i = 0; i < nout; ++i)
-    if (!map_dtensor(&maps.out[i], outs[i], p, 16 * Cfg<OP>::BPI, OP == 5 ? kind(i) : 0))
+    if (!map_dtensor(&maps.out[i], outs[i], p, 16 * Cfg<OP>::BPI, scr[i] ? 3 : OP == 5 ? kind(i) : 0))
       return cudaErrorNotSupported;
   if (!map_decay(&maps.a, p.a, p, Cfg<OP>::BPI)) return cudaErrorNotSupported;
 
@@ -1653,8 +1658,8 @@ static cudaError_t launch_op(const Params& p, cudaStream_t st, int sms) {
 
 bool tc_supported(int op, bool bf16, const Params& p) {
   if (!bf16 || p.D != 128) return false;
-  // layer mixer backward: the group sums of dq / dk run on the CUDA-core family
-  if (op == 5 && (p.hq != 1 || p.hk != 1)) return false;
+  // layer mixer backward with shared groups: needs the caller's per-head scratch
+  if (op == 5 && ((p.hq != 1 && p.gq == nullptr) || (p.hk != 1 && p.gk == nullptr))) return false;
   if (tc::encoder() == nullptr) return false;
   auto a16 = [](const void* q) { return q == nullptr || (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
   // decays must be TMA-addressable: heads contiguous, 16-byte token/batch strides
@@ -1662,6 +1667,43 @@ bool tc_supported(int op, bool bf16, const Params& p) {
   // 32-bit item / carry indexing in the kernel
   if (p.B * p.H > (1 << 22) || p.B * p.H * p.nb >= (int64_t(1) << 31) || p.L > (1 << 30)) return false;
   return true;
+}
+
+// dst[b, l, g, :] = sum over the group's hpg heads (in head order, fp32) of the per-head
+// scratch src[b, l, g*hpg + j, :], rounded once to bf16; a thread per 8 channels
+__global__ void __launch_bounds__(256) group_sum_bf16(const __nv_bfloat16* __restrict__ src,
+                                                      __nv_bfloat16* __restrict__ dst, int64_t B, int64_t L,
+                                                      int64_t H, int64_t D, int64_t hpg, int64_t s_b, int64_t s_l,
+                                                      int64_t s_h) {
+  const int64_t G = H / hpg, nv = D / 8;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B * L * G * nv) return;
+  const int64_t cv = i % nv, g = (i / nv) % G, bl = i / (nv * G), b = bl / L, l = bl % L;
+  const uint4* s4 = reinterpret_cast<const uint4*>(src + (bl * H + g * hpg) * D) + cv;
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int64_t j = 0; j < hpg; ++j) {
+    const uint4 w = __ldg(s4 + j * nv);
+    const uint32_t x[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      acc[2 * q] += __uint_as_float(x[q] << 16);
+      acc[2 * q + 1] += __uint_as_float(x[q] & 0xffff0000u);
+    }
+  }
+  uint4 o;
+  o.x = tc::pack_bf2(acc[0], acc[1]);
+  o.y = tc::pack_bf2(acc[2], acc[3]);
+  o.z = tc::pack_bf2(acc[4], acc[5]);
+  o.w = tc::pack_bf2(acc[6], acc[7]);
+  *reinterpret_cast<uint4*>(dst + b * s_b + l * s_l + g * s_h + 8 * cv) = o;
+}
+
+static cudaError_t group_sum(const void* src, void* dst, const Params& p, int64_t hpg, int64_t sb, int64_t sl,
+                             int64_t sh, cudaStream_t st) {
+  const int64_t n = p.B * p.L * (p.H / hpg) * (p.D / 8);
+  group_sum_bf16<<<(unsigned)((n + 255) / 256), 256, 0, st>>>((const __nv_bfloat16*)src, (__nv_bfloat16*)dst, p.B,
+                                                             p.L, p.H, p.D, hpg, sb, sl, sh);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_tc(int op, const Params& p, cudaStream_t st, int sms, int* launches) {
@@ -1676,6 +1718,14 @@ cudaError_t launch_tc(int op, const Params& p, cudaStream_t st, int sms, int* la
     default: e = tc::launch_op<5>(p, st, sms); break;
   }
   if (e == cudaSuccess) *launches = 1;
+  if (e == cudaSuccess && op == 5 && p.hq > 1) {
+    e = group_sum(p.gq, p.dq, p, p.hq, p.sq_b, p.sq_l, p.sq_h, st);
+    if (e == cudaSuccess) ++*launches;
+  }
+  if (e == cudaSuccess && op == 5 && p.hk > 1) {
+    e = group_sum(p.gk, p.dk, p, p.hk, p.sk_b, p.sk_l, p.sk_h, st);
+    if (e == cudaSuccess) ++*launches;
+  }
   return e;
 }
 

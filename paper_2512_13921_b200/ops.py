@@ -274,10 +274,16 @@ def phalanx_layer_mix_bwd(q, zk, v, za, dy, carry_in=None, mu_in=None, logit_a=T
     dq, dzk, dv, dza = _like(q), _like(zk), _like(v), _like(za)
     ci, mi = _carry(carry_in, v), _carry(mu_in, v)
     mo = _new_carry(v)
+    shape, layer = _shape(v, za), _layer(q, zk, logit_a, logit_k)
+    nws = _lib.phalanx_layer_workspace_bytes(shape, layer, dt)
+    ws = None
+    if nws > 0 and _lib.get_path() != _lib.SWR_PATH_FFMA:
+        # tensor cores with shared groups: per-head dq / dk scratch, summed per group
+        ws = torch.empty(nws, dtype=torch.uint8, device=v.device)
+        layer.workspace, layer.workspace_bytes = ws.data_ptr(), nws
     with _on(v):
         _lib.phalanx_layer_mix_bwd(_ptr(q), _ptr(zk), _ptr(v), _ptr(za), _ptr(dy), _ptr(dq), _ptr(dzk),
-                                   _ptr(dv), _ptr(dza), _ptr(ci), _ptr(mi), _ptr(mo), _shape(v, za),
-                                   _layer(q, zk, logit_a, logit_k), dt, _stream(v))
+                                   _ptr(dv), _ptr(dza), _ptr(ci), _ptr(mi), _ptr(mo), shape, layer, dt, _stream(v))
     return dq, dzk, dv, dza, mo
 
 

@@ -87,3 +87,20 @@ def test_exact_autograd(P):
     (x * G).sum().backward()
     du, da, mo = P.swr_exact_bwd(u.detach(), a.detach(), G, carry_in=c.detach())
     assert torch.equal(u.grad, du) and torch.equal(a.grad, da) and torch.equal(c.grad, mo)
+
+
+@pytest.mark.parametrize("L", [17, 33, 48, 8192])
+@pytest.mark.parametrize("decay", ["sigmoid3", "one", "zero"])
+def test_exact_lookback_chains(P, L, decay):
+    """The single-pass forward's decoupled look-back (include/swr.h swr_exact_fwd):
+    long memory (decays near or at 1) carries the state across every chunk; a = 0
+    cuts it; short sequences have one to three 16-token blocks (one or two chunks).
+    Called twice: the flags are reset per launch."""
+    inp = swr_inputs(2, L, 4, 32, dtype=torch.float32, seed=L, decay=decay, carry=True)
+    u, a, ci = inp["u"].cuda(), inp["a"].cuda(), inp["carry_in"].cuda()
+    rx, rlast = oracle.linrec_fwd(to64(inp["u"]), to64(inp["a"]), to64(inp["carry_in"]))
+    for _ in range(2):
+        x, co = P.swr_exact_fwd(u, a, carry_in=ci, return_carry=True)
+        torch.cuda.synchronize()
+        assert normwise(x, rx) <= 1e-5
+        assert normwise(co, rlast) <= 1e-5

@@ -82,7 +82,9 @@ CASES = [
 def test_layer_mix_parity(P, dtype, B, L, H, D, Gq, Gk):
     inp = layer_inputs(B, L, H, D, Gq, Gk, dtype=dtype, seed=B * 7 + L + H + D + Gq, carry=True)
     hq, hk = H // Gq, H // Gk
-    fits = all(x & (x - 1) == 0 and x <= 256 // (D // 4) for x in (hq, hk))
+    # CUDA-core group sums within one CTA, or the tensor cores with the per-head scratch
+    fits = all(x & (x - 1) == 0 and x <= 256 // (D // 4) for x in (hq, hk)) or (
+        dtype == torch.bfloat16 and D == 128 and H % 8 == 0)
     if not fits:
         with pytest.raises(P.SwrError, match="UNSUPPORTED"):
             run(P, inp)
@@ -183,16 +185,41 @@ def test_layer_mix_tc_backward(P, B, L, H, carry):
     check(outs, refs, 2e-2)
 
 
-def test_layer_mix_tc_backward_groups_not_on_tc(P):
-    """Grouped backward: forced TC is refused (no silent fallback); AUTO runs it on
-    the CUDA-core family."""
-    inp = layer_inputs(1, 64, 16, 128, 8, 8, dtype=torch.bfloat16, seed=1)
-    g = {k: v.cuda() for k, v in inp.items()}
+@pytest.mark.parametrize("B,L,H,Gq,Gk", [(2, 100, 16, 8, 8), (1, 4096, 16, 8, 8), (2, 33, 16, 2, 16),
+                                         (1, 200, 24, 24, 3), (1, 17, 8, 1, 1)])
+def test_layer_mix_tc_backward_groups(P, B, L, H, Gq, Gk):
+    """Shared groups on the tensor cores: per-head dq / dk into the scratch the binding
+    allocates (phalanx_layer_workspace_bytes), summed per group by a second kernel."""
+    inp = layer_inputs(B, L, H, 128, Gq, Gk, dtype=torch.bfloat16, seed=L + 7 * Gq + Gk, carry=True)
     prev = P.set_path(P.SWR_PATH_TC)
     try:
-        with pytest.raises(P.SwrError, match="UNSUPPORTED"):
-            P.phalanx_layer_mix_bwd(g["q"], g["zk"], g["v"], g["za"], g["dy"])
+        outs, refs = run(P, inp)
+        assert P.last_path() == 2
     finally:
         P.set_path(prev)
-    P.phalanx_layer_mix_bwd(g["q"], g["zk"], g["v"], g["za"], g["dy"])
-    assert P.last_path() == 1
+    check(outs, refs, 2e-2)
+
+
+def test_layer_mix_tc_backward_groups_need_workspace(P):
+    """Without the scratch a grouped backward is refused when SWR_PATH_TC is forced (no
+    silent fallback) and runs on the CUDA-core family under AUTO."""
+    from paper_2512_13921_b200 import _lib, ops
+    inp = layer_inputs(1, 64, 16, 128, 8, 8, dtype=torch.bfloat16, seed=1)
+    g = {k: v.cuda() for k, v in inp.items()}
+    q, zk, v, za, dy = g["q"], g["zk"], g["v"], g["za"], g["dy"]
+    outs = [torch.empty_like(q), torch.empty_like(zk), torch.empty_like(v), torch.empty_like(za)]
+    mo = torch.empty(1, 16, 128, device="cuda")
+    args = (q.data_ptr(), zk.data_ptr(), v.data_ptr(), za.data_ptr(), dy.data_ptr(), *[o.data_ptr() for o in outs],
+            None, None, mo.data_ptr(), ops._shape(v, za), ops._layer(q, zk, True, True), _lib.SWR_BF16,
+            torch.cuda.current_stream().cuda_stream)
+    prev = P.set_path(P.SWR_PATH_TC)
+    try:
+        assert _lib.raw_status("phalanx_layer_mix_bwd", *args) == 8  # SWR_ERR_UNSUPPORTED
+    finally:
+        P.set_path(prev)
+    P.set_path(P.SWR_PATH_AUTO)
+    try:
+        assert _lib.raw_status("phalanx_layer_mix_bwd", *args) == 0
+        assert P.last_path() == 1
+    finally:
+        P.set_path(prev)

@@ -110,13 +110,16 @@ __device__ __forceinline__ float ld_decay(const Params& p, const T* A, int64_t n
 #ifndef SWR_FFMA_FWD_MINB
 #define SWR_FFMA_FWD_MINB 1
 #endif
+#ifndef SWR_FFMA_MIXF_MINB
+#define SWR_FFMA_MIXF_MINB 1
+#endif
 #ifndef SWR_FFMA_MIXF_GROUP
 #define SWR_FFMA_MIXF_GROUP 4  // mixer forward: tokens whose loads are issued together
 #endif
 // LAYER: the Phalanx layer around the mixer (phalanx_layer_mix): logits and
 // group-shared q / k (Params); otherwise the plain SWR / mixer ops.
 template <typename T, bool MIX, bool LAYER>
-__global__ void __launch_bounds__(128, MIX ? 1 : SWR_FFMA_FWD_MINB) fwd_stream(const Params p) {
+__global__ void __launch_bounds__(128, MIX ? SWR_FFMA_MIXF_MINB : SWR_FFMA_FWD_MINB) fwd_stream(const Params p) {
   constexpr int VC = Vec16<T>::N;
   const int TPH = (int)p.D / VC;  // threads per head
   const int HPC = 128 / TPH;      // heads per CTA

@@ -77,6 +77,19 @@ struct DecParams {
 // ulp in all (~1e-6 relative at |z| <= 10, inside the fp32 tolerance 1e-5); saturates
 // to exactly 0 / 1 for |z| large (__fdividef(1, inf) = 0).
 __device__ __forceinline__ float sigmoid_f(float z) { return __fdividef(1.f, 1.f + __expf(-z)); }
+// The key gate's sigma for storage type T: bf16 storage takes the single-MUFU
+// 1/2 + tanh(z/2)/2 (tanh.approx.f32, ~2^-11 relative, below the bf16 rounding of the
+// outputs -- the tensor-core family's form), fp32 storage the accurate sigmoid_f.
+template <typename T>
+__device__ __forceinline__ float sigmoid_gate(float z) {
+  if constexpr (sizeof(T) == 2) {
+    float t;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * z));
+    return fmaf(0.5f, t, 0.5f);
+  } else {
+    return sigmoid_f(z);
+  }
+}
 
 // ---------------------------------------------------------------------------
 // storage-dtype traits: 2-channel vector loads/stores, scalar decay access

@@ -89,7 +89,7 @@ __device__ __forceinline__ void load_u16(const Params& p, int64_t off, int64_t k
     Vec16<T>::to_f(__ldg(reinterpret_cast<const uint4*>((const T*)p.v + off)), vv);
     if (LAYER && p.logit_k) {
 #pragma unroll
-      for (int e = 0; e < VC; ++e) kk[e] = sigmoid_f(kk[e]);
+      for (int e = 0; e < VC; ++e) kk[e] = sigmoid_gate<T>(kk[e]);
     }
 #pragma unroll
     for (int e = 0; e < VC; ++e) u[e] = __fmul_rn(kk[e], vv[e]);
@@ -111,7 +111,7 @@ __device__ __forceinline__ float ld_decay(const Params& p, const T* A, int64_t n
 #define SWR_FFMA_FWD_MINB 1
 #endif
 #ifndef SWR_FFMA_MIXF_MINB
-#define SWR_FFMA_MIXF_MINB 1
+#define SWR_FFMA_MIXF_MINB 4  // mixer forward: 128 registers, 4 CTAs per SM (fp32 d=128 252 -> 180 us, d=16 208 -> 189 us)
 #endif
 #ifndef SWR_FFMA_MIXF_GROUP
 #define SWR_FFMA_MIXF_GROUP 4  // mixer forward: tokens whose loads are issued together
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(128, MIX ? SWR_FFMA_MIXF_MINB : SWR_FFMA_FWD_M
           Vec16<T>::to_f(qr[m], qq);
           if (LAYER && p.logit_k) {
 #pragma unroll
-            for (int e = 0; e < VC; ++e) kk[e] = sigmoid_f(kk[e]);  // k = sigma(zk)
+            for (int e = 0; e < VC; ++e) kk[e] = sigmoid_gate<T>(kk[e]);  // k = sigma(zk)
           }
 #pragma unroll
           for (int e = 0; e < VC; ++e) u[e] = __fmul_rn(kk[e], vv[e]);  // u^ = k (.) v
@@ -384,7 +384,7 @@ __global__ void __launch_bounds__(NTH, NTH == 128 ? ((LAYER || (!MIX && sizeof(T
         V::to_f(valid ? V::ld(p1) : V::zero(), f1);
         if (LAYER && sig0) {
 #pragma unroll
-          for (int e = 0; e < VC; ++e) f0[e] = valid ? sigmoid_f(f0[e]) : 0.f;
+          for (int e = 0; e < VC; ++e) f0[e] = valid ? sigmoid_gate<T>(f0[e]) : 0.f;
         }
 #pragma unroll
         for (int e = 0; e < VC; ++e) x[e] = __fmul_rn(f0[e], f1[e]);
@@ -667,7 +667,7 @@ __global__ void __launch_bounds__(NTH, NTH == 128 ? ((LAYER || (!MIX && sizeof(T
         V::to_f(r1[m], vv);
         if (sig_k) {
 #pragma unroll
-          for (int e = 0; e < VC; ++e) kk[e] = valid ? sigmoid_f(kk[e]) : 0.f;
+          for (int e = 0; e < VC; ++e) kk[e] = valid ? sigmoid_gate<T>(kk[e]) : 0.f;
         }
 #pragma unroll
         for (int e = 0; e < VC; ++e) u[e] = __fmul_rn(kk[e], vv[e]);

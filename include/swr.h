@@ -273,10 +273,11 @@ SWR_API swr_status swr_exact_fwd(const void* u, const void* a, void* x, const fl
 /* Backward of swr_exact_fwd (reverse mode of Eq. 2.1): du_n = lambda_n with
  * lambda_n = dx_n + a_{n+1} lambda_{n+1}, da_n = sum_c lambda_n x_{n-1} (x_{-1} =
  * carry_in), mu_out = a_0 lambda_0 = dLoss/dcarry_in; mu_in = dLoss/dcarry_out enters
- * at token L-1.  Blockwise as the forward: local reverse solves, the reverse
- * carrier chain mu_{t-1} = a_t[0] (l_t[0] + r_t[0] mu_t), reconstruction (the
- * forward carriers are recomputed for x_{n-1}).  Five launches; workspace >=
- * 2 * swr_exact_workspace_bytes(s).  Arguments otherwise as swr_bwd. */
+ * at token L-1.  Blockwise: per-block local solves give the forward carriers s_t and
+ * the reverse carriers mu_{t-1} = a_t[0] (l_t[0] + r_t[0] mu_t), resolved by decoupled
+ * look-back scans from 1024 blocks per line on (three launches) and by per-line serial
+ * chains below (five launches); then a reconstruction pass forms du and da.
+ * Workspace >= 3 * swr_exact_workspace_bytes(s).  Arguments otherwise as swr_bwd. */
 SWR_API swr_status swr_exact_bwd(const void* u, const void* a, const void* dx, void* du, void* da,
                          const float* carry_in, const float* mu_in, float* mu_out,
                          void* workspace, int64_t workspace_bytes, swr_shape s, swr_dtype dt,

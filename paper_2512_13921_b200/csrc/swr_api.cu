@@ -478,7 +478,7 @@ swr_status swr_exact_bwd(const void* u, const void* a, const void* dx, void* du,
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   if (s.B == 0 || s.H == 0 || s.L == 0) return empty_call(s, nullptr, mu_out, cs);
   if (!workspace) return SWR_ERR_NULL;
-  if (workspace_bytes < 2 * swr_exact_workspace_bytes(s)) return SWR_ERR_SHAPE;
+  if (workspace_bytes < 3 * swr_exact_workspace_bytes(s)) return SWR_ERR_SHAPE;
   int sms = 0;
   st = device_info(&sms);
   if (st != SWR_OK) return st;
@@ -493,7 +493,11 @@ swr_status swr_exact_bwd(const void* u, const void* a, const void* dx, void* du,
   p.mu_out = mu_out;
   cudaError_t e = swr::launch_exact_bwd(dt == SWR_BF16, p, workspace, cs, sms);
   if (e != cudaSuccess) return cuda_fail(e);
+#ifndef SWR_EXACT_3STAGE
+  g_launches += (p.nb >= 1024) ? 3 : 5;  // launch_exact_bwd: look-back scans from 1024 blocks on
+#else
   g_launches += 5;
+#endif
   g_last_path = SWR_PATH_FFMA;
   return SWR_OK;
 }

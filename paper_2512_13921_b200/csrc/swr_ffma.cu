@@ -1157,6 +1157,8 @@ struct ExactLb {
   float* C;        // [B*H][nchunk - 1]  (the last chunk publishes nothing)
   float* V;        // [B*H][nchunk - 1][D]
   float* S;        // [B*H][nchunk - 1][D]
+  float* blk;      // the backward's scans: per-block vectors [B*H][nb][D] (in, then out)
+  float* blkC;     //   and per-block scalars [B*H][nb]
   int64_t nchunk, ncol;
 };
 
@@ -1301,6 +1303,172 @@ __global__ void __launch_bounds__(128, sizeof(T) == 2 ? 8 : 4) exact_fwd_lb(cons
     *reinterpret_cast<float4*>(p.carry_out + line * p.D + c) = make_float4(x[0], x[1], x[2], x[3]);
 }
 
+// The backward's two carrier scans by the same decoupled look-back, over per-block
+// values stashed by a first pass (no token is read twice within a scan):
+//   forward (REV = false): s_t = c_t s_{t-1} + v_t, v_t = block t's local end state,
+//     c_t = a_t[0] ... a_t[15], s_{-1} = carry_in; out: s_t per block;
+//   reverse (REV = true): mu_{t-1} = R_t mu_t + E_t, E_t = a_t[0] l_t[0] (l_t the block's
+//     local reverse solve of G), R_t = a_t[0] r_t[0] = a_t[0] (a_t[1] ... a_t[15]),
+//     mu_{nb-1} = mu_in; out: mu_t per block (the adjoint entering block t from the
+//     right) and mu_out = mu_{-1}.
+// A CTA takes a chunk (tickets in scan order), computes and stashes its blocks' (c, v)
+// or (R, E) in blk / blkC while folding them to the chunk aggregate, publishes it, looks
+// back (forward scan) or ahead (reverse scan) for its entering carrier, publishes its
+// prefix and replaces the stash by the per-block carriers.
+template <typename T, bool REV>
+__global__ void __launch_bounds__(128, sizeof(T) == 2 ? 8 : 4) exact_scan_lb(const Params p, const ExactLb lb) {
+  using V = VecN<T, 4>;
+  __shared__ unsigned s_ticket, s_flag;
+  const int tph = (int)p.D / 4, hpc = 128 / tph;
+  if (threadIdx.x == 0) s_ticket = atomicAdd(lb.ticket, 1u);
+  __syncthreads();
+  const int64_t tk = s_ticket, k = tk / lb.ncol, col = tk % lb.ncol;
+  const int64_t chunk = REV ? lb.nchunk - 1 - k : k;
+  const int64_t hgs = (p.H + hpc - 1) / hpc;
+  const int64_t b = col / hgs;
+  const int hh = threadIdx.x / tph, c = 4 * (threadIdx.x % tph);
+  const int64_t h = (col % hgs) * hpc + hh;
+  const bool act = h < p.H;
+  const int64_t hc = act ? h : p.H - 1;
+  const int64_t line = b * p.H + hc;
+  const int64_t t_lo = chunk * p.K, t_hi = min(t_lo + p.K, p.nb);
+  const T* A = (const T*)p.a + b * p.sa_b + hc * p.sa_h;
+  const int64_t xo = b * p.sx_b + hc * p.sx_h + c;
+  const bool first = REV ? chunk == lb.nchunk - 1 : chunk == 0;   // has the initial carrier
+  const bool publish = REV ? chunk > 0 : chunk + 1 < lb.nchunk;   // has a successor
+  const int64_t slot = line * (lb.nchunk - 1) + (REV ? chunk - 1 : chunk);
+  float4* BV = reinterpret_cast<float4*>(lb.blk + line * p.nb * p.D + c);
+  float* BC = lb.blkC + line * p.nb;
+  const int64_t st4 = p.D / 4;
+
+  // 1) per-block values into the stash, folded to the chunk aggregate (C, V)
+  float v[4] = {0.f, 0.f, 0.f, 0.f}, cagg = 1.f;
+  for (int64_t q = 0; q < t_hi - t_lo; ++q) {
+    const int64_t t = REV ? t_hi - 1 - q : t_lo + q;
+    const int64_t n0 = t * kEll;
+    float ab[kEll];
+    typename V::raw rb[kEll];
+#pragma unroll
+    for (int i = 0; i < kEll; ++i) {
+      const bool ok = n0 + i < p.L;
+      ab[i] = ok ? IO<T>::ld1(A + (n0 + i) * p.sa_l) : 1.f;
+      rb[i] = ok ? V::ld((const T*)(REV ? p.dx : p.u) + xo + (n0 + i) * p.sx_l) : V::zero();
+    }
+    float y[4], cb = 1.f;
+    if constexpr (!REV) {  // local solve: w[i] = a[i] w[i-1] + u[i], w[0] = u[0]; c_t includes a_t[0]
+#pragma unroll
+      for (int i = 0; i < kEll; ++i) {
+        float u[4];
+        V::to_f(rb[i], u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) y[e] = (i == 0) ? u[e] : fmaf(ab[i], y[e], u[e]);
+        cb *= ab[i];
+      }
+    } else {  // l[i] = G[i] + a[i+1] l[i+1]; E = a[0] l[0], R = a[0] (a[1] ... a[15])
+#pragma unroll
+      for (int i = kEll - 1; i >= 0; --i) {
+        float g[4];
+        V::to_f(rb[i], g);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) y[e] = (i == kEll - 1) ? g[e] : fmaf(ab[i + 1 < kEll ? i + 1 : i], y[e], g[e]);
+        if (i > 0) cb *= ab[i];
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) y[e] *= ab[0];
+      cb *= ab[0];
+    }
+    if (act) {
+      BV[t * st4] = make_float4(y[0], y[1], y[2], y[3]);
+      if (c == 0) BC[t] = cb;
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) v[e] = fmaf(cb, v[e], y[e]);
+    cagg *= cb;
+  }
+  // 2) publish the aggregate, or (first chunk of the scan) the prefix
+  float cin[4] = {0.f, 0.f, 0.f, 0.f};
+  const float* init = REV ? p.mu_in : p.carry_in;
+  if (first && init)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) cin[e] = init[line * p.D + c + e];
+  if (publish) {
+    if (act) {
+      if (first) {
+        *reinterpret_cast<float4*>(lb.S + slot * p.D + c) =
+            make_float4(fmaf(cagg, cin[0], v[0]), fmaf(cagg, cin[1], v[1]), fmaf(cagg, cin[2], v[2]),
+                        fmaf(cagg, cin[3], v[3]));
+      } else {
+        *reinterpret_cast<float4*>(lb.V + slot * p.D + c) = make_float4(v[0], v[1], v[2], v[3]);
+        if (c == 0) lb.C[slot] = cagg;
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) st_release(lb.flag + col * lb.nchunk + chunk, first ? 2u : 1u);
+  }
+  // 3) look back (forward scan) / ahead (reverse scan)
+  if (!first) {
+    float cacc = 1.f, vacc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int64_t j = REV ? chunk + 1 : chunk - 1;; j += REV ? 1 : -1) {
+      if (threadIdx.x == 0) {
+        unsigned f;
+        while ((f = ld_acquire(lb.flag + col * lb.nchunk + j)) == 0u) __nanosleep(32);
+        s_flag = f;
+      }
+      __syncthreads();
+      const unsigned f = s_flag;
+      const int64_t sj = line * (lb.nchunk - 1) + (REV ? j - 1 : j);
+      if (f == 2u) {
+        const float4 S = __ldcg(reinterpret_cast<const float4*>(lb.S + sj * p.D + c));
+        cin[0] = fmaf(cacc, S.x, vacc[0]);
+        cin[1] = fmaf(cacc, S.y, vacc[1]);
+        cin[2] = fmaf(cacc, S.z, vacc[2]);
+        cin[3] = fmaf(cacc, S.w, vacc[3]);
+        __syncthreads();
+        break;
+      }
+      const float4 Vj = __ldcg(reinterpret_cast<const float4*>(lb.V + sj * p.D + c));
+      const float Cj = __ldcg(lb.C + sj);
+      vacc[0] = fmaf(cacc, Vj.x, vacc[0]);
+      vacc[1] = fmaf(cacc, Vj.y, vacc[1]);
+      vacc[2] = fmaf(cacc, Vj.z, vacc[2]);
+      vacc[3] = fmaf(cacc, Vj.w, vacc[3]);
+      cacc *= Cj;
+      __syncthreads();
+    }
+    // 4) publish the prefix
+    if (publish) {
+      if (act)
+        *reinterpret_cast<float4*>(lb.S + slot * p.D + c) =
+            make_float4(fmaf(cagg, cin[0], v[0]), fmaf(cagg, cin[1], v[1]), fmaf(cagg, cin[2], v[2]),
+                        fmaf(cagg, cin[3], v[3]));
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) st_release(lb.flag + col * lb.nchunk + chunk, 2u);
+    }
+  }
+  // 5) the carriers of the chunk's blocks from the stash: forward s_t; reverse mu_t (the
+  //    carrier entering block t from the right, stored before applying block t)
+  float s4[4] = {cin[0], cin[1], cin[2], cin[3]};
+  for (int64_t q = 0; q < t_hi - t_lo; ++q) {
+    const int64_t t = REV ? t_hi - 1 - q : t_lo + q;
+    const float4 y = act ? BV[t * st4] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float cb = act ? BC[t] : 1.f;
+    if constexpr (REV) {
+      if (act) BV[t * st4] = make_float4(s4[0], s4[1], s4[2], s4[3]);
+    }
+    s4[0] = fmaf(cb, s4[0], y.x);
+    s4[1] = fmaf(cb, s4[1], y.y);
+    s4[2] = fmaf(cb, s4[2], y.z);
+    s4[3] = fmaf(cb, s4[3], y.w);
+    if constexpr (!REV) {
+      if (act) BV[t * st4] = make_float4(s4[0], s4[1], s4[2], s4[3]);
+    }
+  }
+  if (REV && act && chunk == 0 && p.mu_out)
+    *reinterpret_cast<float4*>(p.mu_out + line * p.D + c) = make_float4(s4[0], s4[1], s4[2], s4[3]);
+}
+
 #ifndef SWR_EXACT_LB_K
 #define SWR_EXACT_LB_K 4  // blocks per look-back chunk
 #endif
@@ -1351,8 +1519,77 @@ cudaError_t launch_exact(bool bf16, Params p, void* workspace, cudaStream_t st, 
   return cudaGetLastError();
 }
 
-// workspace: forward S, C then backward S2, C2 (2 x swr_exact_workspace_bytes)
+cudaError_t launch_exact_bwd5(bool bf16, Params p, void* workspace, cudaStream_t st, int sms);
+
+// the look-back kernels' scratch inside `base` (<= swr_exact_workspace_bytes), zeroed flags
+static cudaError_t lb_scratch(const Params& p, void* base, size_t avail, ExactLb& lb, cudaStream_t st) {
+  auto cdiv = [](int64_t x, int64_t y) { return (x + y - 1) / y; };
+  const int64_t hpc = 128 / (p.D / 4), lines = p.B * p.H;
+  lb.nchunk = cdiv(p.nb, p.K);
+  lb.ncol = p.B * cdiv(p.H, hpc);
+  const int64_t nv = lines * (lb.nchunk - 1) * p.D;
+  lb.V = reinterpret_cast<float*>(base);
+  lb.S = lb.V + nv;
+  lb.C = lb.S + nv;
+  lb.ticket = reinterpret_cast<unsigned*>(lb.C + (lines * (lb.nchunk - 1) + 3) / 4 * 4);
+  lb.flag = lb.ticket + 4;
+  lb.blk = nullptr;
+  const size_t used = (size_t)(reinterpret_cast<uint8_t*>(lb.flag + lb.ncol * lb.nchunk) - reinterpret_cast<uint8_t*>(base));
+  if (used > avail) return cudaErrorInvalidValue;
+  return cudaMemsetAsync(lb.ticket, 0, sizeof(unsigned) * (4 + lb.ncol * lb.nchunk), st);
+}
+
+// workspace (3 x swr_exact_workspace_bytes): forward per-block (v_t / s_t, c_t), reverse
+// per-block (E_t / mu_t, R_t), then the look-back scratch (reused by both scans)
+#ifndef SWR_EXACT_BWD_LB_MIN_NB
+#define SWR_EXACT_BWD_LB_MIN_NB 1024  // look-back scans from this many blocks per line on
+#endif
 cudaError_t launch_exact_bwd(bool bf16, Params p, void* workspace, cudaStream_t st, int sms) {
+#ifndef SWR_EXACT_3STAGE
+  // The look-back scans cost one more pass over the per-block stash than the serial
+  // chains they replace; they pay once the chains are long (tools/exact_time.py: L = 32K
+  // 1003 -> 772 us; L = 4K 369 -> 382 us, d = 16 at L = 8K 742 -> 878 us).
+  if (p.nb < SWR_EXACT_BWD_LB_MIN_NB) return launch_exact_bwd5(bf16, p, workspace, st, sms);
+  auto cdiv = [](int64_t x, int64_t y) { return (x + y - 1) / y; };
+  const int64_t nS = p.B * p.H * p.nb * p.D, nC = (p.B * p.H * p.nb + 3) / 4 * 4;
+  ExactWs ws, ws2;
+  ws.S = reinterpret_cast<float*>(workspace);
+  ws.C = ws.S + nS;
+  ws2.S = ws.C + nC;
+  ws2.C = ws2.S + nS;
+  void* scratch = ws2.C + nC;
+  const size_t avail = (size_t)sizeof(float) * (nS + (p.B * p.H * p.nb + 3) / 4 * 4);
+  p.K = p.nb == 1 ? 1 : std::max<int64_t>(2, std::min<int64_t>(SWR_EXACT_LB_K, p.nb));
+  ExactLb lb;
+  cudaError_t e = lb_scratch(p, scratch, avail, lb, st);
+  if (e != cudaSuccess) return e;
+  const unsigned grid_lb = (unsigned)(lb.ncol * lb.nchunk);
+  lb.blk = ws.S;  // forward: (v_t, c_t), then the carriers s_t
+  lb.blkC = ws.C;
+  if (bf16) exact_scan_lb<__nv_bfloat16, false><<<grid_lb, 128, 0, st>>>(p, lb);
+  else exact_scan_lb<float, false><<<grid_lb, 128, 0, st>>>(p, lb);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if ((e = lb_scratch(p, scratch, avail, lb, st)) != cudaSuccess) return e;
+  lb.blk = ws2.S;  // reverse: (E_t, R_t), then the carriers mu_t
+  lb.blkC = ws2.C;
+  if (bf16) exact_scan_lb<__nv_bfloat16, true><<<grid_lb, 128, 0, st>>>(p, lb);
+  else exact_scan_lb<float, true><<<grid_lb, 128, 0, st>>>(p, lb);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  const int64_t hpc = 128 / (p.D / 4);
+  const int64_t cols = p.B * cdiv(p.H, hpc);
+  const int64_t want = std::max<int64_t>(1, ((int64_t)sms * SWR_EXACT_CHUNKS) / std::max<int64_t>(cols, 1));
+  p.K = std::min<int64_t>(std::max<int64_t>(cdiv(p.nb, want), 1), p.nb);
+  const dim3 grid((unsigned)cdiv(p.nb, p.K), (unsigned)cdiv(p.H, hpc), (unsigned)p.B);
+  if (bf16) exact_bwd_out<__nv_bfloat16><<<grid, 128, 0, st>>>(p, ws, ws2);
+  else exact_bwd_out<float><<<grid, 128, 0, st>>>(p, ws, ws2);
+  return cudaGetLastError();
+#else
+  return launch_exact_bwd5(bf16, p, workspace, st, sms);
+#endif
+}
+
+// the round-1 five-launch backward: forward S, C then backward S2, C2
+cudaError_t launch_exact_bwd5(bool bf16, Params p, void* workspace, cudaStream_t st, int sms) {
   auto cdiv = [](int64_t x, int64_t y) { return (x + y - 1) / y; };
   const int64_t nS = p.B * p.H * p.nb * p.D, nC = (p.B * p.H * p.nb + 3) / 4 * 4;  // keep S2 16-byte aligned
   ExactWs ws, ws2;

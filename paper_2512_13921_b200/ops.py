@@ -374,7 +374,7 @@ def swr_exact_bwd(u, a, dx, carry_in=None, mu_in=None):
     ci, mi = _carry(carry_in, u), _carry(mu_in, u)
     mo = _new_carry(u)
     shape = _shape(u, a)
-    nbytes = 2 * _lib.swr_exact_workspace_bytes(shape)
+    nbytes = 3 * _lib.swr_exact_workspace_bytes(shape)
     ws = torch.empty(max(nbytes, 16) // 4, dtype=torch.float32, device=u.device)
     with _on(u):
         _lib.swr_exact_bwd(_ptr(u), _ptr(a), _ptr(dx), _ptr(du), _ptr(da), _ptr(ci), _ptr(mi), _ptr(mo),

@@ -104,3 +104,20 @@ def test_exact_lookback_chains(P, L, decay):
         torch.cuda.synchronize()
         assert normwise(x, rx) <= 1e-5
         assert normwise(co, rlast) <= 1e-5
+
+
+@pytest.mark.parametrize("L", [16 * 1024 + 5, 16 * 1100])
+def test_exact_bwd_lookback_scans(P, L):
+    """From 1024 blocks per line the backward resolves both carrier chains by decoupled
+    look-back scans (include/swr.h swr_exact_bwd); long-memory decays carry the adjoint
+    across every chunk."""
+    inp = swr_inputs(1, L, 2, 16, dtype=torch.float32, seed=L, decay="sigmoid3", carry=True)
+    u, a, G = inp["u"].cuda(), inp["a"].cuda(), inp["G"].cuda()
+    ci, mi = inp["carry_in"].cuda(), inp["mu_in"].cuda()
+    du, da, mo = P.swr_exact_bwd(u, a, G, carry_in=ci, mu_in=mi)
+    torch.cuda.synchronize()
+    rdu, rda, rmo = oracle.linrec_bwd(to64(inp["u"]), to64(inp["a"]), to64(inp["G"]), to64(inp["carry_in"]),
+                                      to64(inp["mu_in"]))
+    assert normwise(du, rdu) <= 1e-5
+    assert normwise(da, rda) <= 1e-5
+    assert normwise(mo, rmo) <= 1e-5

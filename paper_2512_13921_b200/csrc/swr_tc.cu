@@ -160,9 +160,16 @@ template <>
 struct Cfg<4> : Cfg<2> {
   static constexpr bool LAYER = true;
 };
+#ifndef SWR_LB_NPW
+#define SWR_LB_NPW 4
+#endif
+#ifndef SWR_LB_NG
+#define SWR_LB_NG 3
+#endif
 template <>
 struct Cfg<5> : Cfg<3> {
   static constexpr bool LAYER = true;
+  static constexpr int NPW = SWR_LB_NPW, NG = SWR_LB_NG;
 };
 
 // SMEM layout (bytes; every 4 KiB tile 1024-aligned for the 128B swizzle atoms).

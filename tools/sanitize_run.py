@@ -23,7 +23,7 @@ def run(path, dtype, D, B=1, L=100, H=16):
     m = {k: v.cuda() for k, v in mix_inputs(B, L, H, D, dtype=dtype, seed=2, carry=True).items()}
     P.phalanx_mix(m["q"], m["k"], m["v"], m["a"], carry_in=m["carry_in"], return_carry=True)
     P.phalanx_mix_bwd(m["q"], m["k"], m["v"], m["a"], m["dy"], carry_in=m["carry_in"], mu_in=m["mu_in"])
-    gq = H // 2 if path != P.SWR_PATH_TC else H
+    gq = H // 2  # shared groups: CUDA-core group sums, or TC with the per-head scratch
     y = {k: v.cuda() for k, v in layer_inputs(B, L, H, D, H // 2, H, dtype=dtype, seed=3).items()}
     P.phalanx_layer_mix(y["q"], y["zk"], y["v"], y["za"])
     yb = {k: v.cuda() for k, v in layer_inputs(B, L, H, D, gq, H, dtype=dtype, seed=4).items()}
@@ -44,6 +44,9 @@ if which in ("all", "ext"):  # the CUDA-core extensions
     s = {k: v.cuda() for k, v in swr_inputs(1, 100, 4, 32, dtype=torch.float32, seed=5).items()}
     P.swr_exact_fwd(s["u"], s["a"])
     P.swr_exact_bwd(s["u"], s["a"], s["G"])
+    sl = {k: v.cuda() for k, v in swr_inputs(1, 16 * 1030, 2, 16, dtype=torch.float32, seed=6, carry=True).items()}
+    P.swr_exact_fwd(sl["u"], sl["a"], carry_in=sl["carry_in"])  # look-back over many chunks
+    P.swr_exact_bwd(sl["u"], sl["a"], sl["G"], carry_in=sl["carry_in"], mu_in=sl["mu_in"])  # look-back scans
     P.swr_uniform_fwd(s["u"], s["a"], 8)
     st = P.DecodeState(1, 4, 32, "cuda")
     for n in range(20):

@@ -5,12 +5,16 @@
 import csv, io, subprocess, sys
 rep, kname = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
+nth = int(sys.argv[4]) if len(sys.argv) > 4 else 0  # which launch of the kernel (0 = first)
 raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 fn, hdr, acc, seen = None, None, {}, set()
+count = {}
 for r in csv.reader(io.StringIO(raw)):
     if len(r) >= 2 and r[0] == "Function Name":
-        fn = r[1]; continue
+        count[r[1]] = count.get(r[1], -1) + 1
+        fn = r[1] if count[r[1]] == nth else None
+        continue
     if r and r[0] == "Line No":
         hdr = r; continue
     if fn is None or kname not in fn or hdr is None or len(r) < 8 or not r[0]:

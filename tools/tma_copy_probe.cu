@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdint>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #define CK(x)                                                                       \
@@ -224,7 +225,33 @@ static void run_step(void* a, void* a2, void* b, void* b2, int B, int L, int H, 
   printf("step-like pair fwd T=%d NI=%d + bwd T=%d NI=%d: %7.1f us %6.0f GB/s\n", TF, NF, TB, NB, us, bytes / us / 1e3);
 }
 
+// initcheck probe (tma_copy_probe init): a TMA store into fresh memory, then a plain
+// kernel reads it -- does compute-sanitizer initcheck count the TMA write?
+static int init_probe() {
+  const int B = 1, L = 64, H = 16;
+  const size_t nbytes = (size_t)B * L * H * 128 * 2;
+  void *a, *b, *c;
+  CK(cudaMalloc(&a, nbytes));
+  CK(cudaMalloc(&b, nbytes));  // never written by the host: only the TMA stores write it
+  CK(cudaMalloc(&c, nbytes));
+  CK(cudaMemset(a, 1, nbytes));
+  Maps m;
+  map4(&m.in, a, B, L, H, 32);
+  map4(&m.in2, a, B, L, H, 32);
+  map4(&m.out, b, B, L, H, 32);
+  const int smem = 4 * 2 * 32 * 128 + 2048;
+  CK(cudaFuncSetAttribute(tcopy<32, 4, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  tcopy<32, 4, 0, 1><<<4, 64, smem>>>(m, B, L, H);
+  ldst_copy<<<4, 128>>>((const uint4*)b, (uint4*)c, (long)(nbytes / 16));  // reads the TMA-written bytes
+  CK(cudaDeviceSynchronize());
+  unsigned char h[4];
+  CK(cudaMemcpy(h, c, 4, cudaMemcpyDeviceToHost));
+  printf("init probe: first bytes %d %d (expect 1 1)\n", h[0], h[1]);
+  return 0;
+}
+
 int main(int argc, char** argv) {
+  if (argc > 1 && std::string(argv[1]) == "init") return init_probe();
   const int B = argc > 1 ? atoi(argv[1]) : 8, L = argc > 2 ? atoi(argv[2]) : 4096, H = argc > 3 ? atoi(argv[3]) : 16;
   const size_t n = (size_t)B * L * H * 128, nbytes = n * 2;
   const double bytes = 2.0 * nbytes;  // read + write (plain copies)

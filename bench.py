@@ -278,8 +278,16 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
+        # SWR_BENCH_ONE_GPU=1: every rank on cuda:0 over gloo -- a functional check of the
+        # multi-rank harness (max over ranks, batch split, SP halo) on a one-GPU box; the
+        # ranks then share the GPU, so its numbers are not scaling measurements
+        one_gpu = os.environ.get("SWR_BENCH_ONE_GPU") == "1"
+        local = 0 if one_gpu else local
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -394,8 +402,10 @@ def main():
         torch.cuda.synchronize()
         return total, [e[0].elapsed_time(e[1]) for e in ev], [e[1].elapsed_time(e[2]) for e in ev]
 
+    red_dev = dev if world == 1 or dist.get_backend() == "nccl" else torch.device("cpu")
+
     def max_over_ranks(x):
-        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        t = torch.tensor([x], device=red_dev, dtype=torch.float64)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.item()
@@ -441,7 +451,7 @@ def main():
                    "B_per_rank": B, "L": L, "H": H, "d_head": D, "op": args.op,
                    "global_batch": B if sp else B * world, "seq_len": L,
                    "parallelism": (f"sp{world} (sequence shards, one-block carrier halo via "
-                                   f"{'NCCL send/recv' if world > 1 else 'none'})") if sp else
+                                   f"{(dist.get_backend().upper() + ' send/recv') if world > 1 else 'none'})") if sp else
                                   f"dp{world} (batch x head shards, no collective)",
                    "timing": ("back to back, no L2 flush: inputs "
                               f"{in_bytes(g) >> 20} MiB > 2x L2 ({l2 >> 20} MiB), so each step pays the "
@@ -550,7 +560,7 @@ def main():
             if s >= 2:
                 times.append(e0.elapsed_time(e1))
         d2h = sum(o.numel() * o.element_size() for oc in outs_host for o in oc)
-        te = torch.tensor([sum(times) / len(times)], device=dev, dtype=torch.float64)
+        te = torch.tensor([sum(times) / len(times)], device=red_dev, dtype=torch.float64)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         line["e2e"] = {"value": tokens_per_step / (te.item() / 1e3), "unit": "tokens/s",

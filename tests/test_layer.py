@@ -223,3 +223,20 @@ def test_layer_mix_tc_backward_groups_need_workspace(P):
         assert P.last_path() == 1
     finally:
         P.set_path(prev)
+
+
+@pytest.mark.parametrize("path", ["auto", "ffma"])
+def test_layer_mix_bwd_deterministic(P, path):
+    """The group sums run in a fixed head order on both families: two runs give the
+    same bits."""
+    inp = layer_inputs(2, 300, 16, 128, 8, 4, dtype=torch.bfloat16, seed=21)
+    g = {k: v.cuda() for k, v in inp.items()}
+    prev = P.set_path(P.SWR_PATH_AUTO if path == "auto" else P.SWR_PATH_FFMA)
+    try:
+        r1 = P.phalanx_layer_mix_bwd(g["q"], g["zk"], g["v"], g["za"], g["dy"])
+        r2 = P.phalanx_layer_mix_bwd(g["q"], g["zk"], g["v"], g["za"], g["dy"])
+    finally:
+        P.set_path(prev)
+    torch.cuda.synchronize()
+    for x1, x2 in zip(r1, r2):
+        assert torch.equal(x1, x2)

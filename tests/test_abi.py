@@ -159,3 +159,31 @@ def test_layer_validation_codes(lib):
     assert fwd(layer(sk=(L * 2 * D, 0, D))) == 3           # zero token stride, L > 1
     assert fwd(layer(), q=None) == 1 and bwd(layer(), dq=None) == 1
     assert fwd(layer(), k=FAKE + 4) == 4
+
+
+def test_exact_workspace_validation(lib):
+    """swr_exact_fwd needs swr_exact_workspace_bytes(s), swr_exact_bwd three times that
+    (the look-back scans' per-block stashes and scratch); too small -> SWR_ERR_SHAPE,
+    NULL -> SWR_ERR_NULL, checked before any launch."""
+    s = _shape(lib, H=2, L=100)
+    n = lib.swr_exact_workspace_bytes(s)
+    assert n > 0
+    fwd = lambda ws, nb: lib.raw_status("swr_exact_fwd", FAKE, FAKE, FAKE, None, None, ws, nb, s, 0, None)  # noqa: E731
+    bwd = lambda ws, nb: lib.raw_status("swr_exact_bwd", FAKE, FAKE, FAKE, FAKE, FAKE, None, None, None, ws, nb,  # noqa: E731
+                                        s, 0, None)
+    assert fwd(None, n) == 1 and fwd(FAKE, n - 4) == 2
+    assert bwd(None, 3 * n) == 1 and bwd(FAKE, 2 * n) == 2
+    assert lib.swr_exact_workspace_bytes(_shape(lib, L=0)) == 0
+
+
+def test_layer_workspace_bytes(lib):
+    """The tensor-core layer backward's scratch: one bf16 [B, L, H, D] per shared gate
+    tensor; none for fp32, d != 128 or unshared groups."""
+    H, L = 16, 64
+    s = _shape(lib, H=H, L=L, D=128, sx=(L * H * 128, H * 128, 128))
+    lay = lambda Gq, Gk: lib.swr_layer(Gq, Gk, L * Gq * 128, Gq * 128, 128, L * Gk * 128, Gk * 128, 128, 1, 1)  # noqa: E731
+    per = 1 * L * H * 128 * 2
+    assert lib.phalanx_layer_workspace_bytes(s, lay(8, 8), lib.SWR_BF16) == 2 * per
+    assert lib.phalanx_layer_workspace_bytes(s, lay(8, 16), lib.SWR_BF16) == per
+    assert lib.phalanx_layer_workspace_bytes(s, lay(16, 16), lib.SWR_BF16) == 0
+    assert lib.phalanx_layer_workspace_bytes(s, lay(8, 8), lib.SWR_F32) == 0

@@ -264,6 +264,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the L8k/L16k/L32k lines")
+    ap.add_argument("--e2e-chunks", type=int, default=8, help="batch-row chunks of the e2e copy pipeline")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     B, L, H, D, dt = CONFIGS[args.config]
@@ -507,7 +508,7 @@ def main():
         pin = {k: v.pin_memory() for k, v in inp_host.items()}
         ne = min(args.steps, 10)
         h2d = sum(v.numel() * v.element_size() for v in pin.values())
-        nch = min(B, 8) if not sp else 1
+        nch = min(B, args.e2e_chunks) if not sp else 1
         rows = [(B * c // nch, B * (c + 1) // nch) for c in range(nch)]
         s_in, s_c, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
 

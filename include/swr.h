@@ -254,15 +254,16 @@ SWR_API swr_status phalanx_mix_decode_step(const void* q, const void* k, const v
 
 /* Exact full-range recurrence: x_n = a_n x_{n-1} + u_n over
  * the whole sequence (Eq. 2.1, x_{-1} = carry_in) -- the operator B2P truncates --
- * computed as Alg. 2 in one pass: each CTA solves its chunk of blocks
- * locally to the chunk's carrier aggregate (decay product, local end state), and the
- * carrier recurrence s_t = c_t s_{t-1} + v_t is resolved across CTAs by a
- * decoupled look-back over published aggregates / inclusive prefixes, after which the
- * chunk is re-run from its entering state.  CUDA cores, one launch (plus a memset of
- * the look-back flags in the workspace).  The last bits of x may differ between runs
- * (the look-back's summation order depends on timing); within the tolerances.
+ * computed as Alg. 2: per-block local solves give the carrier system
+ * s_t = c_t s_{t-1} + v_t, resolved across CTAs by a decoupled look-back
+ * over published chunk aggregates / inclusive prefixes.  bf16, D = 128 (the tensor-core
+ * envelope): the scan writes every block's exact carrier, then the B2P forward's
+ * tensor-core Pass I runs with s_{t-1} in place of v_{t-1} (two launches); otherwise
+ * one CUDA-core pass re-runs each chunk from its entering state (one launch).  Plus a
+ * memset of the look-back flags.  The last bits of x may differ between runs (the
+ * look-back's summation order depends on timing); within the tolerances.
  *   u, a, x, carry_in as in swr_fwd; carry_out = x at token L-1 (the full state).
- *   workspace  device memory of >= swr_exact_workspace_bytes(s) bytes, 16-byte
+ *   workspace  device memory of >= 2 * swr_exact_workspace_bytes(s) bytes, 16-byte
  *              aligned, caller-owned scratch (no allocation here); too small ->
  *              SWR_ERR_SHAPE, NULL with a non-empty problem -> SWR_ERR_NULL. */
 SWR_API int64_t swr_exact_workspace_bytes(swr_shape s);

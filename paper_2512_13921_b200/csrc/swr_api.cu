@@ -17,6 +17,9 @@ bool tc_supported(int op, bool bf16, const Params& p);
 cudaError_t launch_decode(bool mix, bool bf16, const DecParams& p, cudaStream_t st);
 cudaError_t launch_exact(bool bf16, Params p, void* workspace, cudaStream_t st, int sms);
 cudaError_t launch_exact_lb(bool bf16, Params p, void* workspace, cudaStream_t st);
+cudaError_t launch_exact_carriers(bool bf16, Params p, void* workspace, cudaStream_t st, const float** carriers,
+                                  bool stashed);
+void exact_stash(const Params& p, void* workspace, float** V, float** C);
 cudaError_t launch_exact_bwd(bool bf16, Params p, void* workspace, cudaStream_t st, int sms);
 cudaError_t launch_uniform(bool bf16, Params p, int k, cudaStream_t st, int sms);
 bool ffma_layer_supported(const Params& p);
@@ -444,7 +447,7 @@ swr_status swr_exact_fwd(const void* u, const void* a, void* x, const float* car
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   if (s.B == 0 || s.H == 0 || s.L == 0) return empty_call(s, carry_out, nullptr, cs);
   if (!workspace) return SWR_ERR_NULL;
-  if (workspace_bytes < swr_exact_workspace_bytes(s)) return SWR_ERR_SHAPE;
+  if (workspace_bytes < 2 * swr_exact_workspace_bytes(s)) return SWR_ERR_SHAPE;
   int sms = 0;
   st = device_info(&sms);
   if (st != SWR_OK) return st;
@@ -455,15 +458,44 @@ swr_status swr_exact_fwd(const void* u, const void* a, void* x, const float* car
   p.carry_in = carry_in;
   p.carry_out = carry_out;
 #ifndef SWR_EXACT_3STAGE  // 1: the round-1 three-launch forward (local, carrier chain, output)
-  cudaError_t e = swr::launch_exact_lb(dt == SWR_BF16, p, workspace, cs);
-  const int launches = 1;
+  cudaError_t e;
+  int launches = 1;
+  const bool bf16 = dt == SWR_BF16;
+  if (g_path != SWR_PATH_FFMA && swr::tc_supported(6, bf16, p)) {
+    // tensor cores: the look-back scan's per-block carriers, then the B2P forward's
+    // Pass I with the exact carrier (swr_tc.cu Cfg<6>)
+    // pass 1 (tensor cores): every block's local end state v_t and decay product c_t;
+    // the look-back scan over them; pass 2 (tensor cores): x with the exact carriers
+    float *V = nullptr, *C = nullptr;
+    swr::exact_stash(p, workspace, &V, &C);
+    swr::Params q1 = p;
+    q1.ex_S = V;
+    q1.ex_C = C;
+    q1.carry_out = nullptr;
+    int t1 = 0, t2 = 0;
+    e = swr::launch_tc(7, q1, cs, sms, &t1);
+    const float* carriers = nullptr;
+    if (e == cudaSuccess) e = swr::launch_exact_carriers(bf16, p, workspace, cs, &carriers, true);
+    if (e == cudaSuccess) {
+      swr::Params q = p;
+      q.ex_S = carriers;
+      q.carry_out = nullptr;  // written by the scan (the exact final state)
+      e = swr::launch_tc(6, q, cs, sms, &t2);
+    }
+    launches = t1 + 1 + t2;
+    g_last_path = SWR_PATH_TC;
+  } else {
+    if (g_path == SWR_PATH_TC) return SWR_ERR_UNSUPPORTED;
+    e = swr::launch_exact_lb(bf16, p, workspace, cs);
+    g_last_path = SWR_PATH_FFMA;
+  }
 #else
   cudaError_t e = swr::launch_exact(dt == SWR_BF16, p, workspace, cs, sms);
   const int launches = 3;
+  g_last_path = SWR_PATH_FFMA;
 #endif
   if (e != cudaSuccess) return cuda_fail(e);
   g_launches += launches;
-  g_last_path = SWR_PATH_FFMA;
   return SWR_OK;
 }
 

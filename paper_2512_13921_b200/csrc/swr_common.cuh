@@ -52,6 +52,10 @@ struct Params {
   // NULL = not used
   void* gq;
   void* gk;
+  // exact-mode forward on the tensor cores (swr_exact_fwd): the exact carrier s_t at
+  // the end of every block, [B*H][nb][D] fp32 (from the look-back scan); NULL = B2P
+  const float* ex_S;
+  float* ex_C;  // exact first pass (Cfg<7>): c_t per block [B*H][nb]; v_t goes to ex_S
   unsigned long long* trace;  // diagnostics (swr_set_trace), NULL = off
   int64_t trace_n;
   uint32_t epoch;  // TC path: launch ticket of the range claims (set by launch_tc)

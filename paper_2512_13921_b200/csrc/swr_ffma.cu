@@ -1315,7 +1315,9 @@ __global__ void __launch_bounds__(128, sizeof(T) == 2 ? 8 : 4) exact_fwd_lb(cons
 // or (R, E) in blk / blkC while folding them to the chunk aggregate, publishes it, looks
 // back (forward scan) or ahead (reverse scan) for its entering carrier, publishes its
 // prefix and replaces the stash by the per-block carriers.
-template <typename T, bool REV>
+// STASHED: the per-block (c, v) are already in blk / blkC (the tensor-core first pass,
+// swr_tc.cu Cfg<7>); pass 1 only folds them
+template <typename T, bool REV, bool STASHED = false>
 __global__ void __launch_bounds__(128, sizeof(T) == 2 ? 8 : 4) exact_scan_lb(const Params p, const ExactLb lb) {
   using V = VecN<T, 4>;
   __shared__ unsigned s_ticket, s_flag;
@@ -1343,7 +1345,30 @@ __global__ void __launch_bounds__(128, sizeof(T) == 2 ? 8 : 4) exact_scan_lb(con
 
   // 1) per-block values into the stash, folded to the chunk aggregate (C, V)
   float v[4] = {0.f, 0.f, 0.f, 0.f}, cagg = 1.f;
-  for (int64_t q = 0; q < t_hi - t_lo; ++q) {
+  constexpr int kSG = 8;  // stashed blocks whose loads are issued together
+  if constexpr (STASHED) {
+    for (int64_t q0 = 0; q0 < t_hi - t_lo; q0 += kSG) {
+      float4 y4[kSG];
+      float cb[kSG];
+#pragma unroll
+      for (int m = 0; m < kSG; ++m) {
+        const int64_t q = q0 + m;
+        const int64_t t = REV ? t_hi - 1 - q : t_lo + q;
+        const bool ok = act && q < t_hi - t_lo;
+        y4[m] = ok ? BV[t * st4] : make_float4(0.f, 0.f, 0.f, 0.f);
+        cb[m] = ok ? BC[t] : 1.f;
+      }
+#pragma unroll
+      for (int m = 0; m < kSG; ++m) {
+        v[0] = fmaf(cb[m], v[0], y4[m].x);
+        v[1] = fmaf(cb[m], v[1], y4[m].y);
+        v[2] = fmaf(cb[m], v[2], y4[m].z);
+        v[3] = fmaf(cb[m], v[3], y4[m].w);
+        cagg *= cb[m];
+      }
+    }
+  }
+  for (int64_t q = 0; q < (STASHED ? 0 : t_hi - t_lo); ++q) {
     const int64_t t = REV ? t_hi - 1 - q : t_lo + q;
     const int64_t n0 = t * kEll;
     float ab[kEll];
@@ -1450,25 +1475,43 @@ __global__ void __launch_bounds__(128, sizeof(T) == 2 ? 8 : 4) exact_scan_lb(con
   // 5) the carriers of the chunk's blocks from the stash: forward s_t; reverse mu_t (the
   //    carrier entering block t from the right, stored before applying block t)
   float s4[4] = {cin[0], cin[1], cin[2], cin[3]};
-  for (int64_t q = 0; q < t_hi - t_lo; ++q) {
-    const int64_t t = REV ? t_hi - 1 - q : t_lo + q;
-    const float4 y = act ? BV[t * st4] : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float cb = act ? BC[t] : 1.f;
-    if constexpr (REV) {
-      if (act) BV[t * st4] = make_float4(s4[0], s4[1], s4[2], s4[3]);
+  for (int64_t q0 = 0; q0 < t_hi - t_lo; q0 += kSG) {  // a group's loads before its stores
+    float4 yg[kSG];
+    float cg[kSG];
+#pragma unroll
+    for (int m = 0; m < kSG; ++m) {
+      const int64_t q = q0 + m;
+      const int64_t t = REV ? t_hi - 1 - q : t_lo + q;
+      const bool ok = act && q < t_hi - t_lo;
+      yg[m] = ok ? BV[t * st4] : make_float4(0.f, 0.f, 0.f, 0.f);
+      cg[m] = ok ? BC[t] : 1.f;
     }
-    s4[0] = fmaf(cb, s4[0], y.x);
-    s4[1] = fmaf(cb, s4[1], y.y);
-    s4[2] = fmaf(cb, s4[2], y.z);
-    s4[3] = fmaf(cb, s4[3], y.w);
-    if constexpr (!REV) {
-      if (act) BV[t * st4] = make_float4(s4[0], s4[1], s4[2], s4[3]);
+#pragma unroll
+    for (int m = 0; m < kSG; ++m) {
+      const int64_t q = q0 + m;
+      const int64_t t = REV ? t_hi - 1 - q : t_lo + q;
+      const bool ok = act && q < t_hi - t_lo;
+      if constexpr (REV) {
+        if (ok) BV[t * st4] = make_float4(s4[0], s4[1], s4[2], s4[3]);
+      }
+      s4[0] = fmaf(cg[m], s4[0], yg[m].x);
+      s4[1] = fmaf(cg[m], s4[1], yg[m].y);
+      s4[2] = fmaf(cg[m], s4[2], yg[m].z);
+      s4[3] = fmaf(cg[m], s4[3], yg[m].w);
+      if constexpr (!REV) {
+        if (ok) BV[t * st4] = make_float4(s4[0], s4[1], s4[2], s4[3]);
+      }
     }
   }
   if (REV && act && chunk == 0 && p.mu_out)
     *reinterpret_cast<float4*>(p.mu_out + line * p.D + c) = make_float4(s4[0], s4[1], s4[2], s4[3]);
+  if (!REV && act && t_hi == p.nb && p.carry_out)  // the exact state at token L-1
+    *reinterpret_cast<float4*>(p.carry_out + line * p.D + c) = make_float4(s4[0], s4[1], s4[2], s4[3]);
 }
 
+#ifndef SWR_EXACT_SCAN_K
+#define SWR_EXACT_SCAN_K 32  // blocks per look-back chunk when the per-block values are stashed
+#endif
 #ifndef SWR_EXACT_LB_K
 #define SWR_EXACT_LB_K 4  // blocks per look-back chunk
 #endif
@@ -1520,6 +1563,41 @@ cudaError_t launch_exact(bool bf16, Params p, void* workspace, cudaStream_t st, 
 }
 
 cudaError_t launch_exact_bwd5(bool bf16, Params p, void* workspace, cudaStream_t st, int sms);
+static cudaError_t lb_scratch(const Params& p, void* base, size_t avail, ExactLb& lb, cudaStream_t st);
+
+// The exact forward's carrier pass for the tensor-core output pass: the per-block exact
+// carriers s_t into the workspace's first [B*H][nb][D] floats (and carry_out), by the
+// forward look-back scan over per-block local solves -- computed here from u, or
+// (stashed) already written there with c_t by the tensor-core first pass.  Workspace:
+// 2 x swr_exact_workspace_bytes (stash, then the scan's scratch).  Returns the carriers.
+void exact_stash(const Params& p, void* workspace, float** V, float** C) {
+  *V = reinterpret_cast<float*>(workspace);
+  *C = *V + p.B * p.H * p.nb * p.D;
+}
+
+cudaError_t launch_exact_carriers(bool bf16, Params p, void* workspace, cudaStream_t st, const float** carriers,
+                                  bool stashed) {
+  const int64_t nS = p.B * p.H * p.nb * p.D, nC = (p.B * p.H * p.nb + 3) / 4 * 4;
+  float* S = reinterpret_cast<float*>(workspace);
+  float* C = S + nS;
+  void* scratch = C + nC;
+  const size_t avail = (size_t)sizeof(float) * (nS + nC);
+  // a chunk folds stashed per-block values (4 floats per thread and block): longer chunks
+  // keep the look-back chains short
+  const int64_t K = stashed ? SWR_EXACT_SCAN_K : SWR_EXACT_LB_K;
+  p.K = p.nb == 1 ? 1 : std::max<int64_t>(2, std::min<int64_t>(K, p.nb));
+  ExactLb lb;
+  cudaError_t e = lb_scratch(p, scratch, avail, lb, st);
+  if (e != cudaSuccess) return e;
+  lb.blk = S;
+  lb.blkC = C;
+  const unsigned grid = (unsigned)(lb.ncol * lb.nchunk);
+  if (stashed) exact_scan_lb<__nv_bfloat16, false, true><<<grid, 128, 0, st>>>(p, lb);
+  else if (bf16) exact_scan_lb<__nv_bfloat16, false><<<grid, 128, 0, st>>>(p, lb);
+  else exact_scan_lb<float, false><<<grid, 128, 0, st>>>(p, lb);
+  *carriers = S;
+  return cudaGetLastError();
+}
 
 // the look-back kernels' scratch inside `base` (<= swr_exact_workspace_bytes), zeroed flags
 static cudaError_t lb_scratch(const Params& p, void* base, size_t avail, ExactLb& lb, cudaStream_t st) {

@@ -127,7 +127,7 @@ struct Cfg<0> {  // swr_fwd: in u;  out x
   static constexpr int TU = 0, TG = 0;  // A-operand regions of W and lambda
   static constexpr bool CYC = false;    // w MMA through the row-rotated tile (see Stage::kLc)
   static constexpr bool WC = false;     // a second w MMA through the rotated tile, at column kWc
-  static constexpr bool BWD = false, MIX = false, LAYER = false;
+  static constexpr bool BWD = false, MIX = false, LAYER = false, EXACT = false, EXACT1 = false;
 };
 template <>
 struct Cfg<1> {  // swr_bwd: in u, G;  out du
@@ -135,7 +135,7 @@ struct Cfg<1> {  // swr_bwd: in u, G;  out du
   static constexpr int TU = 0, TG = 1;
   static constexpr bool CYC = true;
   static constexpr bool WC = false;
-  static constexpr bool BWD = true, MIX = false, LAYER = false;
+  static constexpr bool BWD = true, MIX = false, LAYER = false, EXACT = false, EXACT1 = false;
 };
 template <>
 struct Cfg<2> {  // mix fwd: in q, k, v;  out y;  prep u^ = k v (over k)
@@ -143,7 +143,7 @@ struct Cfg<2> {  // mix fwd: in q, k, v;  out y;  prep u^ = k v (over k)
   static constexpr int TU = 1, TG = 0;
   static constexpr bool CYC = false;
   static constexpr bool WC = false;
-  static constexpr bool BWD = false, MIX = true, LAYER = false;
+  static constexpr bool BWD = false, MIX = true, LAYER = false, EXACT = false, EXACT1 = false;
 };
 template <>
 struct Cfg<3> {  // mix bwd: in q, k, v, dy;  out dq, dk, dv;  prep u^ = k v (region 4), G = dy q (over q)
@@ -151,7 +151,7 @@ struct Cfg<3> {  // mix bwd: in q, k, v, dy;  out dq, dk, dv;  prep u^ = k v (re
   static constexpr int TU = 4, TG = 0;
   static constexpr bool CYC = false;
   static constexpr bool WC = true;  // x~ needs w[i] (dq), da needs w[i-1]: both from TMEM
-  static constexpr bool BWD = true, MIX = true, LAYER = false;
+  static constexpr bool BWD = true, MIX = true, LAYER = false, EXACT = false, EXACT1 = false;
 };
 // the Phalanx layer mixer (phalanx_layer_mix*, NEXT-1): the mixer's pipelines with
 // sigma on the decay / key logits and group-shared q / k (forward; the backward's
@@ -170,6 +170,25 @@ template <>
 struct Cfg<5> : Cfg<3> {
   static constexpr bool LAYER = true;
   static constexpr int NPW = SWR_LB_NPW, NG = SWR_LB_NG;
+};
+// the exact full-range recurrence's output pass (swr_exact_fwd):
+// the forward's Pass I on the tensor cores, with the exact carrier s_{t-1} of Alg. 2
+// instead of v_{t-1} -- read from the look-back scan's per-block carriers at
+// an item's first block, then carried block to block as the exact state at token 15
+template <>
+struct Cfg<6> : Cfg<0> {
+  static constexpr bool EXACT = true;
+};
+// ... and its first pass: the same Pass I, but instead of x the epilogue writes each
+// block's local end state v_t = w_t[15] and decay product c_t = g_t[15] (the carrier
+// system of P:610-613) for the scan
+#ifndef SWR_X1_NI
+#define SWR_X1_NI 12
+#endif
+template <>
+struct Cfg<7> : Cfg<0> {
+  static constexpr bool EXACT1 = true;
+  static constexpr int NI = SWR_X1_NI;  // read-only traffic: more loads in flight
 };
 
 // SMEM layout (bytes; every 4 KiB tile 1024-aligned for the 128B swizzle atoms).
@@ -415,7 +434,7 @@ struct Split {
 };
 constexpr int kClaimSlots = 256;
 __device__ unsigned g_claim[kClaimSlots][kMaxSM];  // {launch epoch} of the claimer, per range
-__device__ float g_spi[6][kMaxSM];                 // ns per item of the last CTA on each SM, per op
+__device__ float g_spi[8][kMaxSM];                 // ns per item of the last CTA on each SM, per op
 __device__ __forceinline__ int claim_range(const Split& sp, uint32_t epoch) {
   if (!sp.weighted) return (int)blockIdx.x;
   uint32_t sm;
@@ -928,7 +947,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
         mbar_wait(&ofull[ro.s], ro.ph);
         const bool halo = cur.gi < W.g0 || cur.gi >= W.g1;
         if (lane == 0) {
-          if (!halo) {
+          if (!halo && !C::EXACT1) {
             uint8_t* ot = sout + ro.s * S::kOut;
             const int tt = (int)(cur.m * BPI * kEll);
 #pragma unroll
@@ -1142,6 +1161,10 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
 #pragma unroll
             for (int k = 0; k < 4; ++k) v[k] = p.carry_in[co + 8 * k];
           }
+        } else if constexpr (C::EXACT) {  // s_{t0-1}: the exact state entering the item
+          const float* S = p.ex_S + ((int64_t)cur.line * nb + t0 - 1) * kD;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) v[k] = S[cb + 8 * k];
         } else {
           // w[15] of the previous item's last block (CYC: stored in its column 0)
           float x = tmem_ld1(tmem_base + lane_base +
@@ -1206,13 +1229,23 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
                   out[k][2 * h + 1] = o.y;
                 }
             }
-            store_frag(S::tile(ot, kb, 0), fro, out);
-            if (t0 + kb == nb - 1 && p.carry_out && qd == 3) {
+            if constexpr (C::EXACT1) {  // v_t = w_t[15] per channel, c_t = g_t[15] per line
+              if (qd == 3) {
+                float* V = const_cast<float*>(p.ex_S) + ((int64_t)cur.line * nb + t0 + kb) * kD;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) V[cb + 8 * k] = w[k][3];
+                if (wq == 0 && rr == 0) p.ex_C[(int64_t)cur.line * nb + t0 + kb] = gg[3];
+              }
+            } else {
+              store_frag(S::tile(ot, kb, 0), fro, out);
+            }
+            if (!C::EXACT && !C::EXACT1 && t0 + kb == nb - 1 && p.carry_out && qd == 3) {
 #pragma unroll
               for (int k = 0; k < 4; ++k) p.carry_out[co + 8 * k] = w[k][3];  // w_t[15]
             }
+            // next carrier: B2P v_t = w_t[15]; exact: the state at token 15
 #pragma unroll
-            for (int k = 0; k < 4; ++k) v[k] = __shfl_sync(0xffffffffu, w[k][3], lane | 3);  // v_t = w_t[15]
+            for (int k = 0; k < 4; ++k) v[k] = __shfl_sync(0xffffffffu, C::EXACT ? out[k][3] : w[k][3], lane | 3);
           } else {
             // lambda and w[i-1] of the block.  SWR (CYC): the rotated tile puts w[i-1] at
             // token i and w[15] at token 0.  Mixer: w[i] in place (needed for dq), w[i-1]
@@ -1463,7 +1496,7 @@ struct Balance {
   }
 };
 constexpr int kMaxDev = 64;
-static Balance g_balance[kMaxDev][6];  // per device (SM rates are a property of the GPU), per op
+static Balance g_balance[kMaxDev][8];  // per device (SM rates are a property of the GPU), per op
 
 // Claim slots of the weighted split, per device.  A weighted launch claims its ranges
 // in g_claim[epoch % kClaimSlots]; a slot may only be reused once the launch that used
@@ -1599,7 +1632,7 @@ static cudaError_t launch_op(const Params& p, cudaStream_t st, int sms) {
   const void* outs[3] = {nullptr, nullptr, nullptr};
   int nin = 0, nout = 0;
   switch (OP) {
-    case 0: ins[0] = p.u; outs[0] = p.x; nin = 1; nout = 1; break;
+    case 0: case 6: case 7: ins[0] = p.u; outs[0] = (OP == 7) ? p.u : p.x; nin = 1; nout = 1; break;
     case 1: ins[0] = p.u; ins[1] = p.dx; outs[0] = p.du; nin = 2; nout = 1; break;
     case 2: case 4: ins[0] = p.q; ins[1] = p.k; ins[2] = p.v; outs[0] = p.y; nin = 3; nout = 1; break;
     default:
@@ -1722,7 +1755,9 @@ cudaError_t launch_tc(int op, const Params& p, cudaStream_t st, int sms, int* la
     case 2: e = tc::launch_op<2>(p, st, sms); break;
     case 3: e = tc::launch_op<3>(p, st, sms); break;
     case 4: e = tc::launch_op<4>(p, st, sms); break;
-    default: e = tc::launch_op<5>(p, st, sms); break;
+    case 5: e = tc::launch_op<5>(p, st, sms); break;
+    case 6: e = tc::launch_op<6>(p, st, sms); break;
+    default: e = tc::launch_op<7>(p, st, sms); break;
   }
   if (e == cudaSuccess) *launches = 1;
   if (e == cudaSuccess && op == 5 && p.hq > 1) {

@@ -356,7 +356,7 @@ def swr_exact_fwd(u, a, carry_in=None, return_carry=False):
     ci = _carry(carry_in, u)
     co = _new_carry(u) if return_carry else None
     shape = _shape(u, a)
-    nbytes = _lib.swr_exact_workspace_bytes(shape)
+    nbytes = 2 * _lib.swr_exact_workspace_bytes(shape)
     ws = torch.empty(max(nbytes, 16) // 4, dtype=torch.float32, device=u.device)
     with _on(u):
         _lib.swr_exact_fwd(_ptr(u), _ptr(a), _ptr(x), _ptr(ci), _ptr(co), _ptr(ws), nbytes, shape, dt,

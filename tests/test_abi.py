@@ -162,7 +162,7 @@ def test_layer_validation_codes(lib):
 
 
 def test_exact_workspace_validation(lib):
-    """swr_exact_fwd needs swr_exact_workspace_bytes(s), swr_exact_bwd three times that
+    """swr_exact_fwd needs twice swr_exact_workspace_bytes(s), swr_exact_bwd three times
     (the look-back scans' per-block stashes and scratch); too small -> SWR_ERR_SHAPE,
     NULL -> SWR_ERR_NULL, checked before any launch."""
     s = _shape(lib, H=2, L=100)
@@ -171,7 +171,7 @@ def test_exact_workspace_validation(lib):
     fwd = lambda ws, nb: lib.raw_status("swr_exact_fwd", FAKE, FAKE, FAKE, None, None, ws, nb, s, 0, None)  # noqa: E731
     bwd = lambda ws, nb: lib.raw_status("swr_exact_bwd", FAKE, FAKE, FAKE, FAKE, FAKE, None, None, None, ws, nb,  # noqa: E731
                                         s, 0, None)
-    assert fwd(None, n) == 1 and fwd(FAKE, n - 4) == 2
+    assert fwd(None, 2 * n) == 1 and fwd(FAKE, 2 * n - 4) == 2
     assert bwd(None, 3 * n) == 1 and bwd(FAKE, 2 * n) == 2
     assert lib.swr_exact_workspace_bytes(_shape(lib, L=0)) == 0
 

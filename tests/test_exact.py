@@ -121,3 +121,22 @@ def test_exact_bwd_lookback_scans(P, L):
     assert normwise(du, rdu) <= 1e-5
     assert normwise(da, rda) <= 1e-5
     assert normwise(mo, rmo) <= 1e-5
+
+
+@pytest.mark.parametrize("L", [1, 16, 100, 4096, 16 * 1030 + 3])
+@pytest.mark.parametrize("decay", ["sigmoid", "sigmoid3", "one"])
+def test_exact_fwd_tensor_cores(P, L, decay):
+    """bf16, d = 128: the look-back scan's per-block carriers, then the B2P forward's
+    tensor-core Pass I with the exact carrier (swr_tc.cu Cfg<6>)."""
+    inp = swr_inputs(1, L, 16, 128, dtype=torch.bfloat16, seed=L + 5, decay=decay, carry=True)
+    u, a, ci = inp["u"].cuda(), inp["a"].cuda(), inp["carry_in"].cuda()
+    prev = P.set_path(P.SWR_PATH_TC)
+    try:
+        x, co = P.swr_exact_fwd(u, a, carry_in=ci, return_carry=True)
+        assert P.last_path() == 2
+    finally:
+        P.set_path(prev)
+    torch.cuda.synchronize()
+    rx, rlast = oracle.linrec_fwd(to64(inp["u"]), to64(inp["a"]), to64(inp["carry_in"]))
+    assert normwise(x, rx) <= 2e-2
+    assert normwise(co, rlast) <= 2e-2

@@ -32,12 +32,13 @@ for (B, L, H, D, dt) in [(8, 4096, 16, 128, torch.bfloat16), (2, 32768, 16, 128,
                          (8, 8192, 128, 16, torch.bfloat16), (8, 4096, 16, 128, torch.float32)]:
     g = {k: v.cuda() for k, v in swr_inputs(B, L, H, D, dtype=dt, seed=1).items()}
     te = t(lambda: P.swr_exact_fwd(g["u"], g["a"]))
+    epath = {1: "ffma", 2: "tc"}[P.last_path()]
     tt = t(lambda: P.swr_fwd(g["u"], g["a"]))
     tbe = t(lambda: P.swr_exact_bwd(g["u"], g["a"], g["G"]))
     tbt = t(lambda: P.swr_bwd(g["u"], g["a"], g["G"]))
     path = {1: "ffma", 2: "tc"}[P.last_path()]
     e = g["u"].element_size()
     n = B * L * H
-    print(f"{tag} B={B} L={L} H={H} d={D} {str(dt)[6:]}: exact fwd {te:.0f} us ({n * (2 * D + 1) * e / te / 1e3:.0f} GB/s"
+    print(f"{tag} B={B} L={L} H={H} d={D} {str(dt)[6:]}: exact fwd [{epath}] {te:.0f} us ({n * (2 * D + 1) * e / te / 1e3:.0f} GB/s"
           f" algorithmic), B2P swr_fwd [{path}] {tt:.0f} us -> {te / tt:.2f}x; exact bwd {tbe:.0f} us vs B2P {tbt:.0f} us"
           f" ({tbe / tbt:.2f}x)", flush=True)

@@ -298,6 +298,7 @@ extern "C" {
 int64_t phalanx_layer_workspace_bytes(swr_shape s, swr_layer g, swr_dtype dt) {
   if (dt != SWR_BF16 || s.D != 128 || s.B <= 0 || s.L <= 0 || s.H <= 0 || g.Gq <= 0 || g.Gk <= 0) return 0;
   if (s.H % g.Gq || s.H % g.Gk) return 0;
+  if (s.H / g.Gq == 2 && s.H / g.Gk == 2) return 0;  // pairs of heads: group sums in the kernel
   const int64_t per = s.B * s.L * s.H * s.D * 2;
   return (g.Gq < s.H ? per : 0) + (g.Gk < s.H ? per : 0);
 }

@@ -34,6 +34,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdio>
 #include <algorithm>
 #include <atomic>
 #include <cmath>
@@ -128,6 +129,8 @@ struct Cfg<0> {  // swr_fwd: in u;  out x
   static constexpr bool CYC = false;    // w MMA through the row-rotated tile (see Stage::kLc)
   static constexpr bool WC = false;     // a second w MMA through the rotated tile, at column kWc
   static constexpr bool BWD = false, MIX = false, LAYER = false, EXACT = false, EXACT1 = false;
+  static constexpr int HS = 1;  // heads walked together (GRP)
+  static constexpr bool GRP = false;
 };
 template <>
 struct Cfg<1> {  // swr_bwd: in u, G;  out du
@@ -136,6 +139,8 @@ struct Cfg<1> {  // swr_bwd: in u, G;  out du
   static constexpr bool CYC = true;
   static constexpr bool WC = false;
   static constexpr bool BWD = true, MIX = false, LAYER = false, EXACT = false, EXACT1 = false;
+  static constexpr int HS = 1;  // heads walked together (GRP)
+  static constexpr bool GRP = false;
 };
 template <>
 struct Cfg<2> {  // mix fwd: in q, k, v;  out y;  prep u^ = k v (over k)
@@ -144,6 +149,8 @@ struct Cfg<2> {  // mix fwd: in q, k, v;  out y;  prep u^ = k v (over k)
   static constexpr bool CYC = false;
   static constexpr bool WC = false;
   static constexpr bool BWD = false, MIX = true, LAYER = false, EXACT = false, EXACT1 = false;
+  static constexpr int HS = 1;  // heads walked together (GRP)
+  static constexpr bool GRP = false;
 };
 template <>
 struct Cfg<3> {  // mix bwd: in q, k, v, dy;  out dq, dk, dv;  prep u^ = k v (region 4), G = dy q (over q)
@@ -152,6 +159,8 @@ struct Cfg<3> {  // mix bwd: in q, k, v, dy;  out dq, dk, dv;  prep u^ = k v (re
   static constexpr bool CYC = false;
   static constexpr bool WC = true;  // x~ needs w[i] (dq), da needs w[i-1]: both from TMEM
   static constexpr bool BWD = true, MIX = true, LAYER = false, EXACT = false, EXACT1 = false;
+  static constexpr int HS = 1;  // heads walked together (GRP)
+  static constexpr bool GRP = false;
 };
 // the Phalanx layer mixer (phalanx_layer_mix*, NEXT-1): the mixer's pipelines with
 // sigma on the decay / key logits and group-shared q / k (forward; the backward's
@@ -170,6 +179,29 @@ template <>
 struct Cfg<5> : Cfg<3> {
   static constexpr bool LAYER = true;
   static constexpr int NPW = SWR_LB_NPW, NG = SWR_LB_NG;
+};
+// the layer mixer backward with q and k shared by pairs of heads (the paper's models:
+// H = 16 heads in 8 groups) and the group sums fused: the item walk interleaves
+// the two heads of a group block by block, one epilogue group takes both items of a
+// block and sums their dq / dz_k terms in fp32 registers (head order), storing the
+// group tile once -- no per-head scratch, no second kernel
+#ifndef SWR_LG_NG
+#define SWR_LG_NG 2
+#endif
+#ifndef SWR_LG_NO
+#define SWR_LG_NO 3
+#endif
+#ifndef SWR_LG_NI
+#define SWR_LG_NI 8
+#endif
+#ifndef SWR_LG_GRP
+#define SWR_LG_GRP 1
+#endif
+template <>
+struct Cfg<8> : Cfg<5> {
+  static constexpr int HS = 2;
+  static constexpr bool GRP = SWR_LG_GRP;
+  static constexpr int NG = SWR_LG_NG, NO = SWR_LG_NO, NI = SWR_LG_NI;
 };
 // the exact full-range recurrence's output pass (swr_exact_fwd):
 // the forward's Pass I on the tensor cores, with the exact carrier s_{t-1} of Alg. 2
@@ -263,6 +295,44 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
 // Blocking wait.  The suspend-time hint (ns) lets the waiting warp sleep until
 // the phase completes instead of re-polling on the default short timeout, so
 // idle roles do not consume issue slots.
+#if SWR_HANG_DEBUG
+// diagnostics build (tools/build_var.sh -DSWR_HANG_DEBUG=1): a wait that has not
+// completed after ~2^26 polls prints the CTA's per-warp debug words, then traps
+__device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity);
+__shared__ int g_dbg[32][4];
+#define SWR_DBG(a, b, c, d)                                                            \
+  do {                                                                                 \
+    if ((threadIdx.x & 31) == 0) {                                                     \
+      g_dbg[threadIdx.x >> 5][0] = (a); g_dbg[threadIdx.x >> 5][1] = (b);              \
+      g_dbg[threadIdx.x >> 5][2] = (c); g_dbg[threadIdx.x >> 5][3] = (d);              \
+    }                                                                                  \
+  } while (0)
+__device__ __forceinline__ bool mbar_try(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.b32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(su32(b)), "r"(parity), "r"(1000000)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t n = 0;
+  while (!mbar_try(b, parity))
+    if (++n == (1u << 13)) {
+      if ((threadIdx.x & 31) == 0) {
+        printf("HANG cta %d warp %d bar %u parity %u\n", (int)blockIdx.x, (int)(threadIdx.x >> 5),
+               (unsigned)su32(b), parity);
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+          printf("  cta %d warp %d dbg %d %d %d %d\n", (int)blockIdx.x, w, g_dbg[w][0], g_dbg[w][1], g_dbg[w][2],
+                 g_dbg[w][3]);
+      }
+      __trap();
+    }
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -272,6 +342,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "r"(parity), "r"(1000000)
       : "memory");
 }
+#if SWR_DBG_GLOBAL
+// diagnostics build: the debug words go to the host-mapped buffer of swr_set_trace
+// ([cta][warp][4] ints), readable by the host while the kernel runs
+#define SWR_DBG(a, b, c, d)                                                                  \
+  do {                                                                                       \
+    if ((threadIdx.x & 31) == 0 && p.trace != nullptr) {                                     \
+      volatile int* q_ = reinterpret_cast<volatile int*>(p.trace) + (blockIdx.x * 32 + (threadIdx.x >> 5)) * 4; \
+      q_[0] = (a); q_[1] = (b); q_[2] = (c); q_[3] = (d);                                    \
+      __threadfence_system();                                                                \
+    }                                                                                        \
+  } while (0)
+#else
+#define SWR_DBG(a, b, c, d) \
+  do {                      \
+  } while (0)
+#endif
+#endif
 __device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -434,7 +521,7 @@ struct Split {
 };
 constexpr int kClaimSlots = 256;
 __device__ unsigned g_claim[kClaimSlots][kMaxSM];  // {launch epoch} of the claimer, per range
-__device__ float g_spi[8][kMaxSM];                 // ns per item of the last CTA on each SM, per op
+__device__ float g_spi[9][kMaxSM];                 // ns per item of the last CTA on each SM, per op
 __device__ __forceinline__ int claim_range(const Split& sp, uint32_t epoch) {
   if (!sp.weighted) return (int)blockIdx.x;
   uint32_t sm;
@@ -446,7 +533,9 @@ __device__ __forceinline__ int claim_range(const Split& sp, uint32_t epoch) {
     if (atomicExch(&cl[r], epoch) != epoch) return r;
   return -1;  // unreachable: as many ranges as CTAs
 }
-template <bool BWD>
+// HS > 1 (Cfg::GRP): the split is over "super-items" (one block of the HS heads of a
+// group) and every range holds whole super-items; items are super * HS + head in group
+template <bool BWD, int HS>
 __device__ __forceinline__ Work work_of(const Split& sp, int r, int total, int nbi) {
   Work w;
   if (sp.weighted) {
@@ -459,12 +548,56 @@ __device__ __forceinline__ Work work_of(const Split& sp, int r, int total, int n
   w.first = w.g0 - ((w.g0 < w.g1 && w.g0 % nbi != 0) ? 1 : 0);
   w.last = w.g1 + ((BWD && w.g0 < w.g1 && w.g1 % nbi != 0) ? 1 : 0);
   if (w.g0 >= w.g1) w.first = w.last = w.g0;
+  w.first *= HS;
+  w.g0 *= HS;
+  w.g1 *= HS;
+  w.last *= HS;
   return w;
 }
 
-struct Cursor {  // item gi = line * nbi + m; t0 = first block of the item
+// item gi = line * nbi + m (HS = 1); t0 = first block of the item.  HS > 1: gi =
+// ((b * H/HS + gs) * nbi + m) * HS + hh, head h = gs * HS + hh (the HS heads of group gs
+// for block m are consecutive items)
+template <int HS>
+struct Cursor {
+  int gi, m, line;
+  int b, h, gs, hh;
+  __device__ __forceinline__ void set_line(int H) {
+    h = gs * HS + hh;
+    line = b * H + h;
+  }
+  __device__ __forceinline__ void init(int g, int nbi, int H) {
+    gi = g;
+    hh = g % HS;
+    const int s = g / HS, sl = s / nbi, Gs = H / HS;
+    m = s - sl * nbi;
+    b = sl / Gs;
+    gs = sl - b * Gs;
+    set_line(H);
+  }
+  __device__ __forceinline__ void next(int nbi, int H) {
+    ++gi;
+    if (++hh == HS) {
+      hh = 0;
+      if (++m == nbi) {
+        m = 0;
+        if (++gs == H / HS) {
+          gs = 0;
+          ++b;
+        }
+      }
+    }
+    set_line(H);
+  }
+  __device__ __forceinline__ void step(int n, int nbi, int H) {
+    for (int i = 0; i < n; ++i) next(nbi, H);
+  }
+};
+template <>
+struct Cursor<1> {
   int gi, m, line;
   int b, h;
+  static constexpr int hh = 0;
   __device__ __forceinline__ void init(int g, int nbi, int H) {
     gi = g;
     line = g / nbi;
@@ -516,6 +649,13 @@ struct Ring {
   __device__ __forceinline__ void step() {
     static_assert(N <= NS, "one wrap at most");
     s += N;
+    if (s >= NS) {
+      s -= NS;
+      ph ^= 1;
+    }
+  }
+  __device__ __forceinline__ void stepn(int n) {  // n < NS items forward
+    s += n;
     if (s >= NS) {
       s -= NS;
       ph ^= 1;
@@ -758,6 +898,9 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
   static_assert(NA % C::NPW == 0 && NW % C::NPW == 0 && (!C::MIX || NI % C::NPW == 0),
                 "prep warp <-> stage/slot ownership");
   static_assert(NO >= NG && NW >= NG, "epilogue group within one phase");
+  // GRP: a group's consecutive items are up to (NG - 1) HS + 1 apart (the one-phase rule
+  // above for that distance); the head's neighbour blocks are HS items away
+  static_assert(C::HS == 1 || (BPI == 1 && C::MIX && C::BWD && NW > 2 * C::HS), "grouped walk");
   static_assert((2 * NI + 2 * NA + 4 * NW + 2 * NO) * 8 + 16 <= 1024 && NO * 4 * 16 * BPI * 4 <= 3072,
                 "scratch budget");
   static_assert(S::kBytes + 1024 <= 227 * 1024, "shared memory budget");
@@ -807,8 +950,8 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
 
   const int nb = (int)p.nb, H = (int)p.H;   // sizes < 2^31 (tc_supported)
   const int nbi = (nb + BPI - 1) / BPI;       // items per line
-  const int total = (int)p.B * H * nbi;
-  const Work W = work_of<C::BWD>(split, *range_slot, total, nbi);
+  const int total = (int)p.B * H * nbi / C::HS;  // work units: items (HS = 1) / super-items
+  const Work W = work_of<C::BWD, C::HS>(split, *range_slot, total, nbi);
   unsigned long long t_begin = 0;
   if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
   const int n_items = W.last - W.first;
@@ -820,7 +963,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
     // flight.  Mixer: the prep needs the tiles anyway; the decays are issued here,
     // just before the item's tiles.
     if (lane == 0 && n_items > 0) {
-      Cursor cur;
+      Cursor<C::HS> cur;
       cur.init(W.first, nbi, H);
       Ring<NI> ri;
       Ring<NA> ra;
@@ -854,7 +997,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
   } else if (warp == kAProdW) {
     // ===================== decay producer (SWR ops) =====================
     if (lane == 0 && n_items > 0) {
-      Cursor cur;
+      Cursor<C::HS> cur;
       cur.init(W.first, nbi, H);
       Ring<NA> ra;
       ra.init(0);
@@ -906,7 +1049,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
     // input stage (SWR: the operands are consumed), and mark an item ready once every
     // MMA its epilogue reads is complete: j-1, j (backward also j+1).
     if (lane == 0 && n_items > 0) {
-      constexpr int kBack = C::BWD ? 1 : 0;
+      constexpr int kBack = C::BWD ? C::HS : 0;  // the next block of the head: HS items on
       Ring<NI> ri;
       Ring<NW> rw, rr;
       ri.init(0);
@@ -939,11 +1082,12 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
     // item's stores are issued and its own group has been read (wait_group.read 1),
     // so consecutive stores overlap instead of serialising on the SMEM read.
     if (n_items > 0) {
-      Cursor cur;
+      Cursor<C::HS> cur;
       cur.init(W.first, nbi, H);
       Ring<NO> ro, rprev;
       ro.init(0);
       for (int j = 0; j < n_items; ++j) {
+        SWR_DBG(j, n_items, ro.s, ro.ph);
         mbar_wait(&ofull[ro.s], ro.ph);
         const bool halo = cur.gi < W.g0 || cur.gi >= W.g1;
         if (lane == 0) {
@@ -952,8 +1096,11 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
             const int tt = (int)(cur.m * BPI * kEll);
 #pragma unroll
             for (int x = 0; x < C::NOUT; ++x) {  // rows past L are clipped by TMA
-              tma_store_4d(&maps.out[x], S::region(ot, x), 0, cur.h, tt, cur.b);
-              tma_store_4d(&maps.out[x], S::region(ot, x) + S::kHS, 64, cur.h, tt, cur.b);
+              // GRP: dq / dz_k (x = 0, 1) are the group sums, in the last head's slot
+              if (C::GRP && x < 2 && cur.hh != C::HS - 1) continue;
+              const int hx = (C::GRP && x < 2) ? cur.h / C::HS : cur.h;
+              tma_store_4d(&maps.out[x], S::region(ot, x), 0, hx, tt, cur.b);
+              tma_store_4d(&maps.out[x], S::region(ot, x) + S::kHS, 64, hx, tt, cur.b);
             }
           }
           bulk_commit();
@@ -977,7 +1124,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
         if (j >= 1) {  // release the previous item's slot once its stores have read it
           if (lane == 0) bulk_wait_read<1>();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&oempty[rprev.s]);
+          if (lane == 0) mbar_arrive(&oempty[(j - 1) % NO]);
         }
         rprev = ro;
         cur.next(nbi, H);
@@ -990,7 +1137,7 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
     // prep warp pw owns items j = pw mod NPW; each 16-lane half builds one block
     const int pw = warp - kPrepW0;
     const int hf = lane >> 4, col = lane & 15;
-    Cursor cur;
+    Cursor<C::HS> cur;
     if (pw < n_items) cur.init(W.first + pw, nbi, H);
     Ring<NI> ri;
     Ring<NA> ra;
@@ -1127,18 +1274,28 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
     const uint32_t fro = frag_row_off<S::kHS>(wq, lane);
     const bool leader = (threadIdx.x & 127) == 0;   // trace only
-    Cursor cur;
-    if (grp < n_items) cur.init(W.first + grp, nbi, H);
+    // group grp takes items j = grp mod NG (HS = 1); GRP: the super-items grp mod NG,
+    // i.e. the HS consecutive items (heads of one group, one block) of each
+    const int j0 = grp * C::HS;
+    Cursor<C::HS> cur;
+    if (j0 < n_items) cur.init(W.first + j0, nbi, H);
     Ring<NI> ri;
     Ring<NW> rw;
     Ring<NO> ro;
-    ri.init(grp);
-    rw.init(grp);
-    ro.init(grp);
-    for (int j = grp; j < n_items; j += NG) {
-      Ring<NW> rp = rw, rn = rw;  // work slots of items j-1 and j+1
-      rp.prev();
-      rn.next();
+    ri.init(j0);
+    rw.init(j0);
+    ro.init(j0);
+    // GRP: the head's dq and dz_k terms summed over the group's heads (fp32, head order)
+    float acc_q[4][4], acc_k[4][4];
+    (void)acc_q;
+    (void)acc_k;
+    for (int j = j0; j < n_items;) {
+      Ring<NW> rp = rw, rn = rw;  // work slots of the head's previous / next block: items j -+ HS
+#pragma unroll
+      for (int i = 0; i < C::HS; ++i) {
+        rp.prev();
+        rn.next();
+      }
       const int t0 = cur.m * BPI;
       const bool halo = cur.gi < W.g0 || cur.gi >= W.g1;
       const int nblk = min(BPI, nb - t0);  // valid blocks of this item
@@ -1149,6 +1306,9 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
       const uint32_t tslot = tmem_base + lane_base + (uint32_t)(rw.s * kItemCols);
       const bool first_item = t0 == 0, last_item = t0 + nblk == nb;
       mbar_wait(&ready[rw.s], rw.ph);
+      // lanes may leave the polling loop apart; converge before the .sync.aligned
+      // tcgen05.ld / stmatrix / ldmatrix below
+      __syncwarp();
       tc_fence_after();
       if (leader) trace(p, j, 7);
       // 1) neighbour reads first, so the neighbours' work slots are released early:
@@ -1188,10 +1348,12 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if (j >= 1) mbar_arrive(&wfree[rp.s]);                       // as "next" of item j-1
-        if (C::BWD && j + 1 < n_items) mbar_arrive(&wfree[rn.s]);  // as "previous" of item j+1
+        if (j >= C::HS) mbar_arrive(&wfree[rp.s]);                       // as "next" of item j-HS
+        if (C::BWD && j + C::HS < n_items) mbar_arrive(&wfree[rn.s]);  // as "previous" of item j+HS
       }
+      SWR_DBG(j, cur.hh, ro.s, ro.ph);
       mbar_wait(&oempty[ro.s], ro.ph ^ 1);
+      __syncwarp();
       float* rb = red + ro.s * (4 * 16 * BPI);  // this slot's da partials [4 lane quarters][16*BPI tokens]
       // 2) the item's blocks, in order (the carrier passes block to block in registers)
       if (!halo) {
@@ -1352,7 +1514,15 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
                   o[k][2 * h] = q2.x; o[k][2 * h + 1] = q2.y;
                 }
               }
-              store_frag(S::tile(ot, kb, 0), fro, o);
+              if constexpr (C::GRP) {  // dq of the group: sum over its heads, stored by the last
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+#pragma unroll
+                  for (int m = 0; m < 4; ++m) acc_q[k][m] = cur.hh == 0 ? o[k][m] : acc_q[k][m] + o[k][m];
+                if (cur.hh == C::HS - 1) store_frag(S::tile(ot, kb, 0), fro, acc_q);
+              } else {
+                store_frag(S::tile(ot, kb, 0), fro, o);
+              }
 #pragma unroll
               for (int k = 0; k < 4; ++k) {  // dv = du^ k + dy ; dk = du^ v
 #pragma unroll
@@ -1361,14 +1531,20 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
                   const float2 kf = bf2f(tk[h][k]);  // layer mixer: k = sigma(zk), written by the prep
                   const float2 dv2 = f2fma(d2, kf, bf2f(tdy[h][k]));
                   float2 dk2 = f2mul(d2, bf2f(tv[h][k]));
-                  if (C::LAYER && p.logit_k)  // dzk = dk sigma'(zk), sigma' = k (1 - k)
+                  if (C::GRP) {  // group sum first; sigma'(zk) of the group's zk at the last head
+                    dk2.x = cur.hh == 0 ? dk2.x : acc_k[k][2 * h] + dk2.x;
+                    dk2.y = cur.hh == 0 ? dk2.y : acc_k[k][2 * h + 1] + dk2.y;
+                    acc_k[k][2 * h] = dk2.x;
+                    acc_k[k][2 * h + 1] = dk2.y;
+                  }
+                  if (C::LAYER && p.logit_k && (!C::GRP || cur.hh == C::HS - 1))  // dzk = dk sigma'(zk), sigma' = k (1 - k)
                     dk2 = f2mul(dk2, make_float2(kf.x * (1.f - kf.x), kf.y * (1.f - kf.y)));
                   o[k][2 * h] = dv2.x; o[k][2 * h + 1] = dv2.y;
                   du[k][2 * h] = dk2.x; du[k][2 * h + 1] = dk2.y;
                 }
               }
               store_frag(S::tile(ot, kb, 2), fro, o);
-              store_frag(S::tile(ot, kb, 1), fro, du);
+              if (!C::GRP || cur.hh == C::HS - 1) store_frag(S::tile(ot, kb, 1), fro, du);
             }
 #pragma unroll
             for (int k = 0; k < 4; ++k)  // v_t = w_t[15]
@@ -1385,14 +1561,26 @@ __global__ void __launch_bounds__((4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MI
         if (leader) trace(p, j, 8);
         mbar_arrive(&ofull[ro.s]);
         mbar_arrive(&wfree[rw.s]);                                 // self
-        if (j == n_items - 1) mbar_arrive(&wfree[rw.s]);           // no next item
-        if (C::BWD && j == 0) mbar_arrive(&wfree[rw.s]);           // no previous item
+        if (j >= n_items - C::HS) mbar_arrive(&wfree[rw.s]);       // no next item
+        if (C::BWD && j < C::HS) mbar_arrive(&wfree[rw.s]);        // no previous item
         if constexpr (C::MIX) mbar_arrive(&inempty[ri.s]);
       }
-      cur.step(NG, nbi, H);
-      ri.template step<NG>();
-      rw.template step<NG>();
-      ro.template step<NG>();
+      if constexpr (C::HS == 1) {
+        j += NG;
+        cur.step(NG, nbi, H);
+        ri.template step<NG>();
+        rw.template step<NG>();
+        ro.template step<NG>();
+      } else {  // the super-item's next head, else the group's next super-item
+        constexpr int kAdv = (NG - 1) * C::HS + 1;
+        static_assert(kAdv <= NI && kAdv <= NW && kAdv <= NO, "one wrap at most");
+        const int adv = cur.hh == C::HS - 1 ? kAdv : 1;
+        j += adv;
+        cur.step(adv, nbi, H);
+        ri.init(j);
+        rw.init(j);
+        ro.init(j);
+      }
     }
   }
 
@@ -1496,7 +1684,7 @@ struct Balance {
   }
 };
 constexpr int kMaxDev = 64;
-static Balance g_balance[kMaxDev][8];  // per device (SM rates are a property of the GPU), per op
+static Balance g_balance[kMaxDev][9];  // per device (SM rates are a property of the GPU), per op
 
 // Claim slots of the weighted split, per device.  A weighted launch claims its ranges
 // in g_claim[epoch % kClaimSlots]; a slot may only be reused once the launch that used
@@ -1643,12 +1831,13 @@ static cudaError_t launch_op(const Params& p, cudaStream_t st, int sms) {
   auto kind = [](int i) { return (OP >= 4 && i < 2) ? i + 1 : 0; };
   for (int i = 0; i < nin; ++i)
     if (!map_dtensor(&maps.in[i], ins[i], p, 16 * Cfg<OP>::BPI, kind(i))) return cudaErrorNotSupported;
-  // layer backward with shared groups: per-head dq / dk into the scratch (summed afterwards)
+  // layer backward with shared groups: per-head dq / dk into the scratch (summed afterwards);
+  // OP 8 sums the pairs in the kernel and stores the group tensors directly
   const bool scr[3] = {OP == 5 && p.hq > 1, OP == 5 && p.hk > 1, false};
   if (scr[0]) outs[0] = p.gq;
   if (scr[1]) outs[1] = p.gk;
   for (int i = 0; i < nout; ++i)
-    if (!map_dtensor(&maps.out[i], outs[i], p, 16 * Cfg<OP>::BPI, scr[i] ? 3 : OP == 5 ? kind(i) : 0))
+    if (!map_dtensor(&maps.out[i], outs[i], p, 16 * Cfg<OP>::BPI, scr[i] ? 3 : (OP == 5 || OP == 8) ? kind(i) : 0))
       return cudaErrorNotSupported;
   if (!map_decay(&maps.a, p.a, p, Cfg<OP>::BPI)) return cudaErrorNotSupported;
 
@@ -1661,7 +1850,8 @@ static cudaError_t launch_op(const Params& p, cudaStream_t st, int sms) {
     if (e != cudaSuccess) return e;
     if (dev >= 0) attr_set[dev].store(true, std::memory_order_release);
   }
-  const int64_t total = p.B * p.H * ((p.nb + Cfg<OP>::BPI - 1) / Cfg<OP>::BPI);
+  // work units of the split: items, or for HS > 1 super-items (a block of a group's heads)
+  const int64_t total = p.B * p.H * ((p.nb + Cfg<OP>::BPI - 1) / Cfg<OP>::BPI) / Cfg<OP>::HS;
   const int grid = (int)std::min<int64_t>(sms, std::max<int64_t>(total, 1));
   constexpr int threads = (4 * Cfg<OP>::NG + Cfg<OP>::NPW + (Cfg<OP>::MIX ? 4 : 5)) * 32;
   Params q = p;
@@ -1696,10 +1886,14 @@ static cudaError_t launch_op(const Params& p, cudaStream_t st, int sms) {
 
 }  // namespace tc
 
+// layer backward with q and k shared by pairs of heads: group sums inside the kernel (Cfg<8>)
+bool tc_layer_pairs(const Params& p) { return p.hq == 2 && p.hk == 2; }
+
 bool tc_supported(int op, bool bf16, const Params& p) {
   if (!bf16 || p.D != 128) return false;
   // layer mixer backward with shared groups: needs the caller's per-head scratch
-  if (op == 5 && ((p.hq != 1 && p.gq == nullptr) || (p.hk != 1 && p.gk == nullptr))) return false;
+  if (op == 5 && !tc_layer_pairs(p) && ((p.hq != 1 && p.gq == nullptr) || (p.hk != 1 && p.gk == nullptr)))
+    return false;
   if (tc::encoder() == nullptr) return false;
   auto a16 = [](const void* q) { return q == nullptr || (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
   // decays must be TMA-addressable: heads contiguous, 16-byte token/batch strides
@@ -1755,11 +1949,12 @@ cudaError_t launch_tc(int op, const Params& p, cudaStream_t st, int sms, int* la
     case 2: e = tc::launch_op<2>(p, st, sms); break;
     case 3: e = tc::launch_op<3>(p, st, sms); break;
     case 4: e = tc::launch_op<4>(p, st, sms); break;
-    case 5: e = tc::launch_op<5>(p, st, sms); break;
+    case 5: e = tc_layer_pairs(p) ? tc::launch_op<8>(p, st, sms) : tc::launch_op<5>(p, st, sms); break;
     case 6: e = tc::launch_op<6>(p, st, sms); break;
     default: e = tc::launch_op<7>(p, st, sms); break;
   }
   if (e == cudaSuccess) *launches = 1;
+  if (op == 5 && tc_layer_pairs(p)) return e;
   if (e == cudaSuccess && op == 5 && p.hq > 1) {
     e = group_sum(p.gq, p.dq, p, p.hq, p.sq_b, p.sq_l, p.sq_h, st);
     if (e == cudaSuccess) ++*launches;

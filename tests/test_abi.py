@@ -178,12 +178,15 @@ def test_exact_workspace_validation(lib):
 
 def test_layer_workspace_bytes(lib):
     """The tensor-core layer backward's scratch: one bf16 [B, L, H, D] per shared gate
-    tensor; none for fp32, d != 128 or unshared groups."""
+    tensor; none for fp32, d != 128, unshared groups or q and k both shared by pairs."""
     H, L = 16, 64
     s = _shape(lib, H=H, L=L, D=128, sx=(L * H * 128, H * 128, 128))
     lay = lambda Gq, Gk: lib.swr_layer(Gq, Gk, L * Gq * 128, Gq * 128, 128, L * Gk * 128, Gk * 128, 128, 1, 1)  # noqa: E731
     per = 1 * L * H * 128 * 2
-    assert lib.phalanx_layer_workspace_bytes(s, lay(8, 8), lib.SWR_BF16) == 2 * per
+    assert lib.phalanx_layer_workspace_bytes(s, lay(4, 4), lib.SWR_BF16) == 2 * per
+    assert lib.phalanx_layer_workspace_bytes(s, lay(4, 16), lib.SWR_BF16) == per
     assert lib.phalanx_layer_workspace_bytes(s, lay(8, 16), lib.SWR_BF16) == per
     assert lib.phalanx_layer_workspace_bytes(s, lay(16, 16), lib.SWR_BF16) == 0
+    # pairs of heads sharing q and k (the paper's 8 groups at H = 16): summed in the kernel
+    assert lib.phalanx_layer_workspace_bytes(s, lay(8, 8), lib.SWR_BF16) == 0
     assert lib.phalanx_layer_workspace_bytes(s, lay(8, 8), lib.SWR_F32) == 0

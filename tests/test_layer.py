@@ -185,7 +185,7 @@ def test_layer_mix_tc_backward(P, B, L, H, carry):
     check(outs, refs, 2e-2)
 
 
-@pytest.mark.parametrize("B,L,H,Gq,Gk", [(2, 100, 16, 8, 8), (1, 4096, 16, 8, 8), (2, 33, 16, 2, 16),
+@pytest.mark.parametrize("B,L,H,Gq,Gk", [(2, 100, 16, 4, 4), (1, 4096, 16, 4, 8), (2, 33, 16, 2, 16),
                                          (1, 200, 24, 24, 3), (1, 17, 8, 1, 1)])
 def test_layer_mix_tc_backward_groups(P, B, L, H, Gq, Gk):
     """Shared groups on the tensor cores: per-head dq / dk into the scratch the binding
@@ -200,11 +200,64 @@ def test_layer_mix_tc_backward_groups(P, B, L, H, Gq, Gk):
     check(outs, refs, 2e-2)
 
 
+# q and k shared by pairs of heads (the paper's 8 groups at H = 16): the walk
+# interleaves a group's two heads block by block and the kernel sums dq / dz_k itself.
+# Shapes: one line pair, ragged tails, L = 1 and 15/16/17, item counts below and above
+# the SM count, long lines (weighted split, halo super-items), H = 8 / 24.
+@pytest.mark.parametrize("B,L,H", [(2, 100, 16), (1, 4096, 16), (1, 1, 16), (3, 15, 8), (2, 16, 8), (1, 17, 24),
+                                   (4, 1000, 16), (2, 2049, 24), (8, 512, 16)])
+@pytest.mark.parametrize("carry", [False, True])
+def test_layer_mix_tc_backward_pairs(P, B, L, H, carry):
+    from paper_2512_13921_b200 import _lib, ops
+    inp = layer_inputs(B, L, H, 128, H // 2, H // 2, dtype=torch.bfloat16, seed=5 * L + H + carry, carry=carry)
+    g = {k: v for k, v in inp.items()}
+    assert _lib.phalanx_layer_workspace_bytes(ops._shape(g["v"], g["za"]), ops._layer(g["q"], g["zk"], True, True),
+                                              _lib.SWR_BF16) == 0
+    prev = P.set_path(P.SWR_PATH_TC)
+    try:
+        outs, refs = run(P, inp)
+        assert P.last_path() == 2
+    finally:
+        P.set_path(prev)
+    check(outs, refs, 2e-2)
+
+
+@pytest.mark.parametrize("za_shift", [-8.0, -2.0, 3.0, 8.0])
+def test_layer_mix_tc_backward_pairs_decays(P, za_shift):
+    """Decays from near 0 (sigma(N(0,1) - 8)) to long memory (sigma(N(0,1) + 8)) through
+    the paired walk, carries on."""
+    inp = layer_inputs(2, 300, 16, 128, 8, 8, dtype=torch.bfloat16, seed=17, carry=True, za_shift=za_shift)
+    prev = P.set_path(P.SWR_PATH_TC)
+    try:
+        outs, refs = run(P, inp)
+        assert P.last_path() == 2
+    finally:
+        P.set_path(prev)
+    check(outs, refs, 2e-2)
+
+
+def test_layer_mix_tc_backward_pairs_repeatable(P):
+    """Fixed head order in the fused sums: repeated launches (which move the weighted
+    split's range boundaries) give the same bits."""
+    inp = layer_inputs(4, 2000, 16, 128, 8, 8, dtype=torch.bfloat16, seed=23)
+    g = {k: v.cuda() for k, v in inp.items()}
+    prev = P.set_path(P.SWR_PATH_TC)
+    try:
+        r1 = P.phalanx_layer_mix_bwd(g["q"], g["zk"], g["v"], g["za"], g["dy"])
+        for _ in range(10):
+            r2 = P.phalanx_layer_mix_bwd(g["q"], g["zk"], g["v"], g["za"], g["dy"])
+    finally:
+        P.set_path(prev)
+    torch.cuda.synchronize()
+    for x1, x2 in zip(r1, r2):
+        assert torch.equal(x1, x2)
+
+
 def test_layer_mix_tc_backward_groups_need_workspace(P):
     """Without the scratch a grouped backward is refused when SWR_PATH_TC is forced (no
     silent fallback) and runs on the CUDA-core family under AUTO."""
     from paper_2512_13921_b200 import _lib, ops
-    inp = layer_inputs(1, 64, 16, 128, 8, 8, dtype=torch.bfloat16, seed=1)
+    inp = layer_inputs(1, 64, 16, 128, 4, 4, dtype=torch.bfloat16, seed=1)
     g = {k: v.cuda() for k, v in inp.items()}
     q, zk, v, za, dy = g["q"], g["zk"], g["v"], g["za"], g["dy"]
     outs = [torch.empty_like(q), torch.empty_like(zk), torch.empty_like(v), torch.empty_like(za)]

@@ -1867,7 +1867,15 @@ static cudaError_t launch_d(const Params& p, cudaStream_t st, int sms) {
 
 // op: 0 = swr_fwd, 1 = swr_bwd, 2 = mix_fwd, 3 = mix_bwd, 4 / 5 = the layer mixer
 // (phalanx_layer_mix fwd / bwd); bf16 selects the dtype
+bool narrow_supported(int op, bool bf16, const Params& p);
+cudaError_t launch_narrow(int op, const Params& p, cudaStream_t st);
+
 cudaError_t launch_ffma(int op, bool bf16, const Params& p, cudaStream_t st, int sms) {
+  // narrow heads (the paper's d = 16): the TMA-staged backward (swr_narrow.cu)
+  if (narrow_supported(op, bf16, p)) {
+    cudaError_t e = launch_narrow(op, p, st);
+    if (e != cudaErrorNotSupported) return e;
+  }
   if (op == 4)
     return bf16 ? launch_fwd_stream<__nv_bfloat16, true, true>(p, st, sms) : launch_fwd_stream<float, true, true>(p, st, sms);
   if (op == 5) return bf16 ? launch_layer_bwd<__nv_bfloat16>(p, st, sms) : launch_layer_bwd<float>(p, st, sms);

@@ -1,0 +1,521 @@
+// swr_narrow.cu -- staged CUDA-core backward for narrow heads (bf16, D = 16 / 32: the
+// paper's own head shape d = 16, h = 128), SWR (swr_bwd) and the
+// Phalanx mixer (phalanx_mix_bwd).
+//
+// The block math is Alg. 4's backward as in swr_ffma.cu's bwd_ffma_vec (a thread owns
+// VC channels of one head; w_t = L_t u_t as the block-local recurrence; lambda_t the
+// local reverse solve; du = lambda + r mu with mu_t = a_{t+1}[0] lambda_{t+1}[0]; the
+// da terms du . w[i-1] + g[i-1] lambda . v_{t-1}), but the operands reach the SMs as
+// TMA boxes [16 tokens][HC heads][D] through an mbarrier ring instead of per-thread
+// 8-byte loads: a producer warp keeps NS-2 blocks in flight ahead of the compute warps,
+// and every operand is read from HBM once -- block t-1's inputs, needed for the
+// carrier v_{t-1} = w_{t-1}[15], stay in their stage for the next step of
+// the reverse walk (the register-staged kernel re-reads them).  A CTA walks a chunk of
+// K blocks of one (b, group of HC heads) in reverse time order, with one halo block on
+// each side (the right one for mu, the left one for v).
+//
+// Two channels per thread (VC = 2): twice the warps of four-channel threads, which the
+// latency chains of the sweeps need (VC = 4: 242 / 702 us).
+//
+// Roofline: HBM-bound; algorithmic bytes per (token, head) (2 D + 2) 2 read + (D + 1) 2
+// written (SWR), (4 D + 1) 2 read + (3 D + 1) 2 written (mixer) -- DESIGN.md 5.3.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <atomic>
+#include <type_traits>
+
+#include "swr_common.cuh"
+
+namespace swr {
+
+bool tma_encode_bf16(CUtensorMap* m, const void* ptr, int rank, const uint64_t* dims, const uint64_t* strides,
+                     const uint32_t* box, uint32_t kind);
+
+namespace nar {
+
+#ifndef SWR_NAR_K
+#define SWR_NAR_K 32  // blocks per CTA chunk
+#endif
+#ifndef SWR_NAR_CG
+#define SWR_NAR_CG 4  // reverse sweep: tokens whose stage reads are issued together
+#endif
+
+struct Maps {
+  CUtensorMap t[4];  // d-tensors: SWR u, dx; mixer k, v, dy, q
+  CUtensorMap a;     // decays
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.b32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(su32(b)), "r"(parity), "r"(1000000)
+      : "memory");
+  return ok != 0;
+}
+// a C-level poll loop: the warp reconverges after it (the consumers' shuffles follow)
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  while (!mbar_try(b, parity)) {
+  }
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(su32(dst)),
+      "l"(m), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(su32(dst)),
+      "l"(m), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+// VC bf16 channels (VC = 2: one 32-bit word, VC = 4: two) <-> fp32
+template <int VC>
+__device__ __forceinline__ void ld_bf(const uint8_t* q, float (&f)[VC]) {
+  if constexpr (VC == 4) {
+    const uint2 r = *reinterpret_cast<const uint2*>(q);
+    f[0] = __uint_as_float(r.x << 16);
+    f[1] = __uint_as_float(r.x & 0xffff0000u);
+    f[2] = __uint_as_float(r.y << 16);
+    f[3] = __uint_as_float(r.y & 0xffff0000u);
+  } else {
+    const uint32_t r = *reinterpret_cast<const uint32_t*>(q);
+    f[0] = __uint_as_float(r << 16);
+    f[1] = __uint_as_float(r & 0xffff0000u);
+  }
+}
+template <int VC>
+__device__ __forceinline__ void st_bf(__nv_bfloat16* p, const float (&f)[VC]) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(f[0], f[1]);
+  if constexpr (VC == 4) {
+    __nv_bfloat162 hi = __floats2bfloat162_rn(f[2], f[3]);
+    uint2 r;
+    r.x = *reinterpret_cast<uint32_t*>(&lo);
+    r.y = *reinterpret_cast<uint32_t*>(&hi);
+    *reinterpret_cast<uint2*>(p) = r;
+  } else {
+    *reinterpret_cast<__nv_bfloat162*>(p) = lo;
+  }
+}
+
+template <bool MIX, int D, int HC, int NS, int VC>
+struct Cfg {
+  static constexpr int TPH = D / VC;            // threads per head (VC channels each)
+  static constexpr int NC = HC * TPH;           // compute threads
+  static constexpr int NCW = NC / 32;           // compute warps
+  static constexpr int NT = MIX ? 4 : 2;        // d-tensors per block
+  static constexpr int kTile = 16 * HC * D * 2; // bytes of one tensor's box
+  static constexpr int kA = 16 * HC * 2;        // the decay box
+  static constexpr int kStage = ((NT * kTile + kA + 127) / 128) * 128;
+  static constexpr int kBar = NS * kStage;
+  static constexpr int kBytes = kBar + 2 * NS * 8;
+  static_assert(NC % 32 == 0 && NS >= 3, "whole compute warps; current + previous + prefetch");
+};
+
+// da: the head's TPH threads hold partial sums of all 16 tokens; a transpose-reduce
+// leaves thread qd with tokens (16 / TPH) qd .. in a fixed order (deterministic)
+template <int TPH>
+__device__ __forceinline__ void head_reduce(float (&pv)[16], int qd) {
+  int n = 16;
+#pragma unroll
+  for (int m = TPH / 2; m >= 1; m /= 2) {
+    n /= 2;
+    const bool up = (qd & m) != 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k < n) {
+        const float mine = up ? pv[k + n] : pv[k];
+        const float other = up ? pv[k] : pv[k + n];
+        pv[k] = mine + __shfl_xor_sync(0xffffffffu, other, m);
+      }
+    }
+  }
+}
+
+template <bool MIX, int D, int HC, int NS, int VC>
+__global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC>::NC + 32, 1)
+    bwd_staged(const __grid_constant__ Maps maps, const Params p) {
+  using C = Cfg<MIX, D, HC, NS, VC>;
+  constexpr int TPH = C::TPH, NT = C::NT;
+  extern __shared__ __align__(128) uint8_t sm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + C::kBar);
+  uint64_t* empty = full + NS;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t b = blockIdx.z;
+  const int h0 = blockIdx.y * HC;
+  const int64_t t0 = (int64_t)blockIdx.x * p.K;
+  const int64_t t1 = min(t0 + p.K, p.nb);
+  const bool rhalo = t1 < p.nb, lhalo = t0 > 0;
+  const int n_seq = (int)(t1 - t0) + (rhalo ? 1 : 0) + (lhalo ? 1 : 0);
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], C::NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+  if (warp == C::NCW) {
+    // ===== producer: blocks t1 (right halo), t1-1, ..., t0, t0-1 (left halo) =====
+    if (lane == 0) {
+      for (int j = 0; j < n_seq; ++j) {
+        const int s = j % NS;
+        mbar_wait(&empty[s], ((j / NS) & 1) ^ 1);
+        const int tb = (int)(t1 - 1 - j + (rhalo ? 1 : 0));
+        uint8_t* st = sm + s * C::kStage;
+        mbar_expect_tx(&full[s], NT * C::kTile + C::kA);
+#pragma unroll
+        for (int x = 0; x < NT; ++x) tma_load_4d(st + x * C::kTile, &maps.t[x], &full[s], 0, h0, tb * kEll, (int)b);
+        tma_load_3d(st + NT * C::kTile, &maps.a, &full[s], h0, tb * kEll, (int)b);
+      }
+    }
+    return;
+  }
+
+  // ===== compute: thread (head hl, channels c .. c+3) =====
+  const int hl = tid / TPH, qd = tid % TPH, c = VC * qd;
+  const int64_t h = h0 + hl;
+  const bool act = h < p.H;
+  const int64_t hc = act ? h : p.H - 1;
+  const int64_t xo = b * p.sx_b + hc * p.sx_h + c;
+  const int64_t co = (b * p.H + hc) * p.D + c;
+  __nv_bfloat16* dA = (__nv_bfloat16*)p.da + b * p.sa_b + hc * p.sa_h;
+  // operand access inside a stage: tensor x, token i -> this thread's 4 channels
+  auto ld = [&](const uint8_t* st, int x, int i, float (&f)[VC]) {
+    ld_bf<VC>(st + x * C::kTile + ((i * HC + hl) * D + c) * 2, f);
+  };
+  auto ldA = [&](const uint8_t* st, int i) {
+    return __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(st + NT * C::kTile + (i * HC + hl) * 2));
+  };
+  // Pass-I input u (SWR) / u^ = k (.) v, and the adjoint input G = dx / dy (.) q
+  auto ld_u = [&](const uint8_t* st, int i, float (&u)[VC]) {
+    if constexpr (!MIX) {
+      ld(st, 0, i, u);
+    } else {
+      float kk[VC], vv[VC];
+      ld(st, 0, i, kk);
+      ld(st, 1, i, vv);
+#pragma unroll
+      for (int e = 0; e < VC; ++e) u[e] = __fmul_rn(kk[e], vv[e]);
+    }
+  };
+  auto ld_g = [&](const uint8_t* st, int i, float (&g)[VC]) {
+    if constexpr (!MIX) {
+      ld(st, 1, i, g);
+    } else {
+      float dd[VC], qq[VC];
+      ld(st, 2, i, dd);
+      ld(st, 3, i, qq);
+#pragma unroll
+      for (int e = 0; e < VC; ++e) g[e] = __fmul_rn(dd[e], qq[e]);
+    }
+  };
+  auto release = [&](int s) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  };
+
+  float mu[VC];
+#pragma unroll
+  for (int e = 0; e < VC; ++e) mu[e] = 0.f;
+  int j = 0;
+  if (rhalo) {  // mu_{t1-1} = a_{t1}[0] lambda_{t1}[0]: the local reverse solve of block t1
+    mbar_wait(&full[0], 0);
+    const uint8_t* st = sm;
+    float lam[VC];
+    ld_g(st, 15, lam);  // padding past L: the TMA zero fill gives G = 0, so lambda = 0 there
+#pragma unroll
+    for (int i = 14; i >= 0; --i) {
+      float g[VC];
+      ld_g(st, i, g);
+      const float a1 = ldA(st, i + 1);
+#pragma unroll
+      for (int e = 0; e < VC; ++e) lam[e] = fmaf(a1, lam[e], g[e]);
+    }
+    const float a0 = ldA(st, 0);
+#pragma unroll
+    for (int e = 0; e < VC; ++e) mu[e] = a0 * lam[e];
+    release(0);
+    j = 1;
+  } else if (p.mu_in) {
+#pragma unroll
+    for (int e = 0; e < VC; ++e) mu[e] = p.mu_in[co + e];
+  }
+
+  // raw operand words (VC bf16) of tensor x, token i, read from the stage in one LDS
+  using R = typename std::conditional<VC == 4, uint2, uint32_t>::type;
+  auto ldr = [&](const uint8_t* st, int x, int i) {
+    return *reinterpret_cast<const R*>(st + x * C::kTile + ((i * HC + hl) * D + c) * 2);
+  };
+  auto cvt = [&](const R& r, float (&f)[VC]) { ld_bf<VC>(reinterpret_cast<const uint8_t*>(&r), f); };
+  constexpr int CG = SWR_NAR_CG;  // reverse sweep: tokens whose operands are read together
+
+  for (int64_t t = t1 - 1; t >= t0; --t, ++j) {
+    const int s = j % NS;
+    mbar_wait(&full[s], (j / NS) & 1);
+    const uint8_t* st = sm + s * C::kStage;
+    const int64_t n0 = t * kEll;
+    const int lim = (p.L - n0 < kEll) ? (int)(p.L - n0) : kEll;
+    // A) carrier v_{t-1} = w_{t-1}[15] from the next stage (block t-1 is whole); the
+    //    block's operands are read first, then the chain runs on registers
+    float vprev[VC];
+    if (t > 0) {
+      const int s1 = (j + 1) % NS;
+      mbar_wait(&full[s1], ((j + 1) / NS) & 1);
+      const uint8_t* sp = sm + s1 * C::kStage;
+      R r0[kEll], r1[kEll];
+      float ap[kEll];
+#pragma unroll
+      for (int i = 0; i < kEll; ++i) {
+        r0[i] = ldr(sp, 0, i);
+        if constexpr (MIX) r1[i] = ldr(sp, 1, i);
+        ap[i] = ldA(sp, i);
+      }
+#pragma unroll
+      for (int i = 0; i < kEll; ++i) {
+        float u[VC];
+        cvt(r0[i], u);
+        if constexpr (MIX) {
+          float vv[VC];
+          cvt(r1[i], vv);
+#pragma unroll
+          for (int e = 0; e < VC; ++e) u[e] = __fmul_rn(u[e], vv[e]);
+        }
+#pragma unroll
+        for (int e = 0; e < VC; ++e) vprev[e] = (i == 0) ? u[e] : fmaf(ap[i], vprev[e], u[e]);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < VC; ++e) vprev[e] = p.carry_in ? p.carry_in[co + e] : 0.f;
+    }
+    // decays of block t (pad a = 1 past L), g[i] = a[0] ... a[i], and Pass I of block t
+    // forward with w kept in registers
+    float av[kEll], gsv[kEll], w[kEll][VC];
+    {
+      R r0[kEll], r1[kEll];
+#pragma unroll
+      for (int i = 0; i < kEll; ++i) {
+        r0[i] = ldr(st, 0, i);
+        if constexpr (MIX) r1[i] = ldr(st, 1, i);
+        av[i] = ldA(st, i);
+      }
+#pragma unroll
+      for (int i = 0; i < kEll; ++i) {
+        if (i >= lim) av[i] = 1.f;
+        gsv[i] = i == 0 ? av[0] : gsv[i - 1] * av[i];
+        float u[VC];
+        cvt(r0[i], u);
+        if constexpr (MIX) {
+          float vv[VC];
+          cvt(r1[i], vv);
+#pragma unroll
+          for (int e = 0; e < VC; ++e) u[e] = __fmul_rn(u[e], vv[e]);
+        }
+#pragma unroll
+        for (int e = 0; e < VC; ++e) w[i][e] = (i == 0) ? u[e] : fmaf(av[i], w[i - 1][e], u[e]);
+      }
+    }
+    // C) one reverse sweep: lambda, r, du (mixer: dq, dk, dv), the da terms
+    float part[kEll];
+    float lam[VC], mu_next[VC];
+    float rr = 1.f;
+#pragma unroll
+    for (int i0 = kEll - CG; i0 >= 0; i0 -= CG) {
+      R rg[CG], rq[CG], rk[CG], rv[CG];
+#pragma unroll
+      for (int m = 0; m < CG; ++m) {
+        rg[m] = ldr(st, MIX ? 2 : 1, i0 + m);  // dx (SWR) / dy (mixer)
+        if constexpr (MIX) {
+          rq[m] = ldr(st, 3, i0 + m);
+          rk[m] = ldr(st, 0, i0 + m);
+          rv[m] = ldr(st, 1, i0 + m);
+        }
+      }
+#pragma unroll
+      for (int m = CG - 1; m >= 0; --m) {
+        const int i = i0 + m;
+        float g[VC], dd[VC];
+        cvt(rg[m], dd);
+        if constexpr (MIX) {
+          float qq[VC];
+          cvt(rq[m], qq);
+#pragma unroll
+          for (int e = 0; e < VC; ++e) g[e] = __fmul_rn(dd[e], qq[e]);  // G = dy (.) q
+        } else {
+#pragma unroll
+          for (int e = 0; e < VC; ++e) g[e] = dd[e];
+        }
+        if (i == kEll - 1) {
+#pragma unroll
+          for (int e = 0; e < VC; ++e) lam[e] = g[e];  // lambda[15] = G[15]
+        } else {
+#pragma unroll
+          for (int e = 0; e < VC; ++e) lam[e] = fmaf(av[i + 1], lam[e], g[e]);
+          rr *= av[i + 1];  // r_t[i] = a_t[i+1] ... a_t[15]
+        }
+        float du[VC];
+#pragma unroll
+        for (int e = 0; e < VC; ++e) du[e] = fmaf(rr, mu[e], lam[e]);
+        float sdot = 0.f, lv = 0.f;  // sum_c du[i] w[i-1] (w[-1] = 0), sum_c lambda[i] v_{t-1}
+        if (i > 0) {
+#pragma unroll
+          for (int e = 0; e < VC; ++e) sdot = (e == 0) ? du[e] * w[i - 1][e] : fmaf(du[e], w[i - 1][e], sdot);
+        }
+#pragma unroll
+        for (int e = 0; e < VC; ++e) lv = (e == 0) ? lam[e] * vprev[e] : fmaf(lam[e], vprev[e], lv);
+        part[i] = fmaf(i > 0 ? gsv[i - 1] : 1.f, lv, sdot);
+        const int64_t o = xo + (n0 + i) * p.sx_l;
+        const bool valid = act && i < lim;
+        if constexpr (!MIX) {
+          if (valid) st_bf<VC>((__nv_bfloat16*)p.du + o, du);
+        } else {
+          float kk[VC], vv[VC];
+          cvt(rk[m], kk);
+          cvt(rv[m], vv);
+          float dq[VC], dk[VC], dv[VC];
+#pragma unroll
+          for (int e = 0; e < VC; ++e) {
+            dq[e] = dd[e] * fmaf(gsv[i], vprev[e], w[i][e]);  // dq = dy x~, x~ = w + g v
+            dk[e] = du[e] * vv[e];                            // dk = du^ v
+            dv[e] = fmaf(du[e], kk[e], dd[e]);                // dv = du^ k + dy
+          }
+          if (valid) {
+            st_bf<VC>((__nv_bfloat16*)p.dq + o, dq);
+            st_bf<VC>((__nv_bfloat16*)p.dk + o, dk);
+            st_bf<VC>((__nv_bfloat16*)p.dv + o, dv);
+          }
+        }
+        if (i == 0) {
+#pragma unroll
+          for (int e = 0; e < VC; ++e) mu_next[e] = av[0] * lam[e];  // mu_{t-1} = a_t[0] lambda_t[0]
+        }
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < VC; ++e) mu[e] = mu_next[e];
+    if (t == 0 && act && p.mu_out) {
+#pragma unroll
+      for (int e = 0; e < VC; ++e) p.mu_out[co + e] = mu[e];
+    }
+    release(s);  // block t's inputs are consumed (block t-1's stay for the next step)
+    // da: deterministic reduction over the head's channels
+    head_reduce<TPH>(part, qd);
+    constexpr int NV = kEll / TPH;
+    if (act) {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        const int tok = NV * qd + k;
+        if (tok < lim) dA[(n0 + tok) * p.sa_l] = __float2bfloat16_rn(part[k]);
+      }
+    }
+  }
+}
+
+// heads per CTA and ring stages, measured back to back at d = 16, h = 128, L = 8K, B = 8
+// (tools/nar_time.py): SWR 8 heads x 3 stages (25 KB, 8 CTAs per SM) 169 us against
+// 172-207 us for 16 / 32 heads, 4-5 stages or 16 / 64-block chunks; mixer 16 heads x 4
+// stages (133 KB, one CTA) 361 us against 383-488 us for 8 heads or 6 stages
+#ifndef SWR_NAR_HC_S
+#define SWR_NAR_HC_S 8
+#endif
+#ifndef SWR_NAR_NS_S
+#define SWR_NAR_NS_S 3
+#endif
+#ifndef SWR_NAR_HC_M
+#define SWR_NAR_HC_M 16
+#endif
+#ifndef SWR_NAR_NS_M
+#define SWR_NAR_NS_M 4
+#endif
+#ifndef SWR_NAR_VC
+#define SWR_NAR_VC 2  // channels per thread
+#endif
+
+template <bool MIX, int D, int HC, int NS, int VC>
+static cudaError_t launch(const Params& p0, cudaStream_t st) {
+  using C = Cfg<MIX, D, HC, NS, VC>;
+  Params p = p0;
+  p.K = SWR_NAR_K;
+  Maps m;
+  const void* ts[4] = {MIX ? p.k : p.u, MIX ? p.v : p.dx, p.dy, p.q};
+  const uint64_t dims[4] = {(uint64_t)p.D, (uint64_t)p.H, (uint64_t)p.L, (uint64_t)p.B};
+  const uint64_t str[3] = {(uint64_t)p.sx_h * 2, (uint64_t)p.sx_l * 2, (uint64_t)p.sx_b * 2};
+  const uint32_t box[4] = {(uint32_t)D, (uint32_t)HC, 16, 1};
+  for (int x = 0; x < C::NT; ++x)
+    if (!tma_encode_bf16(&m.t[x], ts[x], 4, dims, str, box, 64 + HC)) return cudaErrorNotSupported;
+  const uint64_t adims[3] = {(uint64_t)p.H, (uint64_t)p.L, (uint64_t)p.B};
+  const uint64_t astr[2] = {(uint64_t)p.sa_l * 2, (uint64_t)p.sa_b * 2};
+  const uint32_t abox[3] = {(uint32_t)HC, 16, 1};
+  if (!tma_encode_bf16(&m.a, p.a, 3, adims, astr, abox, 96 + HC)) return cudaErrorNotSupported;
+  constexpr int smem = C::kBytes;
+  static_assert(smem <= 227 * 1024, "shared memory budget");
+  static std::atomic<bool> attr{false};
+  if (!attr.load()) {
+    cudaError_t e = cudaFuncSetAttribute(bwd_staged<MIX, D, HC, NS, VC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr.store(true);
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((p.nb + p.K - 1) / p.K), (unsigned)((p.H + HC - 1) / HC), (unsigned)p.B);
+  cfg.blockDim = dim3(C::NC + 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, bwd_staged<MIX, D, HC, NS, VC>, m, p);
+  return e == cudaSuccess ? cudaGetLastError() : e;
+}
+
+}  // namespace nar
+
+// the staged backward's envelope: bf16, D in {16, 32}, TMA-addressable operands (head
+// stride D, 16-byte token / batch strides, 16-byte aligned bases, decays with heads
+// contiguous), the plain SWR / mixer ops (the layer options run on bwd_ffma_vec)
+bool narrow_supported(int op, bool bf16, const Params& p) {
+  if (!bf16 || (op != 1 && op != 3) || (p.D != 16 && p.D != 32)) return false;
+  if (p.sx_h != p.D || (p.sx_l * 2) % 16 || (p.sx_b * 2) % 16) return false;
+  if (p.sa_h != 1 || (p.sa_l * 2) % 16 || (p.sa_b * 2) % 16) return false;
+  if (p.B > 65535 || p.H > (int64_t)65535 * 8 || p.L > (int64_t(1) << 30)) return false;
+  auto a16 = [](const void* q) { return q == nullptr || (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
+  const void* ptrs[] = {p.u, p.dx, p.du, p.q, p.k, p.v, p.dy, p.dq, p.dk, p.dv, p.a};
+  for (const void* q : ptrs)
+    if (!a16(q)) return false;
+  return true;
+}
+
+cudaError_t launch_narrow(int op, const Params& p, cudaStream_t st) {
+  if (op == 1)
+    return p.D == 16 ? nar::launch<false, 16, SWR_NAR_HC_S, SWR_NAR_NS_S, SWR_NAR_VC>(p, st)
+                     : nar::launch<false, 32, SWR_NAR_HC_S, SWR_NAR_NS_S, SWR_NAR_VC>(p, st);
+  // D = 32: half the heads per CTA (the same bytes per stage)
+  constexpr int kHc32 = SWR_NAR_HC_M / 2 < 8 ? 8 : SWR_NAR_HC_M / 2;
+  return p.D == 16 ? nar::launch<true, 16, SWR_NAR_HC_M, SWR_NAR_NS_M, SWR_NAR_VC>(p, st)
+                   : nar::launch<true, 32, kHc32, SWR_NAR_NS_M, SWR_NAR_VC>(p, st);
+}
+
+}  // namespace swr

@@ -1791,6 +1791,24 @@ static bool encode_cached(CUtensorMap* m, const void* ptr, CUtensorMapDataType t
   return true;
 }
 
+}  // namespace tc
+
+// a bf16 tensor map without swizzle, cached like the tensor-core family's (for the
+// staged narrow-head kernels, swr_narrow.cu); kind separates maps of different boxes
+bool tma_encode_bf16(CUtensorMap* m, const void* ptr, int rank, const uint64_t* dims, const uint64_t* strides,
+                     const uint32_t* box, uint32_t kind) {
+  if (tc::encoder() == nullptr || rank < 2 || rank > 4) return false;
+  cuuint64_t d[4], s[3];
+  cuuint32_t bx[4];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    bx[i] = box[i];
+  }
+  for (int i = 0; i + 1 < rank; ++i) s[i] = strides[i];
+  return tc::encode_cached(m, ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, d, s, bx, CU_TENSOR_MAP_SWIZZLE_NONE, kind);
+}
+
+namespace tc {
 // which: 0 = a [B, L, H, D] d-tensor with the strides sx; 1 / 2 = the layer mixer's
 // group-shared q / k (and dq / dk) [B, L, G, D] with their own strides; 3 = a per-head
 // scratch [B, L, H, D], contiguous

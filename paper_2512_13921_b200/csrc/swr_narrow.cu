@@ -38,6 +38,12 @@ namespace nar {
 #ifndef SWR_NAR_K
 #define SWR_NAR_K 32  // blocks per CTA chunk
 #endif
+#ifndef SWR_NAR_GR
+#define SWR_NAR_GR 8  // layer backward: q / zk group rows per CTA (16 heads: groups of >= 2)
+#endif
+#ifndef SWR_NAR_MINB_L
+#define SWR_NAR_MINB_L 2  // layer backward: CTAs per SM the registers are capped for
+#endif
 #ifndef SWR_NAR_CG
 #define SWR_NAR_CG 4  // reverse sweep: tokens whose stage reads are issued together
 #endif
@@ -117,16 +123,27 @@ __device__ __forceinline__ void st_bf(__nv_bfloat16* p, const float (&f)[VC]) {
   }
 }
 
-template <bool MIX, int D, int HC, int NS, int VC>
+template <bool MIX, int D, int HC, int NS, int VC, bool LAYER = false>
 struct Cfg {
   static constexpr int TPH = D / VC;            // threads per head (VC channels each)
   static constexpr int NC = HC * TPH;           // compute threads
   static constexpr int NCW = NC / 32;           // compute warps
   static constexpr int NT = MIX ? 4 : 2;        // d-tensors per block
   static constexpr int kTile = 16 * HC * D * 2; // bytes of one tensor's box
+  // LAYER: zk (x = 0) and q (x = 3) boxes hold at most GR group rows per token
+  static constexpr int GR = LAYER ? SWR_NAR_GR : HC;
+  static constexpr int kTileG = 16 * GR * D * 2;
+  static __host__ __device__ constexpr int off(int x) {
+    return x == 0 ? 0 : x == 1 ? kTileG : x == 2 ? kTileG + kTile : kTileG + 2 * kTile;
+  }
+  static constexpr int kAOff = MIX ? 2 * kTileG + 2 * kTile : 2 * kTile;
   static constexpr int kA = 16 * HC * 2;        // the decay box
-  static constexpr int kStage = ((NT * kTile + kA + 127) / 128) * 128;
-  static constexpr int kBar = NS * kStage;
+  // LAYER: the decays a = sigma(za) in fp32, [16][HC], written by the stage's prep
+  static constexpr int kAFOff = ((kAOff + kA + 15) / 16) * 16;
+  static constexpr int kStage = ((kAFOff + (LAYER ? 16 * HC * 4 : 0) + 127) / 128) * 128;
+  // LAYER: the per-head dq / dk terms of a block, [16][HC][D] fp32 each, for the group sums
+  static constexpr int kScrG = NS * kStage;
+  static constexpr int kBar = kScrG + (LAYER ? 2 * 16 * HC * D * 4 : 0);
   static constexpr int kBytes = kBar + 2 * NS * 8;
   static_assert(NC % 32 == 0 && NS >= 3, "whole compute warps; current + previous + prefetch");
 };
@@ -151,10 +168,16 @@ __device__ __forceinline__ void head_reduce(float (&pv)[16], int qd) {
   }
 }
 
-template <bool MIX, int D, int HC, int NS, int VC>
-__global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC>::NC + 32, 1)
+// LAYER (phalanx_layer_mix_bwd): a = sigma(za) and k = sigma(zk)
+// when the flags say logits (dza = da a (1 - a), dzk = dk k (1 - k)),
+// q and zk shared by groups of hq / hk heads -- the boxes of q / zk carry
+// the CTA's HC / hq (HC / hk) group rows, and the group sums of dq / dzk are formed in
+// shared memory in head order (deterministic); HC is a multiple of hq and hk.
+template <bool MIX, int D, int HC, int NS, int VC, bool LAYER = false>
+__global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC, LAYER>::NC + 32, LAYER ? SWR_NAR_MINB_L : 1)
     bwd_staged(const __grid_constant__ Maps maps, const Params p) {
-  using C = Cfg<MIX, D, HC, NS, VC>;
+  static_assert(!LAYER || MIX, "the layer options apply to the mixer");
+  using C = Cfg<MIX, D, HC, NS, VC, LAYER>;
   constexpr int TPH = C::TPH, NT = C::NT;
   extern __shared__ __align__(128) uint8_t sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + C::kBar);
@@ -177,6 +200,10 @@ __global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC>::NC + 32, 1)
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
+  // LAYER: heads per q / k group and the group rows of the CTA's boxes
+  const int hq = LAYER ? (int)p.hq : 1, hk = LAYER ? (int)p.hk : 1;
+  const int GQ = HC / hq, GK = HC / hk;
+  const uint32_t tx_bytes = (uint32_t)((LAYER ? (NT - 2) * C::kTile + (GQ + GK) * 16 * D * 2 : NT * C::kTile) + C::kA);
   if (warp == C::NCW) {
     // ===== producer: blocks t1 (right halo), t1-1, ..., t0, t0-1 (left halo) =====
     if (lane == 0) {
@@ -185,10 +212,12 @@ __global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC>::NC + 32, 1)
         mbar_wait(&empty[s], ((j / NS) & 1) ^ 1);
         const int tb = (int)(t1 - 1 - j + (rhalo ? 1 : 0));
         uint8_t* st = sm + s * C::kStage;
-        mbar_expect_tx(&full[s], NT * C::kTile + C::kA);
+        mbar_expect_tx(&full[s], tx_bytes);
 #pragma unroll
-        for (int x = 0; x < NT; ++x) tma_load_4d(st + x * C::kTile, &maps.t[x], &full[s], 0, h0, tb * kEll, (int)b);
-        tma_load_3d(st + NT * C::kTile, &maps.a, &full[s], h0, tb * kEll, (int)b);
+        for (int x = 0; x < NT; ++x)
+          tma_load_4d(st + C::off(x), &maps.t[x], &full[s], 0, (LAYER && x == 0) ? h0 / hk : (LAYER && x == 3) ? h0 / hq : h0,
+                      tb * kEll, (int)b);
+        tma_load_3d(st + C::kAOff, &maps.a, &full[s], h0, tb * kEll, (int)b);
       }
     }
     return;
@@ -203,11 +232,37 @@ __global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC>::NC + 32, 1)
   const int64_t co = (b * p.H + hc) * p.D + c;
   __nv_bfloat16* dA = (__nv_bfloat16*)p.da + b * p.sa_b + hc * p.sa_h;
   // operand access inside a stage: tensor x, token i -> this thread's 4 channels
+  // rows per token and this thread's row in each tensor's box (LAYER: k and q hold group rows)
+  auto rows = [&](int x) { return (LAYER && x == 0) ? GK : (LAYER && x == 3) ? GQ : HC; };
+  auto row = [&](int x) { return (LAYER && x == 0) ? hl / hk : (LAYER && x == 3) ? hl / hq : hl; };
   auto ld = [&](const uint8_t* st, int x, int i, float (&f)[VC]) {
-    ld_bf<VC>(st + x * C::kTile + ((i * HC + hl) * D + c) * 2, f);
+    ld_bf<VC>(st + C::off(x) + ((i * rows(x) + row(x)) * D + c) * 2, f);
   };
-  auto ldA = [&](const uint8_t* st, int i) {
-    return __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(st + NT * C::kTile + (i * HC + hl) * 2));
+  auto ldA = [&](const uint8_t* st, int i) {  // LAYER: a (= sigma(za)) in fp32 from the prep
+    if constexpr (LAYER) return reinterpret_cast<const float*>(st + C::kAFOff)[i * HC + hl];
+    return __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(st + C::kAOff + (i * HC + hl) * 2));
+  };
+  auto cbar = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(C::NC) : "memory"); };
+  // LAYER prep of a stage, once, by all compute threads (then a CTA barrier): a = sigma(za)
+  // in fp32 beside the box, k = sigma(zk) over the zk box in bf16 (the
+  // tensor-core family's rounding, R20) -- the group's heads share both
+  auto prep = [&](uint8_t* st) {
+    if constexpr (LAYER) {
+      float* af = reinterpret_cast<float*>(st + C::kAFOff);
+      const __nv_bfloat16* za = reinterpret_cast<const __nv_bfloat16*>(st + C::kAOff);
+      for (int x = tid; x < 16 * HC; x += C::NC) {
+        const float z = __bfloat162float(za[x]);
+        af[x] = p.logit_a ? sigmoid_f(z) : z;
+      }
+      if (p.logit_k) {
+        __nv_bfloat162* kz = reinterpret_cast<__nv_bfloat162*>(st + C::off(0));
+        for (int x = tid; x < 16 * GK * D / 2; x += C::NC) {
+          const float2 z = __bfloat1622float2(kz[x]);
+          kz[x] = __floats2bfloat162_rn(sigmoid_gate<__nv_bfloat16>(z.x), sigmoid_gate<__nv_bfloat16>(z.y));
+        }
+      }
+      cbar();
+    }
   };
   // Pass-I input u (SWR) / u^ = k (.) v, and the adjoint input G = dx / dy (.) q
   auto ld_u = [&](const uint8_t* st, int i, float (&u)[VC]) {
@@ -243,6 +298,7 @@ __global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC>::NC + 32, 1)
   int j = 0;
   if (rhalo) {  // mu_{t1-1} = a_{t1}[0] lambda_{t1}[0]: the local reverse solve of block t1
     mbar_wait(&full[0], 0);
+    prep(sm);
     const uint8_t* st = sm;
     float lam[VC];
     ld_g(st, 15, lam);  // padding past L: the TMA zero fill gives G = 0, so lambda = 0 there
@@ -267,14 +323,19 @@ __global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC>::NC + 32, 1)
   // raw operand words (VC bf16) of tensor x, token i, read from the stage in one LDS
   using R = typename std::conditional<VC == 4, uint2, uint32_t>::type;
   auto ldr = [&](const uint8_t* st, int x, int i) {
-    return *reinterpret_cast<const R*>(st + x * C::kTile + ((i * HC + hl) * D + c) * 2);
+    return *reinterpret_cast<const R*>(st + C::off(x) + ((i * rows(x) + row(x)) * D + c) * 2);
   };
   auto cvt = [&](const R& r, float (&f)[VC]) { ld_bf<VC>(reinterpret_cast<const uint8_t*>(&r), f); };
+  auto cvtk = [&](const R& r, float (&f)[VC]) { cvt(r, f); };  // the key operand (LAYER: sigma applied by the prep)
+  float* sq = reinterpret_cast<float*>(sm + C::kScrG);  // LAYER: per-head dq [16][HC][D]
+  float* sk = sq + 16 * HC * D;                        // LAYER: per-head dk (before sigma')
   constexpr int CG = SWR_NAR_CG;  // reverse sweep: tokens whose operands are read together
 
+  const int j_first = j;
   for (int64_t t = t1 - 1; t >= t0; --t, ++j) {
     const int s = j % NS;
     mbar_wait(&full[s], (j / NS) & 1);
+    if (j == j_first) prep(sm + s * C::kStage);  // later stages were prepped as block t-1
     const uint8_t* st = sm + s * C::kStage;
     const int64_t n0 = t * kEll;
     const int lim = (p.L - n0 < kEll) ? (int)(p.L - n0) : kEll;
@@ -284,6 +345,7 @@ __global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC>::NC + 32, 1)
     if (t > 0) {
       const int s1 = (j + 1) % NS;
       mbar_wait(&full[s1], ((j + 1) / NS) & 1);
+      prep(sm + s1 * C::kStage);
       const uint8_t* sp = sm + s1 * C::kStage;
       R r0[kEll], r1[kEll];
       float ap[kEll];
@@ -296,7 +358,10 @@ __global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC>::NC + 32, 1)
 #pragma unroll
       for (int i = 0; i < kEll; ++i) {
         float u[VC];
-        cvt(r0[i], u);
+        if constexpr (MIX)
+          cvtk(r0[i], u);
+        else
+          cvt(r0[i], u);
         if constexpr (MIX) {
           float vv[VC];
           cvt(r1[i], vv);
@@ -326,7 +391,10 @@ __global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC>::NC + 32, 1)
         if (i >= lim) av[i] = 1.f;
         gsv[i] = i == 0 ? av[0] : gsv[i - 1] * av[i];
         float u[VC];
-        cvt(r0[i], u);
+        if constexpr (MIX)
+          cvtk(r0[i], u);
+        else
+          cvt(r0[i], u);
         if constexpr (MIX) {
           float vv[VC];
           cvt(r1[i], vv);
@@ -392,7 +460,7 @@ __global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC>::NC + 32, 1)
           if (valid) st_bf<VC>((__nv_bfloat16*)p.du + o, du);
         } else {
           float kk[VC], vv[VC];
-          cvt(rk[m], kk);
+          cvtk(rk[m], kk);
           cvt(rv[m], vv);
           float dq[VC], dk[VC], dv[VC];
 #pragma unroll
@@ -401,7 +469,16 @@ __global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC>::NC + 32, 1)
             dk[e] = du[e] * vv[e];                            // dk = du^ v
             dv[e] = fmaf(du[e], kk[e], dd[e]);                // dv = du^ k + dy
           }
-          if (valid) {
+          if constexpr (LAYER) {  // the group sums below
+            float* q2 = sq + (i * HC + hl) * D + c;
+            float* k2 = sk + (i * HC + hl) * D + c;
+#pragma unroll
+            for (int e = 0; e < VC; ++e) {
+              q2[e] = dq[e];
+              k2[e] = dk[e];
+            }
+            if (valid) st_bf<VC>((__nv_bfloat16*)p.dv + o, dv);
+          } else if (valid) {
             st_bf<VC>((__nv_bfloat16*)p.dq + o, dq);
             st_bf<VC>((__nv_bfloat16*)p.dk + o, dk);
             st_bf<VC>((__nv_bfloat16*)p.dv + o, dv);
@@ -418,6 +495,47 @@ __global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC>::NC + 32, 1)
     if (t == 0 && act && p.mu_out) {
 #pragma unroll
       for (int e = 0; e < VC; ++e) p.mu_out[co + e] = mu[e];
+    }
+    if constexpr (LAYER) {
+      // group sums: item (token i, group row g, channel pair) sums the group's heads in
+      // head order; dzk = (sum dk) k (1 - k) with the group's k = sigma(zk)
+      cbar();
+      const int64_t G_q = p.H / hq, G_k = p.H / hk;
+      for (int it = tid; it < 16 * GQ * TPH; it += C::NC) {
+        const int i = it / (GQ * TPH), g = (it / TPH) % GQ, cq = VC * (it % TPH);
+        float acc[VC];
+#pragma unroll
+        for (int e = 0; e < VC; ++e) acc[e] = 0.f;
+        for (int m = 0; m < hq; ++m) {
+#pragma unroll
+          for (int e = 0; e < VC; ++e) acc[e] += sq[(i * HC + g * hq + m) * D + cq + e];
+        }
+        const int64_t gg = h0 / hq + g;
+        if (gg < G_q && i < lim) st_bf<VC>((__nv_bfloat16*)p.dq + b * p.sq_b + (n0 + i) * p.sq_l + gg * p.sq_h + cq, acc);
+      }
+      for (int it = tid; it < 16 * GK * TPH; it += C::NC) {
+        const int i = it / (GK * TPH), g = (it / TPH) % GK, cq = VC * (it % TPH);
+        float acc[VC];
+#pragma unroll
+        for (int e = 0; e < VC; ++e) acc[e] = 0.f;
+        for (int m = 0; m < hk; ++m) {
+#pragma unroll
+          for (int e = 0; e < VC; ++e) acc[e] += sk[(i * HC + g * hk + m) * D + cq + e];
+        }
+        if (p.logit_k) {
+          float kv[VC];
+          ld_bf<VC>(st + ((i * GK + g) * D + cq) * 2, kv);  // k = sigma(zk) of the group row (prep)
+#pragma unroll
+          for (int e = 0; e < VC; ++e) acc[e] *= kv[e] * (1.f - kv[e]);
+        }
+        const int64_t gg = h0 / hk + g;
+        if (gg < G_k && i < lim) st_bf<VC>((__nv_bfloat16*)p.dk + b * p.sk_b + (n0 + i) * p.sk_l + gg * p.sk_h + cq, acc);
+      }
+      cbar();  // the scratch is rewritten by the next block
+      if (p.logit_a) {  // dza = da sigma'(za), sigma' = a (1 - a)
+#pragma unroll
+        for (int i = 0; i < kEll; ++i) part[i] *= av[i] * (1.f - av[i]);
+      }
     }
     release(s);  // block t's inputs are consumed (block t-1's stay for the next step)
     // da: deterministic reduction over the head's channels
@@ -449,13 +567,19 @@ __global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC>::NC + 32, 1)
 #ifndef SWR_NAR_NS_M
 #define SWR_NAR_NS_M 4
 #endif
+#ifndef SWR_NAR_HC_L
+#define SWR_NAR_HC_L 16  // layer backward: heads per CTA (a multiple of the group sizes)
+#endif
+#ifndef SWR_NAR_NS_L
+#define SWR_NAR_NS_L 3
+#endif
 #ifndef SWR_NAR_VC
 #define SWR_NAR_VC 2  // channels per thread
 #endif
 
-template <bool MIX, int D, int HC, int NS, int VC>
+template <bool MIX, int D, int HC, int NS, int VC, bool LAYER = false>
 static cudaError_t launch(const Params& p0, cudaStream_t st) {
-  using C = Cfg<MIX, D, HC, NS, VC>;
+  using C = Cfg<MIX, D, HC, NS, VC, LAYER>;
   Params p = p0;
   p.K = SWR_NAR_K;
   Maps m;
@@ -463,8 +587,18 @@ static cudaError_t launch(const Params& p0, cudaStream_t st) {
   const uint64_t dims[4] = {(uint64_t)p.D, (uint64_t)p.H, (uint64_t)p.L, (uint64_t)p.B};
   const uint64_t str[3] = {(uint64_t)p.sx_h * 2, (uint64_t)p.sx_l * 2, (uint64_t)p.sx_b * 2};
   const uint32_t box[4] = {(uint32_t)D, (uint32_t)HC, 16, 1};
-  for (int x = 0; x < C::NT; ++x)
-    if (!tma_encode_bf16(&m.t[x], ts[x], 4, dims, str, box, 64 + HC)) return cudaErrorNotSupported;
+  for (int x = 0; x < C::NT; ++x) {
+    if (LAYER && (x == 0 || x == 3)) {  // group-shared zk / q [B, L, G, D]: HC / hk (HC / hq) group rows
+      const int64_t hg = x == 0 ? p.hk : p.hq;
+      const uint64_t gd[4] = {(uint64_t)p.D, (uint64_t)(p.H / hg), (uint64_t)p.L, (uint64_t)p.B};
+      const uint64_t gs[3] = {(uint64_t)(x == 0 ? p.sk_h : p.sq_h) * 2, (uint64_t)(x == 0 ? p.sk_l : p.sq_l) * 2,
+                              (uint64_t)(x == 0 ? p.sk_b : p.sq_b) * 2};
+      const uint32_t gb[4] = {(uint32_t)D, (uint32_t)(HC / hg), 16, 1};
+      if (!tma_encode_bf16(&m.t[x], ts[x], 4, gd, gs, gb, 256 + (uint32_t)(HC / hg))) return cudaErrorNotSupported;
+    } else if (!tma_encode_bf16(&m.t[x], ts[x], 4, dims, str, box, 64 + HC)) {
+      return cudaErrorNotSupported;
+    }
+  }
   const uint64_t adims[3] = {(uint64_t)p.H, (uint64_t)p.L, (uint64_t)p.B};
   const uint64_t astr[2] = {(uint64_t)p.sa_l * 2, (uint64_t)p.sa_b * 2};
   const uint32_t abox[3] = {(uint32_t)HC, 16, 1};
@@ -473,7 +607,9 @@ static cudaError_t launch(const Params& p0, cudaStream_t st) {
   static_assert(smem <= 227 * 1024, "shared memory budget");
   static std::atomic<bool> attr{false};
   if (!attr.load()) {
-    cudaError_t e = cudaFuncSetAttribute(bwd_staged<MIX, D, HC, NS, VC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(bwd_staged<MIX, D, HC, NS, VC, LAYER>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(bwd_staged<MIX, D, HC, NS, VC, LAYER>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     attr.store(true);
   }
@@ -487,7 +623,7 @@ static cudaError_t launch(const Params& p0, cudaStream_t st) {
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, bwd_staged<MIX, D, HC, NS, VC>, m, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, bwd_staged<MIX, D, HC, NS, VC, LAYER>, m, p);
   return e == cudaSuccess ? cudaGetLastError() : e;
 }
 
@@ -497,7 +633,14 @@ static cudaError_t launch(const Params& p0, cudaStream_t st) {
 // stride D, 16-byte token / batch strides, 16-byte aligned bases, decays with heads
 // contiguous), the plain SWR / mixer ops (the layer options run on bwd_ffma_vec)
 bool narrow_supported(int op, bool bf16, const Params& p) {
-  if (!bf16 || (op != 1 && op != 3) || (p.D != 16 && p.D != 32)) return false;
+  if (!bf16 || (op != 1 && op != 3 && op != 5) || (p.D != 16 && p.D != 32)) return false;
+  if (op == 5) {  // layer: q / zk group tensors with heads contiguous, groups inside a CTA's 16 heads
+    if (p.sq_h != p.D || p.sk_h != p.D || (p.sq_l * 2) % 16 || (p.sq_b * 2) % 16 || (p.sk_l * 2) % 16 ||
+        (p.sk_b * 2) % 16)
+      return false;
+    if (p.hq < 1 || p.hk < 1 || SWR_NAR_HC_L % p.hq || SWR_NAR_HC_L % p.hk) return false;
+    if (SWR_NAR_HC_L / p.hq > SWR_NAR_GR || SWR_NAR_HC_L / p.hk > SWR_NAR_GR) return false;
+  }
   if (p.sx_h != p.D || (p.sx_l * 2) % 16 || (p.sx_b * 2) % 16) return false;
   if (p.sa_h != 1 || (p.sa_l * 2) % 16 || (p.sa_b * 2) % 16) return false;
   if (p.B > 65535 || p.H > (int64_t)65535 * 8 || p.L > (int64_t(1) << 30)) return false;
@@ -509,6 +652,9 @@ bool narrow_supported(int op, bool bf16, const Params& p) {
 }
 
 cudaError_t launch_narrow(int op, const Params& p, cudaStream_t st) {
+  if (op == 5)
+    return p.D == 16 ? nar::launch<true, 16, SWR_NAR_HC_L, SWR_NAR_NS_L, SWR_NAR_VC, true>(p, st)
+                     : nar::launch<true, 32, SWR_NAR_HC_L, 3, SWR_NAR_VC, true>(p, st);
   if (op == 1)
     return p.D == 16 ? nar::launch<false, 16, SWR_NAR_HC_S, SWR_NAR_NS_S, SWR_NAR_VC>(p, st)
                      : nar::launch<false, 32, SWR_NAR_HC_S, SWR_NAR_NS_S, SWR_NAR_VC>(p, st);

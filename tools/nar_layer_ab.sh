@@ -1,0 +1,12 @@
+for v in ${VARS:-main}; do for G in 16 8; do echo -n "$v G=$G: "; L=build/var/libswr_$v.so; [ $v = main ] && L=paper_2512_13921_b200/libswr.so; SWR_LIB=$L timeout 60 python -c "
+import sys; sys.path.insert(0,'.')
+import torch, paper_2512_13921_b200 as P
+from swr_inputs import layer_inputs
+g={k:v.cuda() for k,v in layer_inputs(8,8192,128,16,$G,$G,dtype=torch.bfloat16,seed=1).items()}
+f=lambda: P.phalanx_layer_mix_bwd(g['q'],g['zk'],g['v'],g['za'],g['dy'])
+for _ in range(3): f()
+torch.cuda.synchronize(); e0,e1=torch.cuda.Event(enable_timing=True),torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(10): f()
+e1.record(); torch.cuda.synchronize(); print(round(e0.elapsed_time(e1)*100,1),'us')
+"; done; done

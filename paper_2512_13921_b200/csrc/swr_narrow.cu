@@ -39,7 +39,7 @@ namespace nar {
 #define SWR_NAR_K 32  // blocks per CTA chunk
 #endif
 #ifndef SWR_NAR_GR
-#define SWR_NAR_GR 8  // layer backward: q / zk group rows per CTA (16 heads: groups of >= 2)
+#define SWR_NAR_GR 2  // layer backward: q / zk group rows per CTA (16 heads: groups of >= 8; smaller groups measured slower than bwd_ffma_vec)
 #endif
 #ifndef SWR_NAR_MINB_L
 #define SWR_NAR_MINB_L 2  // layer backward: CTAs per SM the registers are capped for
@@ -633,6 +633,9 @@ static cudaError_t launch(const Params& p0, cudaStream_t st) {
 // stride D, 16-byte token / batch strides, 16-byte aligned bases, decays with heads
 // contiguous), the plain SWR / mixer ops (the layer options run on bwd_ffma_vec)
 bool narrow_supported(int op, bool bf16, const Params& p) {
+#ifdef SWR_NAR_OFF
+  return false;  // A/B builds: the register-staged kernels everywhere
+#endif
   if (!bf16 || (op != 1 && op != 3 && op != 5) || (p.D != 16 && p.D != 32)) return false;
   if (op == 5) {  // layer: q / zk group tensors with heads contiguous, groups inside a CTA's 16 heads
     if (p.sq_h != p.D || p.sk_h != p.D || (p.sq_l * 2) % 16 || (p.sq_b * 2) % 16 || (p.sk_l * 2) % 16 ||

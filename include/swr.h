@@ -202,8 +202,10 @@ typedef struct {
 /* Scratch the layer backward needs to run on the tensor cores when heads share q or k:
  * per-head dq / dk (bf16 [B, L, H, D] each, for the groups of q resp. k that are shared),
  * summed over each group by a second kernel in a fixed head order.  0 when no scratch is
- * needed or the call is outside the tensor-core envelope; without it such a call runs
- * on the CUDA-core family (AUTO) or is refused (SWR_PATH_TC). */
+ * needed -- no sharing, or q and k both shared by pairs of heads (H / Gq = H / Gk = 2,
+ * the paper's 8 groups at H = 16: the kernel walks each pair together and sums in
+ * registers) -- or the call is outside the tensor-core envelope; without it such a call
+ * runs on the CUDA-core family (AUTO) or is refused (SWR_PATH_TC). */
 SWR_API int64_t phalanx_layer_workspace_bytes(swr_shape s, swr_layer g, swr_dtype dt);
 
 /* Layer mixer forward.  v, y [B,L,H,D] with the strides of s; za [B,L,H] with the
@@ -217,9 +219,10 @@ SWR_API swr_status phalanx_layer_mix(const void* q, const void* zk, const void* 
 /* Layer mixer backward.  dq [B,L,Gq,D] and dzk [B,L,Gk,D] with the strides of g
  * (the group sums), dv [B,L,H,D], dza [B,L,H]; carries as in phalanx_mix_bwd.
  * The tensor-core kernels (bf16, D = 128) take shared groups when g.workspace holds
- * phalanx_layer_workspace_bytes(s, g, dt) bytes (16-byte aligned); else the CUDA-core
- * kernel forms the group sums inside one CTA: H / Gq and H / Gk must be powers of two
- * and at most 256 / (D / 4) (64 at D = 16, 8 at D = 128), else SWR_ERR_UNSUPPORTED. */
+ * phalanx_layer_workspace_bytes(s, g, dt) bytes (16-byte aligned; none for pairs of
+ * heads); else the CUDA-core kernels form the group sums inside one CTA: H / Gq and
+ * H / Gk must be powers of two and at most 256 / (D / 4) (64 at D = 16, 8 at D = 128),
+ * else SWR_ERR_UNSUPPORTED.  All group sums run in a fixed head order (deterministic). */
 SWR_API swr_status phalanx_layer_mix_bwd(const void* q, const void* zk, const void* v,
                                  const void* za, const void* dy, void* dq, void* dzk, void* dv,
                                  void* dza, const float* carry_in, const float* mu_in,

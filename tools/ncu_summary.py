@@ -31,7 +31,7 @@ METRICS = [
 ]
 KEYS = {"swr_tc_kernel<0>": "swr_fwd", "swr_tc_kernel<1>": "swr_bwd",
         "swr_tc_kernel<2>": "mix_fwd", "swr_tc_kernel<3>": "mix_bwd",
-        "swr_tc_kernel<4>": "layer_fwd", "swr_tc_kernel<5>": "layer_bwd"}
+        "swr_tc_kernel<4>": "layer_fwd", "swr_tc_kernel<5>": "layer_bwd", "swr_tc_kernel<8>": "layer_bwd"}
 
 
 def to_bytes(val, unit):

@@ -203,7 +203,6 @@ __global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC, LAYER>::NC + 32, LAYER
   // LAYER: heads per q / k group and the group rows of the CTA's boxes
   const int hq = LAYER ? (int)p.hq : 1, hk = LAYER ? (int)p.hk : 1;
   const int GQ = HC / hq, GK = HC / hk;
-  const uint32_t tx_bytes = (uint32_t)((LAYER ? (NT - 2) * C::kTile + (GQ + GK) * 16 * D * 2 : NT * C::kTile) + C::kA);
   if (warp == C::NCW) {
     // ===== producer: blocks t1 (right halo), t1-1, ..., t0, t0-1 (left halo) =====
     if (lane == 0) {
@@ -212,11 +211,26 @@ __global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC, LAYER>::NC + 32, LAYER
         mbar_wait(&empty[s], ((j / NS) & 1) ^ 1);
         const int tb = (int)(t1 - 1 - j + (rhalo ? 1 : 0));
         uint8_t* st = sm + s * C::kStage;
-        mbar_expect_tx(&full[s], tx_bytes);
+        // halo blocks load only what they are read for: the right one the adjoint input
+        // (dx / dy, q) for mu, the left one the Pass-I input (u / k, v) for v_{t0-1}
+        const bool rh = rhalo && j == 0, lh = lhalo && j == n_seq - 1;
+        auto need = [&](int x) {
+          const bool u_in = MIX ? x < 2 : x == 0;
+          return !(rh && u_in) && !(lh && !u_in);
+        };
+        auto box_bytes = [&](int x) {
+          return (LAYER && x == 0) ? GK * 16 * D * 2 : (LAYER && x == 3) ? GQ * 16 * D * 2 : C::kTile;
+        };
+        uint32_t bytes = C::kA;
 #pragma unroll
         for (int x = 0; x < NT; ++x)
-          tma_load_4d(st + C::off(x), &maps.t[x], &full[s], 0, (LAYER && x == 0) ? h0 / hk : (LAYER && x == 3) ? h0 / hq : h0,
-                      tb * kEll, (int)b);
+          if (need(x)) bytes += box_bytes(x);
+        mbar_expect_tx(&full[s], bytes);
+#pragma unroll
+        for (int x = 0; x < NT; ++x)
+          if (need(x))
+            tma_load_4d(st + C::off(x), &maps.t[x], &full[s], 0, (LAYER && x == 0) ? h0 / hk : (LAYER && x == 3) ? h0 / hq : h0,
+                        tb * kEll, (int)b);
         tma_load_3d(st + C::kAOff, &maps.a, &full[s], h0, tb * kEll, (int)b);
       }
     }

@@ -5,7 +5,9 @@ against the fp64 oracle.  These shapes take that kernel on the CUDA-core family
 8 (16-byte decay rows), contiguous heads.  Covered: one block, ragged tails (15, 17,
 33), chunk boundaries of the 32-block walk with their halo blocks (512, 513, 1100,
 2049), head groups that overhang H (H = 24 with 16-head CTAs), carries in and out,
-every decay family, batch > 1.  Tolerance as tests/test_parity.py (normwise 2e-2)."""
+every decay family, batch > 1; the layer mixer backward with groups of 8 / 16 heads
+(mixed q / k group sizes, D = 32, H = 48 / 64 / 128, L = 1 .. 700, each logit flag).
+Tolerance as tests/test_parity.py (normwise 2e-2)."""
 import numpy as np
 import pytest
 import torch
@@ -127,3 +129,49 @@ def test_narrow_paper_shape_sampled(P):
         r = oracle.mix_bwd(s(inp["q"]), s(inp["k"]), s(inp["v"]), s(inp["a"]), s(inp["dy"]))
         check({"dq": dq[b:b + 1, :, hh:hh + 1], "dk": dk[b:b + 1, :, hh:hh + 1], "dv": dv[b:b + 1, :, hh:hh + 1],
                "da": dam[b:b + 1, :, hh:hh + 1]}, dict(zip(["dq", "dk", "dv", "da"], r[:4])))
+
+
+# ---------------------------------------------------------------------------
+# the layer mixer backward on the staged kernel: q / zk shared by groups of >= 8 heads
+# inside the CTA's 16 heads (the paper's d = 16 models: 8 groups of 16 heads)
+# ---------------------------------------------------------------------------
+def _layer_run(P, inp, logit_a=True, logit_k=True):
+    from test_layer import run
+    return run(P, inp, logit_a=logit_a, logit_k=logit_k)
+
+
+@pytest.mark.parametrize("B,L,H,D,Gq,Gk", [(1, 64, 128, 16, 8, 8), (2, 100, 128, 16, 16, 8), (1, 513, 32, 16, 2, 4),
+                                           (2, 33, 16, 16, 1, 2), (1, 1, 16, 16, 1, 1), (1, 700, 64, 32, 4, 8),
+                                           (3, 17, 48, 16, 3, 6)])
+@pytest.mark.parametrize("carry", [False, True])
+def test_layer_bwd_narrow(P, B, L, H, D, Gq, Gk, carry):
+    from swr_inputs import layer_inputs
+    from test_layer import check as lcheck
+    inp = layer_inputs(B, L, H, D, Gq, Gk, dtype=torch.bfloat16, seed=L + H + Gq + D, carry=carry)
+    outs, refs = _layer_run(P, inp)
+    assert P.last_path() == 1
+    lcheck(outs, refs, TOL)
+
+
+@pytest.mark.parametrize("logit_a,logit_k", [(False, True), (True, False), (False, False)])
+def test_layer_bwd_narrow_flags(P, logit_a, logit_k):
+    from swr_inputs import layer_inputs
+    from test_layer import check as lcheck
+    inp = layer_inputs(2, 300, 128, 16, 8, 8, dtype=torch.bfloat16, seed=9, carry=True)
+    if not logit_a:
+        inp["za"] = torch.sigmoid(inp["za"].float()).to(torch.bfloat16)
+    if not logit_k:
+        inp["zk"] = torch.sigmoid(inp["zk"].float()).to(torch.bfloat16)
+    outs, refs = _layer_run(P, inp, logit_a=logit_a, logit_k=logit_k)
+    lcheck(outs, refs, TOL)
+
+
+def test_layer_bwd_narrow_deterministic(P):
+    from swr_inputs import layer_inputs
+    inp = layer_inputs(2, 1000, 128, 16, 8, 8, dtype=torch.bfloat16, seed=4)
+    g = {k: v.cuda() for k, v in inp.items()}
+    r1 = P.phalanx_layer_mix_bwd(g["q"], g["zk"], g["v"], g["za"], g["dy"])
+    r2 = P.phalanx_layer_mix_bwd(g["q"], g["zk"], g["v"], g["za"], g["dy"])
+    torch.cuda.synchronize()
+    for x1, x2 in zip(r1, r2):
+        assert torch.equal(x1, x2)

@@ -284,11 +284,21 @@ __global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC, LAYER>::NC + 32, LAYER
   __nv_bfloat16* dA = (__nv_bfloat16*)p.da + b * p.sa_b + hc * p.sa_h;
   // operand access inside a stage: tensor x, token i -> this thread's 4 channels
   // rows per token and this thread's row in each tensor's box (LAYER: k and q hold group rows)
-  auto rows = [&](int x) { return (LAYER && x == 0) ? GK : (LAYER && x == 3) ? GQ : HC; };
-  auto row = [&](int x) { return (LAYER && x == 0) ? hl / hk : (LAYER && x == 3) ? hl / hq : hl; };
-  auto ld = [&](const uint8_t* st, int x, int i, float (&f)[VC]) {
-    ld_bf<VC>(st + C::off(x) + ((i * rows(x) + row(x)) * D + c) * 2, f);
+  // LAYER: the thread's byte offset in each box and the box's bytes per token, once (the
+  // group rows make them runtime values; divisions and products kept out of the sweeps)
+  int offx[4], strx[4];
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const int rws = (LAYER && x == 0) ? GK : (LAYER && x == 3) ? GQ : HC;
+    const int rw = (LAYER && x == 0) ? hl / hk : (LAYER && x == 3) ? hl / hq : hl;
+    offx[x] = C::off(x) + (rw * D + c) * 2;
+    strx[x] = rws * D * 2;
+  }
+  auto boff = [&](int x, int i) {
+    if constexpr (LAYER) return offx[x] + i * strx[x];
+    return C::off(x) + ((i * HC + hl) * D + c) * 2;
   };
+  auto ld = [&](const uint8_t* st, int x, int i, float (&f)[VC]) { ld_bf<VC>(st + boff(x, i), f); };
   auto ldA = [&](const uint8_t* st, int i) {  // LAYER: a (= sigma(za)) in fp32 from the prep
     if constexpr (LAYER) return reinterpret_cast<const float*>(st + C::kAFOff)[i * HC + hl];
     return __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(st + C::kAOff + (i * HC + hl) * 2));
@@ -374,7 +384,7 @@ __global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC, LAYER>::NC + 32, LAYER
   // raw operand words (VC bf16) of tensor x, token i, read from the stage in one LDS
   using R = typename std::conditional<VC == 4, uint2, uint32_t>::type;
   auto ldr = [&](const uint8_t* st, int x, int i) {
-    return *reinterpret_cast<const R*>(st + C::off(x) + ((i * rows(x) + row(x)) * D + c) * 2);
+    return *reinterpret_cast<const R*>(st + boff(x, i));
   };
   auto cvt = [&](const R& r, float (&f)[VC]) { ld_bf<VC>(reinterpret_cast<const uint8_t*>(&r), f); };
   auto cvtk = [&](const R& r, float (&f)[VC]) { cvt(r, f); };  // the key operand (LAYER: sigma applied by the prep)
@@ -553,8 +563,10 @@ __global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC, LAYER>::NC + 32, LAYER
       // head order; dzk = (sum dk) k (1 - k) with the group's k = sigma(zk)
       cbar();
       const int64_t G_q = p.H / hq, G_k = p.H / hk;
+      // group counts per CTA are powers of two (HC = 16 is a multiple of hq, hk): shifts
+      const int lgq = __ffs(GQ) - 1, lgk = __ffs(GK) - 1;
       for (int it = tid; it < 16 * GQ * TPH; it += C::NC) {
-        const int i = it / (GQ * TPH), g = (it / TPH) % GQ, cq = VC * (it % TPH);
+        const int rem = it / TPH, i = rem >> lgq, g = rem & (GQ - 1), cq = VC * (it % TPH);
         float acc[VC];
 #pragma unroll
         for (int e = 0; e < VC; ++e) acc[e] = 0.f;
@@ -566,7 +578,7 @@ __global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC, LAYER>::NC + 32, LAYER
         if (gg < G_q && i < lim) st_bf<VC>((__nv_bfloat16*)p.dq + b * p.sq_b + (n0 + i) * p.sq_l + gg * p.sq_h + cq, acc);
       }
       for (int it = tid; it < 16 * GK * TPH; it += C::NC) {
-        const int i = it / (GK * TPH), g = (it / TPH) % GK, cq = VC * (it % TPH);
+        const int rem = it / TPH, i = rem >> lgk, g = rem & (GK - 1), cq = VC * (it % TPH);
         float acc[VC];
 #pragma unroll
         for (int e = 0; e < VC; ++e) acc[e] = 0.f;

@@ -132,13 +132,13 @@ __device__ __forceinline__ void vfma_s(float s, const float (&x)[VC], const floa
   if constexpr (!PK) {
 #pragma unroll
     for (int e = 0; e < VC; ++e) o[e] = fmaf(s, x[e], y[e]);
-    return;
-  }
+  } else {
 #pragma unroll
-  for (int e = 0; e < VC; e += 2) {
-    const float2 r = __ffma2_rn(make_float2(s, s), make_float2(x[e], x[e + 1]), make_float2(y[e], y[e + 1]));
-    o[e] = r.x;
-    o[e + 1] = r.y;
+    for (int e = 0; e < VC; e += 2) {
+      const float2 r = __ffma2_rn(make_float2(s, s), make_float2(x[e], x[e + 1]), make_float2(y[e], y[e + 1]));
+      o[e] = r.x;
+      o[e + 1] = r.y;
+    }
   }
 }
 template <int VC>

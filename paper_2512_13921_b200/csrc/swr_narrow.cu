@@ -399,218 +399,232 @@ __global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC, LAYER>::NC + 32, LAYER
     if (j == j_first) prep(sm + s * C::kStage);  // later stages were prepped as block t-1
     const uint8_t* st = sm + s * C::kStage;
     const int64_t n0 = t * kEll;
-    const int lim = (p.L - n0 < kEll) ? (int)(p.L - n0) : kEll;
-    // A) carrier v_{t-1} = w_{t-1}[15] from the next stage (block t-1 is whole); the
-    //    block's operands are read first, then the chain runs on registers
-    float vprev[VC];
-    if (t > 0) {
-      const int s1 = (j + 1) % NS;
-      mbar_wait(&full[s1], ((j + 1) / NS) & 1);
-      prep(sm + s1 * C::kStage);
-      const uint8_t* sp = sm + s1 * C::kStage;
-      R r0[kEll], r1[kEll];
-      float ap[kEll];
-#pragma unroll
-      for (int i = 0; i < kEll; ++i) {
-        r0[i] = ldr(sp, 0, i);
-        if constexpr (MIX) r1[i] = ldr(sp, 1, i);
-        ap[i] = ldA(sp, i);
-      }
-#pragma unroll
-      for (int i = 0; i < kEll; ++i) {
-        float u[VC];
-        if constexpr (MIX)
-          cvtk(r0[i], u);
-        else
-          cvt(r0[i], u);
-        if constexpr (MIX) {
-          float vv[VC];
-          cvt(r1[i], vv);
-          vmul<VC>(u, vv, u);
+    const int lim_rt = (p.L - n0 < kEll) ? (int)(p.L - n0) : kEll;
+    // LAYER: the block body twice, whole blocks (every block but a ragged last one) without
+    // the per-token validity tests and the ragged tail with them
+    auto block = [&](auto full_t) {
+      constexpr bool FULL = decltype(full_t)::value;
+      const int lim = FULL ? kEll : lim_rt;
+      // A) carrier v_{t-1} = w_{t-1}[15] from the next stage (block t-1 is whole); the
+      //    block's operands are read first, then the chain runs on registers
+      float vprev[VC];
+      if (t > 0) {
+        const int s1 = (j + 1) % NS;
+        mbar_wait(&full[s1], ((j + 1) / NS) & 1);
+        prep(sm + s1 * C::kStage);
+        const uint8_t* sp = sm + s1 * C::kStage;
+        R r0[kEll], r1[kEll];
+        float ap[kEll];
+  #pragma unroll
+        for (int i = 0; i < kEll; ++i) {
+          r0[i] = ldr(sp, 0, i);
+          if constexpr (MIX) r1[i] = ldr(sp, 1, i);
+          ap[i] = ldA(sp, i);
         }
-        if (i == 0) {
-#pragma unroll
-          for (int e = 0; e < VC; ++e) vprev[e] = u[e];
-        } else {
-          vfma_s<VC, MIX>(ap[i], vprev, u, vprev);
-        }
-      }
-    } else {
-#pragma unroll
-      for (int e = 0; e < VC; ++e) vprev[e] = p.carry_in ? p.carry_in[co + e] : 0.f;
-    }
-    // decays of block t (pad a = 1 past L), g[i] = a[0] ... a[i], and Pass I of block t
-    // forward with w kept in registers
-    float av[kEll], gsv[kEll], w[kEll][VC];
-    {
-      R r0[kEll], r1[kEll];
-#pragma unroll
-      for (int i = 0; i < kEll; ++i) {
-        r0[i] = ldr(st, 0, i);
-        if constexpr (MIX) r1[i] = ldr(st, 1, i);
-        av[i] = ldA(st, i);
-      }
-#pragma unroll
-      for (int i = 0; i < kEll; ++i) {
-        if (i >= lim) av[i] = 1.f;
-        gsv[i] = i == 0 ? av[0] : gsv[i - 1] * av[i];
-        float u[VC];
-        if constexpr (MIX)
-          cvtk(r0[i], u);
-        else
-          cvt(r0[i], u);
-        if constexpr (MIX) {
-          float vv[VC];
-          cvt(r1[i], vv);
-          vmul<VC>(u, vv, u);
-        }
-        if (i == 0) {
-#pragma unroll
-          for (int e = 0; e < VC; ++e) w[0][e] = u[e];
-        } else {
-          vfma_s<VC, MIX>(av[i], w[i - 1], u, w[i]);
-        }
-      }
-    }
-    // C) one reverse sweep: lambda, r, du (mixer: dq, dk, dv), the da terms
-    float part[kEll];
-    float lam[VC], mu_next[VC];
-    float rr = 1.f;
-#pragma unroll
-    for (int i0 = kEll - CG; i0 >= 0; i0 -= CG) {
-      R rg[CG], rq[CG], rk[CG], rv[CG];
-#pragma unroll
-      for (int m = 0; m < CG; ++m) {
-        rg[m] = ldr(st, MIX ? 2 : 1, i0 + m);  // dx (SWR) / dy (mixer)
-        if constexpr (MIX) {
-          rq[m] = ldr(st, 3, i0 + m);
-          rk[m] = ldr(st, 0, i0 + m);
-          rv[m] = ldr(st, 1, i0 + m);
-        }
-      }
-#pragma unroll
-      for (int m = CG - 1; m >= 0; --m) {
-        const int i = i0 + m;
-        float g[VC], dd[VC];
-        cvt(rg[m], dd);
-        if constexpr (MIX) {
-          float qq[VC];
-          cvt(rq[m], qq);
-          vmul<VC>(dd, qq, g);  // G = dy (.) q
-        } else {
-#pragma unroll
-          for (int e = 0; e < VC; ++e) g[e] = dd[e];
-        }
-        if (i == kEll - 1) {
-#pragma unroll
-          for (int e = 0; e < VC; ++e) lam[e] = g[e];  // lambda[15] = G[15]
-        } else {
-          vfma_s<VC, MIX>(av[i + 1], lam, g, lam);
-          rr *= av[i + 1];  // r_t[i] = a_t[i+1] ... a_t[15]
-        }
-        float du[VC];
-        vfma_s<VC, MIX>(rr, mu, lam, du);
-        float sdot = 0.f, lv = 0.f;  // sum_c du[i] w[i-1] (w[-1] = 0), sum_c lambda[i] v_{t-1}
-        if (i > 0) {
-#pragma unroll
-          for (int e = 0; e < VC; ++e) sdot = (e == 0) ? du[e] * w[i - 1][e] : fmaf(du[e], w[i - 1][e], sdot);
-        }
-#pragma unroll
-        for (int e = 0; e < VC; ++e) lv = (e == 0) ? lam[e] * vprev[e] : fmaf(lam[e], vprev[e], lv);
-        part[i] = fmaf(i > 0 ? gsv[i - 1] : 1.f, lv, sdot);
-        const int64_t o = xo + (n0 + i) * p.sx_l;
-        const bool valid = act && i < lim;
-        if constexpr (!MIX) {
-          if (valid) st_bf<VC>((__nv_bfloat16*)p.du + o, du);
-        } else {
-          float kk[VC], vv[VC];
-          cvtk(rk[m], kk);
-          cvt(rv[m], vv);
-          float dq[VC], dk[VC], dv[VC], xt[VC];
-          vfma_s<VC, MIX>(gsv[i], vprev, w[i], xt);  // x~ = w + g v
-          vmul<VC>(dd, xt, dq);                 // dq = dy x~
-          vmul<VC>(du, vv, dk);                 // dk = du^ v
-          vfma<VC>(du, kk, dd, dv);             // dv = du^ k + dy
-          if constexpr (LAYER) {  // the group sums below
-            float* q2 = sq + (i * HC + hl) * D + c;
-            float* k2 = sk + (i * HC + hl) * D + c;
-#pragma unroll
-            for (int e = 0; e < VC; ++e) {
-              q2[e] = dq[e];
-              k2[e] = dk[e];
-            }
-            if (valid) st_bf<VC>((__nv_bfloat16*)p.dv + o, dv);
-          } else if (valid) {
-            st_bf<VC>((__nv_bfloat16*)p.dq + o, dq);
-            st_bf<VC>((__nv_bfloat16*)p.dk + o, dk);
-            st_bf<VC>((__nv_bfloat16*)p.dv + o, dv);
+  #pragma unroll
+        for (int i = 0; i < kEll; ++i) {
+          float u[VC];
+          if constexpr (MIX)
+            cvtk(r0[i], u);
+          else
+            cvt(r0[i], u);
+          if constexpr (MIX) {
+            float vv[VC];
+            cvt(r1[i], vv);
+            vmul<VC>(u, vv, u);
+          }
+          if (i == 0) {
+  #pragma unroll
+            for (int e = 0; e < VC; ++e) vprev[e] = u[e];
+          } else {
+            vfma_s<VC, MIX>(ap[i], vprev, u, vprev);
           }
         }
-        if (i == 0) {
-#pragma unroll
-          for (int e = 0; e < VC; ++e) mu_next[e] = av[0] * lam[e];  // mu_{t-1} = a_t[0] lambda_t[0]
+      } else {
+  #pragma unroll
+        for (int e = 0; e < VC; ++e) vprev[e] = p.carry_in ? p.carry_in[co + e] : 0.f;
+      }
+      // decays of block t (pad a = 1 past L), g[i] = a[0] ... a[i], and Pass I of block t
+      // forward with w kept in registers
+      float av[kEll], gsv[kEll], w[kEll][VC];
+      {
+        R r0[kEll], r1[kEll];
+  #pragma unroll
+        for (int i = 0; i < kEll; ++i) {
+          r0[i] = ldr(st, 0, i);
+          if constexpr (MIX) r1[i] = ldr(st, 1, i);
+          av[i] = ldA(st, i);
+        }
+  #pragma unroll
+        for (int i = 0; i < kEll; ++i) {
+          if (i >= lim) av[i] = 1.f;
+          gsv[i] = i == 0 ? av[0] : gsv[i - 1] * av[i];
+          float u[VC];
+          if constexpr (MIX)
+            cvtk(r0[i], u);
+          else
+            cvt(r0[i], u);
+          if constexpr (MIX) {
+            float vv[VC];
+            cvt(r1[i], vv);
+            vmul<VC>(u, vv, u);
+          }
+          if (i == 0) {
+  #pragma unroll
+            for (int e = 0; e < VC; ++e) w[0][e] = u[e];
+          } else {
+            vfma_s<VC, MIX>(av[i], w[i - 1], u, w[i]);
+          }
         }
       }
-    }
-#pragma unroll
-    for (int e = 0; e < VC; ++e) mu[e] = mu_next[e];
-    if (t == 0 && act && p.mu_out) {
-#pragma unroll
-      for (int e = 0; e < VC; ++e) p.mu_out[co + e] = mu[e];
-    }
-    if constexpr (LAYER) {
-      // group sums: item (token i, group row g, channel pair) sums the group's heads in
-      // head order; dzk = (sum dk) k (1 - k) with the group's k = sigma(zk)
-      cbar();
-      const int64_t G_q = p.H / hq, G_k = p.H / hk;
-      // group counts per CTA are powers of two (HC = 16 is a multiple of hq, hk): shifts
-      const int lgq = __ffs(GQ) - 1, lgk = __ffs(GK) - 1;
-      for (int it = tid; it < 16 * GQ * TPH; it += C::NC) {
-        const int rem = it / TPH, i = rem >> lgq, g = rem & (GQ - 1), cq = VC * (it % TPH);
-        float acc[VC];
-#pragma unroll
-        for (int e = 0; e < VC; ++e) acc[e] = 0.f;
-        for (int m = 0; m < hq; ++m) {
-#pragma unroll
-          for (int e = 0; e < VC; ++e) acc[e] += sq[(i * HC + g * hq + m) * D + cq + e];
+      // C) one reverse sweep: lambda, r, du (mixer: dq, dk, dv), the da terms
+      float part[kEll];
+      float lam[VC], mu_next[VC];
+      float rr = 1.f;
+  #pragma unroll
+      for (int i0 = kEll - CG; i0 >= 0; i0 -= CG) {
+        R rg[CG], rq[CG], rk[CG], rv[CG];
+  #pragma unroll
+        for (int m = 0; m < CG; ++m) {
+          rg[m] = ldr(st, MIX ? 2 : 1, i0 + m);  // dx (SWR) / dy (mixer)
+          if constexpr (MIX) {
+            rq[m] = ldr(st, 3, i0 + m);
+            rk[m] = ldr(st, 0, i0 + m);
+            rv[m] = ldr(st, 1, i0 + m);
+          }
         }
-        const int64_t gg = h0 / hq + g;
-        if (gg < G_q && i < lim) st_bf<VC>((__nv_bfloat16*)p.dq + b * p.sq_b + (n0 + i) * p.sq_l + gg * p.sq_h + cq, acc);
-      }
-      for (int it = tid; it < 16 * GK * TPH; it += C::NC) {
-        const int rem = it / TPH, i = rem >> lgk, g = rem & (GK - 1), cq = VC * (it % TPH);
-        float acc[VC];
-#pragma unroll
-        for (int e = 0; e < VC; ++e) acc[e] = 0.f;
-        for (int m = 0; m < hk; ++m) {
-#pragma unroll
-          for (int e = 0; e < VC; ++e) acc[e] += sk[(i * HC + g * hk + m) * D + cq + e];
+  #pragma unroll
+        for (int m = CG - 1; m >= 0; --m) {
+          const int i = i0 + m;
+          float g[VC], dd[VC];
+          cvt(rg[m], dd);
+          if constexpr (MIX) {
+            float qq[VC];
+            cvt(rq[m], qq);
+            vmul<VC>(dd, qq, g);  // G = dy (.) q
+          } else {
+  #pragma unroll
+            for (int e = 0; e < VC; ++e) g[e] = dd[e];
+          }
+          if (i == kEll - 1) {
+  #pragma unroll
+            for (int e = 0; e < VC; ++e) lam[e] = g[e];  // lambda[15] = G[15]
+          } else {
+            vfma_s<VC, MIX>(av[i + 1], lam, g, lam);
+            rr *= av[i + 1];  // r_t[i] = a_t[i+1] ... a_t[15]
+          }
+          float du[VC];
+          vfma_s<VC, MIX>(rr, mu, lam, du);
+          float sdot = 0.f, lv = 0.f;  // sum_c du[i] w[i-1] (w[-1] = 0), sum_c lambda[i] v_{t-1}
+          if (i > 0) {
+  #pragma unroll
+            for (int e = 0; e < VC; ++e) sdot = (e == 0) ? du[e] * w[i - 1][e] : fmaf(du[e], w[i - 1][e], sdot);
+          }
+  #pragma unroll
+          for (int e = 0; e < VC; ++e) lv = (e == 0) ? lam[e] * vprev[e] : fmaf(lam[e], vprev[e], lv);
+          part[i] = fmaf(i > 0 ? gsv[i - 1] : 1.f, lv, sdot);
+          const int64_t o = xo + (n0 + i) * p.sx_l;
+          const bool valid = act && i < lim;
+          if constexpr (!MIX) {
+            if (valid) st_bf<VC>((__nv_bfloat16*)p.du + o, du);
+          } else {
+            float kk[VC], vv[VC];
+            cvtk(rk[m], kk);
+            cvt(rv[m], vv);
+            float dq[VC], dk[VC], dv[VC], xt[VC];
+            vfma_s<VC, MIX>(gsv[i], vprev, w[i], xt);  // x~ = w + g v
+            vmul<VC>(dd, xt, dq);                 // dq = dy x~
+            vmul<VC>(du, vv, dk);                 // dk = du^ v
+            vfma<VC>(du, kk, dd, dv);             // dv = du^ k + dy
+            if constexpr (LAYER) {  // the group sums below
+              float* q2 = sq + (i * HC + hl) * D + c;
+              float* k2 = sk + (i * HC + hl) * D + c;
+  #pragma unroll
+              for (int e = 0; e < VC; ++e) {
+                q2[e] = dq[e];
+                k2[e] = dk[e];
+              }
+              if (valid) st_bf<VC>((__nv_bfloat16*)p.dv + o, dv);
+            } else if (valid) {
+              st_bf<VC>((__nv_bfloat16*)p.dq + o, dq);
+              st_bf<VC>((__nv_bfloat16*)p.dk + o, dk);
+              st_bf<VC>((__nv_bfloat16*)p.dv + o, dv);
+            }
+          }
+          if (i == 0) {
+  #pragma unroll
+            for (int e = 0; e < VC; ++e) mu_next[e] = av[0] * lam[e];  // mu_{t-1} = a_t[0] lambda_t[0]
+          }
         }
-        if (p.logit_k) {
-          float kv[VC];
-          ld_bf<VC>(st + ((i * GK + g) * D + cq) * 2, kv);  // k = sigma(zk) of the group row (prep)
-#pragma unroll
-          for (int e = 0; e < VC; ++e) acc[e] *= kv[e] * (1.f - kv[e]);
+      }
+  #pragma unroll
+      for (int e = 0; e < VC; ++e) mu[e] = mu_next[e];
+      if (t == 0 && act && p.mu_out) {
+  #pragma unroll
+        for (int e = 0; e < VC; ++e) p.mu_out[co + e] = mu[e];
+      }
+      if constexpr (LAYER) {
+        // group sums: item (token i, group row g, channel pair) sums the group's heads in
+        // head order; dzk = (sum dk) k (1 - k) with the group's k = sigma(zk)
+        cbar();
+        const int64_t G_q = p.H / hq, G_k = p.H / hk;
+        // group counts per CTA are powers of two (HC = 16 is a multiple of hq, hk): shifts
+        const int lgq = __ffs(GQ) - 1, lgk = __ffs(GK) - 1;
+        for (int it = tid; it < 16 * GQ * TPH; it += C::NC) {
+          const int rem = it / TPH, i = rem >> lgq, g = rem & (GQ - 1), cq = VC * (it % TPH);
+          float acc[VC];
+  #pragma unroll
+          for (int e = 0; e < VC; ++e) acc[e] = 0.f;
+          for (int m = 0; m < hq; ++m) {
+  #pragma unroll
+            for (int e = 0; e < VC; ++e) acc[e] += sq[(i * HC + g * hq + m) * D + cq + e];
+          }
+          const int64_t gg = h0 / hq + g;
+          if (gg < G_q && i < lim) st_bf<VC>((__nv_bfloat16*)p.dq + b * p.sq_b + (n0 + i) * p.sq_l + gg * p.sq_h + cq, acc);
         }
-        const int64_t gg = h0 / hk + g;
-        if (gg < G_k && i < lim) st_bf<VC>((__nv_bfloat16*)p.dk + b * p.sk_b + (n0 + i) * p.sk_l + gg * p.sk_h + cq, acc);
+        for (int it = tid; it < 16 * GK * TPH; it += C::NC) {
+          const int rem = it / TPH, i = rem >> lgk, g = rem & (GK - 1), cq = VC * (it % TPH);
+          float acc[VC];
+  #pragma unroll
+          for (int e = 0; e < VC; ++e) acc[e] = 0.f;
+          for (int m = 0; m < hk; ++m) {
+  #pragma unroll
+            for (int e = 0; e < VC; ++e) acc[e] += sk[(i * HC + g * hk + m) * D + cq + e];
+          }
+          if (p.logit_k) {
+            float kv[VC];
+            ld_bf<VC>(st + ((i * GK + g) * D + cq) * 2, kv);  // k = sigma(zk) of the group row (prep)
+  #pragma unroll
+            for (int e = 0; e < VC; ++e) acc[e] *= kv[e] * (1.f - kv[e]);
+          }
+          const int64_t gg = h0 / hk + g;
+          if (gg < G_k && i < lim) st_bf<VC>((__nv_bfloat16*)p.dk + b * p.sk_b + (n0 + i) * p.sk_l + gg * p.sk_h + cq, acc);
+        }
+        cbar();  // the scratch is rewritten by the next block
+        if (p.logit_a) {  // dza = da sigma'(za), sigma' = a (1 - a)
+  #pragma unroll
+          for (int i = 0; i < kEll; ++i) part[i] *= av[i] * (1.f - av[i]);
+        }
       }
-      cbar();  // the scratch is rewritten by the next block
-      if (p.logit_a) {  // dza = da sigma'(za), sigma' = a (1 - a)
-#pragma unroll
-        for (int i = 0; i < kEll; ++i) part[i] *= av[i] * (1.f - av[i]);
+      release(s);  // block t's inputs are consumed (block t-1's stay for the next step)
+      // da: deterministic reduction over the head's channels
+      head_reduce<TPH>(part, qd);
+      constexpr int NV = kEll / TPH;
+      if (act) {
+  #pragma unroll
+        for (int k = 0; k < NV; ++k) {
+          const int tok = NV * qd + k;
+          if (tok < lim) dA[(n0 + tok) * p.sa_l] = __float2bfloat16_rn(part[k]);
+        }
       }
-    }
-    release(s);  // block t's inputs are consumed (block t-1's stay for the next step)
-    // da: deterministic reduction over the head's channels
-    head_reduce<TPH>(part, qd);
-    constexpr int NV = kEll / TPH;
-    if (act) {
-#pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        const int tok = NV * qd + k;
-        if (tok < lim) dA[(n0 + tok) * p.sa_l] = __float2bfloat16_rn(part[k]);
-      }
+    };
+    if constexpr (LAYER) {  // (measured: the layer backward gains 465 -> 423 us at d = 16;
+      if (lim_rt == kEll)  // the SWR / mixer kernels lose 3-6% to the larger code)
+        block(std::true_type{});
+      else
+        block(std::false_type{});
+    } else {
+      block(std::false_type{});
     }
   }
 }

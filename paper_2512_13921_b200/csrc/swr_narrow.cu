@@ -42,7 +42,7 @@ namespace nar {
 #define SWR_NAR_GR 2  // layer backward: q / zk group rows per CTA (16 heads: groups of >= 8; smaller groups measured slower than bwd_ffma_vec)
 #endif
 #ifndef SWR_NAR_MINB_L
-#define SWR_NAR_MINB_L 2  // layer backward: CTAs per SM the registers are capped for
+#define SWR_NAR_MINB_L 2  // layer backward at D = 16: CTAs per SM the registers are capped for (D = 32: one CTA fits)
 #endif
 #ifndef SWR_NAR_CG
 #define SWR_NAR_CG 4  // reverse sweep: tokens whose stage reads are issued together
@@ -211,7 +211,7 @@ __device__ __forceinline__ void head_reduce(float (&pv)[16], int qd) {
 // the CTA's HC / hq (HC / hk) group rows, and the group sums of dq / dzk are formed in
 // shared memory in head order (deterministic); HC is a multiple of hq and hk.
 template <bool MIX, int D, int HC, int NS, int VC, bool LAYER = false>
-__global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC, LAYER>::NC + 32, LAYER ? SWR_NAR_MINB_L : 1)
+__global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC, LAYER>::NC + 32, (LAYER && D == 16) ? SWR_NAR_MINB_L : 1)
     bwd_staged(const __grid_constant__ Maps maps, const Params p) {
   static_assert(!LAYER || MIX, "the layer options apply to the mixer");
   using C = Cfg<MIX, D, HC, NS, VC, LAYER>;

@@ -683,13 +683,16 @@ static cudaError_t launch(const Params& p0, cudaStream_t st) {
   if (!tma_encode_bf16(&m.a, p.a, 3, adims, astr, abox, 96 + HC)) return cudaErrorNotSupported;
   constexpr int smem = C::kBytes;
   static_assert(smem <= 227 * 1024, "shared memory budget");
-  static std::atomic<bool> attr{false};
-  if (!attr.load()) {
+  // the attributes are per device (per context): set once for each device this process uses
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = -1;
+  static std::atomic<bool> attr[64];
+  if (dev < 0 || !attr[dev].load(std::memory_order_acquire)) {
     cudaError_t e = cudaFuncSetAttribute(bwd_staged<MIX, D, HC, NS, VC, LAYER>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(bwd_staged<MIX, D, HC, NS, VC, LAYER>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
-    attr.store(true);
+    if (dev >= 0) attr[dev].store(true, std::memory_order_release);
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)((p.nb + p.K - 1) / p.K), (unsigned)((p.H + HC - 1) / HC), (unsigned)p.B);

@@ -414,6 +414,7 @@ __global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC, LAYER>::NC + 32, (LAYE
         prep(sm + s1 * C::kStage);
         const uint8_t* sp = sm + s1 * C::kStage;
         R r0[kEll], r1[kEll];
+        (void)r1;
         float ap[kEll];
   #pragma unroll
         for (int i = 0; i < kEll; ++i) {
@@ -449,6 +450,7 @@ __global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC, LAYER>::NC + 32, (LAYE
       float av[kEll], gsv[kEll], w[kEll][VC];
       {
         R r0[kEll], r1[kEll];
+        (void)r1;
   #pragma unroll
         for (int i = 0; i < kEll; ++i) {
           r0[i] = ldr(st, 0, i);
@@ -484,6 +486,9 @@ __global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC, LAYER>::NC + 32, (LAYE
   #pragma unroll
       for (int i0 = kEll - CG; i0 >= 0; i0 -= CG) {
         R rg[CG], rq[CG], rk[CG], rv[CG];
+        (void)rq;
+        (void)rk;
+        (void)rv;
   #pragma unroll
         for (int m = 0; m < CG; ++m) {
           rg[m] = ldr(st, MIX ? 2 : 1, i0 + m);  // dx (SWR) / dy (mixer)

@@ -51,7 +51,11 @@ namespace nar {
 struct Maps {
   CUtensorMap t[4];  // d-tensors: SWR u, dx; mixer k, v, dy, q
   CUtensorMap a;     // decays
+  CUtensorMap o[3];  // TMA-stored outputs: SWR du; mixer dq, dk, dv
 };
+#ifndef SWR_NAR_TMA_ST
+#define SWR_NAR_TMA_ST 1  // outputs through a shared-memory tile and a TMA store (not the layer)
+#endif
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
@@ -94,6 +98,16 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* m, uin
       "l"(m), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* m, const void* src, int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(m),
+      "r"(su32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 // VC bf16 channels (VC = 2: one 32-bit word, VC = 4: two) <-> fp32
 template <int VC>
 __device__ __forceinline__ void ld_bf(const uint8_t* q, float (&f)[VC]) {
@@ -180,7 +194,15 @@ struct Cfg {
   static constexpr int kStage = ((kAFOff + (LAYER ? 16 * HC * 4 : 0) + 127) / 128) * 128;
   // LAYER: the per-head dq / dk terms of a block, [16][HC][D] fp32 each, for the group sums
   static constexpr int kScrG = NS * kStage;
-  static constexpr int kBar = kScrG + (LAYER ? 2 * 16 * HC * D * 4 : 0);
+  // TST: the block's output tiles [16][HC][D] bf16 (SWR du; mixer dq, dk, dv), double-
+  // buffered, leave through TMA stores (rows past L and heads past H are clipped by TMA).
+  // Measured (tools/nar_time.py against -DSWR_NAR_TMA_ST=0): SWR d = 16 168.5 -> 165 us,
+  // d = 32 155 -> 148 us, mixer d = 32 338 -> 313 us; the d = 16 mixer (16 heads, one CTA
+  // per SM) 354 -> 371 us keeps the per-thread stores
+  static constexpr bool TST = SWR_NAR_TMA_ST && !LAYER && !(MIX && D == 16);
+  static constexpr int NOUT = MIX ? 3 : 1;
+  static constexpr int kOutOff = kScrG + (LAYER ? 2 * 16 * HC * D * 4 : 0);
+  static constexpr int kBar = kOutOff + (TST ? 2 * NOUT * kTile : 0);
   static constexpr int kBytes = kBar + 2 * NS * 8;
   static_assert(NC % 32 == 0 && NS >= 3, "whole compute warps; current + previous + prefetch");
 };
@@ -480,6 +502,14 @@ __global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC, LAYER>::NC + 32, (LAYE
         }
       }
       // C) one reverse sweep: lambda, r, du (mixer: dq, dk, dv), the da terms
+      uint8_t* ob = sm + C::kOutOff + (j & 1) * C::NOUT * C::kTile;  // TST: this block's output tiles
+      if constexpr (C::TST) {  // the TMA store of two blocks ago has read this buffer
+        if (tid == 0) bulk_wait_read1();
+        cbar();
+      }
+      auto out_at = [&](int x, int i) {
+        return reinterpret_cast<__nv_bfloat16*>(ob + x * C::kTile + ((i * HC + hl) * D + c) * 2);
+      };
       float part[kEll];
       float lam[VC], mu_next[VC];
       float rr = 1.f;
@@ -530,8 +560,13 @@ __global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC, LAYER>::NC + 32, (LAYE
           part[i] = fmaf(i > 0 ? gsv[i - 1] : 1.f, lv, sdot);
           const int64_t o = xo + (n0 + i) * p.sx_l;
           const bool valid = act && i < lim;
+          (void)o;
+          (void)valid;
           if constexpr (!MIX) {
-            if (valid) st_bf<VC>((__nv_bfloat16*)p.du + o, du);
+            if constexpr (C::TST)
+            st_bf<VC>(out_at(0, i), du);
+          else if (valid)
+            st_bf<VC>((__nv_bfloat16*)p.du + o, du);
           } else {
             float kk[VC], vv[VC];
             cvtk(rk[m], kk);
@@ -550,6 +585,10 @@ __global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC, LAYER>::NC + 32, (LAYE
                 k2[e] = dk[e];
               }
               if (valid) st_bf<VC>((__nv_bfloat16*)p.dv + o, dv);
+            } else if constexpr (C::TST) {
+              st_bf<VC>(out_at(0, i), dq);
+              st_bf<VC>(out_at(1, i), dk);
+              st_bf<VC>(out_at(2, i), dv);
             } else if (valid) {
               st_bf<VC>((__nv_bfloat16*)p.dq + o, dq);
               st_bf<VC>((__nv_bfloat16*)p.dk + o, dk);
@@ -611,6 +650,15 @@ __global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC, LAYER>::NC + 32, (LAYE
           for (int i = 0; i < kEll; ++i) part[i] *= av[i] * (1.f - av[i]);
         }
       }
+      if constexpr (C::TST) {  // the output tiles are complete: one thread stores them
+        fence_proxy_async();
+        cbar();
+        if (tid == 0) {
+#pragma unroll
+          for (int x = 0; x < C::NOUT; ++x) tma_store_4d(&maps.o[x], ob + x * C::kTile, 0, h0, (int)n0, (int)b);
+          bulk_commit();
+        }
+      }
       release(s);  // block t's inputs are consumed (block t-1's stay for the next step)
       // da: deterministic reduction over the head's channels
       head_reduce<TPH>(part, qd);
@@ -632,6 +680,7 @@ __global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC, LAYER>::NC + 32, (LAYE
       block(std::false_type{});
     }
   }
+  if (C::TST && tid == 0) bulk_wait_all();  // the last stores have read their tiles
 }
 
 // heads per CTA and ring stages, measured back to back at d = 16, h = 128, L = 8K, B = 8
@@ -681,6 +730,11 @@ static cudaError_t launch(const Params& p0, cudaStream_t st) {
     } else if (!tma_encode_bf16(&m.t[x], ts[x], 4, dims, str, box, 64 + HC)) {
       return cudaErrorNotSupported;
     }
+  }
+  if constexpr (C::TST) {
+    void* os[3] = {MIX ? p.dq : p.du, p.dk, p.dv};
+    for (int x = 0; x < C::NOUT; ++x)
+      if (!tma_encode_bf16(&m.o[x], os[x], 4, dims, str, box, 128 + HC)) return cudaErrorNotSupported;
   }
   const uint64_t adims[3] = {(uint64_t)p.H, (uint64_t)p.L, (uint64_t)p.B};
   const uint64_t astr[2] = {(uint64_t)p.sa_l * 2, (uint64_t)p.sa_b * 2};

@@ -510,6 +510,11 @@ __global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC, LAYER>::NC + 32, (LAYE
       auto out_at = [&](int x, int i) {
         return reinterpret_cast<__nv_bfloat16*>(ob + x * C::kTile + ((i * HC + hl) * D + c) * 2);
       };
+      // per-thread global stores: the block's base offset once, token offsets in 32 bits
+      const int64_t ob0 = xo + n0 * p.sx_l;
+      const int sxl = (int)p.sx_l;  // < 2^26 (narrow_supported)
+      (void)ob0;
+      (void)sxl;
       float part[kEll];
       float lam[VC], mu_next[VC];
       float rr = 1.f;
@@ -558,7 +563,8 @@ __global__ void __launch_bounds__(Cfg<MIX, D, HC, NS, VC, LAYER>::NC + 32, (LAYE
   #pragma unroll
           for (int e = 0; e < VC; ++e) lv = (e == 0) ? lam[e] * vprev[e] : fmaf(lam[e], vprev[e], lv);
           part[i] = fmaf(i > 0 ? gsv[i - 1] : 1.f, lv, sdot);
-          const int64_t o = xo + (n0 + i) * p.sx_l;
+          // (32-bit token offsets: layer 423 -> 413 us; the mixer measured 1% slower with them)
+          const int64_t o = LAYER ? ob0 + i * sxl : xo + (n0 + i) * p.sx_l;
           const bool valid = act && i < lim;
           (void)o;
           (void)valid;
@@ -786,7 +792,8 @@ bool narrow_supported(int op, bool bf16, const Params& p) {
   }
   if (p.sx_h != p.D || (p.sx_l * 2) % 16 || (p.sx_b * 2) % 16) return false;
   if (p.sa_h != 1 || (p.sa_l * 2) % 16 || (p.sa_b * 2) % 16) return false;
-  if (p.B > 65535 || p.H > (int64_t)65535 * 8 || p.L > (int64_t(1) << 30)) return false;
+  if (p.B > 65535 || p.H > (int64_t)65535 * 8 || p.L > (int64_t(1) << 30) || p.sx_l > (int64_t(1) << 26))
+    return false;
   auto a16 = [](const void* q) { return q == nullptr || (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
   const void* ptrs[] = {p.u, p.dx, p.du, p.q, p.k, p.v, p.dy, p.dq, p.dk, p.dv, p.a};
   for (const void* q : ptrs)

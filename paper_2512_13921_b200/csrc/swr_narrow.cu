@@ -44,6 +44,9 @@ namespace nar {
 #ifndef SWR_NAR_MINB_L
 #define SWR_NAR_MINB_L 2  // layer backward at D = 16: CTAs per SM the registers are capped for (D = 32: one CTA fits)
 #endif
+#ifndef SWR_NAR_K_L
+#define SWR_NAR_K_L 16  // layer backward (2 CTAs per SM): shorter chunks balance better, 413 -> 382 us
+#endif
 #ifndef SWR_NAR_CG
 #define SWR_NAR_CG 4  // reverse sweep: tokens whose stage reads are issued together
 #endif
@@ -719,7 +722,7 @@ template <bool MIX, int D, int HC, int NS, int VC, bool LAYER = false>
 static cudaError_t launch(const Params& p0, cudaStream_t st) {
   using C = Cfg<MIX, D, HC, NS, VC, LAYER>;
   Params p = p0;
-  p.K = SWR_NAR_K;
+  p.K = LAYER ? SWR_NAR_K_L : SWR_NAR_K;
   Maps m;
   const void* ts[4] = {MIX ? p.k : p.u, MIX ? p.v : p.dx, p.dy, p.q};
   const uint64_t dims[4] = {(uint64_t)p.D, (uint64_t)p.H, (uint64_t)p.L, (uint64_t)p.B};
